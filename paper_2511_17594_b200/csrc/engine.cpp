@@ -1,0 +1,525 @@
+// engine.cpp -- operator dispatch (src/kernels.cpp:465-531), the
+// input-aware scheduler (src/scheduler.cpp:18-247) and the CSR attention
+// pipeline (src/attention.cpp:9-46) over device graphs.
+//
+// Decision procedure (decide_common, src/scheduler.cpp:86-167), unchanged:
+//   key = (device_sig, graph_sig, F, op) -> forced env knobs -> cache hit
+//   (cached / replayed) -> replay-only miss (warn + baseline, or ReplayMiss)
+//   -> features -> roofline shortlist[:top_k] -> probe lock -> time the
+//   baseline kernel, then each candidate (strict < keeps the first of equal
+//   medians) -> accept iff best >= 0 and t* <= alpha * t_b -> cache put.
+// B200 changes: the probe sample (a degree-stratified induced row slice)
+// is built on device and only when a probe actually runs -- the reference
+// builds it before the cache lookup (src/scheduler.cpp:198-199); graph_sig
+// is memoized per graph handle; probes are timed with CUDA events on the
+// probe stream.
+#include "engine.hpp"
+#include "ops.hpp"
+
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <mutex>
+
+namespace asb {
+
+namespace {
+
+std::atomic<std::uint64_t> g_probe_launches{0};
+std::mutex g_probe_mutex;  // one probe in flight per process (src/scheduler.cpp:20-22)
+
+std::optional<as_variant> forced_env_variant(int op) {  // src/scheduler.cpp:46-59
+    auto ft = env::get_int("AUTOSAGE_FTILE");
+    auto wpb = env::get_int("AUTOSAGE_WPB");
+    auto hub = env::get_int("AUTOSAGE_HUB_T");
+    if (!ft && !wpb && !hub) return std::nullopt;
+    as_variant v = default_variant();
+    v.op = op;
+    v.mapping = hub ? AS_MAP_HUBSPLIT : AS_MAP_ROWPARALLEL;
+    if (ft && *ft > 0) v.f_tile = std::uint64_t(*ft);
+    if (wpb && *wpb > 0) v.rows_per_chunk = std::uint64_t(*wpb);
+    if (hub && *hub > 0) v.hub_threshold = std::uint64_t(*hub);
+    v.vectorized = 0;
+    return v;
+}
+
+void set_key(as_decision& d, const as_device_profile& dp, std::uint64_t sig, std::uint64_t f,
+             int op) {
+    std::snprintf(d.key.device_sig, sizeof d.key.device_sig, "%s", dp.device_sig);
+    d.key.graph_sig = sig;
+    d.key.f = f;
+    d.key.op = op;
+}
+
+std::string choice_string(const as_decision& d) {
+    return d.has_choice ? variant_to_string(d.choice) : std::string("baseline");
+}
+
+void from_record(const Record& rec, int source, as_decision& d) {  // src/scheduler.cpp:61-70
+    d.key = key_to_c(rec.key);
+    d.alpha = rec.alpha;
+    d.source = source;
+    d.has_choice = rec.choice != "baseline";
+    if (d.has_choice) d.choice = variant_from_string(rec.choice);
+    d.baseline_ms = rec.t_b;
+    d.t_star = rec.t_star;
+}
+
+Record to_record(const as_decision& d) {  // src/scheduler.cpp:72-82
+    Record rec;
+    rec.key = key_from_c(d.key);
+    rec.choice = choice_string(d);
+    rec.t_b = d.baseline_ms;
+    rec.t_star = d.t_star;
+    rec.alpha = d.alpha;
+    rec.timestamp = unix_now();
+    rec.toolchain = toolchain_tag();
+    return rec;
+}
+
+TimeOnce event_timer(cudaStream_t s) {
+    return [s](const std::string&, const std::function<void()>& run) {
+        cudaEvent_t e0, e1;
+        ASB_CUDA(cudaEventCreate(&e0));
+        ASB_CUDA(cudaEventCreate(&e1));
+        ASB_CUDA(cudaEventRecord(e0, s));
+        run();
+        ASB_CUDA(cudaEventRecord(e1, s));
+        ASB_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        ASB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        return double(ms);
+    };
+}
+
+struct ProbeHooks {
+    std::function<as_features()> features;                 // full-graph features
+    std::function<std::uint64_t()> prepare;                // build the sample, return its rows
+    std::function<void()> run_baseline;
+    std::function<void(const as_variant&)> run_candidate;
+    cudaStream_t stream = nullptr;
+};
+
+as_decision decide_common(const Context& ctx, const as_probe_config& cfg,
+                          const as_device_profile& dp, const std::function<std::uint64_t()>& sig,
+                          std::uint64_t f, int op, ProbeHooks& hooks) {
+    check_probe_config(cfg);
+    as_decision d{};
+    d.best_index = -1;
+    set_key(d, dp, sig(), f, op);
+    d.alpha = cfg.alpha;
+
+    if (auto forced = forced_env_variant(op)) {
+        d.has_choice = 1;
+        d.choice = *forced;
+        d.source = AS_SRC_FORCED_ENV;
+        return d;
+    }
+    if (ctx.cache) {
+        if (auto rec = ctx.cache->get(key_from_c(d.key))) {
+            from_record(*rec, ctx.replay.replay_only ? AS_SRC_REPLAYED : AS_SRC_CACHED, d);
+            return d;
+        }
+    }
+    if (ctx.replay.replay_only) {
+        const std::string k = key_from_c(d.key).to_string();
+        if (ctx.replay.strict) throw ReplayMissError("replay miss for key " + k);
+        std::fprintf(stderr, "autosage: warning: replay miss for %s, using baseline\n", k.c_str());
+        d.source = AS_SRC_REPLAYED;
+        d.has_choice = 0;
+        return d;
+    }
+
+    const as_features gf = hooks.features();
+    auto candidates = shortlist(gf, f, op, dp);
+    if (candidates.size() > std::size_t(cfg.top_k)) candidates.resize(std::size_t(cfg.top_k));
+    const std::uint64_t sample_rows = hooks.prepare ? hooks.prepare() : 0;
+
+    TimeOnce timer = ctx.timer ? ctx.timer : event_timer(hooks.stream);
+    std::lock_guard<std::mutex> probe_lock(g_probe_mutex);
+    cudaStream_t ps = hooks.stream;
+    set_warmup_sync(ps ? std::function<void()>([ps] { cudaStreamSynchronize(ps); })
+                       : std::function<void()>());
+    const auto wall0 = std::chrono::steady_clock::now();
+
+    d.sample_rows = sample_rows;
+    auto tb = time_kernel("baseline", hooks.run_baseline, cfg.iters, cfg.cap_ms, timer);
+    g_probe_launches += std::uint64_t(tb.launches);
+    d.baseline_ms = tb.median_ms;
+    d.baseline_completed = tb.completed;
+    d.baseline_capped = tb.capped;
+    d.max_single_run_ms = tb.max_run_ms;
+
+    double t_star = std::numeric_limits<double>::infinity();
+    int best = -1;
+    for (std::size_t c = 0; c < candidates.size(); ++c) {
+        const as_variant cand = candidates[c];
+        auto st = time_kernel(variant_to_string(cand), [&] { hooks.run_candidate(cand); },
+                              cfg.iters, cfg.cap_ms, timer);
+        g_probe_launches += std::uint64_t(st.launches);
+        if (d.n_candidates < AS_MAX_CANDIDATES) {
+            as_candidate_timing& ct = d.candidates[d.n_candidates++];
+            ct.variant = cand;
+            ct.median_ms = st.median_ms;
+            ct.completed = st.completed;
+            ct.capped = st.capped;
+        }
+        d.max_single_run_ms = std::max(d.max_single_run_ms, st.max_run_ms);
+        if (st.median_ms < t_star) {
+            t_star = st.median_ms;
+            best = int(c);
+        }
+    }
+    set_warmup_sync({});
+    d.t_star = t_star;
+    d.best_index = best;
+    d.probe_wall_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
+    if (best >= 0 && t_star <= cfg.alpha * d.baseline_ms) {
+        d.has_choice = 1;
+        d.choice = candidates[std::size_t(best)];
+    } else {
+        d.has_choice = 0;
+    }
+    d.source = AS_SRC_PROBED;
+    if (ctx.cache) ctx.cache->put(to_record(d));
+    return d;
+}
+
+const as_device_profile& profile_for(const Context& ctx, int device) {
+    return ctx.device ? *ctx.device : gpu_profile(device);
+}
+
+struct TimedRegion {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaStream_t s;
+    bool on;
+    TimedRegion(cudaStream_t st, bool enable) : s(st), on(enable) {
+        if (!on) return;
+        ASB_CUDA(cudaEventCreate(&e0));
+        ASB_CUDA(cudaEventCreate(&e1));
+        ASB_CUDA(cudaEventRecord(e0, s));
+    }
+    double stop() {
+        if (!on) return 0.0;
+        ASB_CUDA(cudaEventRecord(e1, s));
+        ASB_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        ASB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        return double(ms);
+    }
+    ~TimedRegion() {
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+    }
+};
+
+void check_spmm_dims(const Graph& a, std::uint64_t b_rows) {  // src/kernels.cpp:33-37
+    if (a.n_cols != b_rows) throw InvalidArgument("spmm: a.n_cols != b.n_rows");
+}
+
+void check_sddmm_dims(const Graph& p, std::uint64_t x_rows, std::uint64_t y_rows) {
+    if (x_rows != p.n_rows) throw InvalidArgument("sddmm: x.n_rows != pattern.n_rows");
+    if (y_rows != p.n_cols) throw InvalidArgument("sddmm: y.n_rows != pattern.n_cols");
+}
+
+void run_spmm_variant(const as_variant& v, Graph& a, const float* vals, const float* b,
+                      std::uint64_t f, float* c, cudaStream_t s, bool vec) {
+    switch (v.mapping) {
+        case AS_MAP_BASELINE:
+            launch_spmm_baseline(a, vals, b, std::uint32_t(f), c, s);
+            break;
+        case AS_MAP_ROWPARALLEL:
+            ensure_order(a);
+            launch_spmm_rows(a, vals, a.order.get(), a.n_rows, b, std::uint32_t(f), c, v.f_tile, vec,
+                             std::uint32_t(std::min<std::uint64_t>(v.rows_per_chunk, 16)), s);
+            break;
+        case AS_MAP_HUBSPLIT:
+            launch_spmm_hubsplit(a, vals, b, std::uint32_t(f), c, v.f_tile, vec,
+                                 std::uint32_t(std::min<std::uint64_t>(v.rows_per_chunk, 16)),
+                                 v.hub_threshold, s);
+            break;
+    }
+}
+
+} // namespace
+
+// ---- operators --------------------------------------------------------------
+
+void spmm_baseline(Graph& a, const float* vals, const float* b, std::uint64_t b_rows,
+                   std::uint64_t f, float* c, cudaStream_t s) {
+    check_spmm_dims(a, b_rows);
+    DeviceGuard dg(a.device);
+    launch_spmm_baseline(a, vals, b, std::uint32_t(f), c, s);
+}
+
+void spmm_mapped(const as_variant& v, int expect_mapping, Graph& a, const float* vals,
+                 const float* b, std::uint64_t b_rows, std::uint64_t f, float* c, cudaStream_t s) {
+    check_spmm_dims(a, b_rows);
+    check_variant(v);
+    if (v.mapping != expect_mapping)
+        throw InvalidArgument(expect_mapping == AS_MAP_ROWPARALLEL
+                                  ? "spmm_rowparallel: variant mapping mismatch"
+                                  : "spmm_hubsplit: variant mapping mismatch");
+    DeviceGuard dg(a.device);
+    const void* bases[1] = {b};
+    const bool vec = v.vectorized && vec4_eligible(f, bases, 1);
+    run_spmm_variant(v, a, graph_values(a, vals), b, f, c, s, vec);
+}
+
+KernelResult dispatch_spmm(const as_variant& v, Graph& a, const float* vals, const float* b,
+                           std::uint64_t b_rows, std::uint64_t f, float* c, cudaStream_t s,
+                           bool timed) {
+    if (v.op != AS_OP_SPMM)
+        throw InvalidArgument("dispatch: spmm operands given to a non-spmm variant");
+    check_spmm_dims(a, b_rows);
+    KernelResult r;
+    r.variant = apply_env_overrides(v);
+    check_variant(r.variant);
+    const void* bases[1] = {b};
+    const bool vec = r.variant.vectorized && vec4_eligible(f, bases, 1);
+    DeviceGuard dg(a.device);
+    if (r.variant.mapping == AS_MAP_ROWPARALLEL) ensure_order(a);
+    if (r.variant.mapping == AS_MAP_HUBSPLIT) ensure_hub_plan(a, r.variant.hub_threshold);
+    TimedRegion tr(s, timed);
+    run_spmm_variant(r.variant, a, graph_values(a, vals), b, f, c, s, vec);
+    r.elapsed_ms = tr.stop();
+    r.vectorized_path = vec && r.variant.mapping != AS_MAP_BASELINE;
+    return r;
+}
+
+void sddmm_baseline(Graph& p, const float* x, std::uint64_t x_rows, const float* y,
+                    std::uint64_t y_rows, std::uint64_t f, float* out, cudaStream_t s) {
+    check_sddmm_dims(p, x_rows, y_rows);
+    DeviceGuard dg(p.device);
+    launch_sddmm_baseline(p, x, y, std::uint32_t(f), out, s);
+}
+
+void sddmm_mapped(const as_variant& v, Graph& p, const float* x, std::uint64_t x_rows,
+                  const float* y, std::uint64_t y_rows, std::uint64_t f, float* out,
+                  cudaStream_t s) {
+    check_sddmm_dims(p, x_rows, y_rows);
+    check_variant(v);
+    if (v.mapping == AS_MAP_BASELINE)
+        throw InvalidArgument("sddmm_rowparallel: variant mapping mismatch");
+    const void* bases[2] = {x, y};
+    const bool vec = v.vectorized && vec4_eligible(f, bases, 2);
+    DeviceGuard dg(p.device);
+    launch_sddmm_chunks(p, x, y, std::uint32_t(f), out, v.f_tile, vec,
+                        std::uint32_t(std::min<std::uint64_t>(v.rows_per_chunk, 16)), s);
+}
+
+KernelResult dispatch_sddmm(const as_variant& v, Graph& p, const float* x, std::uint64_t x_rows,
+                            const float* y, std::uint64_t y_rows, std::uint64_t f, float* out,
+                            cudaStream_t s, bool timed) {
+    if (v.op != AS_OP_SDDMM)
+        throw InvalidArgument("dispatch: sddmm operands given to a non-sddmm variant");
+    check_sddmm_dims(p, x_rows, y_rows);
+    KernelResult r;
+    r.variant = apply_env_overrides(v);
+    check_variant(r.variant);
+    const void* bases[2] = {x, y};
+    const bool vec = r.variant.vectorized && vec4_eligible(f, bases, 2);
+    DeviceGuard dg(p.device);
+    ensure_chunk_rows(p);
+    TimedRegion tr(s, timed);
+    if (r.variant.mapping == AS_MAP_BASELINE)
+        launch_sddmm_baseline(p, x, y, std::uint32_t(f), out, s);
+    else
+        launch_sddmm_chunks(p, x, y, std::uint32_t(f), out, r.variant.f_tile, vec,
+                            std::uint32_t(std::min<std::uint64_t>(r.variant.rows_per_chunk, 16)), s);
+    r.elapsed_ms = tr.stop();
+    r.vectorized_path = vec && r.variant.mapping != AS_MAP_BASELINE;
+    return r;
+}
+
+void row_softmax(Graph& m, const float* vin, float* vout, cudaStream_t s) {
+    if (m.nnz > 0 && vin == nullptr) throw InvalidArgument("row_softmax: values required");
+    DeviceGuard dg(m.device);
+    launch_row_softmax(m, vin, vout, s);
+}
+
+// ---- scheduler ---------------------------------------------------------------
+
+as_decision decide_spmm(const Context& ctx, const as_probe_config& cfg, Graph& a,
+                        const float* vals, const float* b, std::uint64_t b_rows, std::uint64_t f) {
+    if (a.n_cols != b_rows) throw InvalidArgument("decide_spmm: dimension mismatch");
+    DeviceGuard dg(a.device);
+    cudaStream_t s = ctx.stream ? ctx.stream : a.stream;
+    std::unique_ptr<Graph> sample;
+    DevBuf<float> cbuf;
+    ProbeHooks h;
+    h.stream = s;
+    h.features = [&] { return graph_features(a, kDefaultHubThreshold); };
+    h.prepare = [&]() -> std::uint64_t {
+        const auto rows = sample_row_indices(a, cfg.frac, cfg.min_rows);
+        sample = slice_rows(a, rows, graph_values(a, vals));
+        ensure_order(*sample);
+        cbuf.alloc(std::max<std::uint64_t>(rows.size() * f, 1));
+        return rows.size();
+    };
+    h.run_baseline = [&] {
+        launch_spmm_baseline(*sample, graph_values(*sample, nullptr), b, std::uint32_t(f), cbuf.get(), s);
+    };
+    h.run_candidate = [&](const as_variant& v) {
+        dispatch_spmm(v, *sample, nullptr, b, b_rows, f, cbuf.get(), s, false);
+    };
+    const as_device_profile& dp = profile_for(ctx, a.device);
+    return decide_common(ctx, cfg, dp, [&] { return graph_sig(a); }, f, AS_OP_SPMM, h);
+}
+
+as_decision decide_sddmm(const Context& ctx, const as_probe_config& cfg, Graph& p,
+                         const float* x, std::uint64_t x_rows, const float* y,
+                         std::uint64_t y_rows, std::uint64_t f) {
+    if (x_rows != p.n_rows || y_rows != p.n_cols)
+        throw InvalidArgument("decide_sddmm: dimension mismatch");
+    DeviceGuard dg(p.device);
+    cudaStream_t s = ctx.stream ? ctx.stream : p.stream;
+    std::unique_ptr<Graph> sample;
+    DevBuf<float> xs, obuf;
+    std::uint64_t ns = 0;
+    ProbeHooks h;
+    h.stream = s;
+    h.features = [&] { return graph_features(p, kDefaultHubThreshold); };
+    h.prepare = [&]() -> std::uint64_t {
+        const auto rows = sample_row_indices(p, cfg.frac, cfg.min_rows);
+        sample = slice_rows(p, rows, nullptr);  // SDDMM ignores pattern values
+        ensure_chunk_rows(*sample);
+        // the slice renumbers rows: gather the matching x rows (src/scheduler.cpp:214-220)
+        ns = rows.size();
+        xs.alloc(std::max<std::uint64_t>(ns * f, 1));
+        gather_dense_rows(x, f, rows, xs.get(), s);
+        obuf.alloc(std::max<std::uint64_t>(sample->nnz, 1));
+        return ns;
+    };
+    h.run_baseline = [&] { launch_sddmm_baseline(*sample, xs.get(), y, std::uint32_t(f), obuf.get(), s); };
+    h.run_candidate = [&](const as_variant& v) {
+        dispatch_sddmm(v, *sample, xs.get(), ns, y, y_rows, f, obuf.get(), s, false);
+    };
+    const as_device_profile& dp = profile_for(ctx, p.device);
+    return decide_common(ctx, cfg, dp, [&] { return graph_sig(p); }, f, AS_OP_SDDMM, h);
+}
+
+as_decision decide_host(const Context& ctx, const as_probe_config& cfg, std::uint64_t sig,
+                        const as_features& gf, std::uint64_t f, int op, std::uint64_t sample_rows) {
+    if (!ctx.device) throw InvalidArgument("decide_host: a device profile is required");
+    if (!ctx.timer) throw InvalidArgument("decide_host: a timer is required");
+    ProbeHooks h;
+    h.features = [&] { return gf; };
+    h.prepare = [&] { return sample_rows; };
+    h.run_baseline = [] {};
+    h.run_candidate = [](const as_variant&) {};
+    return decide_common(ctx, cfg, *ctx.device, [&] { return sig; }, f, op, h);
+}
+
+void spmm_auto(const Context& ctx, const as_probe_config& cfg, Graph& a, const float* vals,
+               const float* b, std::uint64_t b_rows, std::uint64_t f, float* c, as_decision* out) {
+    const as_decision d = decide_spmm(ctx, cfg, a, vals, b, b_rows, f);
+    cudaStream_t s = ctx.stream ? ctx.stream : a.stream;
+    if (d.has_choice) dispatch_spmm(d.choice, a, vals, b, b_rows, f, c, s, false);
+    else spmm_baseline(a, graph_values(a, vals), b, b_rows, f, c, s);
+    if (out) *out = d;
+}
+
+void sddmm_auto(const Context& ctx, const as_probe_config& cfg, Graph& p, const float* x,
+                std::uint64_t x_rows, const float* y, std::uint64_t y_rows, std::uint64_t f,
+                float* out, as_decision* dout) {
+    const as_decision d = decide_sddmm(ctx, cfg, p, x, x_rows, y, y_rows, f);
+    cudaStream_t s = ctx.stream ? ctx.stream : p.stream;
+    if (d.has_choice) dispatch_sddmm(d.choice, p, x, x_rows, y, y_rows, f, out, s, false);
+    else sddmm_baseline(p, x, x_rows, y, y_rows, f, out, s);
+    if (dout) *dout = d;
+}
+
+std::uint64_t probe_launch_count() { return g_probe_launches.load(); }
+void reset_probe_launch_count() { g_probe_launches.store(0); }
+
+// ---- attention (src/attention.cpp:9-46) --------------------------------------
+
+void attention_forward(const Context& ctx, const as_probe_config& cfg, Graph& pattern,
+                       const float* q, std::uint64_t q_rows, const float* k, std::uint64_t k_rows,
+                       const float* v, std::uint64_t v_rows, std::uint64_t f, std::uint64_t fv,
+                       float* out, bool fused, as_decision* sd_out, as_decision* pd_out) {
+    if (q_rows != pattern.n_rows || k_rows != pattern.n_cols || v_rows != pattern.n_cols)
+        throw InvalidArgument("attention: operand row counts incompatible with pattern");
+    DeviceGuard dg(pattern.device);
+    cudaStream_t s = ctx.stream ? ctx.stream : pattern.stream;
+
+    const as_decision sd = decide_sddmm(ctx, cfg, pattern, q, q_rows, k, k_rows, f);
+    pattern.att_buf.ensure(std::max<std::uint64_t>(2 * pattern.nnz, 2));
+    float* scores = pattern.att_buf.get();
+    float* p = scores + pattern.nnz;
+    bool p_ready = false;
+    auto make_p = [&] {
+        if (p_ready) return;
+        if (sd.has_choice) dispatch_sddmm(sd.choice, pattern, q, q_rows, k, k_rows, f, scores, s, false);
+        else sddmm_baseline(pattern, q, q_rows, k, k_rows, f, scores, s);
+        row_softmax(pattern, scores, p, s);
+        p_ready = true;
+    };
+    if (!fused) make_p();
+
+    // decide_spmm on p = softmax(scores): same structure (same graph_sig), the
+    // probe sample slices p's values -- materialized only if a probe runs
+    as_decision pd;
+    {
+        if (pattern.n_cols != v_rows) throw InvalidArgument("decide_spmm: dimension mismatch");
+        std::unique_ptr<Graph> sample;
+        DevBuf<float> cbuf;
+        ProbeHooks h;
+        h.stream = s;
+        h.features = [&] { return graph_features(pattern, kDefaultHubThreshold); };
+        h.prepare = [&]() -> std::uint64_t {
+            make_p();
+            const auto rows = sample_row_indices(pattern, cfg.frac, cfg.min_rows);
+            sample = slice_rows(pattern, rows, p);
+            ensure_order(*sample);
+            cbuf.alloc(std::max<std::uint64_t>(rows.size() * fv, 1));
+            return rows.size();
+        };
+        h.run_baseline = [&] {
+            launch_spmm_baseline(*sample, graph_values(*sample, nullptr), v, std::uint32_t(fv),
+                                 cbuf.get(), s);
+        };
+        h.run_candidate = [&](const as_variant& var) {
+            dispatch_spmm(var, *sample, nullptr, v, v_rows, fv, cbuf.get(), s, false);
+        };
+        pd = decide_common(ctx, cfg, profile_for(ctx, pattern.device),
+                           [&] { return graph_sig(pattern); }, fv, AS_OP_SPMM, h);
+    }
+
+    bool done = false;
+    if (fused && !p_ready) {
+        // numerics the decided unfused pipeline would produce
+        const void* qk[2] = {q, k};
+        const void* vv[1] = {v};
+        as_variant sv = sd.has_choice ? apply_env_overrides(sd.choice) : default_variant();
+        const bool svec = sd.has_choice && sv.mapping != AS_MAP_BASELINE && sv.vectorized &&
+                          vec4_eligible(f, qk, 2);
+        const std::uint64_t sft = effective_tile(sv.f_tile, f);
+        std::uint64_t hub_t = 0;
+        if (pd.has_choice) {
+            const as_variant pv = apply_env_overrides(pd.choice);
+            if (pv.mapping == AS_MAP_HUBSPLIT) hub_t = pv.hub_threshold;
+        }
+        const bool ok = f > 0 && f % 4 == 0 && vec4_eligible(f, qk, 2) && fv > 0 && fv % 4 == 0 &&
+                        fv <= 512 && vec4_eligible(fv, vv, 1) && (!svec || sft % 4 == 0);
+        if (ok) {
+            launch_attention_fused(pattern, q, k, v, std::uint32_t(f), std::uint32_t(fv), out, sft,
+                                   svec, hub_t, s);
+            done = true;
+        }
+    }
+    if (!done) {
+        make_p();
+        if (pd.has_choice) dispatch_spmm(pd.choice, pattern, p, v, v_rows, fv, out, s, false);
+        else spmm_baseline(pattern, p, v, v_rows, fv, out, s);
+    }
+    if (sd_out) *sd_out = sd;
+    if (pd_out) *pd_out = pd;
+}
+
+} // namespace asb

@@ -1,0 +1,77 @@
+// engine.hpp -- operator dispatch, the input-aware scheduler and the
+// attention pipeline over device graphs (host C++).
+#pragma once
+
+#include "cache.hpp"
+#include "graph.hpp"
+#include "policy.hpp"
+
+namespace asb {
+
+const as_device_profile& gpu_profile(int device);
+
+struct KernelResult {
+    as_variant variant{};
+    bool vectorized_path = false;
+    double elapsed_ms = 0.0;
+};
+
+// Value array a graph operator reads: explicit override, else the graph's.
+inline const float* graph_values(const Graph& g, const float* override_vals) {
+    if (override_vals) return override_vals;
+    return g.has_val ? g.val.get() : nullptr;
+}
+
+// spmm_baseline (src/kernels.cpp:210-228): no variant, no env overrides.
+void spmm_baseline(Graph& a, const float* vals, const float* b, std::uint64_t b_rows,
+                   std::uint64_t f, float* c, cudaStream_t s);
+// spmm_rowparallel / spmm_hubsplit with the reference's mapping checks.
+void spmm_mapped(const as_variant& v, int expect_mapping, Graph& a, const float* vals,
+                 const float* b, std::uint64_t b_rows, std::uint64_t f, float* c, cudaStream_t s);
+// dispatch (src/kernels.cpp:485-531); `timed` synchronizes and fills
+// elapsed_ms from CUDA events.
+KernelResult dispatch_spmm(const as_variant& v, Graph& a, const float* vals, const float* b,
+                           std::uint64_t b_rows, std::uint64_t f, float* c, cudaStream_t s,
+                           bool timed);
+void sddmm_baseline(Graph& p, const float* x, std::uint64_t x_rows, const float* y,
+                    std::uint64_t y_rows, std::uint64_t f, float* out, cudaStream_t s);
+// sddmm_rowparallel (src/kernels.cpp:357-429): variant as given, no env.
+void sddmm_mapped(const as_variant& v, Graph& p, const float* x, std::uint64_t x_rows,
+                  const float* y, std::uint64_t y_rows, std::uint64_t f, float* out,
+                  cudaStream_t s);
+KernelResult dispatch_sddmm(const as_variant& v, Graph& p, const float* x, std::uint64_t x_rows,
+                            const float* y, std::uint64_t y_rows, std::uint64_t f, float* out,
+                            cudaStream_t s, bool timed);
+void row_softmax(Graph& m, const float* vin, float* vout, cudaStream_t s);
+
+// ScheduleContext (include/autosage/scheduler.hpp:61-69)
+struct Context {
+    const as_device_profile* device = nullptr;  // nullptr: calibrated GPU profile
+    ScheduleCache* cache = nullptr;
+    TimeOnce timer;                              // empty: CUDA events
+    as_replay_policy replay{};
+    cudaStream_t stream = nullptr;               // nullptr: the graph's stream
+};
+
+as_decision decide_spmm(const Context& ctx, const as_probe_config& cfg, Graph& a,
+                        const float* vals, const float* b, std::uint64_t b_rows, std::uint64_t f);
+as_decision decide_sddmm(const Context& ctx, const as_probe_config& cfg, Graph& p,
+                         const float* x, std::uint64_t x_rows, const float* y,
+                         std::uint64_t y_rows, std::uint64_t f);
+as_decision decide_host(const Context& ctx, const as_probe_config& cfg, std::uint64_t sig,
+                        const as_features& gf, std::uint64_t f, int op, std::uint64_t sample_rows);
+void spmm_auto(const Context& ctx, const as_probe_config& cfg, Graph& a, const float* vals,
+               const float* b, std::uint64_t b_rows, std::uint64_t f, float* c, as_decision* d);
+void sddmm_auto(const Context& ctx, const as_probe_config& cfg, Graph& p, const float* x,
+                std::uint64_t x_rows, const float* y, std::uint64_t y_rows, std::uint64_t f,
+                float* out, as_decision* d);
+
+std::uint64_t probe_launch_count();
+void reset_probe_launch_count();
+
+void attention_forward(const Context& ctx, const as_probe_config& cfg, Graph& pattern,
+                       const float* q, std::uint64_t q_rows, const float* k, std::uint64_t k_rows,
+                       const float* v, std::uint64_t v_rows, std::uint64_t f, std::uint64_t fv,
+                       float* out, bool fused, as_decision* sd, as_decision* pd);
+
+} // namespace asb

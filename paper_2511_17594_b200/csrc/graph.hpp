@@ -1,0 +1,140 @@
+// graph.hpp -- device-resident CSR graph handle (the B200 home of the
+// reference's CsrMatrix, include/autosage/csr.hpp:24-45) and the derived
+// per-graph schedule data memoized on it.
+//
+// HBM layout per graph (one allocation each, 256-B aligned by cudaMalloc):
+//   rowptr  u64[n_rows+1]   colind u32[nnz]   val f32[nnz] (optional)
+//   order   u32[n_rows]     rows sorted by degree descending, stable
+//                           (the probe sampling order, src/generate.cpp:143-147;
+//                           also the LPT launch order of the row kernels)
+//   chunk_row u32[ceil(nnz/32)]  row holding nnz 32*k (SDDMM nnz-chunk map)
+//   hub plans (per threshold): light-row list, 2048-nnz pieces, reduce list
+#pragma once
+
+#include "internal.hpp"
+
+#include <map>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+namespace asb {
+
+template <class T>
+class DevBuf {
+public:
+    DevBuf() = default;
+    explicit DevBuf(std::uint64_t n) { alloc(n); }
+    ~DevBuf() { release(); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) { release(); p_ = o.p_; n_ = o.n_; o.p_ = nullptr; o.n_ = 0; }
+        return *this;
+    }
+    void alloc(std::uint64_t n) {
+        release();
+        if (n == 0) return;
+        ASB_CUDA(cudaMalloc(&p_, n * sizeof(T)));
+        n_ = n;
+    }
+    void ensure(std::uint64_t n) { if (n > n_) alloc(n); }
+    void release() {
+        if (p_) cudaFree(p_);
+        p_ = nullptr;
+        n_ = 0;
+    }
+    T* get() const { return p_; }
+    std::uint64_t size() const { return n_; }
+
+private:
+    T* p_ = nullptr;
+    std::uint64_t n_ = 0;
+};
+
+// Heavy/light split for HubSplit at one threshold (src/kernels.cpp:271-286).
+struct HubPlan {
+    std::uint64_t threshold = 0;
+    std::uint64_t n_light = 0;
+    DevBuf<std::uint32_t> light_rows;  // light rows, degree-descending
+    std::uint64_t n_pieces = 0;
+    DevBuf<std::uint32_t> piece_row;
+    DevBuf<std::uint64_t> piece_e0;
+    DevBuf<std::uint32_t> piece_len;
+    DevBuf<std::uint32_t> piece_slot;  // partial slot, or UINT32_MAX: write C directly
+    std::uint64_t n_slots = 0;         // partial rows needed (pieces of multi-piece rows)
+    std::uint64_t n_red = 0;           // multi-piece heavy rows
+    DevBuf<std::uint32_t> red_row;
+    DevBuf<std::uint32_t> red_first;   // first slot
+    DevBuf<std::uint32_t> red_count;   // pieces
+    std::uint64_t n_heavy = 0;
+};
+
+struct Graph {
+    int device = 0;
+    std::uint64_t n_rows = 0, n_cols = 0, nnz = 0;
+    bool has_val = false;
+    DevBuf<std::uint64_t> rowptr;
+    DevBuf<std::uint32_t> colind;
+    DevBuf<float> val;
+    std::vector<std::uint64_t> h_rowptr;  // host mirror (8 B/row)
+    cudaStream_t stream = nullptr;
+
+    std::mutex mu;
+    std::optional<std::uint64_t> sig;
+    bool order_ready = false;
+    DevBuf<std::uint32_t> order;       // degree-descending stable row order
+    DevBuf<std::uint32_t> sorted_deg;  // degrees in that order
+    bool chunk_ready = false;
+    DevBuf<std::uint32_t> chunk_row;
+    std::map<std::uint64_t, std::unique_ptr<HubPlan>> hub_plans;
+    std::map<std::uint64_t, as_features> features;
+    DevBuf<double> scratch;            // hub partials
+    DevBuf<float> tmp;                 // fused-attention scores
+    DevBuf<float> att_buf;             // unfused attention: scores | probabilities
+    DevBuf<float> stage_in, stage_out; // host-buffer entry points
+    DevBuf<float> stage_in2;
+
+    ~Graph();
+};
+
+// RAII device guard
+struct DeviceGuard {
+    int prev = 0;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (dev != prev) ASB_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        if (cur != prev) cudaSetDevice(prev);
+    }
+};
+
+std::unique_ptr<Graph> graph_create_host(const std::uint64_t* rowptr, const std::uint32_t* colind,
+                                         const float* val, std::uint64_t n_rows,
+                                         std::uint64_t n_cols, std::uint64_t nnz, int device,
+                                         bool validate);
+std::unique_ptr<Graph> graph_create_device(const std::uint64_t* rowptr, const std::uint32_t* colind,
+                                           const float* val, std::uint64_t n_rows,
+                                           std::uint64_t n_cols, std::uint64_t nnz, int device);
+cudaStream_t resolve_stream(Graph& g, void* stream);
+
+std::uint64_t graph_sig(Graph& g);
+void ensure_order(Graph& g);
+void ensure_chunk_rows(Graph& g);
+const HubPlan& ensure_hub_plan(Graph& g, std::uint64_t threshold);
+as_features graph_features(Graph& g, std::uint64_t hub_threshold);
+std::vector<std::uint64_t> sample_row_indices(Graph& g, double frac, std::uint64_t min_rows);
+// vals: the value array to slice (nullptr: pattern-only sample).
+std::unique_ptr<Graph> slice_rows(Graph& g, const std::vector<std::uint64_t>& rows,
+                                  const float* vals);
+std::unique_ptr<Graph> row_range(Graph& g, std::uint64_t r0, std::uint64_t r1);
+// Gathers rows of a dense n x f device matrix (SDDMM probe x-sample,
+// src/scheduler.cpp:214-220).
+void gather_dense_rows(const float* src, std::uint64_t f, const std::vector<std::uint64_t>& rows,
+                       float* dst, cudaStream_t s);
+
+} // namespace asb

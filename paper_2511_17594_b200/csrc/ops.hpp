@@ -1,0 +1,46 @@
+// ops.hpp -- kernel launchers (device pointers, one stream) used by the
+// dispatch layer and the scheduler.
+#pragma once
+
+#include "graph.hpp"
+
+namespace asb {
+
+// ---- SpMM (src/kernels.cpp:210-334) ------------------------------------
+// K1: warp per row, lane per feature, scalar loads, natural row order.
+void launch_spmm_baseline(Graph& g, const float* val, const float* b, std::uint32_t f, float* c, cudaStream_t s);
+// K2: row groups over rows in degree-descending order; f_tile splits the
+// feature dimension into independent work items; wpb warps per CTA.
+void launch_spmm_rows(Graph& g, const float* val, const std::uint32_t* rowlist, std::uint64_t n_list,
+                      const float* b, std::uint32_t f, float* c, std::uint64_t f_tile, bool vec,
+                      std::uint32_t wpb, cudaStream_t s);
+// K3: hub split -- light rows via K2 plus 2048-nnz pieces with ordered
+// fp64 partial reduction.
+void launch_spmm_hubsplit(Graph& g, const float* val, const float* b, std::uint32_t f, float* c,
+                          std::uint64_t f_tile, bool vec, std::uint32_t wpb,
+                          std::uint64_t hub_threshold, cudaStream_t s);
+
+// ---- SDDMM (src/kernels.cpp:336-429) -----------------------------------
+// order: 0 = sequential (scalar variants and the baseline), 1 = per-f_tile
+// four-way partial sums (vec variants, src/kernels.cpp:103-127).
+void launch_sddmm_baseline(Graph& g, const float* x, const float* y, std::uint32_t f, float* out,
+                           cudaStream_t s);
+void launch_sddmm_chunks(Graph& g, const float* x, const float* y, std::uint32_t f, float* out,
+                         std::uint64_t f_tile, bool vec, std::uint32_t wpb, cudaStream_t s);
+
+// ---- row softmax (src/kernels.cpp:431-461) ----------------------------
+void launch_row_softmax(Graph& g, const float* vin, float* vout, cudaStream_t s);
+
+// ---- fused attention (src/attention.cpp:9-40 in one pass) --------------
+// scores kept on chip per row; sddmm order/ft as for launch_sddmm_chunks;
+// SpMM part in CSR order (bit-equal to the row-parallel mapping), or with
+// 2048-nnz piece partials on rows of degree >= spmm_hub_t (hubsplit; 0 = off).
+void launch_attention_fused(Graph& g, const float* q, const float* k, const float* v,
+                            std::uint32_t f, std::uint32_t fv, float* out, std::uint64_t sddmm_ft,
+                            bool sddmm_vec, std::uint64_t spmm_hub_t, cudaStream_t s);
+
+// ---- calibration (src/device.cpp:42-95 analogue) ------------------------
+double measure_gpu_bandwidth(int device);
+double measure_gpu_flops(int device);
+
+} // namespace asb

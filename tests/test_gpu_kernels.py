@@ -1,0 +1,349 @@
+"""GPU parity of the sm_100a operators against the CPU oracle.
+
+Bar: SpMM (every mapping) and SDDMM (every variant order) are
+bit-exact against the reference arithmetic restated in oracle/oracle.c;
+row-softmax and attention are held to the reference tolerance
+|got-want| <= 1e-6 + 1e-5|want| (proj/tests/test_util.hpp:28) and, in
+practice, to <= 1 f32 ulp (the only source of difference is CUDA's f64 exp
+vs libm's).  Mirrors proj/tests/test_kernels.cpp case by case.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2511_17594_b200 as asb
+from tests.util import (bit_equal, cuda, empty_rows, hub_graph, identity, max_err, n_bit_diff,
+                        random_csr, random_dense, ulp_diff)
+
+pytestmark = pytest.mark.gpu
+
+SP, SD = asb.SPMM, asb.SDDMM
+RP, HS, BL = asb.ROWPARALLEL, asb.HUBSPLIT, asb.BASELINE
+
+
+def V(op, mapping, ft=64, rpc=4, vec=False, hubt=256):
+    return asb.KernelVariant(op, mapping, ft, rpc, vec, hubt)
+
+
+# ---- SpMM: known answers (proj/tests/test_kernels.cpp:43-81) ----------------
+def test_spmm_identity_passes_b_through():
+    rng = np.random.default_rng(1)
+    b = random_dense(rng, 2, 5)
+    assert bit_equal(asb.spmm_baseline(identity(2), b), b)
+
+
+def test_spmm_worked_2x2_example():
+    a = asb.CsrMatrix(2, 2, [0, 1, 1], [1], np.array([2.0], np.float32))
+    b = np.array([[1, 1], [3, 4]], np.float32)
+    c = asb.spmm_baseline(a, b)
+    assert c.tolist() == [[6.0, 8.0], [0.0, 0.0]]
+
+
+def test_spmm_all_empty_rows_give_zeros():
+    rng = np.random.default_rng(2)
+    b = random_dense(rng, 4, 7)
+    for v in (None, V(SP, RP, 32, 4, True), V(SP, HS, 64, 1, False, 1)):
+        c = asb.spmm_baseline(empty_rows(3, 4), b) if v is None else \
+            asb.dispatch(v, empty_rows(3, 4), b).output
+        assert np.all(c == 0.0) and not np.any(np.signbit(c))
+
+
+@pytest.mark.parametrize("f", [1, 2, 4, 33, 63, 64, 100, 128, 256, 300])
+def test_spmm_every_variant_bit_exact_vs_oracle(f):
+    rng = np.random.default_rng(3 + f)
+    a = random_csr(rng, 200, 150, 40)
+    b = random_dense(rng, 150, f)
+    want = oracle.spmm_baseline(a, b)
+    g = asb.Graph.from_csr(a)
+    bd = cuda(b)
+    assert bit_equal(asb.spmm_baseline(g, bd).cpu().numpy(), want)
+    for ft in (1, 16, 32, 64, 128, 1024):
+        for rpc in (1, 4, 16):
+            for vec in (False, True):
+                got = asb.dispatch(V(SP, RP, ft, rpc, vec), g, bd).output.cpu().numpy()
+                assert bit_equal(got, want), (ft, rpc, vec, n_bit_diff(got, want))
+
+
+def test_spmm_pattern_only_uses_implicit_one():
+    rng = np.random.default_rng(4)
+    a = random_csr(rng, 80, 60, 20, with_values=False)
+    b = random_dense(rng, 60, 64)
+    want = oracle.spmm_baseline(a, b)
+    for v in (V(SP, RP, 64, 4, True), V(SP, HS, 32, 1, False, 8)):
+        assert bit_equal(asb.dispatch(v, a, b).output, want)
+    assert bit_equal(asb.spmm_baseline(a, b), want)
+
+
+def test_spmm_identity_exact_for_every_tile():
+    rng = np.random.default_rng(4)
+    b = random_dense(rng, 40, 64)
+    for ft in (32, 64, 128):
+        assert bit_equal(asb.spmm_rowparallel(identity(40), b, V(SP, RP, ft, 4, False)), b)
+
+
+@pytest.mark.parametrize("hub_t", [1, 8, 128, 256, 2048, 5000])
+@pytest.mark.parametrize("f", [16, 63, 64, 128])
+def test_spmm_hubsplit_bit_exact_vs_oracle(hub_t, f):
+    rng = np.random.default_rng(5 + hub_t + f)
+    a = hub_graph(rng, 6000, [5000, 4097, 2049, 2048, 600, 256], 6)
+    b = random_dense(rng, 6000, f)
+    want = oracle.spmm_hubsplit(a, b, hub_t)
+    g = asb.Graph.from_csr(a)
+    bd = cuda(b)
+    for vec in (False, True):
+        for ft in (32, 128):
+            got = asb.dispatch(V(SP, HS, ft, 4, vec, hub_t), g, bd).output.cpu().numpy()
+            assert bit_equal(got, want), (vec, ft, n_bit_diff(got, want))
+
+
+def test_spmm_hubsplit_unreachable_threshold_equals_rowparallel():
+    rng = np.random.default_rng(6)
+    a = random_csr(rng, 128, 128, 10)
+    b = random_dense(rng, 128, 32)
+    hub = asb.spmm_hubsplit(a, b, V(SP, HS, 32, 4, False, (1 << 64) - 1))
+    row = asb.spmm_rowparallel(a, b, V(SP, RP, 32, 4, False))
+    assert bit_equal(hub, row)
+
+
+def test_spmm_hubsplit_threshold_one_matches_dense_oracle():
+    rng = np.random.default_rng(7)
+    a = random_csr(rng, 100, 100, 40)
+    b = random_dense(rng, 100, 33)
+    dense = np.zeros((100, 100))
+    for i in range(100):
+        dense[i, a.row_cols(i)] = a.row_vals(i)
+    got = asb.spmm_hubsplit(a, b, V(SP, HS, 64, 4, False, 1))
+    assert max_err(got, dense @ b.astype(np.float64)) <= 1.0
+
+
+def test_spmm_deterministic_across_runs():
+    rng = np.random.default_rng(8)
+    a = hub_graph(rng, 3000, [2500, 2500], 8)
+    b = random_dense(rng, 3000, 64)
+    g = asb.Graph.from_csr(a)
+    bd = cuda(b)
+    v = V(SP, HS, 64, 4, True, 128)
+    c1 = asb.dispatch(v, g, bd).output.cpu().numpy()
+    c2 = asb.dispatch(v, g, bd).output.cpu().numpy()
+    assert bit_equal(c1, c2)
+
+
+def test_spmm_nan_and_inf_propagate_like_the_reference():
+    rng = np.random.default_rng(9)
+    a = random_csr(rng, 50, 40, 10)
+    b = random_dense(rng, 40, 8)
+    b[3, 2] = np.nan
+    b[7, 5] = np.inf
+    want = oracle.spmm_baseline(a, b)
+    for v in (V(SP, RP, 64, 4, True), V(SP, HS, 32, 1, False, 2)):
+        got = asb.dispatch(v, a, b).output
+        assert bit_equal(np.nan_to_num(got), np.nan_to_num(want))
+        assert np.array_equal(np.isnan(got), np.isnan(want))
+
+
+# ---- SDDMM (proj/tests/test_kernels.cpp:158-240) --------------------------------
+def test_sddmm_identity_gives_row_norms():
+    rng = np.random.default_rng(10)
+    x = random_dense(rng, 6, 17)
+    out = asb.sddmm_baseline(identity(6), x, x)
+    want = np.sum(x.astype(np.float64) ** 2, axis=1)
+    assert max_err(out, want) <= 1.0
+
+
+def test_sddmm_edge_cases():
+    rng = np.random.default_rng(11)
+    p = random_csr(rng, 8, 9, 5, with_values=False)
+    zero = np.zeros((8, 4), np.float32)
+    y = random_dense(rng, 9, 4)
+    assert np.all(asb.sddmm_baseline(p, zero, y) == 0.0)
+    one = asb.CsrMatrix(1, 1, [0, 1], [0])
+    out = asb.sddmm_baseline(one, np.array([[2.0]], np.float32), np.array([[3.0]], np.float32))
+    assert out.tolist() == [6.0]
+
+
+def test_sddmm_ignores_pattern_values():
+    rng = np.random.default_rng(12)
+    p = random_csr(rng, 20, 20, 6)
+    x, y = random_dense(rng, 20, 8), random_dense(rng, 20, 8)
+    assert bit_equal(asb.sddmm_baseline(p, x, y), asb.sddmm_baseline(p.with_values(None), x, y))
+
+
+@pytest.mark.parametrize("f", [1, 3, 4, 17, 32, 63, 64, 100, 128, 256, 520])
+def test_sddmm_every_variant_bit_exact_vs_oracle(f):
+    rng = np.random.default_rng(13 + f)
+    p = hub_graph(rng, 700, [650, 300, 64], 9, with_values=False)
+    x, y = random_dense(rng, 700, f), random_dense(rng, 700, f)
+    g = asb.Graph.from_csr(p)
+    xd, yd = cuda(x), cuda(y)
+    want_seq = oracle.sddmm(p, x, y, 64, False)
+    assert bit_equal(asb.sddmm_baseline(g, xd, yd).cpu().numpy(), want_seq)
+    for mapping in (RP, HS):
+        for ft in (3, 16, 32, 64, 128):
+            for rpc in (1, 4, 16):
+                for vec in (False, True):
+                    got = asb.dispatch(V(SD, mapping, ft, rpc, vec), g, xd, yd).values
+                    got = got.cpu().numpy()
+                    gate = vec and f % 4 == 0
+                    want = oracle.sddmm(p, x, y, ft, True) if gate else want_seq
+                    assert bit_equal(got, want), (mapping, ft, rpc, vec, n_bit_diff(got, want))
+
+
+def test_sddmm_vec_and_scalar_stay_close():
+    rng = np.random.default_rng(13)
+    p = random_csr(rng, 70, 50, 9, with_values=False)
+    x, y = random_dense(rng, 70, 64), random_dense(rng, 50, 64)
+    ref = asb.sddmm_baseline(p, x, y)
+    s = asb.sddmm_rowparallel(p, x, y, V(SD, RP, 32, 4, False))
+    v = asb.sddmm_rowparallel(p, x, y, V(SD, RP, 32, 4, True))
+    assert max_err(s, ref) <= 1.0 and max_err(v, ref) <= 1.0
+    assert max_err(v, s, 1e-6, 1e-7) <= 1.0
+    empty = empty_rows(4, 50)
+    assert asb.sddmm_rowparallel(empty, np.zeros((4, 64), np.float32), y,
+                                 V(SD, RP, 32, 4, False)).size == 0
+
+
+def test_sddmm_duality_full_row_matches_gram():
+    rng = np.random.default_rng(14)
+    m = 37
+    p = asb.CsrMatrix(1, m, [0, m], np.arange(m))
+    x, y = random_dense(rng, 1, 24), random_dense(rng, m, 24)
+    out = asb.sddmm_baseline(p, x, y)
+    assert max_err(out, (x.astype(np.float64) @ y.astype(np.float64).T).ravel()) <= 1.0
+
+
+# ---- row softmax (proj/tests/test_kernels.cpp:242-297) --------------------------
+def test_row_softmax_basics():
+    m = asb.CsrMatrix(3, 4, [0, 1, 3, 5], [0, 0, 1, 2, 3],
+                      np.array([1000.0, 2.5, 2.5, 1000.0, 1001.0], np.float32))
+    sm = asb.row_softmax(m)
+    assert sm.val[0] == pytest.approx(1.0)
+    assert sm.val[1] == pytest.approx(0.5) and sm.val[2] == pytest.approx(0.5)
+    assert sm.val[3] == pytest.approx(0.26894, rel=1e-4)
+    assert sm.val[4] == pytest.approx(0.73106, rel=1e-4)
+    assert np.array_equal(sm.rowptr, m.rowptr) and np.array_equal(sm.colind, m.colind)
+
+
+def test_row_softmax_sums_to_one_and_shift_invariant():
+    rng = np.random.default_rng(15)
+    m = random_csr(rng, 300, 300, 30, with_values=False)
+    vals = (rng.integers(-64000, 64001, size=m.nnz) / 64.0).astype(np.float32)
+    s0 = asb.row_softmax(m.with_values(vals))
+    s1 = asb.row_softmax(m.with_values(vals + np.float32(1000.0)))
+    for i in range(m.n_rows):
+        if m.degree(i):
+            assert abs(np.sum(s0.row_vals(i).astype(np.float64)) - 1.0) <= 1e-6
+    assert np.max(np.abs(s0.val.astype(np.float64) - s1.val)) <= 1e-6
+
+
+def test_row_softmax_nan_and_values_required():
+    m = asb.CsrMatrix(1, 2, [0, 2], [0, 1], np.array([np.nan, 1.0], np.float32))
+    assert np.all(np.isnan(asb.row_softmax(m).val))
+    m2 = asb.CsrMatrix(1, 2, [0, 2], [0, 1], np.array([1.0, np.nan], np.float32))
+    assert np.all(np.isnan(asb.row_softmax(m2).val))
+    with pytest.raises(asb.InvalidArgument):
+        asb.row_softmax(m.with_values(None))
+
+
+@pytest.mark.parametrize("hub", [0, 5000])
+def test_row_softmax_vs_oracle(hub):
+    rng = np.random.default_rng(16 + hub)
+    m = hub_graph(rng, 8000, [hub] if hub else [], 40)
+    vals = rng.normal(0, 8, size=m.nnz).astype(np.float32)
+    got = asb.row_softmax(m.with_values(vals)).val
+    want = oracle.row_softmax(m, vals)
+    assert max_err(got, want) <= 1.0
+    assert ulp_diff(got, want) <= 1
+
+
+# ---- dispatch (proj/tests/test_kernels.cpp:299-363) ------------------------------
+def test_dispatch_vec4_gate_and_path_marker():
+    rng = np.random.default_rng(16)
+    a = random_csr(rng, 32, 32, 6)
+    g = asb.Graph.from_csr(a)
+    v = V(SP, RP, 32, 4, True)
+    aligned = cuda(random_dense(rng, 32, 64))
+    assert asb.dispatch(v, g, aligned).vectorized_path
+    odd = random_dense(rng, 32, 63)
+    r = asb.dispatch(v, g, cuda(odd))
+    assert not r.vectorized_path
+    assert bit_equal(r.output.cpu().numpy(), oracle.spmm_baseline(a, odd))
+    import torch
+    buf = torch.zeros(32 * 64 + 2, dtype=torch.float32, device="cuda")
+    under = buf[2:].view(32, 64)  # 8-byte aligned base
+    under.copy_(aligned)
+    assert under.data_ptr() % 16 != 0
+    r2 = asb.dispatch(v, g, under)
+    assert not r2.vectorized_path
+    assert bit_equal(r2.output.cpu().numpy(), asb.dispatch(v, g, aligned).output.cpu().numpy())
+    assert not asb.dispatch(V(SP, RP, 32, 4, False), g, aligned).vectorized_path
+    assert not asb.dispatch(V(SP, BL, 32, 4, True), g, aligned).vectorized_path
+
+
+def test_dispatch_rejects_op_operand_mismatch():
+    rng = np.random.default_rng(17)
+    a = random_csr(rng, 8, 8, 3)
+    b = random_dense(rng, 8, 4)
+    with pytest.raises(asb.InvalidArgument):
+        asb.dispatch(V(SD, RP, 32, 4, False), a, b)
+    with pytest.raises(asb.InvalidArgument):
+        asb.dispatch(V(SP, RP, 32, 4, False), a, b, b)
+    with pytest.raises(asb.InvalidArgument):
+        asb.spmm_baseline(a, np.zeros((9, 4), np.float32))
+    with pytest.raises(asb.InvalidArgument):
+        asb.spmm_rowparallel(a, b, V(SP, HS, 32, 4, False))
+    with pytest.raises(asb.InvalidArgument):
+        asb.dispatch(V(SP, RP, 0, 4, False), a, b)
+
+
+def test_dispatch_honors_kernel_env_overrides(monkeypatch):
+    rng = np.random.default_rng(18)
+    a = random_csr(rng, 16, 16, 4)
+    b = random_dense(rng, 16, 8)
+    v = V(SP, RP, 64, 4, False)
+    monkeypatch.setenv("AUTOSAGE_FTILE", "16")
+    monkeypatch.setenv("AUTOSAGE_WPB", "2")
+    r = asb.dispatch(v, a, b)
+    monkeypatch.delenv("AUTOSAGE_FTILE")
+    monkeypatch.delenv("AUTOSAGE_WPB")
+    assert r.variant.f_tile == 16 and r.variant.rows_per_chunk == 2
+    plain = asb.dispatch(v, a, b)
+    assert plain.variant.f_tile == 64
+    assert bit_equal(r.output, plain.output)
+
+
+def test_dispatch_reports_elapsed_time():
+    rng = np.random.default_rng(19)
+    a = random_csr(rng, 500, 500, 50)
+    r = asb.dispatch(V(SP, RP, 64, 4, True), asb.Graph.from_csr(a), cuda(random_dense(rng, 500, 64)))
+    assert r.elapsed_ms > 0.0
+
+
+# ---- attention kernels (fused / unfused) -------------------------------------------
+@pytest.mark.parametrize("fused", [False, True])
+@pytest.mark.parametrize("f,fv", [(16, 16), (64, 64), (64, 100), (128, 32)])
+def test_attention_vs_oracle(fused, f, fv):
+    rng = np.random.default_rng(20 + f + fv)
+    p = hub_graph(rng, 3000, [2600, 900], 12, with_values=False)
+    q, k, v = random_dense(rng, 3000, f), random_dense(rng, 3000, f), random_dense(rng, 3000, fv)
+    ctx = asb.ScheduleContext(device=asb.DeviceProfile.fixed(20e9, 40e9, 2, "test"),
+                              cache=asb.ScheduleCache())
+    run = asb.attention_probe_breakdown(p, q, k, v, asb.ProbeConfig(iters=2), ctx, fused=fused)
+    sd, pd = run.sddmm_decision, run.spmm_decision
+    sv = sd.choice
+    s_vec = sv is not None and sv.vectorized and f % 4 == 0
+    hub_t = pd.choice.hub_threshold if (pd.choice and pd.choice.mapping == HS) else 0
+    want = oracle.attention(p, q, k, v, sv.f_tile if sv else 64, s_vec, hub_t)
+    assert max_err(run.output, want) <= 1.0
+    assert ulp_diff(run.output, want) <= 2
+
+
+def test_fused_attention_equals_unfused_bitwise():
+    rng = np.random.default_rng(21)
+    p = hub_graph(rng, 5000, [4500, 2100, 700], 30, with_values=False)
+    q, k, v = (random_dense(rng, 5000, 64) for _ in range(3))
+    cache = asb.ScheduleCache()
+    ctx = asb.ScheduleContext(device=asb.DeviceProfile.fixed(20e9, 40e9, 2, "test"), cache=cache)
+    cold = asb.attention_probe_breakdown(p, q, k, v, asb.ProbeConfig(iters=2), ctx)
+    warm = asb.attention_probe_breakdown(p, q, k, v, asb.ProbeConfig(iters=2), ctx, fused=True)
+    assert warm.sddmm_decision.source == asb.CACHED
+    assert bit_equal(cold.output, warm.output)
