@@ -36,6 +36,8 @@ CONFIGS = {
     "c1": (100_000, 1_600_000, 2.5, 6, 2000, 64),
     "reddit": (232_965, 114_615_892, 2.2, 100, 21_657, 64),
     "products": (2_449_029, 123_718_280, 2.0, 8, 17_481, 100),
+    # diagnostics: Reddit volume with the degree tail capped
+    "reddit_cap2k": (232_965, 114_615_892, 2.2, 100, 2048, 64),
 }
 L2_FLUSH_BYTES = 256 << 20
 PEAK_FALLBACK_GBS = 6650.0

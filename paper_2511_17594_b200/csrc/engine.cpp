@@ -232,16 +232,20 @@ void run_spmm_variant(const as_variant& v, Graph& a, const float* vals, const fl
         case AS_MAP_BASELINE:
             launch_spmm_baseline(a, vals, b, std::uint32_t(f), c, s);
             break;
-        case AS_MAP_ROWPARALLEL:
+        case AS_MAP_ROWPARALLEL: {
             ensure_order(a);
-            launch_spmm_rows(a, vals, a.order.get(), a.n_rows, b, std::uint32_t(f), c, v.f_tile, vec,
-                             std::uint32_t(std::min<std::uint64_t>(v.rows_per_chunk, 16)), s);
+            const unsigned* fin = finite_flag(a, b, a.n_cols * f, s);
+            launch_spmm_rows(a, vals, 0, a.n_rows, b, std::uint32_t(f), c, v.f_tile, vec,
+                             std::uint32_t(std::min<std::uint64_t>(v.rows_per_chunk, 16)), s, fin);
             break;
-        case AS_MAP_HUBSPLIT:
+        }
+        case AS_MAP_HUBSPLIT: {
+            const unsigned* fin = finite_flag(a, b, a.n_cols * f, s);
             launch_spmm_hubsplit(a, vals, b, std::uint32_t(f), c, v.f_tile, vec,
                                  std::uint32_t(std::min<std::uint64_t>(v.rows_per_chunk, 16)),
-                                 v.hub_threshold, s);
+                                 v.hub_threshold, s, fin);
             break;
+        }
     }
 }
 
@@ -308,8 +312,9 @@ void sddmm_mapped(const as_variant& v, Graph& p, const float* x, std::uint64_t x
     const void* bases[2] = {x, y};
     const bool vec = v.vectorized && vec4_eligible(f, bases, 2);
     DeviceGuard dg(p.device);
+    const unsigned* fin = finite_flag(p, y, y_rows * f, s);
     launch_sddmm_chunks(p, x, y, std::uint32_t(f), out, v.f_tile, vec,
-                        std::uint32_t(std::min<std::uint64_t>(v.rows_per_chunk, 16)), s);
+                        std::uint32_t(std::min<std::uint64_t>(v.rows_per_chunk, 16)), s, fin);
 }
 
 KernelResult dispatch_sddmm(const as_variant& v, Graph& p, const float* x, std::uint64_t x_rows,
@@ -326,11 +331,14 @@ KernelResult dispatch_sddmm(const as_variant& v, Graph& p, const float* x, std::
     DeviceGuard dg(p.device);
     ensure_chunk_rows(p);
     TimedRegion tr(s, timed);
-    if (r.variant.mapping == AS_MAP_BASELINE)
+    if (r.variant.mapping == AS_MAP_BASELINE) {
         launch_sddmm_baseline(p, x, y, std::uint32_t(f), out, s);
-    else
+    } else {
+        const unsigned* fin = finite_flag(p, y, y_rows * f, s);
         launch_sddmm_chunks(p, x, y, std::uint32_t(f), out, r.variant.f_tile, vec,
-                            std::uint32_t(std::min<std::uint64_t>(r.variant.rows_per_chunk, 16)), s);
+                            std::uint32_t(std::min<std::uint64_t>(r.variant.rows_per_chunk, 16)), s,
+                            fin);
+    }
     r.elapsed_ms = tr.stop();
     r.vectorized_path = vec && r.variant.mapping != AS_MAP_BASELINE;
     return r;

@@ -108,6 +108,38 @@ Graph::~Graph() {
         cudaStreamSynchronize(stream);
         cudaStreamDestroy(stream);
     }
+    if (aux) {
+        cudaStreamSynchronize(aux);
+        cudaStreamDestroy(aux);
+    }
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+}
+
+std::uint64_t rows_with_degree_at_least(Graph& g, std::uint64_t d) {
+    std::lock_guard<std::mutex> lk(g.mu);
+    auto it = g.ge_count.find(d);
+    if (it != g.ge_count.end()) return it->second;
+    std::uint64_t n = 0;
+    for (std::uint64_t i = 0; i < g.n_rows; ++i) n += (g.h_rowptr[i + 1] - g.h_rowptr[i]) >= d;
+    g.ge_count[d] = n;
+    return n;
+}
+
+cudaStream_t graph_fork(Graph& g, cudaStream_t s) {
+    if (!g.aux) {
+        ASB_CUDA(cudaStreamCreateWithFlags(&g.aux, cudaStreamNonBlocking));
+        ASB_CUDA(cudaEventCreateWithFlags(&g.ev_fork, cudaEventDisableTiming));
+        ASB_CUDA(cudaEventCreateWithFlags(&g.ev_join, cudaEventDisableTiming));
+    }
+    ASB_CUDA(cudaEventRecord(g.ev_fork, s));
+    ASB_CUDA(cudaStreamWaitEvent(g.aux, g.ev_fork, 0));
+    return g.aux;
+}
+
+void graph_join(Graph& g, cudaStream_t s) {
+    ASB_CUDA(cudaEventRecord(g.ev_join, g.aux));
+    ASB_CUDA(cudaStreamWaitEvent(s, g.ev_join, 0));
 }
 
 cudaStream_t resolve_stream(Graph& g, void* stream) {
@@ -435,10 +467,22 @@ const HubPlan& ensure_hub_plan(Graph& g, std::uint64_t threshold) {
     plan->n_slots = slots;
     plan->n_red = rrow.size();
     // light rows are the degree-descending order's tail past the heavy prefix
-    plan->light_rows.alloc(std::max<std::uint64_t>(plan->n_light, 1));
-    if (plan->n_light)
-        ASB_CUDA(cudaMemcpyAsync(plan->light_rows.get(), g.order.get() + heavy, plan->n_light * 4,
-                                 cudaMemcpyDeviceToDevice, g.stream));
+    // (launched by offset); pieces go longest-first so a warp's groups get
+    // equal-length pieces and the long ones start early (LPT)
+    {
+        std::vector<std::uint32_t> perm(prow.size());
+        for (std::size_t i = 0; i < perm.size(); ++i) perm[i] = std::uint32_t(i);
+        std::stable_sort(perm.begin(), perm.end(),
+                         [&](std::uint32_t a, std::uint32_t b) { return plen[a] > plen[b]; });
+        auto apply = [&](auto& v) {
+            auto tmp = v;
+            for (std::size_t i = 0; i < perm.size(); ++i) v[i] = tmp[perm[i]];
+        };
+        apply(prow);
+        apply(pe0);
+        apply(plen);
+        apply(pslot);
+    }
     auto up32 = [&](DevBuf<std::uint32_t>& d, const std::vector<std::uint32_t>& h) {
         d.alloc(std::max<std::size_t>(h.size(), 1));
         if (!h.empty())
@@ -473,3 +517,46 @@ void gather_dense_rows(const float* src, std::uint64_t f, const std::vector<std:
 }
 
 } // namespace asb
+
+namespace asb {
+
+namespace {
+__global__ void finite_check_kernel(const float* __restrict__ p, std::uint64_t n,
+                                    unsigned* __restrict__ flag) {
+    bool bad = false;
+    const std::uint64_t stride = std::uint64_t(gridDim.x) * blockDim.x;
+    std::uint64_t i = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
+    if ((reinterpret_cast<std::uintptr_t>(p) & 15) == 0) {
+        const std::uint64_t n4 = n / 4;
+        const uint4* p4 = reinterpret_cast<const uint4*>(p);
+        for (std::uint64_t k = i; k < n4; k += stride) {
+            const uint4 v = __ldg(p4 + k);
+            bad |= ((v.x & 0x7F800000u) == 0x7F800000u) | ((v.y & 0x7F800000u) == 0x7F800000u) |
+                   ((v.z & 0x7F800000u) == 0x7F800000u) | ((v.w & 0x7F800000u) == 0x7F800000u);
+        }
+        for (std::uint64_t k = n4 * 4 + i; k < n; k += stride)
+            bad |= (__float_as_uint(p[k]) & 0x7F800000u) == 0x7F800000u;
+    } else {
+        for (std::uint64_t k = i; k < n; k += stride)
+            bad |= (__float_as_uint(p[k]) & 0x7F800000u) == 0x7F800000u;
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *flag = 0u;
+}
+}  // namespace
+
+const unsigned* finite_flag(Graph& g, const float* p, std::uint64_t n, cudaStream_t s) {
+    g.flag.ensure(1);
+    ASB_CUDA(cudaMemsetAsync(g.flag.get(), 0, 4, s));
+    if (n == 0 || p == nullptr) return g.flag.get();  // nothing to widen: take the safe path
+    ASB_CUDA(cudaMemsetAsync(g.flag.get(), 1, 1, s));  // little-endian 1u
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const std::uint64_t want = (n / 4 + 255) / 256 + 1;
+    const unsigned blocks = unsigned(std::min<std::uint64_t>(want, std::uint64_t(sms) * 8));
+    finite_check_kernel<<<blocks, 256, 0, s>>>(p, n, g.flag.get());
+    check_launch("finite_check_kernel");
+    return g.flag.get();
+}
+
+}  // namespace asb

@@ -95,6 +95,10 @@ struct Graph {
     DevBuf<float> att_buf;             // unfused attention: scores | probabilities
     DevBuf<float> stage_in, stage_out; // host-buffer entry points
     DevBuf<float> stage_in2;
+    std::map<std::uint64_t, std::uint64_t> ge_count;  // rows with degree >= key
+    DevBuf<unsigned> flag;             // finiteness flag of the current dense operand
+    cudaStream_t aux = nullptr;        // fork/join stream for concurrent kernels
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
     ~Graph();
 };
@@ -123,6 +127,12 @@ std::unique_ptr<Graph> graph_create_device(const std::uint64_t* rowptr, const st
 cudaStream_t resolve_stream(Graph& g, void* stream);
 
 std::uint64_t graph_sig(Graph& g);
+// number of rows with degree >= d (host count from the rowptr mirror, cached)
+std::uint64_t rows_with_degree_at_least(Graph& g, std::uint64_t d);
+// fork: returns the graph's aux stream ordered after `s`; join: `s` waits
+// for the aux stream's work
+cudaStream_t graph_fork(Graph& g, cudaStream_t s);
+void graph_join(Graph& g, cudaStream_t s);
 void ensure_order(Graph& g);
 void ensure_chunk_rows(Graph& g);
 const HubPlan& ensure_hub_plan(Graph& g, std::uint64_t threshold);

@@ -11,14 +11,18 @@ namespace asb {
 void launch_spmm_baseline(Graph& g, const float* val, const float* b, std::uint32_t f, float* c, cudaStream_t s);
 // K2: row groups over rows in degree-descending order; f_tile splits the
 // feature dimension into independent work items; wpb warps per CTA.
-void launch_spmm_rows(Graph& g, const float* val, const std::uint32_t* rowlist, std::uint64_t n_list,
+// Rows order[offset, offset+n_list) of the degree-descending order; rows of
+// degree >= 2048 among them go to the CTA-per-row cp.async ring kernel on a
+// forked stream (same numerics).
+void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uint64_t n_list,
                       const float* b, std::uint32_t f, float* c, std::uint64_t f_tile, bool vec,
-                      std::uint32_t wpb, cudaStream_t s);
+                      std::uint32_t wpb, cudaStream_t s, const unsigned* finite = nullptr);
 // K3: hub split -- light rows via K2 plus 2048-nnz pieces with ordered
 // fp64 partial reduction.
 void launch_spmm_hubsplit(Graph& g, const float* val, const float* b, std::uint32_t f, float* c,
                           std::uint64_t f_tile, bool vec, std::uint32_t wpb,
-                          std::uint64_t hub_threshold, cudaStream_t s);
+                          std::uint64_t hub_threshold, cudaStream_t s,
+                          const unsigned* finite = nullptr);
 
 // ---- SDDMM (src/kernels.cpp:336-429) -----------------------------------
 // order: 0 = sequential (scalar variants and the baseline), 1 = per-f_tile
@@ -26,7 +30,13 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const float* b, std::uint3
 void launch_sddmm_baseline(Graph& g, const float* x, const float* y, std::uint32_t f, float* out,
                            cudaStream_t s);
 void launch_sddmm_chunks(Graph& g, const float* x, const float* y, std::uint32_t f, float* out,
-                         std::uint64_t f_tile, bool vec, std::uint32_t wpb, cudaStream_t s);
+                         std::uint64_t f_tile, bool vec, std::uint32_t wpb, cudaStream_t s,
+                         const unsigned* finite = nullptr);
+
+// Device flag: 1 iff p[0..n) has no Inf/NaN (gates the re-bias widening,
+// widen.cuh).  Written into g.flag (one flag per graph; a graph handle runs
+// one operator at a time).
+const unsigned* finite_flag(Graph& g, const float* p, std::uint64_t n, cudaStream_t s);
 
 // ---- row softmax (src/kernels.cpp:431-461) ----------------------------
 void launch_row_softmax(Graph& g, const float* vin, float* vout, cudaStream_t s);

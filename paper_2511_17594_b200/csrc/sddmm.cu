@@ -17,8 +17,10 @@
 // rows in shared memory with an odd 16-byte row pitch, so each lane's
 // sequential dot reads conflict-free LDS.128.
 #include "ops.hpp"
+#include "widen.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace asb {
 
@@ -27,35 +29,58 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int kXRows = 8;  // X rows staged per chunk; further rows read global
 
-__device__ __forceinline__ double dfma(float x, float y, double acc) {
-    return __fma_rn(double(x), double(y), acc);
+__device__ __forceinline__ double dfma(double x, float y, double acc) {
+    return __fma_rn(x, double(y), acc);
 }
+
+// widen y by re-bias (ALU pipe) when MIX; x carries the 2^896 (widen.cuh)
+template <int MIX>
+__device__ __forceinline__ double dfma_r(double x, float y, double acc) {
+    if constexpr (MIX) return __fma_rn(x * kWidenUp, widen_scaled(y), acc);
+    else return __fma_rn(x, double(y), acc);
+}
+
+// x components: f32 from global memory, or f64 pre-widened in shared memory
+struct X4 {
+    double a, b, c, d;
+};
+__device__ __forceinline__ X4 load_x4(const float* p) {
+    const float4 v = *reinterpret_cast<const float4*>(p);
+    return {double(v.x), double(v.y), double(v.z), double(v.w)};
+}
+__device__ __forceinline__ X4 load_x4(const double* p) {
+    const double2 lo = *reinterpret_cast<const double2*>(p);
+    const double2 hi = *reinterpret_cast<const double2*>(p + 2);
+    return {lo.x, lo.y, hi.x, hi.y};
+}
+__device__ __forceinline__ double x_at(const float* p, std::uint32_t t) { return double(p[t]); }
+__device__ __forceinline__ double x_at(const double* p, std::uint32_t t) { return p[t]; }
 
 // Sequential dot over [0, f): VLDS uses 16-byte reads (f % 4 == 0, both
 // pointers 16-byte aligned).
-template <bool VLDS>
-__device__ __forceinline__ double dot_seq(const float* xr, const float* yr, std::uint32_t f) {
+template <bool VLDS, int MIX, class XT>
+__device__ __forceinline__ double dot_seq(const XT* xr, const float* yr, std::uint32_t f) {
     double acc = 0.0;
     if constexpr (VLDS) {
 #pragma unroll 4
         for (std::uint32_t t = 0; t < f; t += 4) {
-            const float4 x = *reinterpret_cast<const float4*>(xr + t);
+            const X4 x = load_x4(xr + t);
             const float4 y = *reinterpret_cast<const float4*>(yr + t);
-            acc = dfma(x.x, y.x, acc);
-            acc = dfma(x.y, y.y, acc);
-            acc = dfma(x.z, y.z, acc);
-            acc = dfma(x.w, y.w, acc);
+            acc = dfma(x.a, y.x, acc);
+            acc = dfma(x.b, y.y, acc);
+            acc = dfma_r<MIX>(x.c, y.z, acc);
+            acc = dfma_r<MIX>(x.d, y.w, acc);
         }
     } else {
 #pragma unroll 4
-        for (std::uint32_t t = 0; t < f; ++t) acc = dfma(xr[t], yr[t], acc);
+        for (std::uint32_t t = 0; t < f; ++t) acc = dfma(x_at(xr, t), yr[t], acc);
     }
     return acc;
 }
 
 // src/kernels.cpp:103-127 vec path.  VLDS requires ft % 4 == 0 too.
-template <bool VLDS>
-__device__ __forceinline__ double dot_vec4blk(const float* xr, const float* yr, std::uint32_t f,
+template <bool VLDS, int MIX, class XT>
+__device__ __forceinline__ double dot_vec4blk(const XT* xr, const float* yr, std::uint32_t f,
                                               std::uint32_t ft) {
     double acc = 0.0;
     for (std::uint32_t b0 = 0; b0 < f; b0 += ft) {
@@ -65,31 +90,32 @@ __device__ __forceinline__ double dot_vec4blk(const float* xr, const float* yr, 
         std::uint32_t t = 0;
 #pragma unroll 2
         for (; t < fw4; t += 4) {
-            float4 x, y;
+            X4 x;
+            float4 y;
             if constexpr (VLDS) {
-                x = *reinterpret_cast<const float4*>(xr + b0 + t);
+                x = load_x4(xr + b0 + t);
                 y = *reinterpret_cast<const float4*>(yr + b0 + t);
             } else {
-                x = make_float4(xr[b0 + t], xr[b0 + t + 1], xr[b0 + t + 2], xr[b0 + t + 3]);
+                x = {x_at(xr, b0 + t), x_at(xr, b0 + t + 1), x_at(xr, b0 + t + 2), x_at(xr, b0 + t + 3)};
                 y = make_float4(yr[b0 + t], yr[b0 + t + 1], yr[b0 + t + 2], yr[b0 + t + 3]);
             }
-            a0 = dfma(x.x, y.x, a0);
-            a1 = dfma(x.y, y.y, a1);
-            a2 = dfma(x.z, y.z, a2);
-            a3 = dfma(x.w, y.w, a3);
+            a0 = dfma(x.a, y.x, a0);
+            a1 = dfma(x.b, y.y, a1);
+            a2 = dfma_r<MIX>(x.c, y.z, a2);
+            a3 = dfma_r<MIX>(x.d, y.w, a3);
         }
         double tail = 0.0;
-        for (; t < fw; ++t) tail = dfma(xr[b0 + t], yr[b0 + t], tail);
+        for (; t < fw; ++t) tail = dfma(x_at(xr, b0 + t), yr[b0 + t], tail);
         acc = __dadd_rn(acc, __dadd_rn(__dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3)), tail));
     }
     return acc;
 }
 
-template <int ORD, bool VLDS>
-__device__ __forceinline__ double dot_ord(const float* xr, const float* yr, std::uint32_t f,
+template <int ORD, bool VLDS, int MIX, class XT>
+__device__ __forceinline__ double dot_ord(const XT* xr, const float* yr, std::uint32_t f,
                                           std::uint32_t ft) {
-    if constexpr (ORD == 0) return dot_seq<VLDS>(xr, yr, f);
-    else return dot_vec4blk<VLDS>(xr, yr, f, ft);
+    if constexpr (ORD == 0) return dot_seq<VLDS, MIX>(xr, yr, f);
+    else return dot_vec4blk<VLDS, MIX>(xr, yr, f, ft);
 }
 
 // Row of entry e, starting from the chunk's first row (chunk_row map).
@@ -101,18 +127,18 @@ __device__ __forceinline__ std::uint32_t row_of(const std::uint64_t* __restrict_
 
 // VLOAD: 16-byte global gathers (vec4 gate passed).  S: smem row pitch in
 // floats (multiple of 4 when VLOAD).
-template <bool VLOAD, int ORD, bool VLDS>
-__global__ void __launch_bounds__(512)
-    sddmm_chunk_kernel(const std::uint64_t* __restrict__ rowptr,
-                       const std::uint32_t* __restrict__ colind,
-                       const std::uint32_t* __restrict__ chunk_row, const float* __restrict__ x,
-                       const float* __restrict__ y, float* __restrict__ out, std::uint64_t nnz,
-                       std::uint32_t f, std::uint32_t S, std::uint32_t ft) {
-    extern __shared__ __align__(16) float smem[];
+template <bool VLOAD, int ORD, bool VLDS, int MIX>
+__device__ __forceinline__ void sddmm_chunk_body(
+    const std::uint64_t* __restrict__ rowptr, const std::uint32_t* __restrict__ colind,
+    const std::uint32_t* __restrict__ chunk_row, const float* __restrict__ x,
+    const float* __restrict__ y, float* __restrict__ out, std::uint64_t nnz, std::uint32_t f,
+    std::uint32_t S, std::uint32_t ft, float* smem) {
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
-    float* ys = smem + std::uint64_t(wib) * (32 + kXRows) * S;
-    float* xs = ys + 32 * S;
+    // per warp: 32 Y rows (f32, pitch S) then kXRows X rows widened to f64
+    float* ys = reinterpret_cast<float*>(reinterpret_cast<char*>(smem) +
+                                         std::uint64_t(wib) * (32ull * S * 4 + kXRows * 8ull * f));
+    double* xs = reinterpret_cast<double*>(ys + 32 * S);
     const std::uint64_t n_chunks = (nnz + 31) / 32;
     const std::uint64_t total_warps = std::uint64_t(gridDim.x) * (blockDim.x >> 5);
     // element walk over a (rows x nv) tile: 32 = dj*nv + dq
@@ -152,36 +178,201 @@ __global__ void __launch_bounds__(512)
                 }
             }
         }
-        // stage up to kXRows X rows
+        // stage up to kXRows X rows, widened to f64 once per chunk (not once
+        // per product): rows r_first.. are contiguous in X
         {
-            const std::uint32_t total = nx * nv;
-            std::uint32_t j = j_start, q = q_start;
-            for (std::uint32_t idx = std::uint32_t(lane); idx < total; idx += 32) {
-                const float* xsrc = x + std::uint64_t(r_first + j) * f;
-                if constexpr (VLOAD) {
-                    *reinterpret_cast<float4*>(xs + j * S + 4 * q) =
-                        __ldg(reinterpret_cast<const float4*>(xsrc) + q);
-                } else {
-                    xs[j * S + q] = __ldg(xsrc + q);
-                }
-                j += dj;
-                q += dq;
-                if (q >= nv) {
-                    q -= nv;
-                    ++j;
-                }
-            }
+            const float* xsrc = x + std::uint64_t(r_first) * f;
+            const std::uint32_t total = nx * f;
+            for (std::uint32_t idx = std::uint32_t(lane); idx < total; idx += 32)
+                xs[idx] = double(__ldg(xsrc + idx));
         }
         __syncwarp();
         if (valid) {
             const float* yr = ys + lane * S;
             double acc;
-            if (r - r_first < nx) acc = dot_ord<ORD, VLDS>(xs + (r - r_first) * S, yr, f, ft);
-            else acc = dot_ord<ORD, false>(x + std::uint64_t(r) * f, yr, f, ft);
+            if (r - r_first < nx) acc = dot_ord<ORD, VLDS, MIX>(xs + std::uint64_t(r - r_first) * f, yr, f, ft);
+            else acc = dot_ord<ORD, false, 0>(x + std::uint64_t(r) * f, yr, f, ft);
             out[e] = float(acc);
         }
         __syncwarp();
     }
+}
+
+// MIX (re-bias half of the Y widening on the ALU pipe) only when the
+// device-side scan found Y finite and the float4 smem path is in use.
+template <bool VLOAD, int ORD, bool VLDS>
+__global__ void __launch_bounds__(512)
+    sddmm_chunk_kernel(const std::uint64_t* __restrict__ rowptr,
+                       const std::uint32_t* __restrict__ colind,
+                       const std::uint32_t* __restrict__ chunk_row, const float* __restrict__ x,
+                       const float* __restrict__ y, float* __restrict__ out, std::uint64_t nnz,
+                       std::uint32_t f, std::uint32_t S, std::uint32_t ft,
+                       const unsigned* __restrict__ finite) {
+    extern __shared__ __align__(16) float smem[];
+    if (VLDS && finite && *finite)
+        sddmm_chunk_body<VLOAD, ORD, VLDS, 1>(rowptr, colind, chunk_row, x, y, out, nnz, f, S, ft, smem);
+    else
+        sddmm_chunk_body<VLOAD, ORD, VLDS, 0>(rowptr, colind, chunk_row, x, y, out, nnz, f, S, ft, smem);
+}
+
+// ---------------------------------------------------------------------------
+// TMA-staged chunk kernel (vec4-eligible operands): per warp, two staging
+// buffers; each lane issues ONE bulk copy (cp.async.bulk, complete_tx on the
+// buffer's mbarrier) for its entry's Y row, lanes < nx copy the chunk's X
+// rows.  The next chunk's copies are in flight while the current chunk's
+// dots run; chunk metadata (colind, chunk_row) is prefetched one chunk ahead
+// in registers, so the warp never stalls on a dependent load before issuing.
+constexpr int kTX = 4;  // X rows staged per chunk
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return unsigned(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(std::uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(std::uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "SDDMM_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra SDDMM_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, std::uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+struct TmaLayout {
+    std::uint32_t ybuf, xbuf, xd, bar, per_warp;  // byte offsets within a warp's slice
+};
+__host__ __device__ inline TmaLayout tma_layout(std::uint32_t f, std::uint32_t S) {
+    TmaLayout L{};
+    std::uint32_t o = 0;
+    L.ybuf = o;
+    o += 2u * 32u * S * 4u;  // 2 buffers x 32 Y rows (pitch S floats)
+    L.xbuf = o;
+    o += 2u * kTX * f * 4u;  // 2 buffers x kTX X rows (f32)
+    o = (o + 15) & ~15u;
+    L.xd = o;
+    o += kTX * (f + 2) * 8u;  // widened X rows, padded pitch
+    o = (o + 15) & ~15u;
+    L.bar = o;
+    o += 16;
+    L.per_warp = (o + 127) & ~127u;
+    return L;
+}
+
+template <int ORD, int MIX>
+__device__ __forceinline__ void sddmm_tma_body(const std::uint64_t* __restrict__ rowptr,
+                                               const std::uint32_t* __restrict__ colind,
+                                               const std::uint32_t* __restrict__ chunk_row,
+                                               std::uint64_t n_rows, const float* __restrict__ x,
+                                               const float* __restrict__ y, float* __restrict__ out,
+                                               std::uint64_t nnz, std::uint32_t f, std::uint32_t S,
+                                               std::uint32_t ft, char* wsm) {
+    const TmaLayout L = tma_layout(f, S);
+    float* ybuf = reinterpret_cast<float*>(wsm + L.ybuf);
+    float* xbuf = reinterpret_cast<float*>(wsm + L.xbuf);
+    double* xd = reinterpret_cast<double*>(wsm + L.xd);
+    std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(wsm + L.bar);
+    const int lane = threadIdx.x & 31;
+    const std::uint32_t xpitch = f + 2;
+    const unsigned row_bytes = f * 4;
+    const std::uint64_t n_chunks = (nnz + 31) / 32;
+    const std::uint64_t stride = std::uint64_t(gridDim.x) * (blockDim.x >> 5);
+    const std::uint64_t c0 = std::uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+
+    if (lane == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+
+    struct Meta {
+        std::uint32_t col, r_first, nx;
+        bool valid;
+    };
+    auto load_meta = [&](std::uint64_t c) {
+        Meta m{0, 0, 0, false};
+        if (c >= n_chunks) return m;
+        const std::uint64_t e = c * 32 + lane;
+        m.valid = e < nnz;
+        m.col = m.valid ? __ldg(colind + e) : 0u;
+        m.r_first = __ldg(chunk_row + c);
+        const std::uint32_t r_bound =
+            c + 1 < n_chunks ? __ldg(chunk_row + c + 1) : std::uint32_t(n_rows - 1);
+        m.nx = min(r_bound - m.r_first + 1, std::uint32_t(kTX));
+        return m;
+    };
+    auto issue = [&](std::uint64_t c, const Meta& m, int b) {
+        const unsigned nvalid = nnz - c * 32 < 32 ? unsigned(nnz - c * 32) : 32u;
+        if (lane == 0) mbar_arrive_expect_tx(&bar[b], (nvalid + m.nx) * row_bytes);
+        __syncwarp();
+        if (m.valid)
+            bulk_g2s(ybuf + std::uint64_t(b) * 32 * S + std::uint64_t(lane) * S,
+                     y + std::uint64_t(m.col) * f, row_bytes, &bar[b]);
+        if (std::uint32_t(lane) < m.nx)
+            bulk_g2s(xbuf + (std::uint64_t(b) * kTX + lane) * f, x + std::uint64_t(m.r_first + lane) * f,
+                     row_bytes, &bar[b]);
+    };
+
+    unsigned phase[2] = {0u, 0u};
+    Meta cur = load_meta(c0);
+    if (c0 < n_chunks) issue(c0, cur, 0);
+    Meta nxt = load_meta(c0 + stride);
+    int b = 0;
+    for (std::uint64_t c = c0; c < n_chunks; c += stride, b ^= 1) {
+        const std::uint64_t cn = c + stride;
+        if (cn < n_chunks) issue(cn, nxt, b ^ 1);
+        const Meta m = cur;
+        cur = nxt;
+        nxt = load_meta(cn + stride);  // in flight during this chunk's dots
+        mbar_wait(&bar[b], phase[b]);
+        phase[b] ^= 1u;
+        // widen this chunk's X rows once
+        const float* xs = xbuf + std::uint64_t(b) * kTX * f;
+        for (std::uint32_t idx = lane; idx < m.nx * f; idx += 32) {
+            const std::uint32_t rr = idx / f, t = idx - rr * f;
+            xd[rr * xpitch + t] = double(xs[idx]);
+        }
+        __syncwarp();
+        const std::uint64_t e = c * 32 + lane;
+        if (m.valid) {
+            const std::uint32_t r = row_of(rowptr, m.r_first, e);
+            const float* yr = ybuf + std::uint64_t(b) * 32 * S + std::uint64_t(lane) * S;
+            double acc;
+            if (r - m.r_first < m.nx) acc = dot_ord<ORD, true, MIX>(xd + (r - m.r_first) * xpitch, yr, f, ft);
+            else acc = dot_ord<ORD, false, 0>(x + std::uint64_t(r) * f, yr, f, ft);
+            out[e] = float(acc);
+        }
+        __syncwarp();  // buffer b and xd free before they are refilled
+    }
+}
+
+template <int ORD>
+__global__ void __launch_bounds__(512)
+    sddmm_tma_kernel(const std::uint64_t* __restrict__ rowptr,
+                     const std::uint32_t* __restrict__ colind,
+                     const std::uint32_t* __restrict__ chunk_row, std::uint64_t n_rows,
+                     const float* __restrict__ x, const float* __restrict__ y,
+                     float* __restrict__ out, std::uint64_t nnz, std::uint32_t f, std::uint32_t S,
+                     std::uint32_t ft, const unsigned* __restrict__ finite) {
+    extern __shared__ __align__(128) char tsmem[];
+    char* wsm = tsmem + std::uint64_t(threadIdx.x >> 5) * tma_layout(f, S).per_warp;
+    if (finite && *finite)
+        sddmm_tma_body<ORD, 1>(rowptr, colind, chunk_row, n_rows, x, y, out, nnz, f, S, ft, wsm);
+    else
+        sddmm_tma_body<ORD, 0>(rowptr, colind, chunk_row, n_rows, x, y, out, nnz, f, S, ft, wsm);
 }
 
 // Guardrail baseline / large-F fallback: lane per entry, both rows read
@@ -199,7 +390,15 @@ __global__ void sddmm_direct_kernel(const std::uint64_t* __restrict__ rowptr,
     const std::uint32_t r = row_of(rowptr, chunk_row[ch], e);
     const float* xr = x + std::uint64_t(r) * f;
     const float* yr = y + std::uint64_t(colind[e]) * f;
-    out[e] = float(dot_ord<ORD, false>(xr, yr, f, ft));
+    out[e] = float(dot_ord<ORD, false, 0>(xr, yr, f, ft));
+}
+
+bool tma_path_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("AUTOSAGE_DEV_SDDMM_TMA");
+        return !(e && e[0] == '0');
+    }();
+    return on;
 }
 
 } // namespace
@@ -216,7 +415,8 @@ void launch_sddmm_baseline(Graph& g, const float* x, const float* y, std::uint32
 }
 
 void launch_sddmm_chunks(Graph& g, const float* x, const float* y, std::uint32_t f, float* out,
-                         std::uint64_t f_tile, bool vec, std::uint32_t wpb, cudaStream_t s) {
+                         std::uint64_t f_tile, bool vec, std::uint32_t wpb, cudaStream_t s,
+                         const unsigned* finite) {
     if (g.nnz == 0) return;
     ensure_chunk_rows(g);
     const std::uint32_t ft = std::uint32_t(effective_tile(f_tile, f));
@@ -230,7 +430,29 @@ void launch_sddmm_chunks(Graph& g, const float* x, const float* y, std::uint32_t
     const bool vload = vec;  // vec4 gate already applied by dispatch
     const bool vlds = vload && (ord == 0 || ft % 4 == 0);
     std::uint32_t S = vload ? 4 * ((f / 4) | 1u) : (f | 1u);
-    const std::uint64_t per_warp = std::uint64_t(32 + kXRows) * S * 4;
+    int dev0 = 0, sms0 = 148;
+    cudaGetDevice(&dev0);
+    cudaDeviceGetAttribute(&sms0, cudaDevAttrMultiProcessorCount, dev0);
+    if (vlds && tma_path_enabled()) {
+        const std::uint32_t per_warp = tma_layout(f, S).per_warp;
+        std::uint32_t w = std::clamp<std::uint32_t>(wpb, 1, 16);
+        while (w > 1 && std::uint64_t(per_warp) * w > 200 * 1024) --w;
+        if (per_warp <= 200 * 1024) {
+            const std::size_t smem = std::size_t(per_warp) * w;
+            auto kern = ord == 0 ? sddmm_tma_kernel<0> : sddmm_tma_kernel<1>;
+            int per_sm = 1;
+            ASB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            ASB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, int(w * 32), smem));
+            const std::uint64_t want = (n_chunks + w - 1) / w;
+            const std::uint64_t cap = std::uint64_t(sms0) * std::max(per_sm, 1);
+            const unsigned blocks = unsigned(std::max<std::uint64_t>(1, std::min(want, cap)));
+            kern<<<blocks, w * 32, smem, s>>>(g.rowptr.get(), g.colind.get(), g.chunk_row.get(), g.n_rows,
+                                              x, y, out, g.nnz, f, S, ft, finite);
+            check_launch("sddmm_tma_kernel");
+            return;
+        }
+    }
+    const std::uint64_t per_warp = 32ull * S * 4 + kXRows * 8ull * f;
     constexpr std::uint64_t kSmemMax = 200 * 1024;
     wpb = std::clamp<std::uint32_t>(wpb, 1, 16);
     while (wpb > 1 && per_warp * wpb > kSmemMax) --wpb;
@@ -257,7 +479,7 @@ void launch_sddmm_chunks(Graph& g, const float* x, const float* y, std::uint32_t
         const std::uint64_t cap = std::uint64_t(sms) * std::max(per_sm, 1) * 4;
         const unsigned blocks = unsigned(std::max<std::uint64_t>(1, std::min(want, cap)));
         kernel<<<blocks, wpb * 32, smem, s>>>(g.rowptr.get(), g.colind.get(), g.chunk_row.get(), x, y,
-                                              out, g.nnz, f, S, ft);
+                                              out, g.nnz, f, S, ft, finite);
         check_launch("sddmm_chunk_kernel");
     };
     if (vload) {

@@ -9,16 +9,23 @@
 // follow src/kernels.cpp:284-332: 2048-nnz pieces, f64 partials, summed in
 // piece order from 0.0.
 //
-// Performance shape: B gathers dominate (4*F bytes per nnz).  Row groups of
-// LPR lanes cover one row's feature tile with float4 (vec) or scalar loads;
-// colind/val are fetched cooperatively (one coalesced load per LPR entries)
-// and broadcast by shuffle, and U gathers per lane are issued before their
-// DFMAs so each warp keeps U*LPR*16 bytes in flight.  Rows are visited in
-// degree-descending order (the graph's stable sort), which packs rows of
-// equal length into a warp and starts the longest rows first.
+// Performance shape (F=64, Reddit-shaped): B gathers are L2 hits, so the
+// budget is the L2 gather rate (~20 TB/s measured, tools/gather_roofline.cu)
+// and the XU pipe that widens f32 to f64.  Hence:
+//  * the group kernel runs small lane groups (float4 per lane) at high
+//    occupancy (register cap), rows in degree-descending order;
+//  * each entry's value is widened once by the lane that loaded it and
+//    shuffled as f64; half of every B float4 is widened by an exact integer
+//    re-bias on the ALU pipe (widen.cuh) when B is known finite;
+//  * rows of degree >= 2048 (whose dependent round trips would dominate a
+//    lane group) go to a CTA-per-row kernel that streams the gathered B rows
+//    through a cp.async shared-memory ring, concurrently on a forked stream.
 #include "ops.hpp"
+#include "widen.cuh"
 
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 namespace asb {
 
@@ -43,7 +50,13 @@ __device__ __forceinline__ float comp(const float4& v, int q) {
 }
 
 __host__ __device__ constexpr int unroll_for(int vec, int nch) {
-    return vec * nch >= 32 ? 1 : (vec * nch >= 16 ? 2 : (vec * nch >= 8 ? 4 : 8));
+    return vec == 4 ? (nch == 1 ? 4 : (nch == 2 ? 2 : 1)) : (nch >= 8 ? 1 : 8 / nch);
+}
+
+__host__ __device__ constexpr int maxreg_for(int vec, int nch) {
+    // float4 single-chunk tiles: keep >= 40 resident warps per SM; wider
+    // tiles keep their in-flight loads in registers
+    return vec == 1 ? (nch == 1 ? 64 : (nch == 2 ? 96 : 128)) : (nch == 1 ? 48 : (nch == 2 ? 64 : 128));
 }
 
 struct SegArgs {
@@ -54,23 +67,25 @@ struct SegArgs {
     float* c;
     double* scratch;
     const std::uint32_t* rowlist;     // row mode: row ids (nullptr: identity)
-    const std::uint32_t* piece_row;   // piece mode when non-null
+    const std::uint32_t* piece_row;   // piece mode
     const std::uint64_t* piece_e0;
     const std::uint32_t* piece_len;
     const std::uint32_t* piece_slot;
+    const unsigned* finite;           // device flag: B has no Inf/NaN (nullable)
     std::uint64_t n_items;
     std::uint32_t n_tiles;
     std::uint32_t f;
     std::uint32_t tile_w;
 };
 
-// K2/K3 gather kernel.  One group of LPR lanes owns one (segment, feature
-// tile) item; segment = a whole row (row mode) or a hub piece.
-template <int VEC, int LPR, int NCH, bool HAS_VAL>
-__global__ void __launch_bounds__(512) spmm_seg_kernel(SegArgs a) {
+// One group of LPR lanes owns one (segment, feature tile) item; segment =
+// a whole row (row mode) or a hub piece (PIECES).  MIX selects the widening
+// of B: 0 = F2F only, 1 = components 2,3 of each float4 (or every scalar)
+// re-biased on the ALU pipe.
+template <int VEC, int LPR, int NCH, bool HAS_VAL, bool PIECES, int U, int MIX>
+__device__ __forceinline__ void seg_body(const SegArgs& a) {
     using VT = typename VecT<VEC>::T;
     constexpr int GPW = 32 / LPR;
-    constexpr int U = unroll_for(VEC, NCH);
     constexpr int W = LPR > U ? LPR : U;
     constexpr int S = W / LPR;
     const int lane = threadIdx.x & 31;
@@ -83,9 +98,12 @@ __global__ void __launch_bounds__(512) spmm_seg_kernel(SegArgs a) {
     std::uint32_t row = 0, tile = 0, deg = 0, slot = 0xffffffffu;
     std::uint64_t e0 = 0;
     if (active) {
-        const std::uint64_t si = item / a.n_tiles;
-        tile = std::uint32_t(item - si * a.n_tiles);
-        if (a.piece_row) {
+        std::uint64_t si = item;
+        if (a.n_tiles != 1) {
+            si = item / a.n_tiles;
+            tile = std::uint32_t(item - si * a.n_tiles);
+        }
+        if constexpr (PIECES) {
             row = a.piece_row[si];
             e0 = a.piece_e0[si];
             deg = a.piece_len[si];
@@ -121,26 +139,26 @@ __global__ void __launch_bounds__(512) spmm_seg_kernel(SegArgs a) {
 
     for (std::uint32_t base = 0; base < maxdeg; base += W) {
         std::uint32_t cs[S];
-        float vs[S];
+        double vs[S];  // widened once here, by the lane that loaded it
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             const std::uint32_t k = base + std::uint32_t(s * LPR + gl);
             const bool ok = k < deg;
             cs[s] = ok ? __ldg(colp + k) : 0u;
-            if constexpr (HAS_VAL) vs[s] = ok ? __ldg(valp + k) : 0.f;
-            else vs[s] = 1.f;
+            if constexpr (HAS_VAL) vs[s] = ok ? double(__ldg(valp + k)) : 0.0;
+            else vs[s] = 1.0;
         }
 #pragma unroll
         for (int j0 = 0; j0 < W; j0 += U) {
             if (base + std::uint32_t(j0) >= maxdeg) break;
             std::uint32_t cj[U];
-            float vj[U];
+            double vj[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int j = j0 + u;
                 cj[u] = __shfl_sync(FULL, cs[j / LPR], int(gbase) + (j % LPR));
                 if constexpr (HAS_VAL) vj[u] = __shfl_sync(FULL, vs[j / LPR], int(gbase) + (j % LPR));
-                else vj[u] = 1.f;
+                else vj[u] = 1.0;
             }
             VT bv[U][NCH];
 #pragma unroll
@@ -156,13 +174,19 @@ __global__ void __launch_bounds__(512) spmm_seg_kernel(SegArgs a) {
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const bool okj = base + std::uint32_t(j0 + u) < deg;
-                const double dv = HAS_VAL ? double(vj[u]) : 1.0;
+                const double v = vj[u];
+                const double vu = MIX ? v * kWidenUp : v;
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch) {
                     if (okj && fok[ch]) {
 #pragma unroll
-                        for (int q = 0; q < VEC; ++q)
-                            acc[ch][q] = __fma_rn(dv, double(comp(bv[u][ch], q)), acc[ch][q]);
+                        for (int q = 0; q < VEC; ++q) {
+                            const bool rebias = MIX && (VEC == 1 || q >= 2);
+                            if (rebias)
+                                acc[ch][q] = __fma_rn(vu, widen_scaled(comp(bv[u][ch], q)), acc[ch][q]);
+                            else
+                                acc[ch][q] = __fma_rn(v, double(comp(bv[u][ch], q)), acc[ch][q]);
+                        }
                     }
                 }
             }
@@ -173,7 +197,7 @@ __global__ void __launch_bounds__(512) spmm_seg_kernel(SegArgs a) {
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) {
         if (!fok[ch]) continue;
-        if (slot == 0xffffffffu) {
+        if (!PIECES || slot == 0xffffffffu) {
             float* cp = a.c + std::uint64_t(row) * a.f + fidx[ch];
 #pragma unroll
             for (int q = 0; q < VEC; ++q) cp[q] = float(acc[ch][q]);
@@ -183,6 +207,13 @@ __global__ void __launch_bounds__(512) spmm_seg_kernel(SegArgs a) {
             for (int q = 0; q < VEC; ++q) sp[q] = acc[ch][q];
         }
     }
+}
+
+template <int VEC, int LPR, int NCH, bool HAS_VAL, bool PIECES, int U = unroll_for(VEC, NCH),
+          int MAXR = maxreg_for(VEC, NCH)>
+__global__ void __launch_bounds__(512) __maxnreg__(MAXR) spmm_seg_kernel(SegArgs a) {
+    if (a.finite && *a.finite) seg_body<VEC, LPR, NCH, HAS_VAL, PIECES, U, 1>(a);
+    else seg_body<VEC, LPR, NCH, HAS_VAL, PIECES, U, 0>(a);
 }
 
 // K3 epilogue: s = 0.0; s += partial[p] in piece order; C = f32(s)
@@ -203,6 +234,210 @@ __global__ void hub_reduce_kernel(const std::uint32_t* __restrict__ red_row,
     }
 }
 
+// ---------------------------------------------------------------------------
+// K2L: one CTA per long row (degree >= long_row_min) with the row-parallel
+// numerics, warp-specialized around the Blackwell bulk-copy engine:
+//   warp 0 (producer): streams the row's column indices/values into an index
+//     ring with 4-byte cp.async (kIdxAhead chunks ahead, so no dependent
+//     global load sits on its path), widens the values once into a f64 ring,
+//     and issues ONE cp.async.bulk (TMA bulk copy) per gathered B row into a
+//     kLongStages-deep shared-memory ring, completion tracked by a "full"
+//     mbarrier per stage (arrive.expect_tx + complete_tx);
+//   warps 1.. (consumers): one thread per feature runs that feature's f64
+//     chain in CSR order out of shared memory, then releases the stage on its
+//     "empty" mbarrier.
+// No __syncthreads in the steady state; a stage holds ch B rows.  Bit-equal
+// to the group kernel.
+constexpr int kLongStages = 8;
+constexpr std::uint32_t kLongStageBytes = 4096;
+constexpr int kIdxAhead = 4;
+constexpr int kIdxRing = 8;
+static_assert(kIdxRing > kIdxAhead, "index ring too small");
+constexpr int kLongMaxConsumers = 256;  // consumer threads; features beyond loop
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return unsigned(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void mbar_init(std::uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(std::uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "LONGROW_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra LONGROW_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, std::uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+struct LongLayout {
+    std::uint32_t ring_off, vd_off, cidx_off, vidx_off, bar_off, total;
+};
+__host__ __device__ inline LongLayout long_layout(std::uint32_t f, std::uint32_t ch) {
+    LongLayout L{};
+    std::uint32_t o = 0;
+    L.ring_off = o;
+    o += std::uint32_t(kLongStages) * ch * f * 4;  // B rows
+    o = (o + 15) & ~15u;
+    L.vd_off = o;
+    o += std::uint32_t(kLongStages) * ch * 8;  // widened values
+    L.cidx_off = o;
+    o += std::uint32_t(kIdxRing) * ch * 4;  // column index ring
+    L.vidx_off = o;
+    o += std::uint32_t(kIdxRing) * ch * 4;  // value ring (f32)
+    o = (o + 15) & ~15u;
+    L.bar_off = o;
+    o += 2 * kLongStages * 8;  // full + empty mbarriers
+    L.total = o;
+    return L;
+}
+
+template <int MIX, bool HAS_VAL>
+__device__ __forceinline__ void longrow_body(const std::uint64_t* __restrict__ rowptr,
+                                             const std::uint32_t* __restrict__ colind,
+                                             const float* __restrict__ val,
+                                             const std::uint32_t* __restrict__ rows,
+                                             const float* __restrict__ b, float* __restrict__ c,
+                                             std::uint32_t f, std::uint32_t ch, char* smem) {
+    constexpr int S = kLongStages;
+    const LongLayout L = long_layout(f, ch);
+    float* ring = reinterpret_cast<float*>(smem + L.ring_off);
+    double* vd = reinterpret_cast<double*>(smem + L.vd_off);
+    std::uint32_t* cidx = reinterpret_cast<std::uint32_t*>(smem + L.cidx_off);
+    float* vidx = reinterpret_cast<float*>(smem + L.vidx_off);
+    std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + L.bar_off);
+    std::uint64_t* empty = full + S;
+    const std::uint32_t n_cons_warps = (blockDim.x >> 5) - 1;
+
+    const std::uint32_t row = rows[blockIdx.x];
+    const std::uint64_t e0 = rowptr[row];
+    const std::uint32_t deg = std::uint32_t(rowptr[row + 1] - e0);
+    const std::uint32_t nchunks = (deg + ch - 1) / ch;
+    const int warp = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 32);  // 32 producer-lane arrivals (+ tx bytes)
+            mbar_init(&empty[s], n_cons_warps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == 0) {
+        // ---------------- producer warp ----------------
+        const unsigned row_bytes = f * 4;
+        auto issue_idx = [&](std::uint32_t k) {
+            if (k < nchunks) {
+                const std::uint32_t base = k * ch, n = min(ch, deg - base);
+                std::uint32_t* cd = cidx + (k % kIdxRing) * ch;
+                float* vdst = vidx + (k % kIdxRing) * ch;
+                for (std::uint32_t j = lane; j < n; j += 32) {
+                    cp_async4(cd + j, colind + e0 + base + j);
+                    if constexpr (HAS_VAL) cp_async4(vdst + j, val + e0 + base + j);
+                }
+            }
+            cp_async_commit();  // one group per call keeps the wait count uniform
+        };
+        for (int k = 0; k < kIdxAhead; ++k) issue_idx(std::uint32_t(k));
+        for (std::uint32_t k = 0; k < nchunks; ++k) {
+            issue_idx(k + kIdxAhead);
+            cp_async_wait<kIdxAhead>();  // chunk k's indices are in (this lane's copies)
+            __syncwarp();                // ... and visible to the whole warp
+            const int s = int(k % S);
+            if (k >= std::uint32_t(S)) mbar_wait(&empty[s], ((k / S) - 1) & 1);
+            const std::uint32_t n = min(ch, deg - k * ch);
+            const std::uint32_t* cs = cidx + (k % kIdxRing) * ch;
+            const float* vs = vidx + (k % kIdxRing) * ch;
+            double* vdst = vd + std::uint64_t(s) * ch;
+            for (std::uint32_t j = lane; j < n; j += 32) vdst[j] = HAS_VAL ? double(vs[j]) : 1.0;
+            __syncwarp();
+            if (lane == 0) mbar_arrive_expect_tx(&full[s], n * row_bytes);
+            else mbar_arrive(&full[s]);
+            float* dst = ring + std::uint64_t(s) * ch * f;
+            for (std::uint32_t j = lane; j < n; j += 32)
+                bulk_g2s(dst + std::uint64_t(j) * f, b + std::uint64_t(cs[j]) * f, row_bytes, &full[s]);
+        }
+        cp_async_wait<0>();
+        return;
+    }
+
+    // ---------------- consumer warps ----------------
+    const std::uint32_t t0 = threadIdx.x - 32;
+    const std::uint32_t n_cons = blockDim.x - 32;
+    constexpr int MAXF = 8;  // features t0, t0 + n_cons, ... (f <= 8 * n_cons)
+    double acc[MAXF];
+#pragma unroll
+    for (int i = 0; i < MAXF; ++i) acc[i] = 0.0;
+    for (std::uint32_t k = 0; k < nchunks; ++k) {
+        const int s = int(k % S);
+        mbar_wait(&full[s], (k / S) & 1);
+        const std::uint32_t n = min(ch, deg - k * ch);
+        const float* src = ring + std::uint64_t(s) * ch * f;
+        const double* vv = vd + std::uint64_t(s) * ch;
+#pragma unroll
+        for (int i = 0; i < MAXF; ++i) {
+            const std::uint32_t t = t0 + i * n_cons;
+            if (t >= f) break;
+            double a = acc[i];
+            std::uint32_t j = 0;
+            // even entries widen on XU, odd entries by re-bias (MIX)
+            for (; j + 2 <= n; j += 2) {
+                const double v0 = vv[j], v1 = vv[j + 1];
+                const float b0 = src[j * f + t], b1 = src[(j + 1) * f + t];
+                a = __fma_rn(v0, double(b0), a);
+                if constexpr (MIX) a = __fma_rn(v1 * kWidenUp, widen_scaled(b1), a);
+                else a = __fma_rn(v1, double(b1), a);
+            }
+            if (j < n) a = __fma_rn(vv[j], double(src[j * f + t]), a);
+            acc[i] = a;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+#pragma unroll
+    for (int i = 0; i < MAXF; ++i) {
+        const std::uint32_t t = t0 + i * n_cons;
+        if (t < f) c[std::uint64_t(row) * f + t] = float(acc[i]);
+    }
+}
+
+template <bool HAS_VAL>
+__global__ void __launch_bounds__(32 + kLongMaxConsumers)
+    spmm_longrow_kernel(const std::uint64_t* __restrict__ rowptr,
+                        const std::uint32_t* __restrict__ colind, const float* __restrict__ val,
+                        const std::uint32_t* __restrict__ rows, const float* __restrict__ b,
+                        float* __restrict__ c, std::uint32_t f, std::uint32_t ch,
+                        const unsigned* __restrict__ finite) {
+    extern __shared__ __align__(16) char lsmem[];
+    if (finite && *finite) longrow_body<1, HAS_VAL>(rowptr, colind, val, rows, b, c, f, ch, lsmem);
+    else longrow_body<0, HAS_VAL>(rowptr, colind, val, rows, b, c, f, ch, lsmem);
+}
+
+// ---------------------------------------------------------------------------
 // K1: the guardrail baseline.  Warp per row in natural order, lane per
 // feature (NF features per lane per pass), scalar loads, no prefetch.
 template <int NF>
@@ -235,16 +470,57 @@ __global__ void spmm_baseline_kernel(const std::uint64_t* __restrict__ rowptr,
     }
 }
 
+// developer tuning knob (AUTOSAGE_DEV_SPMM_TUNE=<U>x<MAXR>) for the F=64
+// shapes; default = the tuned constants above
+int dev_tune() {
+    static const int t = [] {
+        const char* e = std::getenv("AUTOSAGE_DEV_SPMM_TUNE");
+        if (!e) return 0;
+        const std::string v(e);
+        if (v == "2x40") return 1;
+        if (v == "4x40") return 2;
+        if (v == "4x48") return 3;
+        if (v == "8x48") return 4;
+        if (v == "8x64") return 5;
+        if (v == "8x128") return 6;
+        if (v == "2x48") return 7;
+        return 0;
+    }();
+    return t;
+}
+
+template <int VEC, int LPR, int NCH, bool HV, bool PC>
+void launch_tuned(const SegArgs& a, unsigned blocks, unsigned threads, cudaStream_t s) {
+    if constexpr (VEC == 4 && NCH == 1 && (LPR == 16 || LPR == 8) && HV) {
+        switch (dev_tune()) {
+            case 1: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 2, 40><<<blocks, threads, 0, s>>>(a); return;
+            case 2: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 4, 40><<<blocks, threads, 0, s>>>(a); return;
+            case 3: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 4, 48><<<blocks, threads, 0, s>>>(a); return;
+            case 4: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 8, 48><<<blocks, threads, 0, s>>>(a); return;
+            case 5: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 8, 64><<<blocks, threads, 0, s>>>(a); return;
+            case 6: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 8, 128><<<blocks, threads, 0, s>>>(a); return;
+            case 7: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 2, 48><<<blocks, threads, 0, s>>>(a); return;
+            default: break;
+        }
+    }
+    spmm_seg_kernel<VEC, LPR, NCH, HV, PC><<<blocks, threads, 0, s>>>(a);
+}
+
 template <int VEC, int LPR, int NCH>
 void launch_seg(const SegArgs& a, bool has_val, std::uint32_t wpb, cudaStream_t s) {
     constexpr int GPW = 32 / LPR;
     const std::uint64_t groups_per_block = std::uint64_t(wpb) * GPW;
     const std::uint64_t blocks = (a.n_items + groups_per_block - 1) / groups_per_block;
     if (blocks == 0) return;
-    if (has_val)
-        spmm_seg_kernel<VEC, LPR, NCH, true><<<unsigned(blocks), wpb * 32, 0, s>>>(a);
-    else
-        spmm_seg_kernel<VEC, LPR, NCH, false><<<unsigned(blocks), wpb * 32, 0, s>>>(a);
+    const bool pieces = a.piece_row != nullptr;
+    const unsigned nb = unsigned(blocks), nt = wpb * 32;
+    if (has_val) {
+        if (pieces) launch_tuned<VEC, LPR, NCH, true, true>(a, nb, nt, s);
+        else launch_tuned<VEC, LPR, NCH, true, false>(a, nb, nt, s);
+    } else {
+        if (pieces) launch_tuned<VEC, LPR, NCH, false, true>(a, nb, nt, s);
+        else launch_tuned<VEC, LPR, NCH, false, false>(a, nb, nt, s);
+    }
     check_launch("spmm_seg_kernel");
 }
 
@@ -272,7 +548,7 @@ struct TileShape {
 TileShape tile_shape(std::uint32_t f, std::uint64_t f_tile, bool vec) {
     const int v = vec ? 4 : 1;
     std::uint64_t tw = effective_tile(f_tile, f);
-    if (vec) tw = (tw + 3) / 4 * 4;                       // keep float4 alignment
+    if (vec) tw = (tw + 3) / 4 * 4;                                 // keep float4 alignment
     tw = std::min<std::uint64_t>(tw, std::uint64_t(32 * 8 * v));  // at most 8 chunks / lane
     TileShape t;
     t.tile_w = std::uint32_t(std::max<std::uint64_t>(tw, 1));
@@ -281,51 +557,88 @@ TileShape tile_shape(std::uint32_t f, std::uint64_t f_tile, bool vec) {
     return t;
 }
 
+std::uint64_t long_row_min() {
+    static const std::uint64_t v = [] {
+        const char* e = std::getenv("AUTOSAGE_DEV_LONG_ROW");
+        return e ? std::strtoull(e, nullptr, 10) : std::uint64_t(2048);
+    }();
+    return v;
+}
+
 } // namespace
 
-void launch_spmm_baseline(Graph& g, const float* val, const float* b, std::uint32_t f, float* c, cudaStream_t s) {
+void launch_spmm_baseline(Graph& g, const float* val, const float* b, std::uint32_t f, float* c,
+                          cudaStream_t s) {
     if (g.n_rows == 0 || f == 0) return;
     const std::uint64_t threads = g.n_rows * 32;
     const unsigned blocks = unsigned((threads + 255) / 256);
     if (f <= 32)
-        spmm_baseline_kernel<1><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c,
-                                                       g.n_rows, f);
+        spmm_baseline_kernel<1><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f);
     else if (f <= 64)
-        spmm_baseline_kernel<2><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c,
-                                                       g.n_rows, f);
+        spmm_baseline_kernel<2><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f);
     else if (f <= 128)
-        spmm_baseline_kernel<4><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c,
-                                                       g.n_rows, f);
+        spmm_baseline_kernel<4><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f);
     else
-        spmm_baseline_kernel<8><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c,
-                                                       g.n_rows, f);
+        spmm_baseline_kernel<8><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f);
     check_launch("spmm_baseline_kernel");
 }
 
-void launch_spmm_rows(Graph& g, const float* val, const std::uint32_t* rowlist, std::uint64_t n_list, const float* b,
-                      std::uint32_t f, float* c, std::uint64_t f_tile, bool vec, std::uint32_t wpb,
-                      cudaStream_t s) {
+void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uint64_t n_list,
+                      const float* b, std::uint32_t f, float* c, std::uint64_t f_tile, bool vec,
+                      std::uint32_t wpb, cudaStream_t s, const unsigned* finite) {
     if (n_list == 0 || f == 0) return;
-    const TileShape t = tile_shape(f, f_tile, vec);
-    SegArgs a{};
-    a.rowptr = g.rowptr.get();
-    a.colind = g.colind.get();
-    a.val = val;
-    a.b = b;
-    a.c = c;
-    a.rowlist = rowlist;
-    a.n_items = n_list * t.n_tiles;
-    a.n_tiles = t.n_tiles;
-    a.f = f;
-    a.tile_w = t.tile_w;
-    wpb = std::clamp<std::uint32_t>(wpb, 1, 16);
-    if (vec) launch_seg_vec<4>(a, val != nullptr, t.lanes, wpb, s);
-    else launch_seg_vec<1>(a, val != nullptr, t.lanes, wpb, s);
+    ensure_order(g);
+    // long rows (a prefix of the degree-descending order) -> CTA-per-row ring
+    // kernel on a forked stream, concurrent with the group kernel
+    const std::uint64_t lmin = long_row_min();
+    std::uint64_t n_long = 0;
+    std::uint32_t ch = 0;
+    if (lmin > 0 && f <= 2048 && vec && f % 4 == 0) {  // bulk copies need 16-B rows
+        const std::uint64_t ge = rows_with_degree_at_least(g, lmin);
+        n_long = ge > offset ? std::min(ge - offset, n_list) : 0;
+        ch = std::max<std::uint32_t>(4, kLongStageBytes / (4 * f));
+        if (long_layout(f, ch).total > 200 * 1024) n_long = 0;
+    }
+    if (n_long) {
+        const std::uint32_t* rows = g.order.get() + offset;
+        const std::size_t smem = long_layout(f, ch).total;
+        const unsigned threads = 32 + std::min<unsigned>(kLongMaxConsumers, (f + 31) / 32 * 32);
+        cudaStream_t aux = graph_fork(g, s);
+        auto go = [&](auto kern) {
+            ASB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            kern<<<unsigned(n_long), threads, smem, aux>>>(g.rowptr.get(), g.colind.get(), val, rows, b,
+                                                           c, f, ch, finite);
+            check_launch("spmm_longrow_kernel");
+        };
+        if (val) go(spmm_longrow_kernel<true>);
+        else go(spmm_longrow_kernel<false>);
+        offset += n_long;
+        n_list -= n_long;
+    }
+    if (n_list) {
+        const TileShape t = tile_shape(f, f_tile, vec);
+        SegArgs a{};
+        a.rowptr = g.rowptr.get();
+        a.colind = g.colind.get();
+        a.val = val;
+        a.b = b;
+        a.c = c;
+        a.rowlist = g.order.get() + offset;
+        a.finite = finite;
+        a.n_items = n_list * t.n_tiles;
+        a.n_tiles = t.n_tiles;
+        a.f = f;
+        a.tile_w = t.tile_w;
+        wpb = std::clamp<std::uint32_t>(wpb, 1, 16);
+        if (vec) launch_seg_vec<4>(a, val != nullptr, t.lanes, wpb, s);
+        else launch_seg_vec<1>(a, val != nullptr, t.lanes, wpb, s);
+    }
+    if (n_long) graph_join(g, s);
 }
 
 void launch_spmm_hubsplit(Graph& g, const float* val, const float* b, std::uint32_t f, float* c,
                           std::uint64_t f_tile, bool vec, std::uint32_t wpb,
-                          std::uint64_t hub_threshold, cudaStream_t s) {
+                          std::uint64_t hub_threshold, cudaStream_t s, const unsigned* finite) {
     if (g.n_rows == 0 || f == 0) return;
     const HubPlan& plan = ensure_hub_plan(g, hub_threshold);
     wpb = std::clamp<std::uint32_t>(wpb, 1, 16);
@@ -343,6 +656,7 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const float* b, std::uint3
         a.piece_e0 = plan.piece_e0.get();
         a.piece_len = plan.piece_len.get();
         a.piece_slot = plan.piece_slot.get();
+        a.finite = finite;
         a.n_items = plan.n_pieces * t.n_tiles;
         a.n_tiles = t.n_tiles;
         a.f = f;
@@ -351,7 +665,7 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const float* b, std::uint3
         else launch_seg_vec<1>(a, val != nullptr, t.lanes, wpb, s);
     }
     if (plan.n_light)
-        launch_spmm_rows(g, val, plan.light_rows.get(), plan.n_light, b, f, c, f_tile, vec, wpb, s);
+        launch_spmm_rows(g, val, plan.n_heavy, plan.n_light, b, f, c, f_tile, vec, wpb, s, finite);
     if (plan.n_red) {
         const std::uint64_t total = plan.n_red * f;
         const unsigned blocks = unsigned(std::min<std::uint64_t>((total + 255) / 256, 148 * 32));
