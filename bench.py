@@ -248,8 +248,9 @@ def run_ours(args):
     if args.f:
         f = args.f
     n_rows, nnz = m.n_rows, m.nnz
-    cuts = asb.partition_rows(m.rowptr, world)
-    r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+    from paper_2511_17594_b200.dist import RowSharding
+    sh = RowSharding(m.rowptr, world, rank)  # nnz-balanced contiguous row ranges
+    r0, r1 = sh.r0, sh.r1
     full = asb.Graph.from_csr(m, device=local)
     g = full if world == 1 else full.row_range(r0, r1)
     if world > 1:
@@ -258,21 +259,15 @@ def run_ours(args):
     b_host = asb.fill_uniform(m.n_cols * f, args.seed + f, (m.n_cols, f))
     x_host = asb.fill_uniform(n_rows * f, args.seed + f, (n_rows, f))
     y_host = asb.fill_uniform(m.n_cols * f, args.seed + f + 1, (m.n_cols, f))
-    # square graph: rank r owns B/Y rows [cuts[r], cuts[r+1]) (its own node rows)
-    shard = max(int(cuts[i + 1] - cuts[i]) for i in range(world))
+    # square graph: rank r owns the B/Y rows of its own node range
     b_full = torch.from_numpy(b_host).to(dev)
     y_full = torch.from_numpy(y_host).to(dev)
     x_loc = torch.from_numpy(x_host[r0:r1]).to(dev)
     if world > 1:
-        b_shard = torch.zeros((shard, f), dtype=torch.float32, device=dev)
-        y_shard = torch.zeros((shard, f), dtype=torch.float32, device=dev)
-        b_shard[: r1 - r0] = b_full[r0:r1]
-        y_shard[: r1 - r0] = y_full[r0:r1]
-        gathered_b = torch.empty((world * shard, f), dtype=torch.float32, device=dev)
-        gathered_y = torch.empty((world * shard, f), dtype=torch.float32, device=dev)
-        # padded all-gather layout -> global row index map
-        perm = torch.cat([torch.arange(int(cuts[i]), int(cuts[i + 1])) * 0 + i * shard +
-                          torch.arange(0, int(cuts[i + 1] - cuts[i])) for i in range(world)]).to(dev)
+        b_loc = b_full[r0:r1].contiguous()
+        y_loc = y_full[r0:r1].contiguous()
+        pad_b = torch.empty((world * sh.shard, f), dtype=torch.float32, device=dev)
+        pad_y = torch.empty((world * sh.shard, f), dtype=torch.float32, device=dev)
     c = torch.empty((r1 - r0, f), dtype=torch.float32, device=dev)
     sv = torch.empty(max(g.nnz, 1), dtype=torch.float32, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
@@ -291,9 +286,7 @@ def run_ours(args):
     def gather():
         if world == 1:
             return b_full, y_full
-        dist.all_gather_into_tensor(gathered_b, b_shard)
-        dist.all_gather_into_tensor(gathered_y, y_shard)
-        return gathered_b.index_select(0, perm), gathered_y.index_select(0, perm)
+        return sh.allgather_rows(b_loc, out_padded=pad_b), sh.allgather_rows(y_loc, out_padded=pad_y)
 
     def spmm(bm):
         asb._check(lib.as_spmm_auto(C.byref(cctx), C.byref(ccfg), g.handle, P(bm), bm.shape[0], f,

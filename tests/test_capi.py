@@ -1,0 +1,325 @@
+"""Host-side behaviour of the C-ABI (no GPU needed).
+
+Covers the library boundary (every symbol include/autosage_b200.h declares is
+exported) and the reference's host contracts: variant strings
+(test_kernels.cpp:356-363), validate (test_csr.cpp), cost/shortlist
+(test_cost.cpp), time_kernel and the guardrail decision procedure with a
+scripted timer (test_scheduler.cpp), the schedule cache (test_cache.cpp),
+ASCR I/O (test_io.cpp), env parsing, the multi-GPU row partition and the
+synthetic generator.  Expected values come from the oracle and, where
+built, the reference library itself.
+"""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2511_17594_b200 as asb
+from paper_2511_17594_b200 import _capi
+from tests.util import FakeTimer, hub_graph, identity, random_csr
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "autosage_b200.h")
+
+
+def test_every_declared_symbol_is_exported():
+    text = open(HEADER).read()
+    declared = set(re.findall(r"\b(as_[a-z0-9_]+)\s*\(", text))
+    declared -= {"as_time_once_fn"}
+    missing = [s for s in sorted(declared) if not hasattr(_capi.lib, s)]
+    assert not missing, missing
+    assert set(_capi.EXPORTED) <= declared
+    assert _capi.lib.as_abi_version() == 1
+    assert _capi.lib.as_artifact_version().decode() == "autosage-b200-0.1.0"
+
+
+def test_no_cpu_compute_path_in_the_product():
+    # the product library must not link or load the oracle
+    import subprocess
+    out = subprocess.run(["ldd", asb.LIB_PATH], capture_output=True, text=True).stdout
+    assert "oracle" not in out and "autosage_ref" not in out
+    syms = subprocess.run(["nm", "-D", asb.LIB_PATH], capture_output=True, text=True).stdout
+    assert "orc_" not in syms and "ref_" not in syms.replace("_ref_", "")
+
+
+# ---- variants -------------------------------------------------------------------
+def test_variant_strings_round_trip():
+    v = asb.KernelVariant(asb.SDDMM, asb.HUBSPLIT, 128, 16, True, 512)
+    assert asb.variant_to_string(v) == "sddmm:hubsplit:ft=128:rpc=16:vec=1:hubt=512"
+    assert asb.variant_from_string(asb.variant_to_string(v)) == v
+    with pytest.raises(asb.InvalidArgument):
+        asb.variant_from_string("spmm:bogus:ft=1:rpc=1:vec=0:hubt=1")
+    with pytest.raises(asb.InvalidArgument):
+        asb.variant_from_string("nonsense")
+    with pytest.raises(asb.InvalidArgument):
+        asb.variant_from_string("spmm:baseline:ft=x:rpc=1:vec=0:hubt=1")
+    assert asb.KernelVariant() == asb.variant_from_string("spmm:rowparallel:ft=64:rpc=4:vec=0:hubt=256")
+
+
+def test_vec4_gate():
+    a = np.zeros(64 * 4 + 4, np.float32)
+    base = a[(-a.ctypes.data // 4) % 4:]  # 16-byte aligned view
+    assert asb.vec4_eligible(64, base) and not asb.vec4_eligible(63, base)
+    assert not asb.vec4_eligible(64, base[1:]) and not asb.vec4_eligible(0, base)
+
+
+# ---- validate (test_csr.cpp) ------------------------------------------------------
+def test_validate_names_first_violation():
+    ok = asb.CsrMatrix(2, 2, [0, 1, 2], [0, 1])
+    assert asb.validate(ok) is None
+    assert asb.validate(asb.CsrMatrix(2, 2, [0, 2, 1], [0])) == ("rowptr non-decreasing", 2)
+    assert asb.validate(asb.CsrMatrix(1, 2, [0, 1], [2])) == ("colind out of range", 0)
+    assert asb.validate(asb.CsrMatrix(2, 4, [0, 1, 3], [0, 1]))[0] == "rowptr/nnz mismatch"
+    assert asb.validate(asb.CsrMatrix(1, 4, [0, 2], [2, 1])) == ("colind not strictly increasing", 1)
+    assert asb.validate(asb.CsrMatrix(1, 4, [0, 2], [1, 2], np.ones(1, np.float32)))[0] == \
+        "val length mismatch"
+
+
+def test_graph_sig_host_matches_oracle_and_properties():
+    rng = np.random.default_rng(1)
+    m = random_csr(rng, 500, 500, 10)
+    assert asb.graph_sig(m) == oracle.graph_sig(m)
+    assert asb.graph_sig(m) == asb.graph_sig(m.with_values(None))  # values excluded
+    wider = asb.CsrMatrix(m.n_rows, m.n_cols + 1, m.rowptr, m.colind)
+    assert asb.graph_sig(wider) != asb.graph_sig(m)
+    seen = {asb.graph_sig(m)}
+    for k in range(0, min(m.nnz, 400)):
+        ci = m.colind.copy()
+        ci[k] = (ci[k] + 1 + k % 7) % m.n_cols
+        seen.add(asb.graph_sig(asb.CsrMatrix(m.n_rows, m.n_cols, m.rowptr, ci)))
+    assert len(seen) >= 400
+
+
+# ---- cost model (test_cost.cpp) ------------------------------------------------------
+DEV = asb.DeviceProfile.fixed(20e9, 40e9, 4, "test")
+
+
+def feats_of(m, hub_t=256):
+    f = oracle.extract_features(m, hub_t)
+    return asb.GraphFeatures(**{k: (int(v) if isinstance(v, int) else v) for k, v in f.items()})
+
+
+def test_estimate_cost_and_shortlist_match_oracle():
+    rng = np.random.default_rng(2)
+    for m in (hub_graph(rng, 2000, [500], 8, False), hub_graph(rng, 400, [], 6, False)):
+        gf = feats_of(m)
+        of = oracle.extract_features(m)
+        for f, op in ((64, asb.SPMM), (63, asb.SPMM), (128, asb.SDDMM)):
+            got = asb.shortlist(gf, f, op, DEV)
+            want = oracle.shortlist(of, f, op, 20e9, 40e9, 4)
+            assert [(v.op, v.mapping, v.f_tile, v.rows_per_chunk, v.vectorized, v.hub_threshold)
+                    for v in got] == want
+            assert len(got) == (36 if f % 4 == 0 else 18)
+            for v in got:
+                c = asb.estimate_cost(v, gf, f, DEV)
+                assert c == oracle.estimate_cost((v.op, v.mapping, v.f_tile, v.rows_per_chunk,
+                                                  int(v.vectorized), v.hub_threshold),
+                                                 of, f, 20e9, 40e9, 4)
+
+
+def test_cost_model_reference_properties():
+    empty = asb.GraphFeatures(n_rows=100, n_cols=100, nnz=0)
+    assert asb.estimate_cost(asb.KernelVariant(), empty, 64, DEV) == 0.0
+    rng = np.random.default_rng(3)
+    gf = feats_of(random_csr(rng, 2000, 2000, 16, False))
+    v = asb.KernelVariant()
+    ratio = asb.estimate_cost(v, gf, 128, DEV) / asb.estimate_cost(v, gf, 64, DEV)
+    assert 1.9 <= ratio <= 2.1
+    uniform = feats_of(hub_graph(rng, 400, [], 6, False))
+    head = asb.shortlist(uniform, 64, asb.SPMM, DEV)[0]
+    assert (head.mapping, head.f_tile, head.vectorized, head.rows_per_chunk) == \
+        (asb.ROWPARALLEL, 32, True, 1)
+    skew = feats_of(hub_graph(rng, 1000, [400], 5, False))
+    assert asb.shortlist(skew, 128, asb.SDDMM, DEV)[0].mapping == asb.HUBSPLIT
+    scaled = asb.DeviceProfile.fixed(20e9 * 3.7, 40e9 * 3.7, 4, "test")
+    assert asb.shortlist(skew, 64, asb.SPMM, DEV) == asb.shortlist(skew, 64, asb.SPMM, scaled)
+    with pytest.raises(asb.InvalidArgument):
+        asb.estimate_cost(v, gf, 64, asb.DeviceProfile.fixed(0.0, 1.0, 1))
+
+
+# ---- time_kernel and the decision procedure (test_scheduler.cpp) -----------------------
+def test_time_kernel_policy_matches_reference():
+    for script, iters, cap in (([0.1] * 5, 5, 1.0), ([2.0], 5, 1.0), ([3.0, 1.0, 2.0], 3, 1e9),
+                               ([4.0, 1.0, 3.0, 2.0], 4, 1e9), ([0.4] * 4, 4, 1.0)):
+        st = asb.time_kernel("k", lambda: None, iters, cap, FakeTimer(script))
+        want = oracle.time_kernel_policy(script, iters, cap)
+        assert (st.median_ms, st.completed, st.capped) == \
+            (want["median_ms"], want["completed"], want["capped"])
+        assert st.launches == want["launches"]
+    with pytest.raises(asb.InvalidArgument):
+        asb.time_kernel("k", lambda: None, 0, 1.0, FakeTimer([1.0]))
+    with pytest.raises(RuntimeError, match="script exhausted"):
+        asb.time_kernel("k", lambda: None, 3, 1e9, FakeTimer([1.0]))
+
+
+def host_decide(script, alpha=0.95, cache=None, replay=None, f=32, sig=0x1234):
+    rng = np.random.default_rng(99)
+    gf = feats_of(random_csr(rng, 64, 64, 12, False))
+    ctx = asb.ScheduleContext(device=DEV, cache=cache, timer=FakeTimer(script),
+                              replay=replay or asb.ReplayPolicy())
+    cfg = asb.ProbeConfig(iters=1, cap_ms=1e9, top_k=3, alpha=alpha)
+    return asb.decide_host(ctx, cfg, sig, gf, f, asb.SPMM, 64)
+
+
+def test_guardrail_boundary_and_ties():
+    d = host_decide([10.0, 9.4, 11.0, 12.0])
+    assert d.choice is not None and d.t_star == 9.4 and d.source == asb.PROBED
+    d = host_decide([10.0, 9.6, 11.0, 12.0])
+    assert d.choice is None and d.choice_string() == "baseline"
+    assert host_decide([10.0, 0.95 * 10.0, 10.5, 11.5]).choice is not None  # exact tie accepts
+    d = host_decide([10.0, 8.0, 7.5, 7.5])
+    assert d.best_index == 1 and d.t_star == 7.5 and d.choice == d.candidates[1].variant
+    for ts in (0.85, 0.92, 0.96, 0.99):
+        lo = host_decide([1.0, ts, ts + 1, ts + 2], alpha=0.90).choice is not None
+        hi = host_decide([1.0, ts, ts + 1, ts + 2], alpha=0.98).choice is not None
+        assert hi or not lo
+
+
+def test_cache_hit_replay_and_strict_miss():
+    cache = asb.ScheduleCache()
+    cold = host_decide([10.0, 9.0, 9.5, 9.8], cache=cache)
+    assert cold.source == asb.PROBED and cache.size() == 1
+    asb.reset_probe_launch_count()
+    warm = host_decide([], cache=cache)
+    assert warm.source == asb.CACHED and warm.choice_string() == cold.choice_string()
+    assert asb.probe_launch_count() == 0
+    rep = host_decide([], cache=cache, replay=asb.ReplayPolicy(replay_only=True))
+    assert rep.source == asb.REPLAYED and rep.choice_string() == cold.choice_string()
+    miss = host_decide([], cache=cache, replay=asb.ReplayPolicy(replay_only=True), sig=0x99)
+    assert miss.source == asb.REPLAYED and miss.choice is None
+    with pytest.raises(asb.ReplayMiss):
+        host_decide([], cache=cache, replay=asb.ReplayPolicy(True, True), sig=0x99)
+
+
+def test_forced_env_bypasses_probe(monkeypatch):
+    monkeypatch.setenv("AUTOSAGE_FTILE", "32")
+    d = host_decide([])
+    assert d.source == asb.FORCED_ENV and d.choice.f_tile == 32 and d.choice.mapping == asb.ROWPARALLEL
+    assert not d.choice.vectorized
+    monkeypatch.setenv("AUTOSAGE_HUB_T", "128")
+    d = host_decide([])
+    assert d.choice.mapping == asb.HUBSPLIT and d.choice.hub_threshold == 128
+
+
+def test_probe_config_env_and_validation(monkeypatch):
+    for k, v in (("AUTOSAGE_PROBE_FRAC", "0.03"), ("AUTOSAGE_PROBE_ITERS", "7"),
+                 ("AUTOSAGE_PROBE_CAP_MS", "0.5"), ("AUTOSAGE_PROBE_TOPK", "2"),
+                 ("AUTOSAGE_GUARDRAIL", "0.9")):
+        monkeypatch.setenv(k, v)
+    assert asb.ProbeConfig.from_env() == asb.ProbeConfig(0.03, 512, 7, 0.5, 2, 0.9)
+    monkeypatch.setenv("AUTOSAGE_REPLAY_ONLY", "1")
+    monkeypatch.setenv("AUTOSAGE_REPLAY_STRICT", "off")
+    assert asb.ReplayPolicy.from_env() == asb.ReplayPolicy(True, False)
+    rng = np.random.default_rng(1)
+    gf = feats_of(random_csr(rng, 64, 64, 12, False))
+    ctx = asb.ScheduleContext(device=DEV, timer=FakeTimer([1.0] * 8))
+    for bad in (asb.ProbeConfig(alpha=1.5), asb.ProbeConfig(frac=0.0), asb.ProbeConfig(iters=0),
+                asb.ProbeConfig(top_k=0)):
+        with pytest.raises(asb.InvalidArgument):
+            asb.decide_host(ctx, bad, 1, gf, 32, asb.SPMM, 64)
+
+
+# ---- cache persistence (test_cache.cpp) ------------------------------------------------
+def rec(dev, sig, f, op, choice):
+    return asb.CacheRecord(asb.ScheduleKey(dev, sig, f, op), choice, 1.25, 0.75, 0.95, 1700000000, 1,
+                           asb.toolchain_tag())
+
+
+def test_cache_records_and_lines(tmp_path):
+    r = rec("cpu model with spaces|cores=8|v1", 0xDEADBEEFCAFEF00D, 64, asb.SDDMM,
+            "sddmm:hubsplit:ft=128:rpc=4:vec=1:hubt=256")
+    r.t_b = 0.1 + 0.2
+    r.t_star = 1e-7
+    assert asb.record_from_line(asb.record_to_line(r)) == r
+    if oracle.ref_available():
+        assert asb.record_to_line(r) == oracle.ref_record_line(
+            r.key.device_sig, r.key.graph_sig, 64, 1, r.choice, r.t_b, r.t_star, r.alpha,
+            r.timestamp, r.toolchain)
+    c = asb.ScheduleCache()
+    c.put(rec("devA", 1, 64, asb.SPMM, "baseline"))
+    c.put(rec("devA", 1, 128, asb.SPMM, "spmm:rowparallel:ft=32:rpc=1:vec=1:hubt=256"))
+    c.put(rec("devB", 2, 64, asb.SDDMM, "baseline"))
+    assert c.get(asb.ScheduleKey("devA", 1, 64, asb.SPMM)).choice == "baseline"
+    assert c.get(asb.ScheduleKey("devA", 1, 64, asb.SDDMM)) is None
+    p1, p2 = tmp_path / "a.log", tmp_path / "b.log"
+    c.store(p1)
+    c.store(p2)
+    assert p1.read_bytes() == p2.read_bytes() and p1.read_bytes()
+    loaded = asb.ScheduleCache()
+    loaded.load(p1)
+    assert loaded.size() == 3 and loaded.snapshot() == c.snapshot()
+    bad = tmp_path / "bad.log"
+    bad.write_text(asb.record_to_line(rec("dev", 5, 64, 0, "baseline")) + "\nthis is not a record\n")
+    with pytest.raises(asb.CacheError, match=":2:"):
+        loaded.load(bad)
+    line = asb.record_to_line(rec("dev", 5, 64, 0, "baseline"))
+    (tmp_path / "schema.log").write_text("9" + line[1:] + "\n")
+    with pytest.raises(asb.CacheError, match="schema_version"):
+        loaded.load(tmp_path / "schema.log")
+    (tmp_path / "choice.log").write_text(line.replace("baseline", "notakern") + "\n")
+    with pytest.raises(asb.CacheError):
+        loaded.load(tmp_path / "choice.log")
+    with pytest.raises(asb.CacheError):
+        loaded.load(tmp_path / "missing.log")
+
+
+# ---- ASCR I/O (test_io.cpp) and synthetic inputs ---------------------------------------
+def test_ascr_round_trip_and_errors(tmp_path):
+    m = asb.CsrMatrix(3, 3, [0, 1, 2, 3], [0, 1, 2], np.array([1, 2, 3], np.float32))
+    asb.save_csr(m, tmp_path / "id.ascr")
+    assert asb.load_csr(tmp_path / "id.ascr") == m
+    pat = asb.CsrMatrix(2, 2, [0, 1, 2], [1, 0])
+    asb.save_csr(pat, tmp_path / "p.ascr")
+    back = asb.load_csr(tmp_path / "p.ascr")
+    assert back == pat and not back.has_values()
+    asb.save_csr(asb.CsrMatrix(2, 4, [0, 1, 3], [0, 1]), tmp_path / "bad.ascr")
+    with pytest.raises(asb.IoError, match="rowptr/nnz mismatch"):
+        asb.load_csr(tmp_path / "bad.ascr")
+    asb.save_csr(asb.CsrMatrix(1, 4, [0, 2], [2, 1]), tmp_path / "uns.ascr")
+    with pytest.raises(asb.IoError, match="strictly increasing"):
+        asb.load_csr(tmp_path / "uns.ascr")
+    big = asb.gen_powerlaw(100, 100, 500, 2.0, 2, 50, 3)
+    asb.save_csr(big, tmp_path / "t.ascr")
+    raw = (tmp_path / "t.ascr").read_bytes()
+    (tmp_path / "t.ascr").write_bytes(raw[:-8])
+    with pytest.raises(asb.IoError, match="truncated"):
+        asb.load_csr(tmp_path / "t.ascr")
+    (tmp_path / "m.ascr").write_bytes(b"NOPE this is not a csr container")
+    with pytest.raises(asb.IoError, match="magic"):
+        asb.load_csr(tmp_path / "m.ascr")
+    with pytest.raises(asb.IoError):
+        asb.load_csr(tmp_path / "missing.ascr")
+
+
+def test_powerlaw_generator_is_valid_deterministic_and_exact():
+    a = asb.gen_powerlaw(20000, 20000, 500000, 2.1, 4, 3000, 7)
+    assert a.nnz == 500000 and asb.validate(a) is None
+    assert a == asb.gen_powerlaw(20000, 20000, 500000, 2.1, 4, 3000, 7)
+    assert a != asb.gen_powerlaw(20000, 20000, 500000, 2.1, 4, 3000, 8)
+    assert a.degrees().max() <= 3000 and a.val.min() >= 0 and a.val.max() < 1
+    u = asb.fill_uniform(100000, 5)
+    assert u.min() >= -1 and u.max() < 1 and abs(u.mean()) < 0.02
+    assert np.array_equal(u, asb.fill_uniform(100000, 5))
+
+
+def test_partition_rows_matches_oracle():
+    rng = np.random.default_rng(4)
+    m = hub_graph(rng, 3000, [2500, 1000], 9, False)
+    for g in (1, 2, 4, 8):
+        assert np.array_equal(asb.partition_rows(m.rowptr, g), oracle.partition_rows(m.rowptr, g))
+    with pytest.raises(asb.InvalidArgument):
+        asb.partition_rows(m.rowptr, 0)
+
+
+def test_device_entry_points_fail_loudly_without_a_gpu():
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("GPU present")
+    except ImportError:
+        pass
+    with pytest.raises((asb.CudaError, MemoryError, RuntimeError)):
+        asb.Graph.from_csr(identity(4))
