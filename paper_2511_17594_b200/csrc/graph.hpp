@@ -97,6 +97,7 @@ struct Graph {
     DevBuf<float> stage_in2;
     std::map<std::uint64_t, std::uint64_t> ge_count;  // rows with degree >= key
     DevBuf<unsigned> flag;             // finiteness flag of the current dense operand
+    DevBuf<double> xwide;              // SDDMM: X widened to f64 (fixed-width path)
     cudaStream_t aux = nullptr;        // fork/join stream for concurrent kernels
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 

@@ -279,6 +279,156 @@ __global__ void __launch_bounds__(512)
         sddmm_chunk_body<VLOAD, ORD, VLDS, 0, NB>(rowptr, colind, chunk_row, n_rows, x, y, out, nnz, f, S, ft, wsm);
 }
 
+// ---------------------------------------------------------------------------
+// Fixed-width path (F in {16, 32, 64, 128}, X/Y 16-byte aligned): the copy
+// and dot loops unroll completely, X is read pre-widened (f64, one prepass
+// per call) with broadcast loads instead of being staged per chunk, and
+// each lane finds its row from one coalesced read of the 32 row boundaries
+// after the chunk's first row.  Shared memory holds only the 32 staged Y
+// rows (pitch: odd number of 16-byte units).
+// ---------------------------------------------------------------------------
+__global__ void widen_kernel(const float4* __restrict__ x, double2* __restrict__ xd, std::uint64_t n4) {
+    for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+         i += std::uint64_t(gridDim.x) * blockDim.x) {
+        const float4 v = __ldg(x + i);
+        xd[2 * i] = make_double2(double(v.x), double(v.y));
+        xd[2 * i + 1] = make_double2(double(v.z), double(v.w));
+    }
+}
+
+template <int F>
+struct FixedShape {
+    static constexpr int NV = F / 4;                // 16-byte units per row
+    static constexpr int S = 4 * (NV | 1);          // smem pitch in floats
+    static constexpr int kCopies = NV;              // cp.async per lane per chunk (32 rows)
+    static constexpr int KX = F >= 64 ? 1 : 64 / F; // X rows (f64) staged per chunk
+    static constexpr int kXUnits = KX * F / 2;      // their 16-byte units
+    static constexpr std::uint64_t kYBytes = 32ull * S * 4;
+    static constexpr std::uint64_t kWarpBytes = kYBytes + std::uint64_t(KX) * F * 8;
+};
+
+template <bool SMEM>
+__device__ __forceinline__ double2 ld_x2(const double* p) {
+    if constexpr (SMEM) return *reinterpret_cast<const double2*>(p);
+    else return __ldg(reinterpret_cast<const double2*>(p));
+}
+
+// <x, y> over one Y row in shared memory; xr: the lane's X row (f64, global)
+template <int F, int ORD, int FT, bool XS>
+__device__ __forceinline__ double fixed_dot(const double* __restrict__ xr, const float* yr) {
+    if constexpr (ORD == 0) {
+        double acc = 0.0;
+#pragma unroll 8
+        for (int t = 0; t < F; t += 4) {
+            const float4 y4 = *reinterpret_cast<const float4*>(yr + t);
+            const double2 x01 = ld_x2<XS>(xr + t);
+            const double2 x23 = ld_x2<XS>(xr + t + 2);
+            acc = dfma(x01.x, y4.x, acc);
+            acc = dfma(x01.y, y4.y, acc);
+            acc = dfma(x23.x, y4.z, acc);
+            acc = dfma(x23.y, y4.w, acc);
+        }
+        return acc;
+    } else {
+        // src/kernels.cpp:103-127: per f_tile block four stride-4 partials;
+        // F % 4 == 0 and FT % 4 == 0, so every block's scalar tail is empty
+        double acc = 0.0;
+#pragma unroll
+        for (int b0 = 0; b0 < F; b0 += FT) {
+            constexpr int kBlk = FT;
+            const int fw = (F - b0) < kBlk ? (F - b0) : kBlk;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll 4
+            for (int t = 0; t < fw; t += 4) {
+                const float4 y4 = *reinterpret_cast<const float4*>(yr + b0 + t);
+                const double2 x01 = ld_x2<XS>(xr + b0 + t);
+                const double2 x23 = ld_x2<XS>(xr + b0 + t + 2);
+                a0 = dfma(x01.x, y4.x, a0);
+                a1 = dfma(x01.y, y4.y, a1);
+                a2 = dfma(x23.x, y4.z, a2);
+                a3 = dfma(x23.y, y4.w, a3);
+            }
+            const double tail = 0.0;
+            acc = __dadd_rn(acc, __dadd_rn(__dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3)), tail));
+        }
+        return acc;
+    }
+}
+
+template <int F, int ORD, int FT>
+__global__ void __launch_bounds__(256, 3)
+    sddmm_fixed_kernel(const std::uint64_t* __restrict__ rowptr, const std::uint32_t* __restrict__ colind,
+                       const std::uint32_t* __restrict__ chunk_row, std::uint64_t n_rows,
+                       const double* __restrict__ xd, const float* __restrict__ y,
+                       float* __restrict__ out, std::uint64_t nnz) {
+    using Sh = FixedShape<F>;
+    extern __shared__ __align__(16) char smem[];
+    char* wsm = smem + std::uint64_t(threadIdx.x >> 5) * Sh::kWarpBytes;
+    float* ys = reinterpret_cast<float*>(wsm);
+    double* xs = reinterpret_cast<double*>(wsm + Sh::kYBytes);
+    const std::uint64_t x_units = n_rows * F / 2;
+    const int lane = threadIdx.x & 31;
+    const std::uint64_t n_chunks = (nnz + 31) / 32;
+    const std::uint64_t stride = std::uint64_t(gridDim.x) * (blockDim.x >> 5);
+
+    struct Meta {
+        std::uint32_t col, r_first;
+        std::uint64_t bound;  // rowptr[r_first + 1 + lane] (or past-the-end)
+    };
+    auto meta = [&](std::uint64_t c) {
+        Meta m{0u, 0u, ~0ull};
+        if (c >= n_chunks) return m;
+        const std::uint64_t e = c * 32 + lane;
+        m.col = e < nnz ? __ldg(colind + e) : 0u;  // row 0 stands in for the tail's copies
+        m.r_first = __ldg(chunk_row + c);
+        const std::uint64_t bi = std::uint64_t(m.r_first) + 1 + lane;
+        if (bi <= n_rows) m.bound = __ldg(rowptr + bi);
+        return m;
+    };
+
+    std::uint64_t c = std::uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    Meta cur = meta(c);
+    for (; c < n_chunks; c += stride) {
+        // 32 Y rows -> shared memory, 16-byte pieces, rows in lane order
+#pragma unroll
+        for (int it = 0; it < Sh::kCopies; ++it) {
+            const int idx = it * 32 + lane;
+            const int j = idx / Sh::NV, q = idx % Sh::NV;
+            const std::uint32_t cj = __shfl_sync(FULL, cur.col, j);
+            cp_async16(ys + j * Sh::S + 4 * q, y + std::uint64_t(cj) * F + 4 * q);
+        }
+        // X rows r_first .. r_first+KX-1 (contiguous in xd)
+#pragma unroll
+        for (int u = lane; u < Sh::kXUnits; u += 32) {
+            const std::uint64_t gu = std::uint64_t(cur.r_first) * (F / 2) + u;
+            if (gu < x_units) cp_async16(xs + 2 * u, xd + 2 * gu);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        const Meta nxt = meta(c + stride);
+        // the lane's row: count the chunk's row boundaries at or before e
+        const std::uint64_t e0 = c * 32, e = e0 + lane;
+        // (sorted, so the k boundaries inside the chunk sit in lanes 0..k-1)
+        std::uint32_t r = cur.r_first;
+        const unsigned inside = __ballot_sync(FULL, cur.bound <= e0 + 31);
+        if (inside) {
+            const int k = __popc(inside);
+#pragma unroll 1
+            for (int b = 0; b < k; ++b) r += __shfl_sync(FULL, cur.bound, b) <= e ? 1u : 0u;
+            if (k == 32) r = row_of(rowptr, r, e);  // more rows meet in this chunk
+        }
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        __syncwarp();
+        if (e < nnz) {
+            const std::uint32_t rel = r - cur.r_first;
+            const float* yr = ys + lane * Sh::S;
+            out[e] = float(rel < Sh::KX ? fixed_dot<F, ORD, FT, true>(xs + rel * F, yr)
+                                        : fixed_dot<F, ORD, FT, false>(xd + std::uint64_t(r) * F, yr));
+        }
+        __syncwarp();
+        cur = nxt;
+    }
+}
+
 // Guardrail baseline / large-F fallback: lane per entry, both rows read
 // straight from global memory, scalar loads.
 template <int ORD>
@@ -295,6 +445,61 @@ __global__ void sddmm_direct_kernel(const std::uint64_t* __restrict__ rowptr,
     const float* xr = x + std::uint64_t(r) * f;
     const float* yr = y + std::uint64_t(colind[e]) * f;
     out[e] = float(dot_ord<ORD, false, 0>(xr, yr, f, ft));
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15u) == 0; }
+
+// Fixed-width launch; false when (f, ft, alignment) is outside its shapes.
+bool launch_sddmm_fixed(Graph& g, const float* x, const float* y, std::uint32_t f, float* out,
+                        std::uint32_t ft, int ord, cudaStream_t s) {
+    if (!(f == 16 || f == 32 || f == 64 || f == 128)) return false;
+    if (!aligned16(x) || !aligned16(y)) return false;
+    if (ord == 1 && !(ft == 32 || ft == 64 || ft == 128 || ft == f)) return false;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+
+    // X widened to f64 once per call
+    const std::uint64_t nx = g.n_rows * f;
+    g.xwide.ensure(nx);
+    {
+        const std::uint64_t n4 = nx / 4;
+        const unsigned blocks = unsigned(std::min<std::uint64_t>((n4 + 255) / 256, std::uint64_t(sms) * 8));
+        if (n4) {
+            widen_kernel<<<std::max(blocks, 1u), 256, 0, s>>>(reinterpret_cast<const float4*>(x),
+                                                              reinterpret_cast<double2*>(g.xwide.get()), n4);
+            check_launch("widen_kernel");
+        }
+    }
+    const std::uint64_t n_chunks = (g.nnz + 31) / 32;
+    auto go = [&](auto kernel, std::uint64_t warp_bytes) {
+        constexpr int kWarps = 8;
+        const std::size_t smem = std::size_t(warp_bytes * kWarps);
+        ASB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        int per_sm = 1;
+        ASB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kWarps * 32, smem));
+        const std::uint64_t want = (n_chunks + kWarps - 1) / kWarps;
+        const std::uint64_t cap = std::uint64_t(sms) * std::max(per_sm, 1);
+        const unsigned blocks = unsigned(std::max<std::uint64_t>(1, std::min(want, cap)));
+        kernel<<<blocks, kWarps * 32, smem, s>>>(g.rowptr.get(), g.colind.get(), g.chunk_row.get(),
+                                                 g.n_rows, g.xwide.get(), y, out, g.nnz);
+        check_launch("sddmm_fixed_kernel");
+    };
+    auto by_f = [&](auto fc) {
+        constexpr int F = decltype(fc)::value;
+        constexpr std::uint64_t wb = FixedShape<F>::kWarpBytes;
+        if (ord == 0) go(sddmm_fixed_kernel<F, 0, F>, wb);
+        else if (ft >= std::uint32_t(F)) go(sddmm_fixed_kernel<F, 1, F>, wb);
+        else if (ft == 32) go(sddmm_fixed_kernel<F, 1, (F > 32 ? 32 : F)>, wb);
+        else go(sddmm_fixed_kernel<F, 1, (F > 64 ? 64 : F)>, wb);
+    };
+    switch (f) {
+    case 16: by_f(std::integral_constant<int, 16>{}); break;
+    case 32: by_f(std::integral_constant<int, 32>{}); break;
+    case 64: by_f(std::integral_constant<int, 64>{}); break;
+    default: by_f(std::integral_constant<int, 128>{}); break;
+    }
+    return true;
 }
 
 } // namespace
@@ -323,6 +528,9 @@ void launch_sddmm_chunks(Graph& g, const float* x, const float* y, std::uint32_t
         ASB_CUDA(cudaMemsetAsync(out, 0, g.nnz * 4, s));
         return;
     }
+    if (dev_knob("AUTOSAGE_DEV_SDDMM_FIXED", 1) &&
+        launch_sddmm_fixed(g, x, y, f, out, ft, ord, s))
+        return;
     const bool vload = vec;  // vec4 gate already applied by dispatch
     const bool vlds = vload && (ord == 0 || ft % 4 == 0);
     const std::uint32_t S = vload ? 4 * ((f / 4) | 1u) : (f | 1u);
