@@ -287,12 +287,17 @@ __global__ void __launch_bounds__(512)
 // after the chunk's first row.  Shared memory holds only the 32 staged Y
 // rows (pitch: odd number of 16-byte units).
 // ---------------------------------------------------------------------------
-__global__ void widen_kernel(const float4* __restrict__ x, double2* __restrict__ xd, std::uint64_t n4) {
+// X -> f64.  When Y is finite (flag from finite_check_kernel) components 2
+// and 3 of every float4 carry the 2^896 that widen_scaled() takes out of
+// the matching Y components (widen.cuh).
+__global__ void widen_kernel(const float4* __restrict__ x, double2* __restrict__ xd, std::uint64_t n4,
+                             const unsigned* __restrict__ finite) {
+    const double up = (finite && *finite) ? kWidenUp : 1.0;
     for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
          i += std::uint64_t(gridDim.x) * blockDim.x) {
         const float4 v = __ldg(x + i);
         xd[2 * i] = make_double2(double(v.x), double(v.y));
-        xd[2 * i + 1] = make_double2(double(v.z), double(v.w));
+        xd[2 * i + 1] = make_double2(double(v.z) * up, double(v.w) * up);
     }
 }
 
@@ -314,7 +319,7 @@ __device__ __forceinline__ double2 ld_x2(const double* p) {
 }
 
 // <x, y> over one Y row in shared memory; xr: the lane's X row (f64, global)
-template <int F, int ORD, int FT, bool XS>
+template <int F, int ORD, int FT, bool XS, int MIX>
 __device__ __forceinline__ double fixed_dot(const double* __restrict__ xr, const float* yr) {
     if constexpr (ORD == 0) {
         double acc = 0.0;
@@ -325,8 +330,8 @@ __device__ __forceinline__ double fixed_dot(const double* __restrict__ xr, const
             const double2 x23 = ld_x2<XS>(xr + t + 2);
             acc = dfma(x01.x, y4.x, acc);
             acc = dfma(x01.y, y4.y, acc);
-            acc = dfma(x23.x, y4.z, acc);
-            acc = dfma(x23.y, y4.w, acc);
+            acc = __fma_rn(x23.x, widen<MIX>(y4.z), acc);
+            acc = __fma_rn(x23.y, widen<MIX>(y4.w), acc);
         }
         return acc;
     } else {
@@ -345,8 +350,8 @@ __device__ __forceinline__ double fixed_dot(const double* __restrict__ xr, const
                 const double2 x23 = ld_x2<XS>(xr + b0 + t + 2);
                 a0 = dfma(x01.x, y4.x, a0);
                 a1 = dfma(x01.y, y4.y, a1);
-                a2 = dfma(x23.x, y4.z, a2);
-                a3 = dfma(x23.y, y4.w, a3);
+                a2 = __fma_rn(x23.x, widen<MIX>(y4.z), a2);
+                a3 = __fma_rn(x23.y, widen<MIX>(y4.w), a3);
             }
             const double tail = 0.0;
             acc = __dadd_rn(acc, __dadd_rn(__dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3)), tail));
@@ -355,12 +360,13 @@ __device__ __forceinline__ double fixed_dot(const double* __restrict__ xr, const
     }
 }
 
-template <int F, int ORD, int FT>
-__global__ void __launch_bounds__(256, 3)
-    sddmm_fixed_kernel(const std::uint64_t* __restrict__ rowptr, const std::uint32_t* __restrict__ colind,
-                       const std::uint32_t* __restrict__ chunk_row, std::uint64_t n_rows,
-                       const double* __restrict__ xd, const float* __restrict__ y,
-                       float* __restrict__ out, std::uint64_t nnz) {
+template <int F, int ORD, int FT, int MIX>
+__device__ __forceinline__ void sddmm_fixed_body(const std::uint64_t* __restrict__ rowptr,
+                                                 const std::uint32_t* __restrict__ colind,
+                                                 const std::uint32_t* __restrict__ chunk_row,
+                                                 std::uint64_t n_rows, const double* __restrict__ xd,
+                                                 const float* __restrict__ y, float* __restrict__ out,
+                                                 std::uint64_t nnz) {
     using Sh = FixedShape<F>;
     extern __shared__ __align__(16) char smem[];
     char* wsm = smem + std::uint64_t(threadIdx.x >> 5) * Sh::kWarpBytes;
@@ -421,12 +427,24 @@ __global__ void __launch_bounds__(256, 3)
         if (e < nnz) {
             const std::uint32_t rel = r - cur.r_first;
             const float* yr = ys + lane * Sh::S;
-            out[e] = float(rel < Sh::KX ? fixed_dot<F, ORD, FT, true>(xs + rel * F, yr)
-                                        : fixed_dot<F, ORD, FT, false>(xd + std::uint64_t(r) * F, yr));
+            out[e] = float(rel < Sh::KX ? fixed_dot<F, ORD, FT, true, MIX>(xs + rel * F, yr)
+                                        : fixed_dot<F, ORD, FT, false, MIX>(xd + std::uint64_t(r) * F, yr));
         }
         __syncwarp();
         cur = nxt;
     }
+}
+
+template <int F, int ORD, int FT>
+__global__ void __launch_bounds__(256, 3)
+    sddmm_fixed_kernel(const std::uint64_t* __restrict__ rowptr, const std::uint32_t* __restrict__ colind,
+                       const std::uint32_t* __restrict__ chunk_row, std::uint64_t n_rows,
+                       const double* __restrict__ xd, const float* __restrict__ y,
+                       float* __restrict__ out, std::uint64_t nnz, const unsigned* __restrict__ finite) {
+    if (finite && *finite)
+        sddmm_fixed_body<F, ORD, FT, 1>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz);
+    else
+        sddmm_fixed_body<F, ORD, FT, 0>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz);
 }
 
 // Guardrail baseline / large-F fallback: lane per entry, both rows read
@@ -451,7 +469,8 @@ bool aligned16(const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15
 
 // Fixed-width launch; false when (f, ft, alignment) is outside its shapes.
 bool launch_sddmm_fixed(Graph& g, const float* x, const float* y, std::uint32_t f, float* out,
-                        std::uint32_t ft, int ord, cudaStream_t s) {
+                        std::uint32_t ft, int ord, cudaStream_t s, const unsigned* finite) {
+    if (!dev_knob("AUTOSAGE_DEV_SDDMM_MIX", 1)) finite = nullptr;
     if (!(f == 16 || f == 32 || f == 64 || f == 128)) return false;
     if (!aligned16(x) || !aligned16(y)) return false;
     if (ord == 1 && !(ft == 32 || ft == 64 || ft == 128 || ft == f)) return false;
@@ -467,7 +486,7 @@ bool launch_sddmm_fixed(Graph& g, const float* x, const float* y, std::uint32_t 
         const unsigned blocks = unsigned(std::min<std::uint64_t>((n4 + 255) / 256, std::uint64_t(sms) * 8));
         if (n4) {
             widen_kernel<<<std::max(blocks, 1u), 256, 0, s>>>(reinterpret_cast<const float4*>(x),
-                                                              reinterpret_cast<double2*>(g.xwide.get()), n4);
+                                                              reinterpret_cast<double2*>(g.xwide.get()), n4, finite);
             check_launch("widen_kernel");
         }
     }
@@ -482,7 +501,7 @@ bool launch_sddmm_fixed(Graph& g, const float* x, const float* y, std::uint32_t 
         const std::uint64_t cap = std::uint64_t(sms) * std::max(per_sm, 1);
         const unsigned blocks = unsigned(std::max<std::uint64_t>(1, std::min(want, cap)));
         kernel<<<blocks, kWarps * 32, smem, s>>>(g.rowptr.get(), g.colind.get(), g.chunk_row.get(),
-                                                 g.n_rows, g.xwide.get(), y, out, g.nnz);
+                                                 g.n_rows, g.xwide.get(), y, out, g.nnz, finite);
         check_launch("sddmm_fixed_kernel");
     };
     auto by_f = [&](auto fc) {
@@ -529,7 +548,7 @@ void launch_sddmm_chunks(Graph& g, const float* x, const float* y, std::uint32_t
         return;
     }
     if (dev_knob("AUTOSAGE_DEV_SDDMM_FIXED", 1) &&
-        launch_sddmm_fixed(g, x, y, f, out, ft, ord, s))
+        launch_sddmm_fixed(g, x, y, f, out, ft, ord, s, finite))
         return;
     const bool vload = vec;  // vec4 gate already applied by dispatch
     const bool vlds = vload && (ord == 0 || ft % 4 == 0);

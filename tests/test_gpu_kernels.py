@@ -188,6 +188,52 @@ def test_sddmm_every_variant_bit_exact_vs_oracle(f):
                     assert bit_equal(got, want), (mapping, ft, rpc, vec, n_bit_diff(got, want))
 
 
+@pytest.mark.parametrize("f", [16, 32, 64, 128])
+def test_sddmm_special_values_bit_exact(f):
+    """Zeros, subnormals, huge magnitudes (exercise the ALU re-bias widening
+    when Y is finite), then inf/NaN in X and in Y (the all-F2F path)."""
+    rng = np.random.default_rng(40 + f)
+    p = hub_graph(rng, 500, [480, 200], 6, with_values=False)
+    x, y = random_dense(rng, 500, f), random_dense(rng, 500, f)
+    y[::7, ::3] = 0.0
+    y[1::5, 2::4] = np.float32(1e-41)  # subnormal
+    y[2::9, 3::4] = np.float32(-3.0e38)
+    x[::11, 2::4] = np.float32(2.5e38)
+    x[3::13, ::5] = np.float32(-1e-40)
+    g = asb.Graph.from_csr(p)
+    cases = [(x, y)]
+    x2 = x.copy()
+    x2[4, 1] = np.inf
+    cases.append((x2, y))
+    y2 = y.copy()
+    y2[5, 2], y2[9, 3] = np.nan, -np.inf
+    cases.append((x, y2))
+    for xx, yy in cases:
+        for vec, ft in ((False, 64), (True, 32), (True, 64)):
+            got = asb.dispatch(V(SD, RP, ft, 4, vec), g, cuda(xx), cuda(yy)).values.cpu().numpy()
+            want = oracle.sddmm(p, xx, yy, ft, vec)
+            assert np.array_equal(np.isnan(got), np.isnan(want))
+            assert bit_equal(np.nan_to_num(got), np.nan_to_num(want)), (vec, ft)
+
+
+def test_sddmm_chunks_spanning_many_rows():
+    """Degree-0/1/2 rows: one 32-entry chunk meets more than 32 rows."""
+    rng = np.random.default_rng(44)
+    n = 3000
+    deg = rng.choice([0, 1, 1, 2], size=n).astype(np.int64)
+    deg[1500] = 700
+    rp = np.zeros(n + 1, np.uint64)
+    rp[1:] = np.cumsum(deg)
+    cols = np.concatenate([np.sort(rng.choice(n, size=d, replace=False)) for d in deg]).astype(np.uint32)
+    p = asb.CsrMatrix(n, n, rp, cols, None)
+    g = asb.Graph.from_csr(p)
+    for f in (32, 64):
+        x, y = random_dense(rng, n, f), random_dense(rng, n, f)
+        for vec in (False, True):
+            got = asb.dispatch(V(SD, RP, 64, 4, vec), g, cuda(x), cuda(y)).values.cpu().numpy()
+            assert bit_equal(got, oracle.sddmm(p, x, y, 64, vec)), (f, vec)
+
+
 def test_sddmm_vec_and_scalar_stay_close():
     rng = np.random.default_rng(13)
     p = random_csr(rng, 70, 50, 9, with_values=False)
