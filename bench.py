@@ -273,7 +273,11 @@ def run_ours(args):
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
     cache = asb.ScheduleCache()
-    ctx = asb.ScheduleContext(cache=cache, stream=asb.torch_stream_handle(dev))
+    if args.cache and os.path.exists(args.cache):
+        cache.load(args.cache)  # deterministic replay of an earlier run's decisions
+    ctx = asb.ScheduleContext(cache=cache, stream=asb.torch_stream_handle(dev),
+                              replay=asb.ReplayPolicy(replay_only=args.replay_only,
+                                                      strict=args.replay_only))
     cfg = asb.ProbeConfig.from_env()
     cctx, keep = ctx.to_c()
     ccfg = cfg.to_c()
@@ -305,6 +309,8 @@ def run_ours(args):
     cold_ms = (time.perf_counter() - t0) * 1e3
     dec_spmm = asb.ScheduleDecision.from_c(d_spmm)
     dec_sddmm = asb.ScheduleDecision.from_c(d_sddmm)
+    if args.cache and rank == 0 and not args.replay_only:
+        cache.store(args.cache)
 
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
 
@@ -394,6 +400,8 @@ def run_ours(args):
                        "l2": "flushed between steps (256 MiB write, untimed)",
                        "spmm_choice": dec_spmm.choice_string(),
                        "sddmm_choice": dec_sddmm.choice_string(),
+                       "decision_source": {"spmm": dec_spmm.source_name,
+                                           "sddmm": dec_sddmm.source_name},
                        "probe": dataclasses_asdict(cfg)},
             "ms_per_op": {"spmm": t_spmm / K, "sddmm": t_sddmm / K, "allgather": t_gather / K},
             "pct_of_8TBs": value / 8000.0 * 100.0,
@@ -466,6 +474,9 @@ def main():
     ap.add_argument("--cpu-sample-step", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cache", default="", help="schedule cache file: load if present, store after decide")
+    ap.add_argument("--replay-only", action="store_true",
+                    help="decisions must come from --cache (strict replay, no probes)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

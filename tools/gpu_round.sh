@@ -14,7 +14,8 @@ timeout 900 python -m pytest tests -m gpu -q > $out/pytest_gpu_$tag.log 2>&1
 echo "pytest rc=$?" | tee -a $out/status_$tag.txt
 tail -3 $out/pytest_gpu_$tag.log
 
-timeout 900 python bench.py --config $cfg > $out/bench_$tag.json 2> $out/bench_$tag.err
+rm -f $out/sched_$tag.cache
+timeout 900 python bench.py --config $cfg --cache $out/sched_$tag.cache > $out/bench_$tag.json 2> $out/bench_$tag.err
 echo "bench rc=$?" | tee -a $out/status_$tag.txt
 timeout 900 python bench.py --impl reference --config $cfg --steps 2 --warmup 3 > $out/bench_ref_$tag.json 2> $out/bench_ref_$tag.err
 echo "bench_ref rc=$?" | tee -a $out/status_$tag.txt
@@ -22,7 +23,7 @@ echo "bench_ref rc=$?" | tee -a $out/status_$tag.txt
 # launch list of the same bench command (cold-cache, serialised per launch)
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $out/launches_$tag.csv python bench.py --config $cfg --steps 3 --warmup 3 \
-    --no-e2e --no-cpu > $out/ncu_launch_$tag.log 2>&1
+    --no-e2e --no-cpu --cache $out/sched_$tag.cache --replay-only > $out/ncu_launch_$tag.log 2>&1
 echo "ncu_launch rc=$?" | tee -a $out/status_$tag.txt
 
 spmm=$(python -c "import json;print(json.load(open('$out/bench_$tag.json'))['config']['spmm_choice'])" 2>/dev/null)
