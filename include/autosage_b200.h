@@ -185,6 +185,17 @@ as_status as_sddmm_host(const as_variant* v, as_graph pattern, const float* x_ho
                         uint64_t x_rows, const float* y_host, uint64_t y_rows, uint64_t f,
                         float* out_host, as_kernel_result* res);
 as_status as_row_softmax_host(as_graph m, const float* vals_host, float* out_host);
+/* Asynchronous host-buffer forms: queue H2D, kernels and D2H on the graph's
+ * pipeline streams and return; results are in the host buffers after
+ * as_graph_synchronize().  Host buffers should be pinned (as_host_alloc) and
+ * must stay valid until then.  An SpMM and an SDDMM on the same graph may be
+ * in flight together (separate staging); calls of one op are ordered. */
+as_status as_spmm_host_async(const as_variant* v, as_graph a, const float* b_host, uint64_t b_rows,
+                             uint64_t f, float* c_host, as_kernel_result* res);
+as_status as_sddmm_host_async(const as_variant* v, as_graph pattern, const float* x_host,
+                              uint64_t x_rows, const float* y_host, uint64_t y_rows, uint64_t f,
+                              float* out_host, as_kernel_result* res);
+as_status as_graph_synchronize(as_graph g);
 
 /* ------------------------------------------------------------------ */
 /* Device profile -- include/autosage/device.hpp:12-27                  */

@@ -236,6 +236,10 @@ class Graph:
                                     m.n_rows, m.n_cols, m.nnz, device, C.byref(h)))
         return Graph(h.value, device)
 
+    def synchronize(self) -> None:
+        """Wait for every queued host-buffer operation (as_graph_synchronize)."""
+        _check(_lib.as_graph_synchronize(self._h))
+
     def close(self) -> None:
         if self._h:
             _lib.as_graph_destroy(self._h)
@@ -531,6 +535,23 @@ def _spmm_call(v, a, b, result: bool):
     finally:
         if own:
             g.close()
+
+
+def spmm_host_async(v: Optional[KernelVariant], g: "Graph", b: np.ndarray, c: np.ndarray) -> None:
+    """Queue H2D(b) -> SpMM -> D2H(c) on the graph's pipeline and return
+    (as_spmm_host_async); c is valid after g.synchronize().  b and c should
+    be pinned (e.g. torch.empty(..., pin_memory=True).numpy())."""
+    res = _c.as_kernel_result()
+    _check(_lib.as_spmm_host_async(_variant_arg(v), g.handle, _ptr(b), b.shape[0], b.shape[1],
+                                   _ptr(c), C.byref(res)))
+
+
+def sddmm_host_async(v: Optional[KernelVariant], g: "Graph", x: np.ndarray, y: np.ndarray,
+                     out: np.ndarray) -> None:
+    """Queue H2D(x, y) -> SDDMM (in slices) -> D2H(out) (as_sddmm_host_async)."""
+    res = _c.as_kernel_result()
+    _check(_lib.as_sddmm_host_async(_variant_arg(v), g.handle, _ptr(x), x.shape[0], _ptr(y),
+                                    y.shape[0], x.shape[1], _ptr(out), C.byref(res)))
 
 
 def spmm_baseline(a, b):

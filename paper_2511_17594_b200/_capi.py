@@ -143,6 +143,9 @@ _proto("as_row_softmax", st, vp, vp, vp, vp)
 _proto("as_spmm_host", st, P(as_variant), vp, vp, u64, u64, vp, P(as_kernel_result))
 _proto("as_sddmm_host", st, P(as_variant), vp, vp, u64, vp, u64, u64, vp, P(as_kernel_result))
 _proto("as_row_softmax_host", st, vp, vp, vp)
+_proto("as_spmm_host_async", st, P(as_variant), vp, vp, u64, u64, vp, P(as_kernel_result))
+_proto("as_sddmm_host_async", st, P(as_variant), vp, vp, u64, vp, u64, u64, vp, P(as_kernel_result))
+_proto("as_graph_synchronize", st, vp)
 _proto("as_device_profile_gpu", st, C.c_int, P(as_device_profile))
 _proto("as_device_profile_fixed", None, dbl, dbl, u64, cp, P(as_device_profile))
 _proto("as_estimate_cost", st, P(as_variant), P(as_features), u64, P(as_device_profile),
@@ -200,7 +203,8 @@ EXPORTED = [
     "as_graph_features", "as_sample_row_indices", "as_slice_rows", "as_graph_download",
     "as_spmm", "as_spmm_rowparallel", "as_spmm_hubsplit", "as_sddmm", "as_sddmm_rowparallel",
     "as_row_softmax",
-    "as_spmm_host", "as_sddmm_host", "as_row_softmax_host", "as_device_profile_gpu",
+    "as_spmm_host", "as_sddmm_host", "as_row_softmax_host", "as_spmm_host_async",
+    "as_sddmm_host_async", "as_graph_synchronize", "as_device_profile_gpu",
     "as_device_profile_fixed", "as_estimate_cost", "as_shortlist", "as_time_kernel",
     "as_cache_create", "as_cache_destroy", "as_cache_get", "as_cache_put", "as_cache_size",
     "as_cache_snapshot", "as_cache_clear", "as_cache_load", "as_cache_store",

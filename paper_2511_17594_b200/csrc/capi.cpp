@@ -394,69 +394,37 @@ as_status as_row_softmax(as_graph m, const float* vals_dev, float* out_dev, void
     });
 }
 
-// Host-buffer forms: stage through per-graph device buffers on the graph's
-// stream; H2D, kernel, D2H, then synchronize.
+// Host-buffer forms (engine.cpp host pipeline): H2D on the graph's copy-in
+// stream, kernels on its stream, D2H on its copy-out stream; the SDDMM
+// values come back in slices that overlap the remaining kernels.
 as_status as_spmm_host(const as_variant* v, as_graph a, const float* b_host, uint64_t b_rows,
                        uint64_t f, float* c_host, as_kernel_result* res) {
-    return guard([&] {
-        Graph& g = G(a);
-        DeviceGuard dg(g.device);
-        if (g.n_cols != b_rows) throw InvalidArgument("spmm: a.n_cols != b.n_rows");
-        g.stage_in.ensure(std::max<std::uint64_t>(b_rows * f, 1));
-        g.stage_out.ensure(std::max<std::uint64_t>(g.n_rows * f, 1));
-        if (b_rows * f != 0)
-            ASB_CUDA(cudaMemcpyAsync(g.stage_in.get(), b_host, b_rows * f * 4, cudaMemcpyHostToDevice,
-                                     g.stream));
-        KernelResult r;
-        if (v) {
-            r = dispatch_spmm(*v, g, nullptr, g.stage_in.get(), b_rows, f, g.stage_out.get(), g.stream,
-                              false);
-        } else {
-            r.variant = default_variant();
-            r.variant.mapping = AS_MAP_BASELINE;
-            spmm_baseline(g, graph_values(g, nullptr), g.stage_in.get(), b_rows, f, g.stage_out.get(),
-                          g.stream);
-        }
-        if (g.n_rows * f != 0)
-            ASB_CUDA(cudaMemcpyAsync(c_host, g.stage_out.get(), g.n_rows * f * 4,
-                                     cudaMemcpyDeviceToHost, g.stream));
-        ASB_CUDA(cudaStreamSynchronize(g.stream));
-        fill_result(res, r);
-    });
+    return guard([&] { fill_result(res, spmm_host(v, G(a), b_host, b_rows, f, c_host, true)); });
 }
 
 as_status as_sddmm_host(const as_variant* v, as_graph pattern, const float* x_host, uint64_t x_rows,
                         const float* y_host, uint64_t y_rows, uint64_t f, float* out_host,
                         as_kernel_result* res) {
     return guard([&] {
-        Graph& g = G(pattern);
-        DeviceGuard dg(g.device);
-        g.stage_in.ensure(std::max<std::uint64_t>(x_rows * f, 1));
-        g.stage_in2.ensure(std::max<std::uint64_t>(y_rows * f, 1));
-        g.stage_out.ensure(std::max<std::uint64_t>(g.nnz, 1));
-        if (x_rows * f != 0)
-            ASB_CUDA(cudaMemcpyAsync(g.stage_in.get(), x_host, x_rows * f * 4, cudaMemcpyHostToDevice,
-                                     g.stream));
-        if (y_rows * f != 0)
-            ASB_CUDA(cudaMemcpyAsync(g.stage_in2.get(), y_host, y_rows * f * 4, cudaMemcpyHostToDevice,
-                                     g.stream));
-        KernelResult r;
-        if (v) {
-            r = dispatch_sddmm(*v, g, g.stage_in.get(), x_rows, g.stage_in2.get(), y_rows, f,
-                               g.stage_out.get(), g.stream, false);
-        } else {
-            r.variant = default_variant();
-            r.variant.op = AS_OP_SDDMM;
-            r.variant.mapping = AS_MAP_BASELINE;
-            sddmm_baseline(g, g.stage_in.get(), x_rows, g.stage_in2.get(), y_rows, f, g.stage_out.get(),
-                           g.stream);
-        }
-        if (g.nnz)
-            ASB_CUDA(cudaMemcpyAsync(out_host, g.stage_out.get(), g.nnz * 4, cudaMemcpyDeviceToHost,
-                                     g.stream));
-        ASB_CUDA(cudaStreamSynchronize(g.stream));
-        fill_result(res, r);
+        fill_result(res, sddmm_host(v, G(pattern), x_host, x_rows, y_host, y_rows, f, out_host, true));
     });
+}
+
+as_status as_spmm_host_async(const as_variant* v, as_graph a, const float* b_host, uint64_t b_rows,
+                             uint64_t f, float* c_host, as_kernel_result* res) {
+    return guard([&] { fill_result(res, spmm_host(v, G(a), b_host, b_rows, f, c_host, false)); });
+}
+
+as_status as_sddmm_host_async(const as_variant* v, as_graph pattern, const float* x_host,
+                              uint64_t x_rows, const float* y_host, uint64_t y_rows, uint64_t f,
+                              float* out_host, as_kernel_result* res) {
+    return guard([&] {
+        fill_result(res, sddmm_host(v, G(pattern), x_host, x_rows, y_host, y_rows, f, out_host, false));
+    });
+}
+
+as_status as_graph_synchronize(as_graph g) {
+    return guard([&] { host_synchronize(G(g)); });
 }
 
 as_status as_row_softmax_host(as_graph m, const float* vals_host, float* out_host) {

@@ -344,6 +344,139 @@ KernelResult dispatch_sddmm(const as_variant& v, Graph& p, const float* x, std::
     return r;
 }
 
+// ---- host-buffer pipeline ------------------------------------------------------------
+namespace {
+
+void ensure_pipe(Graph& g) {
+    auto& P = g.pipe;
+    if (P.h2d) return;
+    ASB_CUDA(cudaStreamCreateWithFlags(&P.h2d, cudaStreamNonBlocking));
+    ASB_CUDA(cudaStreamCreateWithFlags(&P.d2h, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&P.spmm_in, &P.spmm_done, &P.spmm_out, &P.sddmm_in, &P.sddmm_done,
+                           &P.sddmm_out})
+        ASB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+}
+
+void ensure_slices(Graph& g, std::size_t k) {
+    while (g.pipe.slice.size() < k) {
+        cudaEvent_t e;
+        ASB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        g.pipe.slice.push_back(e);
+    }
+}
+
+std::uint64_t host_slices() {
+    const auto k = env::get_int("AUTOSAGE_HOST_SLICES");
+    return k && *k > 0 ? std::uint64_t(*k) : 8;
+}
+
+}  // namespace
+
+KernelResult spmm_host(const as_variant* v, Graph& g, const float* b_host, std::uint64_t b_rows,
+                       std::uint64_t f, float* c_host, bool sync) {
+    check_spmm_dims(g, b_rows);
+    DeviceGuard dg(g.device);
+    ensure_pipe(g);
+    auto& P = g.pipe;
+    P.b.ensure(std::max<std::uint64_t>(b_rows * f, 1));
+    P.c.ensure(std::max<std::uint64_t>(g.n_rows * f, 1));
+    // the previous SpMM's kernel must have finished reading the staging B
+    ASB_CUDA(cudaStreamWaitEvent(P.h2d, P.spmm_done, 0));
+    if (b_rows * f)
+        ASB_CUDA(cudaMemcpyAsync(P.b.get(), b_host, b_rows * f * 4, cudaMemcpyHostToDevice, P.h2d));
+    ASB_CUDA(cudaEventRecord(P.spmm_in, P.h2d));
+    ASB_CUDA(cudaStreamWaitEvent(g.stream, P.spmm_in, 0));
+    ASB_CUDA(cudaStreamWaitEvent(g.stream, P.spmm_out, 0));  // staging C free again
+    KernelResult r;
+    if (v) {
+        r = dispatch_spmm(*v, g, nullptr, P.b.get(), b_rows, f, P.c.get(), g.stream, false);
+    } else {
+        r.variant = default_variant();
+        r.variant.mapping = AS_MAP_BASELINE;
+        launch_spmm_baseline(g, graph_values(g, nullptr), P.b.get(), std::uint32_t(f), P.c.get(), g.stream);
+    }
+    ASB_CUDA(cudaEventRecord(P.spmm_done, g.stream));
+    ASB_CUDA(cudaStreamWaitEvent(P.d2h, P.spmm_done, 0));
+    if (g.n_rows * f)
+        ASB_CUDA(cudaMemcpyAsync(c_host, P.c.get(), g.n_rows * f * 4, cudaMemcpyDeviceToHost, P.d2h));
+    ASB_CUDA(cudaEventRecord(P.spmm_out, P.d2h));
+    if (sync) ASB_CUDA(cudaEventSynchronize(P.spmm_out));
+    return r;
+}
+
+KernelResult sddmm_host(const as_variant* v, Graph& g, const float* x_host, std::uint64_t x_rows,
+                        const float* y_host, std::uint64_t y_rows, std::uint64_t f, float* out_host,
+                        bool sync) {
+    check_sddmm_dims(g, x_rows, y_rows);
+    DeviceGuard dg(g.device);
+    ensure_pipe(g);
+    ensure_chunk_rows(g);
+    auto& P = g.pipe;
+    KernelResult r;
+    if (v) {
+        if (v->op != AS_OP_SDDMM)
+            throw InvalidArgument("dispatch: sddmm operands given to a non-sddmm variant");
+        r.variant = apply_env_overrides(*v);
+        check_variant(r.variant);
+    } else {
+        r.variant = default_variant();
+        r.variant.op = AS_OP_SDDMM;
+        r.variant.mapping = AS_MAP_BASELINE;
+    }
+    P.x.ensure(std::max<std::uint64_t>(x_rows * f, 1));
+    P.y.ensure(std::max<std::uint64_t>(y_rows * f, 1));
+    P.v.ensure(std::max<std::uint64_t>(g.nnz, 1));
+    ASB_CUDA(cudaStreamWaitEvent(P.h2d, P.sddmm_done, 0));
+    if (x_rows * f)
+        ASB_CUDA(cudaMemcpyAsync(P.x.get(), x_host, x_rows * f * 4, cudaMemcpyHostToDevice, P.h2d));
+    if (y_rows * f)
+        ASB_CUDA(cudaMemcpyAsync(P.y.get(), y_host, y_rows * f * 4, cudaMemcpyHostToDevice, P.h2d));
+    ASB_CUDA(cudaEventRecord(P.sddmm_in, P.h2d));
+    ASB_CUDA(cudaStreamWaitEvent(g.stream, P.sddmm_in, 0));
+    ASB_CUDA(cudaStreamWaitEvent(g.stream, P.sddmm_out, 0));
+
+    const float *x = P.x.get(), *y = P.y.get();
+    float* out = P.v.get();
+    const void* bases[2] = {x, y};
+    const bool vec = r.variant.vectorized && vec4_eligible(f, bases, 2);
+    r.vectorized_path = vec && r.variant.mapping != AS_MAP_BASELINE;
+    const std::uint64_t n_chunks = (g.nnz + 31) / 32;
+    const std::uint64_t k = std::max<std::uint64_t>(1, std::min(host_slices(), n_chunks));
+    const std::uint64_t per = (n_chunks + k - 1) / std::max<std::uint64_t>(k, 1);
+    ensure_slices(g, std::size_t(k));
+    const unsigned* fin = nullptr;
+    const std::uint32_t wpb = std::uint32_t(std::min<std::uint64_t>(r.variant.rows_per_chunk, 16));
+    if (r.variant.mapping != AS_MAP_BASELINE) {
+        fin = finite_flag(g, y, y_rows * f, g.stream);
+        sddmm_chunks_prepare(g, x, y, std::uint32_t(f), r.variant.f_tile, vec, g.stream, fin);
+    }
+    for (std::uint64_t i = 0; i < k && n_chunks; ++i) {
+        const std::uint64_t c0 = i * per, c1 = std::min(n_chunks, c0 + per);
+        if (c0 >= c1) break;
+        if (r.variant.mapping == AS_MAP_BASELINE)
+            launch_sddmm_baseline(g, x, y, std::uint32_t(f), out, g.stream, c0, c1);
+        else
+            launch_sddmm_chunks(g, x, y, std::uint32_t(f), out, r.variant.f_tile, vec, wpb, g.stream, fin, c0,
+                                c1, false);
+        ASB_CUDA(cudaEventRecord(P.slice[i], g.stream));
+        ASB_CUDA(cudaStreamWaitEvent(P.d2h, P.slice[i], 0));
+        const std::uint64_t e0 = c0 * 32, e1 = std::min(c1 * 32, g.nnz);
+        ASB_CUDA(cudaMemcpyAsync(out_host + e0, out + e0, (e1 - e0) * 4, cudaMemcpyDeviceToHost, P.d2h));
+    }
+    ASB_CUDA(cudaEventRecord(P.sddmm_done, g.stream));
+    ASB_CUDA(cudaStreamWaitEvent(P.d2h, P.sddmm_done, 0));
+    ASB_CUDA(cudaEventRecord(P.sddmm_out, P.d2h));
+    if (sync) ASB_CUDA(cudaEventSynchronize(P.sddmm_out));
+    return r;
+}
+
+void host_synchronize(Graph& g) {
+    DeviceGuard dg(g.device);
+    if (g.pipe.d2h) ASB_CUDA(cudaStreamSynchronize(g.pipe.d2h));
+    if (g.pipe.h2d) ASB_CUDA(cudaStreamSynchronize(g.pipe.h2d));
+    ASB_CUDA(cudaStreamSynchronize(g.stream));
+}
+
 void row_softmax(Graph& m, const float* vin, float* vout, cudaStream_t s) {
     if (m.nnz > 0 && vin == nullptr) throw InvalidArgument("row_softmax: values required");
     DeviceGuard dg(m.device);

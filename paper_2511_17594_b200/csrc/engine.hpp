@@ -44,6 +44,19 @@ KernelResult dispatch_sddmm(const as_variant& v, Graph& p, const float* x, std::
                             cudaStream_t s, bool timed);
 void row_softmax(Graph& m, const float* vin, float* vout, cudaStream_t s);
 
+// Host-buffer operators (the reference's by-value API).  Copies in on the
+// graph's h2d stream, kernels on its stream, copies out on its d2h stream;
+// SDDMM values leave in slices so the D2H overlaps the remaining kernels.
+// v == nullptr: baseline.  sync = false returns once everything is queued
+// (host buffers must stay valid -- and should be pinned -- until
+// host_synchronize()).
+KernelResult spmm_host(const as_variant* v, Graph& a, const float* b_host, std::uint64_t b_rows,
+                       std::uint64_t f, float* c_host, bool sync);
+KernelResult sddmm_host(const as_variant* v, Graph& p, const float* x_host, std::uint64_t x_rows,
+                        const float* y_host, std::uint64_t y_rows, std::uint64_t f,
+                        float* out_host, bool sync);
+void host_synchronize(Graph& g);
+
 // ScheduleContext (include/autosage/scheduler.hpp:61-69)
 struct Context {
     const as_device_profile* device = nullptr;  // nullptr: calibrated GPU profile

@@ -114,6 +114,16 @@ Graph::~Graph() {
     }
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
+    for (cudaStream_t q : {pipe.h2d, pipe.d2h}) {
+        if (q) {
+            cudaStreamSynchronize(q);
+            cudaStreamDestroy(q);
+        }
+    }
+    for (cudaEvent_t e : {pipe.spmm_in, pipe.spmm_done, pipe.spmm_out, pipe.sddmm_in, pipe.sddmm_done,
+                          pipe.sddmm_out})
+        if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : pipe.slice) cudaEventDestroy(e);
 }
 
 std::uint64_t rows_with_degree_at_least(Graph& g, std::uint64_t d) {

@@ -101,6 +101,19 @@ struct Graph {
     cudaStream_t aux = nullptr;        // fork/join stream for concurrent kernels
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
+    // host-buffer pipeline (as_*_host, as_*_host_async): copies in on h2d,
+    // kernels on `stream`, copies out on d2h; per-op staging so an SpMM and
+    // an SDDMM can be in flight together.
+    struct HostPipe {
+        cudaStream_t h2d = nullptr, d2h = nullptr;
+        DevBuf<float> b, c, x, y, v;
+        // per op: inputs landed / kernels done (staging readable again) /
+        // outputs copied (staging writable again)
+        cudaEvent_t spmm_in = nullptr, spmm_done = nullptr, spmm_out = nullptr;
+        cudaEvent_t sddmm_in = nullptr, sddmm_done = nullptr, sddmm_out = nullptr;
+        std::vector<cudaEvent_t> slice;  // SDDMM output slices
+    } pipe;
+
     ~Graph();
 };
 

@@ -27,11 +27,20 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const float* b, std::uint3
 // ---- SDDMM (src/kernels.cpp:336-429) -----------------------------------
 // order: 0 = sequential (scalar variants and the baseline), 1 = per-f_tile
 // four-way partial sums (vec variants, src/kernels.cpp:103-127).
+// [c_begin, c_end): range of 32-entry chunks (entries 32*c_begin ..
+// min(32*c_end, nnz)); the host-buffer pipeline launches slices of it so
+// that the D2H of each slice overlaps the next slice's kernel.
+constexpr std::uint64_t kAllChunks = ~0ull;
 void launch_sddmm_baseline(Graph& g, const float* x, const float* y, std::uint32_t f, float* out,
-                           cudaStream_t s);
+                           cudaStream_t s, std::uint64_t c_begin = 0, std::uint64_t c_end = kAllChunks);
+// prepare = run the per-call prepass (X widening of the fixed-width path);
+// slices after the first pass false (sddmm_chunks_prepare runs it alone).
 void launch_sddmm_chunks(Graph& g, const float* x, const float* y, std::uint32_t f, float* out,
                          std::uint64_t f_tile, bool vec, std::uint32_t wpb, cudaStream_t s,
-                         const unsigned* finite = nullptr);
+                         const unsigned* finite = nullptr, std::uint64_t c_begin = 0,
+                         std::uint64_t c_end = kAllChunks, bool prepare = true);
+void sddmm_chunks_prepare(Graph& g, const float* x, const float* y, std::uint32_t f,
+                          std::uint64_t f_tile, bool vec, cudaStream_t s, const unsigned* finite);
 
 // Device flag: 1 iff p[0..n) has no Inf/NaN (gates the re-bias widening,
 // widen.cuh).  Written into g.flag (one flag per graph; a graph handle runs

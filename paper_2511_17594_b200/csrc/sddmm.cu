@@ -163,8 +163,8 @@ template <bool VLOAD, int ORD, bool VLDS, int MIX, int NB>
 __device__ __forceinline__ void sddmm_chunk_body(
     const std::uint64_t* __restrict__ rowptr, const std::uint32_t* __restrict__ colind,
     const std::uint32_t* __restrict__ chunk_row, std::uint64_t n_rows, const float* __restrict__ x,
-    const float* __restrict__ y, float* __restrict__ out, std::uint64_t nnz, std::uint32_t f,
-    std::uint32_t S, std::uint32_t ft, char* wsm) {
+    const float* __restrict__ y, float* __restrict__ out, std::uint64_t nnz, std::uint64_t c_begin,
+    std::uint64_t c_end, std::uint32_t f, std::uint32_t S, std::uint32_t ft, char* wsm) {
     const int lane = threadIdx.x & 31;
     const std::uint64_t sbytes = stage_bytes(f, S);
     double* xd = reinterpret_cast<double*>(wsm + NB * sbytes);
@@ -178,7 +178,7 @@ __device__ __forceinline__ void sddmm_chunk_body(
 
     auto meta = [&](std::uint64_t c) {
         ChunkMeta m{0, 0, 0, 0, false};
-        if (c >= n_chunks) return m;
+        if (c >= c_end) return m;
         const std::uint64_t e = c * 32 + lane;
         m.valid = e < nnz;
         m.col = m.valid ? __ldg(colind + e) : 0u;
@@ -215,23 +215,23 @@ __device__ __forceinline__ void sddmm_chunk_body(
         }
     };
 
-    std::uint64_t c = std::uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    std::uint64_t c = c_begin + std::uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     ChunkMeta cur = meta(c);
     ChunkMeta nxt{};
     if constexpr (NB == 2) {
-        if (c < n_chunks) issue(cur, c, 0);
+        if (c < c_end) issue(cur, c, 0);
         asm volatile("cp.async.commit_group;\n" ::: "memory");
         nxt = meta(c + stride);
     }
     int b = 0;
-    for (; c < n_chunks; c += stride) {
+    for (; c < c_end; c += stride) {
         if constexpr (NB == 1) {
             issue(cur, c, 0);
             asm volatile("cp.async.commit_group;\n" ::: "memory");
             nxt = meta(c + stride);  // resolve the next chunk while the copies fly
             asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         } else {
-            if (c + stride < n_chunks) issue(nxt, c + stride, b ^ 1);
+            if (c + stride < c_end) issue(nxt, c + stride, b ^ 1);
             asm volatile("cp.async.commit_group;\n" ::: "memory");
             asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // chunk c landed
         }
@@ -269,14 +269,17 @@ __global__ void __launch_bounds__(512)
                        const std::uint32_t* __restrict__ colind,
                        const std::uint32_t* __restrict__ chunk_row, std::uint64_t n_rows,
                        const float* __restrict__ x, const float* __restrict__ y,
-                       float* __restrict__ out, std::uint64_t nnz, std::uint32_t f, std::uint32_t S,
-                       std::uint32_t ft, const unsigned* __restrict__ finite, int allow_mix) {
+                       float* __restrict__ out, std::uint64_t nnz, std::uint64_t c_begin,
+                       std::uint64_t c_end, std::uint32_t f, std::uint32_t S, std::uint32_t ft,
+                       const unsigned* __restrict__ finite, int allow_mix) {
     extern __shared__ __align__(16) char smem[];
     char* wsm = smem + std::uint64_t(threadIdx.x >> 5) * warp_slice_bytes(f, S, NB);
     if (VLDS && allow_mix && finite && *finite)
-        sddmm_chunk_body<VLOAD, ORD, VLDS, 1, NB>(rowptr, colind, chunk_row, n_rows, x, y, out, nnz, f, S, ft, wsm);
+        sddmm_chunk_body<VLOAD, ORD, VLDS, 1, NB>(rowptr, colind, chunk_row, n_rows, x, y, out, nnz, c_begin,
+                                                  c_end, f, S, ft, wsm);
     else
-        sddmm_chunk_body<VLOAD, ORD, VLDS, 0, NB>(rowptr, colind, chunk_row, n_rows, x, y, out, nnz, f, S, ft, wsm);
+        sddmm_chunk_body<VLOAD, ORD, VLDS, 0, NB>(rowptr, colind, chunk_row, n_rows, x, y, out, nnz, c_begin,
+                                                  c_end, f, S, ft, wsm);
 }
 
 // ---------------------------------------------------------------------------
@@ -366,7 +369,8 @@ __device__ __forceinline__ void sddmm_fixed_body(const std::uint64_t* __restrict
                                                  const std::uint32_t* __restrict__ chunk_row,
                                                  std::uint64_t n_rows, const double* __restrict__ xd,
                                                  const float* __restrict__ y, float* __restrict__ out,
-                                                 std::uint64_t nnz) {
+                                                 std::uint64_t nnz, std::uint64_t c_begin,
+                                                 std::uint64_t c_end) {
     using Sh = FixedShape<F>;
     extern __shared__ __align__(16) char smem[];
     char* wsm = smem + std::uint64_t(threadIdx.x >> 5) * Sh::kWarpBytes;
@@ -374,7 +378,6 @@ __device__ __forceinline__ void sddmm_fixed_body(const std::uint64_t* __restrict
     double* xs = reinterpret_cast<double*>(wsm + Sh::kYBytes);
     const std::uint64_t x_units = n_rows * F / 2;
     const int lane = threadIdx.x & 31;
-    const std::uint64_t n_chunks = (nnz + 31) / 32;
     const std::uint64_t stride = std::uint64_t(gridDim.x) * (blockDim.x >> 5);
 
     struct Meta {
@@ -383,7 +386,7 @@ __device__ __forceinline__ void sddmm_fixed_body(const std::uint64_t* __restrict
     };
     auto meta = [&](std::uint64_t c) {
         Meta m{0u, 0u, ~0ull};
-        if (c >= n_chunks) return m;
+        if (c >= c_end) return m;
         const std::uint64_t e = c * 32 + lane;
         m.col = e < nnz ? __ldg(colind + e) : 0u;  // row 0 stands in for the tail's copies
         m.r_first = __ldg(chunk_row + c);
@@ -392,9 +395,9 @@ __device__ __forceinline__ void sddmm_fixed_body(const std::uint64_t* __restrict
         return m;
     };
 
-    std::uint64_t c = std::uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    std::uint64_t c = c_begin + std::uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     Meta cur = meta(c);
-    for (; c < n_chunks; c += stride) {
+    for (; c < c_end; c += stride) {
         // 32 Y rows -> shared memory, 16-byte pieces, rows in lane order
 #pragma unroll
         for (int it = 0; it < Sh::kCopies; ++it) {
@@ -440,11 +443,12 @@ __global__ void __launch_bounds__(256, 3)
     sddmm_fixed_kernel(const std::uint64_t* __restrict__ rowptr, const std::uint32_t* __restrict__ colind,
                        const std::uint32_t* __restrict__ chunk_row, std::uint64_t n_rows,
                        const double* __restrict__ xd, const float* __restrict__ y,
-                       float* __restrict__ out, std::uint64_t nnz, const unsigned* __restrict__ finite) {
+                       float* __restrict__ out, std::uint64_t nnz, std::uint64_t c_begin,
+                       std::uint64_t c_end, const unsigned* __restrict__ finite) {
     if (finite && *finite)
-        sddmm_fixed_body<F, ORD, FT, 1>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz);
+        sddmm_fixed_body<F, ORD, FT, 1>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin, c_end);
     else
-        sddmm_fixed_body<F, ORD, FT, 0>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz);
+        sddmm_fixed_body<F, ORD, FT, 0>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin, c_end);
 }
 
 // Guardrail baseline / large-F fallback: lane per entry, both rows read
@@ -454,11 +458,11 @@ __global__ void sddmm_direct_kernel(const std::uint64_t* __restrict__ rowptr,
                                     const std::uint32_t* __restrict__ colind,
                                     const std::uint32_t* __restrict__ chunk_row,
                                     const float* __restrict__ x, const float* __restrict__ y,
-                                    float* __restrict__ out, std::uint64_t nnz, std::uint32_t f,
-                                    std::uint32_t ft) {
-    const std::uint64_t ch = (std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+                                    float* __restrict__ out, std::uint64_t nnz, std::uint64_t c_begin,
+                                    std::uint64_t c_end, std::uint32_t f, std::uint32_t ft) {
+    const std::uint64_t ch = c_begin + ((std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
     const std::uint64_t e = ch * 32 + (threadIdx.x & 31);
-    if (e >= nnz) return;
+    if (ch >= c_end || e >= nnz) return;
     const std::uint32_t r = row_of(rowptr, chunk_row[ch], e);
     const float* xr = x + std::uint64_t(r) * f;
     const float* yr = y + std::uint64_t(colind[e]) * f;
@@ -467,41 +471,47 @@ __global__ void sddmm_direct_kernel(const std::uint64_t* __restrict__ rowptr,
 
 bool aligned16(const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15u) == 0; }
 
-// Fixed-width launch; false when (f, ft, alignment) is outside its shapes.
-bool launch_sddmm_fixed(Graph& g, const float* x, const float* y, std::uint32_t f, float* out,
-                        std::uint32_t ft, int ord, cudaStream_t s, const unsigned* finite) {
-    if (!dev_knob("AUTOSAGE_DEV_SDDMM_MIX", 1)) finite = nullptr;
+// Fixed-width path applies to (f, ft, alignment)?
+bool fixed_eligible(const float* x, const float* y, std::uint32_t f, std::uint32_t ft, int ord) {
+    if (!dev_knob("AUTOSAGE_DEV_SDDMM_FIXED", 1)) return false;
     if (!(f == 16 || f == 32 || f == 64 || f == 128)) return false;
     if (!aligned16(x) || !aligned16(y)) return false;
-    if (ord == 1 && !(ft == 32 || ft == 64 || ft == 128 || ft == f)) return false;
+    return ord == 0 || ft == 32 || ft == 64 || ft == 128 || ft == f;
+}
+
+int sm_count() {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
 
-    // X widened to f64 once per call
+// X widened to f64 (prepass of the fixed path, once per call)
+void widen_x(Graph& g, const float* x, std::uint32_t f, cudaStream_t s, const unsigned* finite) {
     const std::uint64_t nx = g.n_rows * f;
-    g.xwide.ensure(nx);
-    {
-        const std::uint64_t n4 = nx / 4;
-        const unsigned blocks = unsigned(std::min<std::uint64_t>((n4 + 255) / 256, std::uint64_t(sms) * 8));
-        if (n4) {
-            widen_kernel<<<std::max(blocks, 1u), 256, 0, s>>>(reinterpret_cast<const float4*>(x),
-                                                              reinterpret_cast<double2*>(g.xwide.get()), n4, finite);
-            check_launch("widen_kernel");
-        }
-    }
-    const std::uint64_t n_chunks = (g.nnz + 31) / 32;
+    g.xwide.ensure(std::max<std::uint64_t>(nx, 1));
+    const std::uint64_t n4 = nx / 4;
+    if (!n4) return;
+    const unsigned blocks = unsigned(std::min<std::uint64_t>((n4 + 255) / 256, std::uint64_t(sm_count()) * 8));
+    widen_kernel<<<std::max(blocks, 1u), 256, 0, s>>>(reinterpret_cast<const float4*>(x),
+                                                      reinterpret_cast<double2*>(g.xwide.get()), n4, finite);
+    check_launch("widen_kernel");
+}
+
+void launch_sddmm_fixed(Graph& g, const float* y, std::uint32_t f, float* out, std::uint32_t ft, int ord,
+                        cudaStream_t s, const unsigned* finite, std::uint64_t c_begin, std::uint64_t c_end) {
+    const int sms = sm_count();
     auto go = [&](auto kernel, std::uint64_t warp_bytes) {
         constexpr int kWarps = 8;
         const std::size_t smem = std::size_t(warp_bytes * kWarps);
         ASB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         int per_sm = 1;
         ASB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kWarps * 32, smem));
-        const std::uint64_t want = (n_chunks + kWarps - 1) / kWarps;
+        const std::uint64_t want = (c_end - c_begin + kWarps - 1) / kWarps;
         const std::uint64_t cap = std::uint64_t(sms) * std::max(per_sm, 1);
         const unsigned blocks = unsigned(std::max<std::uint64_t>(1, std::min(want, cap)));
-        kernel<<<blocks, kWarps * 32, smem, s>>>(g.rowptr.get(), g.colind.get(), g.chunk_row.get(),
-                                                 g.n_rows, g.xwide.get(), y, out, g.nnz, finite);
+        kernel<<<blocks, kWarps * 32, smem, s>>>(g.rowptr.get(), g.colind.get(), g.chunk_row.get(), g.n_rows,
+                                                 g.xwide.get(), y, out, g.nnz, c_begin, c_end, finite);
         check_launch("sddmm_fixed_kernel");
     };
     auto by_f = [&](auto fc) {
@@ -518,86 +528,95 @@ bool launch_sddmm_fixed(Graph& g, const float* x, const float* y, std::uint32_t 
     case 64: by_f(std::integral_constant<int, 64>{}); break;
     default: by_f(std::integral_constant<int, 128>{}); break;
     }
-    return true;
+}
+
+void launch_direct(Graph& g, const float* x, const float* y, std::uint32_t f, std::uint32_t ft, int ord,
+                   float* out, cudaStream_t s, std::uint64_t c_begin, std::uint64_t c_end) {
+    const unsigned blocks = unsigned(((c_end - c_begin) * 32 + 255) / 256);
+    if (ord == 0)
+        sddmm_direct_kernel<0><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), g.chunk_row.get(), x, y,
+                                                      out, g.nnz, c_begin, c_end, f, ft);
+    else
+        sddmm_direct_kernel<1><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), g.chunk_row.get(), x, y,
+                                                      out, g.nnz, c_begin, c_end, f, ft);
+    check_launch("sddmm_direct_kernel");
 }
 
 } // namespace
 
 void launch_sddmm_baseline(Graph& g, const float* x, const float* y, std::uint32_t f, float* out,
-                           cudaStream_t s) {
+                           cudaStream_t s, std::uint64_t c_begin, std::uint64_t c_end) {
     if (g.nnz == 0) return;
     ensure_chunk_rows(g);
-    const std::uint64_t n_chunks = (g.nnz + 31) / 32;
-    const unsigned blocks = unsigned((n_chunks * 32 + 255) / 256);
-    sddmm_direct_kernel<0><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), g.chunk_row.get(),
-                                                  x, y, out, g.nnz, f, f ? f : 1);
-    check_launch("sddmm_direct_kernel");
+    c_end = std::min(c_end, (g.nnz + 31) / 32);
+    if (c_begin >= c_end) return;
+    launch_direct(g, x, y, f, f ? f : 1, 0, out, s, c_begin, c_end);
+}
+
+void sddmm_chunks_prepare(Graph& g, const float* x, const float* y, std::uint32_t f,
+                          std::uint64_t f_tile, bool vec, cudaStream_t s, const unsigned* finite) {
+    if (g.nnz == 0 || f == 0) return;
+    ensure_chunk_rows(g);
+    const std::uint32_t ft = std::uint32_t(effective_tile(f_tile, f));
+    if (fixed_eligible(x, y, f, ft, vec ? 1 : 0))
+        widen_x(g, x, f, s, dev_knob("AUTOSAGE_DEV_SDDMM_MIX", 1) ? finite : nullptr);
 }
 
 void launch_sddmm_chunks(Graph& g, const float* x, const float* y, std::uint32_t f, float* out,
                          std::uint64_t f_tile, bool vec, std::uint32_t wpb, cudaStream_t s,
-                         const unsigned* finite) {
+                         const unsigned* finite, std::uint64_t c_begin, std::uint64_t c_end,
+                         bool prepare) {
     if (g.nnz == 0) return;
     ensure_chunk_rows(g);
     const std::uint32_t ft = std::uint32_t(effective_tile(f_tile, f));
     const int ord = vec ? 1 : 0;
-    const std::uint64_t n_chunks = (g.nnz + 31) / 32;
+    c_end = std::min(c_end, (g.nnz + 31) / 32);
+    if (c_begin >= c_end) return;
     if (f == 0) {
         // empty dot products: the reference writes 0.0f for every entry
-        ASB_CUDA(cudaMemsetAsync(out, 0, g.nnz * 4, s));
+        const std::uint64_t e0 = c_begin * 32, e1 = std::min(c_end * 32, g.nnz);
+        ASB_CUDA(cudaMemsetAsync(out + e0, 0, (e1 - e0) * 4, s));
         return;
     }
-    if (dev_knob("AUTOSAGE_DEV_SDDMM_FIXED", 1) &&
-        launch_sddmm_fixed(g, x, y, f, out, ft, ord, s, finite))
+    if (fixed_eligible(x, y, f, ft, ord)) {
+        const unsigned* fin = dev_knob("AUTOSAGE_DEV_SDDMM_MIX", 1) ? finite : nullptr;
+        if (prepare) widen_x(g, x, f, s, fin);
+        launch_sddmm_fixed(g, y, f, out, ft, ord, s, fin, c_begin, c_end);
         return;
+    }
     const bool vload = vec;  // vec4 gate already applied by dispatch
     const bool vlds = vload && (ord == 0 || ft % 4 == 0);
     const std::uint32_t S = vload ? 4 * ((f / 4) | 1u) : (f | 1u);
-    const int nb = dev_knob("AUTOSAGE_DEV_SDDMM_NB", 1) == 2 ? 2 : 1;
     const int allow_mix = dev_knob("AUTOSAGE_DEV_SDDMM_MIX", 0);
-    const std::uint64_t per_warp = warp_slice_bytes(f, S, nb);
+    const std::uint64_t per_warp = warp_slice_bytes(f, S, 1);
     constexpr std::uint64_t kSmemMax = 200 * 1024;
     wpb = std::clamp<std::uint32_t>(wpb, 1, 16);
     while (wpb > 1 && per_warp * wpb > kSmemMax) --wpb;
     if (per_warp > kSmemMax) {
-        const unsigned blocks = unsigned((n_chunks * 32 + 255) / 256);
-        if (ord == 0)
-            sddmm_direct_kernel<0><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(),
-                                                          g.chunk_row.get(), x, y, out, g.nnz, f, ft);
-        else
-            sddmm_direct_kernel<1><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(),
-                                                          g.chunk_row.get(), x, y, out, g.nnz, f, ft);
-        check_launch("sddmm_direct_kernel");
+        launch_direct(g, x, y, f, ft, ord, out, s, c_begin, c_end);
         return;
     }
     const std::size_t smem = std::size_t(per_warp * wpb);
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-
+    const int sms = sm_count();
+    int per_sm = 1;
     auto go = [&](auto kernel) {
         ASB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         ASB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, int(wpb * 32), smem));
-        const std::uint64_t want = (n_chunks + wpb - 1) / wpb;
+        const std::uint64_t want = (c_end - c_begin + wpb - 1) / wpb;
         const std::uint64_t cap = std::uint64_t(sms) * std::max(per_sm, 1);
         const unsigned blocks = unsigned(std::max<std::uint64_t>(1, std::min(want, cap)));
         kernel<<<blocks, wpb * 32, smem, s>>>(g.rowptr.get(), g.colind.get(), g.chunk_row.get(), g.n_rows,
-                                              x, y, out, g.nnz, f, S, ft, finite, allow_mix);
+                                              x, y, out, g.nnz, c_begin, c_end, f, S, ft, finite, allow_mix);
         check_launch("sddmm_chunk_kernel");
     };
-    auto pick = [&](auto nbc) {
-        constexpr int NB = decltype(nbc)::value;
-        if (vload) {
-            if (ord == 0) go(sddmm_chunk_kernel<true, 0, true, NB>);
-            else if (vlds) go(sddmm_chunk_kernel<true, 1, true, NB>);
-            else go(sddmm_chunk_kernel<true, 1, false, NB>);
-        } else {
-            if (ord == 0) go(sddmm_chunk_kernel<false, 0, false, NB>);
-            else go(sddmm_chunk_kernel<false, 1, false, NB>);
-        }
-    };
-    if (nb == 2) pick(std::integral_constant<int, 2>{});
-    else pick(std::integral_constant<int, 1>{});
+    if (vload) {
+        if (ord == 0) go(sddmm_chunk_kernel<true, 0, true, 1>);
+        else if (vlds) go(sddmm_chunk_kernel<true, 1, true, 1>);
+        else go(sddmm_chunk_kernel<true, 1, false, 1>);
+    } else {
+        if (ord == 0) go(sddmm_chunk_kernel<false, 0, false, 1>);
+        else go(sddmm_chunk_kernel<false, 1, false, 1>);
+    }
 }
 
 } // namespace asb

@@ -393,3 +393,46 @@ def test_fused_attention_equals_unfused_bitwise():
     warm = asb.attention_probe_breakdown(p, q, k, v, asb.ProbeConfig(iters=2), ctx, fused=True)
     assert warm.sddmm_decision.source == asb.CACHED
     assert bit_equal(cold.output, warm.output)
+
+
+# ---- host-buffer pipeline (as_*_host, as_*_host_async) ------------------------------
+@pytest.mark.parametrize("slices", ["1", "3", "8", "1000000"])
+def test_sddmm_host_slices_bit_exact(monkeypatch, slices):
+    """The SDDMM values leave in slices of 32-entry chunks; every slicing
+    returns the same bytes (odd nnz, fixed-width and generic widths)."""
+    monkeypatch.setenv("AUTOSAGE_HOST_SLICES", slices)
+    rng = np.random.default_rng(51)
+    p = hub_graph(rng, 900, [850, 333, 70], 7, with_values=False)
+    assert p.nnz % 32 != 0
+    g = asb.Graph.from_csr(p)
+    for f in (64, 24):
+        x, y = random_dense(rng, 900, f), random_dense(rng, 900, f)
+        for v in (None, V(SD, RP, 64, 4, True), V(SD, HS, 32, 1, False)):
+            got = asb.sddmm_baseline(g, x, y) if v is None else asb.dispatch(v, g, x, y).values
+            want = oracle.sddmm(p, x, y, 64 if v is None else v.f_tile, v is not None and v.vectorized)
+            assert bit_equal(got, want), (f, v)
+
+
+def test_host_async_spmm_and_sddmm_in_flight_together():
+    """Several async SpMM + SDDMM calls queued on one graph before a single
+    synchronize: per-op staging and event ordering keep every result exact."""
+    import torch
+    rng = np.random.default_rng(52)
+    a = hub_graph(rng, 1200, [1100, 700, 90], 8)
+    g = asb.Graph.from_csr(a)
+    f = 32
+    pin = lambda arr: torch.from_numpy(arr).pin_memory().numpy()  # noqa: E731
+    bs = [pin(random_dense(rng, 1200, f)) for _ in range(3)]
+    xs = [pin(random_dense(rng, 1200, f)) for _ in range(3)]
+    ys = [pin(random_dense(rng, 1200, f)) for _ in range(3)]
+    cs = [pin(np.zeros((1200, f), np.float32)) for _ in range(3)]
+    outs = [pin(np.zeros(a.nnz, np.float32)) for _ in range(3)]
+    vs = V(SP, HS, 32, 4, True, 256)
+    vd = V(SD, RP, 32, 4, True)
+    for i in range(3):
+        asb.spmm_host_async(vs, g, bs[i], cs[i])
+        asb.sddmm_host_async(vd, g, xs[i], ys[i], outs[i])
+    g.synchronize()
+    for i in range(3):
+        assert bit_equal(cs[i], oracle.spmm_hubsplit(a, bs[i], 256))
+        assert bit_equal(outs[i], oracle.sddmm(a, xs[i], ys[i], 32, True))
