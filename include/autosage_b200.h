@@ -205,7 +205,10 @@ typedef struct {
     double bw_eff;    /* bytes/s */
     double flops_eff; /* FLOP/s  */
     uint64_t cores;   /* GPU: SM count */
+    int32_t model;    /* AS_MODEL_REFERENCE: proj/src/cost.cpp as is;
+                         AS_MODEL_B200: the GPU refinement (as_estimate_cost) */
 } as_device_profile;
+enum { AS_MODEL_REFERENCE = 0, AS_MODEL_B200 = 1 };
 /* DeviceProfile::host() re-targeted: calibrated once per device per process
  * (triad + FMA kernels, src/device.cpp:42-95 analogue). */
 as_status as_device_profile_gpu(int device, as_device_profile* out);

@@ -399,6 +399,7 @@ class DeviceProfile:
     bw_eff: float = 0.0
     flops_eff: float = 0.0
     cores: int = 1
+    model: int = 0  # 0: reference cost model, 1: B200 refinement (GPU profiles)
 
     @staticmethod
     def fixed(bw_eff: float, flops_eff: float, cores: int, sig_tag: str = "fixed"):
@@ -414,11 +415,11 @@ class DeviceProfile:
 
     @staticmethod
     def from_c(d) -> "DeviceProfile":
-        return DeviceProfile(d.device_sig.decode(), d.bw_eff, d.flops_eff, d.cores)
+        return DeviceProfile(d.device_sig.decode(), d.bw_eff, d.flops_eff, d.cores, d.model)
 
     def to_c(self) -> _c.as_device_profile:
         return _c.as_device_profile(self.device_sig.encode(), self.bw_eff, self.flops_eff,
-                                    self.cores)
+                                    self.cores, self.model)
 
 
 def estimate_cost(v: KernelVariant, gf: GraphFeatures, f: int, dp: DeviceProfile) -> float:

@@ -54,7 +54,7 @@ class as_features(C.Structure):
 
 class as_device_profile(C.Structure):
     _fields_ = [("device_sig", C.c_char * 256), ("bw_eff", dbl), ("flops_eff", dbl),
-                ("cores", u64)]
+                ("cores", u64), ("model", C.c_int32)]
 
 
 class as_timed_stats(C.Structure):

@@ -133,6 +133,7 @@ const as_device_profile& gpu_profile(int device) {
                   gpu_device_tag(device).c_str(), (unsigned long long)dp.cores, kArtifactVersion);
     dp.bw_eff = measure_gpu_bandwidth(device);
     dp.flops_eff = measure_gpu_flops(device);
+    dp.model = AS_MODEL_B200;
     return profiles.emplace(device, dp).first->second;
 }
 

@@ -135,6 +135,7 @@ as_decision decide_common(const Context& ctx, const as_probe_config& cfg,
 
     const as_features gf = hooks.features();
     auto candidates = shortlist(gf, f, op, dp);
+    if (dp.model == AS_MODEL_B200) candidates = distinct_gpu_configs(candidates, f);
     if (candidates.size() > std::size_t(cfg.top_k)) candidates.resize(std::size_t(cfg.top_k));
     const std::uint64_t sample_rows = hooks.prepare ? hooks.prepare() : 0;
 
@@ -270,8 +271,10 @@ void spmm_mapped(const as_variant& v, int expect_mapping, Graph& a, const float*
                                   : "spmm_hubsplit: variant mapping mismatch");
     DeviceGuard dg(a.device);
     const void* bases[1] = {b};
-    const bool vec = v.vectorized && vec4_eligible(f, bases, 1);
-    run_spmm_variant(v, a, graph_values(a, vals), b, f, c, s, vec);
+    // SpMM numerics do not depend on the vec flag (per-feature CSR order,
+    // src/kernels.cpp:63-80), so the kernels load float4 whenever the gate
+    // passes; `vectorized` only selects what the reference reports.
+    run_spmm_variant(v, a, graph_values(a, vals), b, f, c, s, vec4_eligible(f, bases, 1));
 }
 
 KernelResult dispatch_spmm(const as_variant& v, Graph& a, const float* vals, const float* b,
@@ -289,7 +292,7 @@ KernelResult dispatch_spmm(const as_variant& v, Graph& a, const float* vals, con
     if (r.variant.mapping == AS_MAP_ROWPARALLEL) ensure_order(a);
     if (r.variant.mapping == AS_MAP_HUBSPLIT) ensure_hub_plan(a, r.variant.hub_threshold);
     TimedRegion tr(s, timed);
-    run_spmm_variant(r.variant, a, graph_values(a, vals), b, f, c, s, vec);
+    run_spmm_variant(r.variant, a, graph_values(a, vals), b, f, c, s, vec4_eligible(f, bases, 1));
     r.elapsed_ms = tr.stop();
     r.vectorized_path = vec && r.variant.mapping != AS_MAP_BASELINE;
     return r;

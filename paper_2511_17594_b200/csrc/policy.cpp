@@ -256,6 +256,18 @@ double estimate_cost(const as_variant& v, const as_features& gf, std::uint64_t f
     else
         bytes = 8.0 * nnz + 4.0 * nnz * fd * 2.0 + 4.0 * nnz;
     const double flops = 2.0 * nnz * fd;
+    if (dp.model == AS_MODEL_B200) {
+        // B200 refinement (not in the reference): the sm_100a kernels re-read
+        // colind/val once per f_tile pass of SpMM; SDDMM runs the same
+        // balanced nnz-chunk kernel for both mappings (no imbalance term).
+        if (v.op == AS_OP_SPMM) {
+            const double ft = double(effective_tile(v.f_tile, f));
+            const double passes = std::ceil(fd / std::max(ft, 1.0));
+            bytes += 8.0 * nnz * (passes - 1.0);
+        } else {
+            return std::max(bytes / dp.bw_eff, flops / dp.flops_eff) * 1e3;
+        }
+    }
     const double seconds = std::max(bytes / dp.bw_eff, flops / dp.flops_eff);
     double penalty = 1.0;
     if (v.mapping != AS_MAP_HUBSPLIT) {
@@ -296,6 +308,28 @@ std::vector<as_variant> shortlist(const as_features& gf, std::uint64_t f, int op
     std::stable_sort(grid.begin(), grid.end(),
                      [&](const as_variant& a, const as_variant& b) { return rank(a) < rank(b); });
     return grid;
+}
+
+// B200: several reference variants compile to the same sm_100a launch (SpMM:
+// vec only selects the reported path and rows_per_chunk no longer sizes
+// anything; SDDMM: both mappings run the nnz-chunk kernel, and f_tile only
+// matters to the vec order).  Keep the first of each class in rank order so
+// the top_k probes compare distinct kernels.
+std::vector<as_variant> distinct_gpu_configs(const std::vector<as_variant>& ranked, std::uint64_t f) {
+    std::vector<as_variant> out;
+    std::vector<std::tuple<int, int, std::uint64_t, int, std::uint64_t>> seen;
+    for (const auto& v : ranked) {
+        const std::uint64_t ft = effective_tile(v.f_tile, f);
+        std::tuple<int, int, std::uint64_t, int, std::uint64_t> key;
+        if (v.op == AS_OP_SPMM)
+            key = {v.op, v.mapping, ft, 0, v.mapping == AS_MAP_HUBSPLIT ? v.hub_threshold : 0};
+        else
+            key = {v.op, 0, v.vectorized ? ft : 0, v.vectorized, 0};
+        if (std::find(seen.begin(), seen.end(), key) != seen.end()) continue;
+        seen.push_back(key);
+        out.push_back(v);
+    }
+    return out;
 }
 
 // ---- time_kernel, src/timing.cpp:22-61 -----------------------------------

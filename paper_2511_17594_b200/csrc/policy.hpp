@@ -26,6 +26,8 @@ double estimate_cost(const as_variant& v, const as_features& gf, std::uint64_t f
                      const as_device_profile& dp);
 std::vector<as_variant> shortlist(const as_features& gf, std::uint64_t f, int op,
                                   const as_device_profile& dp);
+// B200 model: drop variants that launch the same kernel as a better-ranked one.
+std::vector<as_variant> distinct_gpu_configs(const std::vector<as_variant>& ranked, std::uint64_t f);
 
 // ProbeTimer::time_once_ms (include/autosage/timing.hpp:10-15)
 using TimeOnce = std::function<double(const std::string&, const std::function<void()>&)>;

@@ -506,6 +506,19 @@ void launch_tuned(const SegArgs& a, unsigned blocks, unsigned threads, cudaStrea
     spmm_seg_kernel<VEC, LPR, NCH, HV, PC><<<blocks, threads, 0, s>>>(a);
 }
 
+// Warps per CTA of the lane-group kernels.  The reference's rows_per_chunk
+// (a CPU parallel_for grain) has no GPU meaning that changes results; one
+// CTA of 1 warp caps residency at 32 warps/SM and 16 warps gives coarse
+// tails, so every rpc runs 4 warps (measured best on Reddit-shape, see
+// DESIGN.md).  AUTOSAGE_DEV_SPMM_WPB overrides for experiments.
+std::uint32_t warps_per_cta(std::uint32_t /*rpc*/) {
+    static const int knob = [] {
+        const char* e = std::getenv("AUTOSAGE_DEV_SPMM_WPB");
+        return e ? std::atoi(e) : 0;
+    }();
+    return knob > 0 ? std::uint32_t(std::min(knob, 16)) : 4u;
+}
+
 template <int VEC, int LPR, int NCH>
 void launch_seg(const SegArgs& a, bool has_val, std::uint32_t wpb, cudaStream_t s) {
     constexpr int GPW = 32 / LPR;
@@ -629,7 +642,7 @@ void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uin
         a.n_tiles = t.n_tiles;
         a.f = f;
         a.tile_w = t.tile_w;
-        wpb = std::clamp<std::uint32_t>(wpb, 1, 16);
+        wpb = warps_per_cta(wpb);
         if (vec) launch_seg_vec<4>(a, val != nullptr, t.lanes, wpb, s);
         else launch_seg_vec<1>(a, val != nullptr, t.lanes, wpb, s);
     }
@@ -641,7 +654,7 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const float* b, std::uint3
                           std::uint64_t hub_threshold, cudaStream_t s, const unsigned* finite) {
     if (g.n_rows == 0 || f == 0) return;
     const HubPlan& plan = ensure_hub_plan(g, hub_threshold);
-    wpb = std::clamp<std::uint32_t>(wpb, 1, 16);
+    wpb = warps_per_cta(wpb);
     const TileShape t = tile_shape(f, f_tile, vec);
     if (plan.n_slots) g.scratch.ensure(plan.n_slots * f);
     if (plan.n_pieces) {
