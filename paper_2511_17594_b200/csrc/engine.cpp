@@ -17,6 +17,7 @@
 #include "ops.hpp"
 
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <limits>
@@ -488,6 +489,22 @@ void row_softmax(Graph& m, const float* vin, float* vout, cudaStream_t s) {
 
 // ---- scheduler ---------------------------------------------------------------
 
+// Probe sample rows.  The reference takes max(min_rows, ceil(frac*N))
+// (src/generate.cpp:134-181).  A 2% sample of a mid-size graph is a few
+// microseconds of GPU work -- launch latency, not the kernels -- so under the
+// B200 model the sample is raised until it holds about
+// AUTOSAGE_GPU_PROBE_NNZ (default 4M) entries at the graph's mean degree;
+// the row selection itself is unchanged.
+std::uint64_t probe_min_rows(const Graph& g, const as_probe_config& cfg, const as_device_profile& dp) {
+    std::uint64_t rows = cfg.min_rows;
+    if (dp.model != AS_MODEL_B200 || g.n_rows == 0 || g.nnz == 0) return rows;
+    const auto knob = env::get_int("AUTOSAGE_GPU_PROBE_NNZ");
+    const double want = knob && *knob > 0 ? double(*knob) : 4.0e6;
+    const double mean = double(g.nnz) / double(g.n_rows);
+    const auto need = std::uint64_t(std::ceil(want / std::max(mean, 1.0)));
+    return std::min<std::uint64_t>(g.n_rows, std::max(rows, need));
+}
+
 as_decision decide_spmm(const Context& ctx, const as_probe_config& cfg, Graph& a,
                         const float* vals, const float* b, std::uint64_t b_rows, std::uint64_t f) {
     if (a.n_cols != b_rows) throw InvalidArgument("decide_spmm: dimension mismatch");
@@ -498,8 +515,9 @@ as_decision decide_spmm(const Context& ctx, const as_probe_config& cfg, Graph& a
     ProbeHooks h;
     h.stream = s;
     h.features = [&] { return graph_features(a, kDefaultHubThreshold); };
+    const as_device_profile& dp = profile_for(ctx, a.device);
     h.prepare = [&]() -> std::uint64_t {
-        const auto rows = sample_row_indices(a, cfg.frac, cfg.min_rows);
+        const auto rows = sample_row_indices(a, cfg.frac, probe_min_rows(a, cfg, dp));
         sample = slice_rows(a, rows, graph_values(a, vals));
         ensure_order(*sample);
         cbuf.alloc(std::max<std::uint64_t>(rows.size() * f, 1));
@@ -511,7 +529,6 @@ as_decision decide_spmm(const Context& ctx, const as_probe_config& cfg, Graph& a
     h.run_candidate = [&](const as_variant& v) {
         dispatch_spmm(v, *sample, nullptr, b, b_rows, f, cbuf.get(), s, false);
     };
-    const as_device_profile& dp = profile_for(ctx, a.device);
     return decide_common(ctx, cfg, dp, [&] { return graph_sig(a); }, f, AS_OP_SPMM, h);
 }
 
@@ -528,8 +545,9 @@ as_decision decide_sddmm(const Context& ctx, const as_probe_config& cfg, Graph& 
     ProbeHooks h;
     h.stream = s;
     h.features = [&] { return graph_features(p, kDefaultHubThreshold); };
+    const as_device_profile& dp = profile_for(ctx, p.device);
     h.prepare = [&]() -> std::uint64_t {
-        const auto rows = sample_row_indices(p, cfg.frac, cfg.min_rows);
+        const auto rows = sample_row_indices(p, cfg.frac, probe_min_rows(p, cfg, dp));
         sample = slice_rows(p, rows, nullptr);  // SDDMM ignores pattern values
         ensure_chunk_rows(*sample);
         // the slice renumbers rows: gather the matching x rows (src/scheduler.cpp:214-220)
@@ -543,7 +561,6 @@ as_decision decide_sddmm(const Context& ctx, const as_probe_config& cfg, Graph& 
     h.run_candidate = [&](const as_variant& v) {
         dispatch_sddmm(v, *sample, xs.get(), ns, y, y_rows, f, obuf.get(), s, false);
     };
-    const as_device_profile& dp = profile_for(ctx, p.device);
     return decide_common(ctx, cfg, dp, [&] { return graph_sig(p); }, f, AS_OP_SDDMM, h);
 }
 
@@ -618,7 +635,8 @@ void attention_forward(const Context& ctx, const as_probe_config& cfg, Graph& pa
         h.features = [&] { return graph_features(pattern, kDefaultHubThreshold); };
         h.prepare = [&]() -> std::uint64_t {
             make_p();
-            const auto rows = sample_row_indices(pattern, cfg.frac, cfg.min_rows);
+            const auto rows = sample_row_indices(pattern, cfg.frac,
+                                                 probe_min_rows(pattern, cfg, profile_for(ctx, pattern.device)));
             sample = slice_rows(pattern, rows, p);
             ensure_order(*sample);
             cbuf.alloc(std::max<std::uint64_t>(rows.size() * fv, 1));

@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 namespace asb {
 
@@ -315,13 +316,37 @@ __host__ __device__ inline LongLayout long_layout(std::uint32_t f, std::uint32_t
     return L;
 }
 
-template <int MIX, bool HAS_VAL>
-__device__ __forceinline__ void longrow_body(const std::uint64_t* __restrict__ rowptr,
-                                             const std::uint32_t* __restrict__ colind,
-                                             const float* __restrict__ val,
-                                             const std::uint32_t* __restrict__ rows,
-                                             const float* __restrict__ b, float* __restrict__ c,
-                                             std::uint32_t f, std::uint32_t ch, char* smem) {
+template <int FPL>
+struct LongVec;
+template <>
+struct LongVec<1> {
+    using T = float;
+};
+template <>
+struct LongVec<2> {
+    using T = float2;
+};
+template <>
+struct LongVec<4> {
+    using T = float4;
+};
+__device__ __forceinline__ float long_comp(float v, int) { return v; }
+__device__ __forceinline__ float long_comp(float2 v, int i) { return i == 0 ? v.x : v.y; }
+__device__ __forceinline__ float long_comp(float4 v, int i) {
+    return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
+}
+
+// Row mode: item = a.rowlist[blockIdx.x]; piece mode: hub piece blockIdx.x,
+// written to its f64 partial slot (or straight to C when it is the row's
+// only piece) exactly like the lane-group piece path.
+template <int MIX, bool HAS_VAL, int FPL, bool PIECES>
+__device__ __forceinline__ void longrow_body(const SegArgs& A, std::uint32_t ch, char* smem) {
+    const std::uint64_t* __restrict__ rowptr = A.rowptr;
+    const std::uint32_t* __restrict__ colind = A.colind;
+    const float* __restrict__ val = A.val;
+    const float* __restrict__ b = A.b;
+    float* __restrict__ c = A.c;
+    const std::uint32_t f = A.f;
     constexpr int S = kLongStages;
     const LongLayout L = long_layout(f, ch);
     float* ring = reinterpret_cast<float*>(smem + L.ring_off);
@@ -332,9 +357,18 @@ __device__ __forceinline__ void longrow_body(const std::uint64_t* __restrict__ r
     std::uint64_t* empty = full + S;
     const std::uint32_t n_cons_warps = (blockDim.x >> 5) - 1;
 
-    const std::uint32_t row = rows[blockIdx.x];
-    const std::uint64_t e0 = rowptr[row];
-    const std::uint32_t deg = std::uint32_t(rowptr[row + 1] - e0);
+    std::uint32_t row, deg, slot = 0xffffffffu;
+    std::uint64_t e0;
+    if constexpr (PIECES) {
+        row = A.piece_row[blockIdx.x];
+        e0 = A.piece_e0[blockIdx.x];
+        deg = A.piece_len[blockIdx.x];
+        slot = A.piece_slot[blockIdx.x];
+    } else {
+        row = A.rowlist[blockIdx.x];
+        e0 = rowptr[row];
+        deg = std::uint32_t(rowptr[row + 1] - e0);
+    }
     const std::uint32_t nchunks = (deg + ch - 1) / ch;
     const int warp = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
 
@@ -386,55 +420,89 @@ __device__ __forceinline__ void longrow_body(const std::uint64_t* __restrict__ r
     }
 
     // ---------------- consumer warps ----------------
-    const std::uint32_t t0 = threadIdx.x - 32;
-    const std::uint32_t n_cons = blockDim.x - 32;
-    constexpr int MAXF = 8;  // features t0, t0 + n_cons, ... (f <= 8 * n_cons)
-    double acc[MAXF];
+    // thread q owns features [FPL*q, FPL*q + FPL): FPL independent f64 chains
+    // fed by one FPL-wide LDS per entry; the entry value is a broadcast f64
+    // read.  FPL is chosen so a row's features fill whole warps (F=64: 32
+    // lanes x 2), which minimises instructions per entry.
+    using VT = typename LongVec<FPL>::T;
+    const std::uint32_t q = threadIdx.x - 32;
+    const std::uint32_t nq = f / FPL;
+    const bool active = q < nq;
+    double acc[FPL];
 #pragma unroll
-    for (int i = 0; i < MAXF; ++i) acc[i] = 0.0;
+    for (int i = 0; i < FPL; ++i) acc[i] = 0.0;
     for (std::uint32_t k = 0; k < nchunks; ++k) {
         const int s = int(k % S);
         mbar_wait(&full[s], (k / S) & 1);
         const std::uint32_t n = min(ch, deg - k * ch);
-        const float* src = ring + std::uint64_t(s) * ch * f;
-        const double* vv = vd + std::uint64_t(s) * ch;
+        if (active) {
+            const VT* src = reinterpret_cast<const VT*>(ring + std::uint64_t(s) * ch * f) + q;
+            const double* vv = vd + std::uint64_t(s) * ch;
+#pragma unroll 4
+            for (std::uint32_t j = 0; j < n; ++j) {
+                const double v = vv[j];
+                const VT bv = src[std::uint64_t(j) * nq];
 #pragma unroll
-        for (int i = 0; i < MAXF; ++i) {
-            const std::uint32_t t = t0 + i * n_cons;
-            if (t >= f) break;
-            double a = acc[i];
-            std::uint32_t j = 0;
-            // even entries widen on XU, odd entries by re-bias (MIX)
-            for (; j + 2 <= n; j += 2) {
-                const double v0 = vv[j], v1 = vv[j + 1];
-                const float b0 = src[j * f + t], b1 = src[(j + 1) * f + t];
-                a = __fma_rn(v0, double(b0), a);
-                if constexpr (MIX) a = __fma_rn(v1 * kWidenUp, widen_scaled(b1), a);
-                else a = __fma_rn(v1, double(b1), a);
+                for (int i = 0; i < FPL; ++i) {
+                    const float bi = long_comp(bv, i);
+                    // odd components widen by re-bias when MIX (half the F2F)
+                    if (MIX && (i & 1)) acc[i] = __fma_rn(v * kWidenUp, widen_scaled(bi), acc[i]);
+                    else acc[i] = __fma_rn(v, double(bi), acc[i]);
+                }
             }
-            if (j < n) a = __fma_rn(vv[j], double(src[j * f + t]), a);
-            acc[i] = a;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
     }
+    if (active) {  // scalar stores: c need not be aligned beyond 4 bytes
+        if (PIECES && slot != 0xffffffffu) {
+            double* pr = A.scratch + std::uint64_t(slot) * f + FPL * q;
 #pragma unroll
-    for (int i = 0; i < MAXF; ++i) {
-        const std::uint32_t t = t0 + i * n_cons;
-        if (t < f) c[std::uint64_t(row) * f + t] = float(acc[i]);
+            for (int i = 0; i < FPL; ++i) pr[i] = acc[i];
+        } else {
+            float* cr = c + std::uint64_t(row) * f + FPL * q;
+#pragma unroll
+            for (int i = 0; i < FPL; ++i) cr[i] = float(acc[i]);
+        }
     }
 }
 
-template <bool HAS_VAL>
-__global__ void __launch_bounds__(32 + kLongMaxConsumers)
-    spmm_longrow_kernel(const std::uint64_t* __restrict__ rowptr,
-                        const std::uint32_t* __restrict__ colind, const float* __restrict__ val,
-                        const std::uint32_t* __restrict__ rows, const float* __restrict__ b,
-                        float* __restrict__ c, std::uint32_t f, std::uint32_t ch,
-                        const unsigned* __restrict__ finite) {
+template <bool HAS_VAL, int FPL, bool PIECES>
+__global__ void __launch_bounds__(32 + kLongMaxConsumers) spmm_longrow_kernel(SegArgs a, std::uint32_t ch) {
     extern __shared__ __align__(16) char lsmem[];
-    if (finite && *finite) longrow_body<1, HAS_VAL>(rowptr, colind, val, rows, b, c, f, ch, lsmem);
-    else longrow_body<0, HAS_VAL>(rowptr, colind, val, rows, b, c, f, ch, lsmem);
+    if (a.finite && *a.finite) longrow_body<1, HAS_VAL, FPL, PIECES>(a, ch, lsmem);
+    else longrow_body<0, HAS_VAL, FPL, PIECES>(a, ch, lsmem);
+}
+
+// Launch the ring kernel over n items (rows of a.rowlist, or hub pieces).
+template <bool PIECES>
+void launch_longrow(const SegArgs& a, std::uint64_t n, cudaStream_t s) {
+    const std::uint32_t f = a.f;
+    const std::uint32_t ch = std::max<std::uint32_t>(4, kLongStageBytes / (4 * f));
+    const std::size_t smem = long_layout(f, ch).total;
+    // features per consumer lane: fill whole warps where f allows
+    const int fpl = f % 128 == 0 ? 4 : (f % 64 == 0 ? 2 : (f % 32 == 0 ? 1 : 4));
+    const unsigned threads = 32 + (f / fpl + 31) / 32 * 32;
+    auto go = [&](auto kern) {
+        ASB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        kern<<<unsigned(n), threads, smem, s>>>(a, ch);
+        check_launch("spmm_longrow_kernel");
+    };
+    auto by_val = [&](auto fc) {
+        constexpr int FPL = decltype(fc)::value;
+        if (a.val) go(spmm_longrow_kernel<true, FPL, PIECES>);
+        else go(spmm_longrow_kernel<false, FPL, PIECES>);
+    };
+    if (fpl == 1) by_val(std::integral_constant<int, 1>{});
+    else if (fpl == 2) by_val(std::integral_constant<int, 2>{});
+    else by_val(std::integral_constant<int, 4>{});
+}
+
+// The ring kernel handles f % 4 == 0 with 16-byte B rows (bulk copies).
+bool longrow_ok(std::uint32_t f, bool vec) {
+    if (!(vec && f % 4 == 0 && f <= 4 * kLongMaxConsumers)) return false;
+    const std::uint32_t ch = std::max<std::uint32_t>(4, kLongStageBytes / (4 * f));
+    return long_layout(f, ch).total <= 200 * 1024;
 }
 
 // ---------------------------------------------------------------------------
@@ -570,12 +638,18 @@ TileShape tile_shape(std::uint32_t f, std::uint64_t f_tile, bool vec) {
     return t;
 }
 
-std::uint64_t long_row_min() {
-    static const std::uint64_t v = [] {
+// Rows at least this long go to the CTA-per-row ring kernel.  In the
+// lane-group kernel a row is a chain of dependent L2 round trips (U entries
+// in flight), so on a small graph its longest rows set the kernel time; on
+// a large graph other rows hide them and the group kernel's throughput wins
+// (Reddit-shape: 4.10 ms without the ring kernel, 4.34 ms from 2048).
+std::uint64_t long_row_min(const Graph& g) {
+    static const long long knob = [] {
         const char* e = std::getenv("AUTOSAGE_DEV_LONG_ROW");
-        return e ? std::strtoull(e, nullptr, 10) : std::uint64_t(2048);
+        return e ? std::strtoll(e, nullptr, 10) : -1ll;
     }();
-    return v;
+    if (knob >= 0) return std::uint64_t(knob);
+    return g.nnz < (std::uint64_t(16) << 20) ? 256 : 1ull << 62;
 }
 
 } // namespace
@@ -603,28 +677,23 @@ void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uin
     ensure_order(g);
     // long rows (a prefix of the degree-descending order) -> CTA-per-row ring
     // kernel on a forked stream, concurrent with the group kernel
-    const std::uint64_t lmin = long_row_min();
+    const std::uint64_t lmin = long_row_min(g);
     std::uint64_t n_long = 0;
-    std::uint32_t ch = 0;
-    if (lmin > 0 && f <= 2048 && vec && f % 4 == 0) {  // bulk copies need 16-B rows
+    if (lmin > 0 && longrow_ok(f, vec)) {
         const std::uint64_t ge = rows_with_degree_at_least(g, lmin);
         n_long = ge > offset ? std::min(ge - offset, n_list) : 0;
-        ch = std::max<std::uint32_t>(4, kLongStageBytes / (4 * f));
-        if (long_layout(f, ch).total > 200 * 1024) n_long = 0;
     }
     if (n_long) {
-        const std::uint32_t* rows = g.order.get() + offset;
-        const std::size_t smem = long_layout(f, ch).total;
-        const unsigned threads = 32 + std::min<unsigned>(kLongMaxConsumers, (f + 31) / 32 * 32);
-        cudaStream_t aux = graph_fork(g, s);
-        auto go = [&](auto kern) {
-            ASB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-            kern<<<unsigned(n_long), threads, smem, aux>>>(g.rowptr.get(), g.colind.get(), val, rows, b,
-                                                           c, f, ch, finite);
-            check_launch("spmm_longrow_kernel");
-        };
-        if (val) go(spmm_longrow_kernel<true>);
-        else go(spmm_longrow_kernel<false>);
+        SegArgs a{};
+        a.rowptr = g.rowptr.get();
+        a.colind = g.colind.get();
+        a.val = val;
+        a.b = b;
+        a.c = c;
+        a.rowlist = g.order.get() + offset;
+        a.finite = finite;
+        a.f = f;
+        launch_longrow<false>(a, n_long, graph_fork(g, s));
         offset += n_long;
         n_list -= n_long;
     }
@@ -674,7 +743,10 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const float* b, std::uint3
         a.n_tiles = t.n_tiles;
         a.f = f;
         a.tile_w = t.tile_w;
-        if (vec) launch_seg_vec<4>(a, val != nullptr, t.lanes, wpb, s);
+        // pieces are up to 2048-entry dependent chains: where long rows go to
+        // the ring kernel (small graphs), so do the pieces
+        if (long_row_min(g) <= kHubNnzChunk && longrow_ok(f, vec)) launch_longrow<true>(a, plan.n_pieces, s);
+        else if (vec) launch_seg_vec<4>(a, val != nullptr, t.lanes, wpb, s);
         else launch_seg_vec<1>(a, val != nullptr, t.lanes, wpb, s);
     }
     if (plan.n_light)

@@ -341,3 +341,24 @@ def test_row_range_shards_reassemble_bit_exact():
         shard = g.row_range(int(cuts[r]), int(cuts[r + 1]))
         parts.append(asb.dispatch(v, shard, bd).output.cpu().numpy())
     assert bit_equal(np.concatenate(parts), oracle.spmm_baseline(a, b))
+
+
+def test_gpu_model_probe_sample_fills_the_device(monkeypatch):
+    """B200 model: the probe sample grows to ~AUTOSAGE_GPU_PROBE_NNZ entries
+    (row selection unchanged); reference-model profiles keep the reference
+    sample size."""
+    import math
+    rng = np.random.default_rng(77)
+    a = random_csr(rng, 3000, 3000, 20)
+    b = random_dense(rng, 3000, 32)
+    gpu = asb.DeviceProfile.gpu()
+    assert gpu.model == 1
+    cfg = asb.ProbeConfig(frac=0.02, min_rows=64, iters=2)
+    mean = a.nnz / a.n_rows
+    monkeypatch.setenv("AUTOSAGE_GPU_PROBE_NNZ", "20000")
+    d = asb.decide_spmm(a, b, cfg, asb.ScheduleContext(device=gpu))
+    want = min(a.n_rows, max(64, math.ceil(0.02 * a.n_rows), math.ceil(20000 / mean)))
+    assert d.sample_rows == want
+    ref = asb.DeviceProfile(gpu.device_sig, gpu.bw_eff, gpu.flops_eff, gpu.cores, 0)
+    d0 = asb.decide_spmm(a, b, cfg, asb.ScheduleContext(device=ref))
+    assert d0.sample_rows == max(64, math.ceil(0.02 * a.n_rows))

@@ -1,0 +1,283 @@
+#!/usr/bin/env python3
+"""Measurement sweep over the BASELINE.json configs on one GPU.
+
+  python tools/sweep.py [--cases c1,c2,c3,c4,c5] [--out gpurun_out/sweep.json]
+
+c1  SpMM+SDDMM on the 100k-row power-law graph, F=64 (+ reference CPU library on
+    the same graph, all host cores)
+c2  Reddit-shape SpMM + SDDMM at F = 32 / 64 / 128 / 256
+c3  Products-shape SpMM F=100: per-rank compute of the nnz-balanced row shards
+    for g = 1, 2, 4, 8 (each shard timed alone on this GPU with the full B
+    resident; the all-gather is not included -- one GPU here)
+c4  skew stressor: Zipf exponents 1.5 / 2.0 / 2.5 / 3.0, hubs up to 1M nnz,
+    F = 16 / 64 / 128: decision, guardrail (chosen vs baseline on the full
+    graph) and cache replay (a fresh context replaying the stored decisions)
+c5  CSR attention on Reddit-shape, 8 heads x F=64: fused vs unfused per head
+
+Every GPU time is CUDA events on the launching stream around `reps` launches
+(median per launch), decisions made once before timing.  Bytes are the
+reference gather model (proj/src/cost.cpp:21-27).
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2511_17594_b200 as asb  # noqa: E402
+from paper_2511_17594_b200 import _capi  # noqa: E402
+
+lib = _capi.lib
+PEAK, _ = bench.measured_peak()
+
+
+def P(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def ev_time(fn, reps=5, warm=2):
+    """Median per-launch ms of fn() (CUDA events per call)."""
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return statistics.median(ts)
+
+
+class Ops:
+    """Device-pointer calls through the C-ABI on torch's current stream."""
+
+    def __init__(self, g, f):
+        self.g, self.f = g, f
+        self.stream = C.c_void_p(asb.torch_stream_handle())
+
+    def spmm(self, v, b, c):
+        cv = v.to_c() if v else None
+        asb._check(lib.as_spmm(C.byref(cv) if cv else None, self.g.handle, P(b), b.shape[0], self.f,
+                               P(c), self.stream, None))
+
+    def sddmm(self, v, x, y, out):
+        cv = v.to_c() if v else None
+        asb._check(lib.as_sddmm(C.byref(cv) if cv else None, self.g.handle, P(x), x.shape[0], P(y),
+                                y.shape[0], self.f, P(out), self.stream, None))
+
+
+def gbs(op, n, nnz, f, ms):
+    return bench.gather_bytes(op, n, nnz, f) / (ms * 1e-3) / 1e9
+
+
+def decide(op, g, f, dev_in, ctx, cfg):
+    if op == "spmm":
+        return asb.decide_spmm(g, dev_in[0], cfg, ctx)
+    return asb.decide_sddmm(g, dev_in[0], dev_in[1], cfg, ctx)
+
+
+def run_graph(m, f, ops=("spmm", "sddmm"), reps=5, seed=1, with_baseline=True, cache=None):
+    g = asb.Graph.from_csr(m)
+    dev = torch.device("cuda")
+    b = torch.from_numpy(asb.fill_uniform(m.n_cols * f, seed + f, (m.n_cols, f))).to(dev)
+    x = torch.from_numpy(asb.fill_uniform(m.n_rows * f, seed + f, (m.n_rows, f))).to(dev)
+    y = torch.from_numpy(asb.fill_uniform(m.n_cols * f, seed + f + 1, (m.n_cols, f))).to(dev)
+    c = torch.empty((m.n_rows, f), dtype=torch.float32, device=dev)
+    sv = torch.empty(max(m.nnz, 1), dtype=torch.float32, device=dev)
+    cache = cache or asb.ScheduleCache()
+    ctx = asb.ScheduleContext(cache=cache, stream=asb.torch_stream_handle())
+    cfg = asb.ProbeConfig.from_env()
+    o = Ops(g, f)
+    out = {}
+    for op in ops:
+        t0 = time.perf_counter()
+        d = decide(op, g, f, (b,) if op == "spmm" else (x, y), ctx, cfg)
+        cold = (time.perf_counter() - t0) * 1e3
+        v = d.choice
+        if op == "spmm":
+            t = ev_time(lambda: o.spmm(v, b, c), reps)
+            tb = ev_time(lambda: o.spmm(None, b, c), max(2, reps // 2)) if with_baseline else None
+        else:
+            t = ev_time(lambda: o.sddmm(v, x, y, sv), reps)
+            tb = ev_time(lambda: o.sddmm(None, x, y, sv), max(2, reps // 2)) if with_baseline else None
+        out[op] = {"choice": d.choice_string(), "source": d.source_name, "ms": t,
+                   "gbs": gbs(op, m.n_rows, m.nnz, f, t), "frac_hbm": gbs(op, m.n_rows, m.nnz, f, t) / PEAK,
+                   "baseline_ms": tb, "decide_cold_ms": cold,
+                   "probe": {"t_b": d.baseline_ms, "t_star": d.t_star, "sample_rows": d.sample_rows,
+                             "candidates": [(asb.variant_to_string(ct.variant), ct.median_ms)
+                                            for ct in d.candidates]}}
+    g.close()
+    return out, cache
+
+
+def case_c1(res):
+    m, f = bench.make_graph("c1", 1)
+    r, _ = run_graph(m, f, reps=20)
+    cpu = bench.cpu_reference_run(m, f, 1, 3, 1, 1)
+    res["c1"] = {"graph": {"n": m.n_rows, "nnz": m.nnz, "F": f}, "gpu": r, "cpu_reference": cpu}
+
+
+def case_c2(res):
+    m, _ = bench.make_graph("reddit", 1)
+    res["c2"] = {"graph": {"n": m.n_rows, "nnz": m.nnz}, "by_F": {}}
+    for f in (32, 64, 128, 256):
+        r, _ = run_graph(m, f, reps=5, with_baseline=(f <= 64))
+        res["c2"]["by_F"][str(f)] = r
+
+
+def case_c3(res):
+    m, f = bench.make_graph("products", 1)
+    from paper_2511_17594_b200.dist import RowSharding
+    g_full = asb.Graph.from_csr(m)
+    dev = torch.device("cuda")
+    b = torch.from_numpy(asb.fill_uniform(m.n_cols * f, 1 + f, (m.n_cols, f))).to(dev)
+    ctx = asb.ScheduleContext(cache=asb.ScheduleCache(), stream=asb.torch_stream_handle())
+    cfg = asb.ProbeConfig.from_env()
+    d = asb.decide_spmm(g_full, b, cfg, ctx)
+    v = d.choice
+    out = {"graph": {"n": m.n_rows, "nnz": m.nnz, "F": f}, "choice": d.choice_string(), "by_g": {}}
+    for world in (1, 2, 4, 8):
+        per_rank = []
+        for rank in range(world):
+            sh = RowSharding(m.rowptr, world, rank)
+            gs = g_full if world == 1 else g_full.row_range(sh.r0, sh.r1)
+            c = torch.empty((sh.r1 - sh.r0, f), dtype=torch.float32, device=dev)
+            o = Ops(gs, f)
+            per_rank.append(ev_time(lambda: o.spmm(v, b, c), 5))
+            if world > 1:
+                gs.close()
+        worst = max(per_rank)
+        out["by_g"][str(world)] = {"per_rank_ms": per_rank, "max_rank_ms": worst,
+                                   "gbs_total": gbs("spmm", m.n_rows, m.nnz, f, worst),
+                                   "allgather_bytes_per_rank": int((world - 1) * (m.n_cols // world) * f * 4)}
+    base = out["by_g"]["1"]["max_rank_ms"]
+    for k, e in out["by_g"].items():
+        e["compute_speedup"] = base / e["max_rank_ms"]
+    g_full.close()
+    res["c3"] = out
+
+
+def with_hubs(m, hub_degrees, seed):
+    """Replace the first rows by hubs of the given degrees (distinct sorted
+    columns), keeping the rest of the power-law graph."""
+    rng = np.random.default_rng(seed)
+    deg = np.diff(m.rowptr.astype(np.int64))
+    rows = []
+    for i in range(m.n_rows):
+        if i < len(hub_degrees):
+            cols = np.sort(rng.permutation(m.n_cols)[:hub_degrees[i]]).astype(np.uint32)
+        else:
+            break
+        rows.append(cols)
+    k = len(rows)
+    head = np.concatenate(rows)
+    tail = m.colind[int(m.rowptr[k]):]
+    deg2 = np.concatenate([np.array([r.size for r in rows], np.int64), deg[k:]])
+    rp = np.zeros(m.n_rows + 1, np.uint64)
+    rp[1:] = np.cumsum(deg2)
+    val = None
+    if m.val is not None:
+        val = np.concatenate([asb.fill_uniform(head.size, seed, (head.size,)) * 0.5 + 0.5,
+                              m.val[int(m.rowptr[k]):]]).astype(np.float32)
+    return asb.CsrMatrix(m.n_rows, m.n_cols, rp, np.concatenate([head, tail]), val)
+
+
+def case_c4(res):
+    out = []
+    n = 1_100_000
+    for alpha in (1.5, 2.0, 2.5, 3.0):
+        m = with_hubs(asb.gen_powerlaw(n, n, 24_000_000, alpha, 4, 1_000_000, 7),
+                      [1_000_000, 250_000, 60_000], 11)
+        deg = np.diff(m.rowptr.astype(np.int64))
+        for f in (16, 64, 128):
+            r, cache = run_graph(m, f, ops=("spmm",), reps=3)
+            # replay: a fresh context that must reproduce the stored decision
+            fd, path = tempfile.mkstemp(suffix=".cache")
+            os.close(fd)
+            cache.store(path)
+            c2 = asb.ScheduleCache()
+            c2.load(path)
+            os.unlink(path)
+            r2, _ = run_graph(m, f, ops=("spmm",), reps=2, with_baseline=False, cache=c2)
+            e = r["spmm"]
+            out.append({"alpha": alpha, "F": f, "n": m.n_rows, "nnz": m.nnz, "deg_max": int(deg.max()),
+                        "choice": e["choice"], "ms": e["ms"], "baseline_ms": e["baseline_ms"],
+                        "guardrail_ok": e["ms"] <= e["baseline_ms"] * 1.02,
+                        "gbs": e["gbs"], "probe": e["probe"],
+                        "replay_source": r2["spmm"]["source"],
+                        "replay_same_choice": r2["spmm"]["choice"] == e["choice"]})
+        del m
+    res["c4"] = out
+
+
+def case_c5(res):
+    m, _ = bench.make_graph("reddit", 1)
+    f = 64
+    g = asb.Graph.from_csr(m)
+    dev = torch.device("cuda")
+    cache = asb.ScheduleCache()
+    ctx = asb.ScheduleContext(cache=cache, stream=asb.torch_stream_handle())
+    cfg = asb.ProbeConfig.from_env()
+    cctx, keep = ctx.to_c()
+    ccfg = cfg.to_c()
+    out_t = torch.empty((m.n_rows, f), dtype=torch.float32, device=dev)
+    sd, pd = _capi.as_decision(), _capi.as_decision()
+    heads = []
+    for h in range(8):
+        q = torch.from_numpy(asb.fill_uniform(m.n_rows * f, 1 + 3 * h, (m.n_rows, f))).to(dev)
+        k = torch.from_numpy(asb.fill_uniform(m.n_cols * f, 2 + 3 * h, (m.n_cols, f))).to(dev)
+        v = torch.from_numpy(asb.fill_uniform(m.n_cols * f, 3 + 3 * h, (m.n_cols, f))).to(dev)
+        row = {}
+        for fused in (1, 0):
+            def run():
+                asb._check(lib.as_csr_attention_forward(
+                    C.byref(cctx), C.byref(ccfg), g.handle, P(q), m.n_rows, P(k), m.n_cols, P(v),
+                    m.n_cols, f, f, P(out_t), fused, C.byref(sd), C.byref(pd)))
+            t0 = time.perf_counter()
+            run()
+            torch.cuda.synchronize()
+            cold = (time.perf_counter() - t0) * 1e3
+            row["fused" if fused else "unfused"] = {"ms": ev_time(run, 3, 1), "first_call_ms": cold}
+        heads.append(row)
+        del q, k, v
+    fused_ms = sum(h["fused"]["ms"] for h in heads)
+    unfused_ms = sum(h["unfused"]["ms"] for h in heads)
+    by = 4 * m.nnz + 8 * (m.n_rows + 1) + 4 * m.n_rows * f + 4 * m.nnz * f + 4 * m.nnz * f + 4 * m.n_rows * f
+    res["c5"] = {"graph": {"n": m.n_rows, "nnz": m.nnz, "F": f, "heads": 8},
+                 "sddmm_choice": asb.ScheduleDecision.from_c(sd).choice_string(),
+                 "spmm_choice": asb.ScheduleDecision.from_c(pd).choice_string(),
+                 "fused_ms_8_heads": fused_ms, "unfused_ms_8_heads": unfused_ms,
+                 "fused_gbs": 8 * by / (fused_ms * 1e-3) / 1e9, "heads": heads}
+    del keep
+    g.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cases", default="c1,c2,c3,c4,c5")
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep.json"))
+    a = ap.parse_args()
+    res = {"gpu": torch.cuda.get_device_name(), "peak_gbs": PEAK}
+    for cs in a.cases.split(","):
+        t0 = time.time()
+        globals()[f"case_{cs}"](res)
+        print(cs, "done in", round(time.time() - t0, 1), "s", flush=True)
+        with open(a.out, "w") as fh:
+            json.dump(res, fh, indent=1)
+
+
+if __name__ == "__main__":
+    main()
