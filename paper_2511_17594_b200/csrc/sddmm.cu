@@ -304,15 +304,16 @@ __global__ void widen_kernel(const float4* __restrict__ x, double2* __restrict__
     }
 }
 
-template <int F>
+// FW = features staged per pass (F = npass * FW, runtime F).
+template <int FW>
 struct FixedShape {
-    static constexpr int NV = F / 4;                // 16-byte units per row
-    static constexpr int S = 4 * (NV | 1);          // smem pitch in floats
-    static constexpr int kCopies = NV;              // cp.async per lane per chunk (32 rows)
-    static constexpr int KX = F >= 64 ? 1 : 64 / F; // X rows (f64) staged per chunk
-    static constexpr int kXUnits = KX * F / 2;      // their 16-byte units
+    static constexpr int NV = FW / 4;                 // 16-byte units per row slice
+    static constexpr int S = 4 * (NV | 1);            // smem pitch in floats (odd # of 16 B)
+    static constexpr int kCopies = NV;                // cp.async per lane per pass (32 rows)
+    static constexpr int KX = FW >= 64 ? 1 : 64 / FW; // X rows (f64) staged per chunk
+    static constexpr int kXUnits = KX * FW / 2;       // their 16-byte units per pass
     static constexpr std::uint64_t kYBytes = 32ull * S * 4;
-    static constexpr std::uint64_t kWarpBytes = kYBytes + std::uint64_t(KX) * F * 8;
+    static constexpr std::uint64_t kWarpBytes = kYBytes + std::uint64_t(KX) * FW * 8;
 };
 
 template <bool SMEM>
@@ -321,63 +322,61 @@ __device__ __forceinline__ double2 ld_x2(const double* p) {
     else return __ldg(reinterpret_cast<const double2*>(p));
 }
 
-// <x, y> over one Y row in shared memory; xr: the lane's X row (f64, global)
-template <int F, int ORD, int FT, bool XS, int MIX>
-__device__ __forceinline__ double fixed_dot(const double* __restrict__ xr, const float* yr) {
-    if constexpr (ORD == 0) {
-        double acc = 0.0;
+__device__ __forceinline__ void fold4(double& acc, double& a0, double& a1, double& a2, double& a3) {
+    // src/kernels.cpp:103-127: block end; F % 4 == 0, so the scalar tail is empty
+    const double tail = 0.0;
+    acc = __dadd_rn(acc, __dadd_rn(__dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3)), tail));
+    a0 = a1 = a2 = a3 = 0.0;
+}
+
+// One pass (features [p*FW, (p+1)*FW)) of the lane's dot, continuing the
+// chain(s).  ORD 0: one sequential chain.  ORD 1: four stride-4 partials per
+// f_tile block; FT = 0 means one block over all F.
+template <int FW, int ORD, int FT, bool XS, int MIX>
+__device__ __forceinline__ void fixed_pass(const double* __restrict__ xr, const float* yr, int p, int npass,
+                                           double& acc, double& a0, double& a1, double& a2, double& a3) {
 #pragma unroll 8
-        for (int t = 0; t < F; t += 4) {
-            const float4 y4 = *reinterpret_cast<const float4*>(yr + t);
-            const double2 x01 = ld_x2<XS>(xr + t);
-            const double2 x23 = ld_x2<XS>(xr + t + 2);
+    for (int t = 0; t < FW; t += 4) {
+        const float4 y4 = *reinterpret_cast<const float4*>(yr + t);
+        const double2 x01 = ld_x2<XS>(xr + t);
+        const double2 x23 = ld_x2<XS>(xr + t + 2);
+        if constexpr (ORD == 0) {
             acc = dfma(x01.x, y4.x, acc);
             acc = dfma(x01.y, y4.y, acc);
             acc = __fma_rn(x23.x, widen<MIX>(y4.z), acc);
             acc = __fma_rn(x23.y, widen<MIX>(y4.w), acc);
+        } else {
+            a0 = dfma(x01.x, y4.x, a0);
+            a1 = dfma(x01.y, y4.y, a1);
+            a2 = __fma_rn(x23.x, widen<MIX>(y4.z), a2);
+            a3 = __fma_rn(x23.y, widen<MIX>(y4.w), a3);
+            if constexpr (FT != 0 && FT <= FW)
+                if ((t + 4) % FT == 0) fold4(acc, a0, a1, a2, a3);
         }
-        return acc;
-    } else {
-        // src/kernels.cpp:103-127: per f_tile block four stride-4 partials;
-        // F % 4 == 0 and FT % 4 == 0, so every block's scalar tail is empty
-        double acc = 0.0;
-#pragma unroll
-        for (int b0 = 0; b0 < F; b0 += FT) {
-            constexpr int kBlk = FT;
-            const int fw = (F - b0) < kBlk ? (F - b0) : kBlk;
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-#pragma unroll 4
-            for (int t = 0; t < fw; t += 4) {
-                const float4 y4 = *reinterpret_cast<const float4*>(yr + b0 + t);
-                const double2 x01 = ld_x2<XS>(xr + b0 + t);
-                const double2 x23 = ld_x2<XS>(xr + b0 + t + 2);
-                a0 = dfma(x01.x, y4.x, a0);
-                a1 = dfma(x01.y, y4.y, a1);
-                a2 = __fma_rn(x23.x, widen<MIX>(y4.z), a2);
-                a3 = __fma_rn(x23.y, widen<MIX>(y4.w), a3);
-            }
-            const double tail = 0.0;
-            acc = __dadd_rn(acc, __dadd_rn(__dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3)), tail));
-        }
-        return acc;
+    }
+    if constexpr (ORD == 1 && (FT == 0 || FT > FW)) {
+        const bool end = p == npass - 1 || (FT != 0 && ((p + 1) * FW) % FT == 0);
+        if (end) fold4(acc, a0, a1, a2, a3);
     }
 }
 
-template <int F, int ORD, int FT, int MIX>
+template <int FW, int ORD, int FT, int MIX, int NP>
 __device__ __forceinline__ void sddmm_fixed_body(const std::uint64_t* __restrict__ rowptr,
                                                  const std::uint32_t* __restrict__ colind,
                                                  const std::uint32_t* __restrict__ chunk_row,
                                                  std::uint64_t n_rows, const double* __restrict__ xd,
                                                  const float* __restrict__ y, float* __restrict__ out,
-                                                 std::uint64_t nnz, std::uint64_t c_begin,
+                                                 std::uint64_t nnz, std::uint32_t F, std::uint64_t c_begin,
                                                  std::uint64_t c_end) {
-    using Sh = FixedShape<F>;
+    using Sh = FixedShape<FW>;
     extern __shared__ __align__(16) char smem[];
     char* wsm = smem + std::uint64_t(threadIdx.x >> 5) * Sh::kWarpBytes;
     float* ys = reinterpret_cast<float*>(wsm);
     double* xs = reinterpret_cast<double*>(wsm + Sh::kYBytes);
-    const std::uint64_t x_units = n_rows * F / 2;
     const int lane = threadIdx.x & 31;
+    // NP > 0: F = NP * FW known at compile time (single-pass shapes)
+    const int npass = NP > 0 ? NP : int(F / FW);
+    if constexpr (NP > 0) F = NP * FW;
     const std::uint64_t stride = std::uint64_t(gridDim.x) * (blockDim.x >> 5);
 
     struct Meta {
@@ -394,29 +393,32 @@ __device__ __forceinline__ void sddmm_fixed_body(const std::uint64_t* __restrict
         if (bi <= n_rows) m.bound = __ldg(rowptr + bi);
         return m;
     };
-
-    std::uint64_t c = c_begin + std::uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    Meta cur = meta(c);
-    for (; c < c_end; c += stride) {
-        // 32 Y rows -> shared memory, 16-byte pieces, rows in lane order
+    // this pass's Y slice of the 32 rows and X slice of rows r_first.. (+KX)
+    auto issue = [&](const Meta& m, int p) {
 #pragma unroll
         for (int it = 0; it < Sh::kCopies; ++it) {
             const int idx = it * 32 + lane;
             const int j = idx / Sh::NV, q = idx % Sh::NV;
-            const std::uint32_t cj = __shfl_sync(FULL, cur.col, j);
-            cp_async16(ys + j * Sh::S + 4 * q, y + std::uint64_t(cj) * F + 4 * q);
+            const std::uint32_t cj = __shfl_sync(FULL, m.col, j);
+            cp_async16(ys + j * Sh::S + 4 * q, y + std::uint64_t(cj) * F + p * FW + 4 * q);
         }
-        // X rows r_first .. r_first+KX-1 (contiguous in xd)
 #pragma unroll
         for (int u = lane; u < Sh::kXUnits; u += 32) {
-            const std::uint64_t gu = std::uint64_t(cur.r_first) * (F / 2) + u;
-            if (gu < x_units) cp_async16(xs + 2 * u, xd + 2 * gu);
+            const int k = u / (FW / 2), uu = u % (FW / 2);
+            const std::uint64_t xr = std::uint64_t(m.r_first) + k;
+            if (xr < n_rows) cp_async16(xs + 2 * u, xd + xr * F + p * FW + 2 * uu);
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+
+    std::uint64_t c = c_begin + std::uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    Meta cur = meta(c);
+    for (; c < c_end; c += stride) {
+        issue(cur, 0);
         const Meta nxt = meta(c + stride);
         // the lane's row: count the chunk's row boundaries at or before e
-        const std::uint64_t e0 = c * 32, e = e0 + lane;
         // (sorted, so the k boundaries inside the chunk sit in lanes 0..k-1)
+        const std::uint64_t e0 = c * 32, e = e0 + lane;
         std::uint32_t r = cur.r_first;
         const unsigned inside = __ballot_sync(FULL, cur.bound <= e0 + 31);
         if (inside) {
@@ -425,30 +427,40 @@ __device__ __forceinline__ void sddmm_fixed_body(const std::uint64_t* __restrict
             for (int b = 0; b < k; ++b) r += __shfl_sync(FULL, cur.bound, b) <= e ? 1u : 0u;
             if (k == 32) r = row_of(rowptr, r, e);  // more rows meet in this chunk
         }
-        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-        __syncwarp();
-        if (e < nnz) {
-            const std::uint32_t rel = r - cur.r_first;
-            const float* yr = ys + lane * Sh::S;
-            out[e] = float(rel < Sh::KX ? fixed_dot<F, ORD, FT, true, MIX>(xs + rel * F, yr)
-                                        : fixed_dot<F, ORD, FT, false, MIX>(xd + std::uint64_t(r) * F, yr));
+        const std::uint32_t rel = r - cur.r_first;
+        const float* yr = ys + lane * Sh::S;
+        double acc = 0.0, a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        for (int p = 0; p < npass; ++p) {
+            if (p > 0) issue(cur, p);
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+            __syncwarp();
+            if (e < nnz) {
+                if (rel < Sh::KX)
+                    fixed_pass<FW, ORD, FT, true, MIX>(xs + rel * FW, yr, p, npass, acc, a0, a1, a2, a3);
+                else
+                    fixed_pass<FW, ORD, FT, false, MIX>(xd + std::uint64_t(r) * F + p * FW, yr, p, npass, acc,
+                                                        a0, a1, a2, a3);
+            }
+            __syncwarp();
         }
-        __syncwarp();
+        if (e < nnz) out[e] = float(acc);
         cur = nxt;
     }
 }
 
-template <int F, int ORD, int FT>
+template <int FW, int ORD, int FT, int NP>
 __global__ void __launch_bounds__(256, 3)
     sddmm_fixed_kernel(const std::uint64_t* __restrict__ rowptr, const std::uint32_t* __restrict__ colind,
                        const std::uint32_t* __restrict__ chunk_row, std::uint64_t n_rows,
                        const double* __restrict__ xd, const float* __restrict__ y,
-                       float* __restrict__ out, std::uint64_t nnz, std::uint64_t c_begin,
+                       float* __restrict__ out, std::uint64_t nnz, std::uint32_t f, std::uint64_t c_begin,
                        std::uint64_t c_end, const unsigned* __restrict__ finite) {
     if (finite && *finite)
-        sddmm_fixed_body<F, ORD, FT, 1>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin, c_end);
+        sddmm_fixed_body<FW, ORD, FT, 1, NP>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, f, c_begin,
+                                             c_end);
     else
-        sddmm_fixed_body<F, ORD, FT, 0>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin, c_end);
+        sddmm_fixed_body<FW, ORD, FT, 0, NP>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, f, c_begin,
+                                             c_end);
 }
 
 // Guardrail baseline / large-F fallback: lane per entry, both rows read
@@ -471,12 +483,24 @@ __global__ void sddmm_direct_kernel(const std::uint64_t* __restrict__ rowptr,
 
 bool aligned16(const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15u) == 0; }
 
-// Fixed-width path applies to (f, ft, alignment)?
+// Fixed-width path: F a multiple of 16, X/Y 16-byte aligned, and an f_tile
+// whose blocks line up with the passes.  FW = features staged per pass.
+int fixed_fw(std::uint32_t f) {
+    if (f == 16 || f == 32 || f == 64) return int(f);
+    if (f % 64 == 0) return 64;
+    if (f % 32 == 0) return 32;
+    if (f % 16 == 0) return 16;
+    return 0;
+}
+
 bool fixed_eligible(const float* x, const float* y, std::uint32_t f, std::uint32_t ft, int ord) {
     if (!dev_knob("AUTOSAGE_DEV_SDDMM_FIXED", 1)) return false;
-    if (!(f == 16 || f == 32 || f == 64 || f == 128)) return false;
+    const int fw = fixed_fw(f);
+    if (!fw || f > 4096) return false;
     if (!aligned16(x) || !aligned16(y)) return false;
-    return ord == 0 || ft == 32 || ft == 64 || ft == 128 || ft == f;
+    if (ord == 0 || ft >= f) return true;
+    if (!(ft == 32 || ft == 64 || ft == 128)) return false;
+    return int(ft) % fw == 0 || fw % int(ft) == 0;
 }
 
 int sm_count() {
@@ -486,7 +510,7 @@ int sm_count() {
     return sms;
 }
 
-// X widened to f64 (prepass of the fixed path, once per call)
+// X widened to f64 (prepass of the fixed-width path, once per call)
 void widen_x(Graph& g, const float* x, std::uint32_t f, cudaStream_t s, const unsigned* finite) {
     const std::uint64_t nx = g.n_rows * f;
     g.xwide.ensure(std::max<std::uint64_t>(nx, 1));
@@ -511,22 +535,31 @@ void launch_sddmm_fixed(Graph& g, const float* y, std::uint32_t f, float* out, s
         const std::uint64_t cap = std::uint64_t(sms) * std::max(per_sm, 1);
         const unsigned blocks = unsigned(std::max<std::uint64_t>(1, std::min(want, cap)));
         kernel<<<blocks, kWarps * 32, smem, s>>>(g.rowptr.get(), g.colind.get(), g.chunk_row.get(), g.n_rows,
-                                                 g.xwide.get(), y, out, g.nnz, c_begin, c_end, finite);
+                                                 g.xwide.get(), y, out, g.nnz, f, c_begin, c_end, finite);
         check_launch("sddmm_fixed_kernel");
     };
-    auto by_f = [&](auto fc) {
-        constexpr int F = decltype(fc)::value;
-        constexpr std::uint64_t wb = FixedShape<F>::kWarpBytes;
-        if (ord == 0) go(sddmm_fixed_kernel<F, 0, F>, wb);
-        else if (ft >= std::uint32_t(F)) go(sddmm_fixed_kernel<F, 1, F>, wb);
-        else if (ft == 32) go(sddmm_fixed_kernel<F, 1, (F > 32 ? 32 : F)>, wb);
-        else go(sddmm_fixed_kernel<F, 1, (F > 64 ? 64 : F)>, wb);
+    // FT: 0 = one block over all of F (ft >= f); else the block width
+    auto by_fw = [&](auto fc, auto npc) {
+        constexpr int FW = decltype(fc)::value, NP = decltype(npc)::value;
+        constexpr std::uint64_t wb = FixedShape<FW>::kWarpBytes;
+        if (ord == 0) go(sddmm_fixed_kernel<FW, 0, 0, NP>, wb);
+        else if (ft >= f) go(sddmm_fixed_kernel<FW, 1, 0, NP>, wb);
+        else if (ft == 32) go(sddmm_fixed_kernel<FW, 1, 32, NP>, wb);
+        else if (ft == 64) go(sddmm_fixed_kernel<FW, 1, 64, NP>, wb);
+        else go(sddmm_fixed_kernel<FW, 1, 128, NP>, wb);
     };
-    switch (f) {
-    case 16: by_f(std::integral_constant<int, 16>{}); break;
-    case 32: by_f(std::integral_constant<int, 32>{}); break;
-    case 64: by_f(std::integral_constant<int, 64>{}); break;
-    default: by_f(std::integral_constant<int, 128>{}); break;
+    using I = std::integral_constant<int, 1>;
+    using R = std::integral_constant<int, 0>;
+    switch (f) {  // single-pass widths compile F in; the rest loop over passes
+    case 16: by_fw(std::integral_constant<int, 16>{}, I{}); break;
+    case 32: by_fw(std::integral_constant<int, 32>{}, I{}); break;
+    case 64: by_fw(std::integral_constant<int, 64>{}, I{}); break;
+    default:
+        switch (fixed_fw(f)) {
+        case 16: by_fw(std::integral_constant<int, 16>{}, R{}); break;
+        case 32: by_fw(std::integral_constant<int, 32>{}, R{}); break;
+        default: by_fw(std::integral_constant<int, 64>{}, R{}); break;
+        }
     }
 }
 
