@@ -1,0 +1,85 @@
+#!/usr/bin/env python3
+"""profiles/<tag>_sweep.md from a tools/sweep.py JSON.
+
+  python tools/summarize_sweep.py gpurun_out/sweep_r01d.json r01d
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def f3(x):
+    return "—" if x is None else f"{x:.3f}"
+
+
+def main():
+    src, tag = sys.argv[1], sys.argv[2]
+    r = json.load(open(src))
+    peak = r.get("peak_gbs", 6550.1)
+    L = [f"# Config sweep ({tag}) — {r.get('gpu', 'B200')}", "",
+         "`python tools/sweep.py` (one GPU). Times are CUDA-event medians per launch after the decision is",
+         "cached; GB/s is the reference gather model (proj/src/cost.cpp:21-27) over that time, so it can exceed",
+         f"HBM when the dense operand is L2-resident. `frac` = GB/s / {peak:.0f} (MEASURED_PEAKS.json).", ""]
+    if "c1" in r:
+        c = r["c1"]
+        g = c["graph"]
+        L += [f"## c1 — power-law N={g['n']}, nnz={g['nnz']}, F={g['F']}", "",
+              "| op | choice | ms | GB/s | frac | baseline ms |", "|---|---|---|---|---|---|"]
+        for op, e in c["gpu"].items():
+            L.append(f"| {op} | `{e['choice']}` | {f3(e['ms'])} | {e['gbs']:.0f} | {e['frac_hbm']:.2f} | "
+                     f"{f3(e['baseline_ms'])} |")
+        cpu = c.get("cpu_reference")
+        if cpu:
+            L += ["", f"Reference CPU library on the same graph ({cpu['cores']} host cores, {cpu['kind']}): "
+                  f"{cpu['value']:.1f} GB/s for SpMM+SDDMM, {cpu['ms_per_step']:.2f} ms per step. "
+                  f"{cpu['sample']}."]
+        L.append("")
+    if "c2" in r:
+        g = r["c2"]["graph"]
+        L += [f"## c2 — Reddit-shape N={g['n']}, nnz={g['nnz']}", "",
+              "| F | op | choice | ms | GB/s | frac | baseline ms |", "|---|---|---|---|---|---|---|"]
+        for f, ops in r["c2"]["by_F"].items():
+            for op, e in ops.items():
+                L.append(f"| {f} | {op} | `{e['choice']}` | {f3(e['ms'])} | {e['gbs']:.0f} | "
+                         f"{e['frac_hbm']:.2f} | {f3(e['baseline_ms'])} |")
+        L.append("")
+    if "c3" in r:
+        c = r["c3"]
+        g = c["graph"]
+        L += [f"## c3 — Products-shape N={g['n']}, nnz={g['nnz']}, SpMM F={g['F']}, row-sharded", "",
+              f"Choice `{c['choice']}`. Each rank's nnz-balanced shard is timed alone on this GPU with the full B",
+              "resident (per-rank compute of a g-GPU step); the all-gather of B shards is not included (one GPU).",
+              "", "| g | max-rank ms | compute speed-up | gather-model GB/s (whole job) | B bytes gathered per rank |",
+              "|---|---|---|---|---|"]
+        for k, e in c["by_g"].items():
+            L.append(f"| {k} | {f3(e['max_rank_ms'])} | {e['compute_speedup']:.2f} | {e['gbs_total']:.0f} | "
+                     f"{e['allgather_bytes_per_rank'] / 1e6:.0f} MB |")
+        L.append("")
+    if "c4" in r:
+        L += ["## c4 — skew stressor (hubs of 1M / 250k / 60k nnz on a 1.1M-row power-law graph)", "",
+              "| α | F | nnz | choice | ms | baseline ms | guardrail | replay | GB/s |",
+              "|---|---|---|---|---|---|---|---|---|"]
+        for e in r["c4"]:
+            L.append(f"| {e['alpha']} | {e['F']} | {e['nnz']} | `{e['choice']}` | {f3(e['ms'])} | "
+                     f"{f3(e['baseline_ms'])} | {'ok' if e['guardrail_ok'] else 'REGRESSED'} | "
+                     f"{e['replay_source']}{'' if e['replay_same_choice'] else ' (DIFFERENT)'} | {e['gbs']:.0f} |")
+        L.append("")
+    if "c5" in r:
+        c = r["c5"]
+        g = c["graph"]
+        L += [f"## c5 — CSR attention, Reddit-shape, {g['heads']} heads × F={g['F']}", "",
+              f"SDDMM `{c['sddmm_choice']}`, SpMM `{c['spmm_choice']}`.", "",
+              "| pipeline | ms (8 heads) | ms / head |", "|---|---|---|",
+              f"| fused kernel | {c['fused_ms_8_heads']:.2f} | {c['fused_ms_8_heads'] / 8:.2f} |",
+              f"| unfused (SDDMM → softmax → SpMM) | {c['unfused_ms_8_heads']:.2f} | "
+              f"{c['unfused_ms_8_heads'] / 8:.2f} |", ""]
+    out = os.path.join(ROOT, "profiles", f"{tag}_sweep.md")
+    with open(out, "w") as fh:
+        fh.write("\n".join(L) + "\n")
+    print("wrote", out)
+
+
+if __name__ == "__main__":
+    main()
