@@ -394,6 +394,7 @@ std::unique_ptr<Graph> slice_rows(Graph& g, const std::vector<std::uint64_t>& ro
     std::uint64_t nnz = 0;
     for (auto r : rows) nnz += g.h_rowptr[r + 1] - g.h_rowptr[r];
     auto out = alloc_graph(s, g.n_cols, nnz, vals != nullptr, g.device);
+    out->plan_nnz = g.plan_nnz ? g.plan_nnz : g.nnz;
     out->h_rowptr.resize(s + 1);
     out->h_rowptr[0] = 0;
     for (std::uint64_t r = 0; r < s; ++r)

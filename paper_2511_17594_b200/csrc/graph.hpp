@@ -75,6 +75,9 @@ struct Graph {
     int device = 0;
     std::uint64_t n_rows = 0, n_cols = 0, nnz = 0;
     bool has_val = false;
+    // kernel-path heuristics see this many entries (a probe sample stands in
+    // for its parent graph, so it takes the parent's paths); 0 = own nnz
+    std::uint64_t plan_nnz = 0;
     DevBuf<std::uint64_t> rowptr;
     DevBuf<std::uint32_t> colind;
     DevBuf<float> val;

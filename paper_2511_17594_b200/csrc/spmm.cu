@@ -649,7 +649,8 @@ std::uint64_t long_row_min(const Graph& g) {
         return e ? std::strtoll(e, nullptr, 10) : -1ll;
     }();
     if (knob >= 0) return std::uint64_t(knob);
-    return g.nnz < (std::uint64_t(16) << 20) ? 256 : 1ull << 62;
+    const std::uint64_t n = g.plan_nnz ? g.plan_nnz : g.nnz;
+    return n < (std::uint64_t(16) << 20) ? 256 : 1ull << 62;
 }
 
 } // namespace
