@@ -55,9 +55,10 @@ __host__ __device__ constexpr int unroll_for(int vec, int nch) {
 }
 
 __host__ __device__ constexpr int maxreg_for(int vec, int nch) {
-    // float4 single-chunk tiles: keep >= 40 resident warps per SM; wider
-    // tiles keep their in-flight loads in registers
-    return vec == 1 ? (nch == 1 ? 64 : (nch == 2 ? 96 : 128)) : (nch == 1 ? 48 : (nch == 2 ? 64 : 128));
+    // float4 single-chunk tiles at 64 registers (32 warps/SM): 48 spilled the
+    // 4 in-flight entries and cost Reddit-shape 2.35 -> 2.41 ms (hubsplit) and
+    // 3.24 -> 4.01 ms (rowparallel); wider tiles keep their loads in registers
+    return vec == 1 ? (nch == 1 ? 64 : (nch == 2 ? 96 : 128)) : (nch == 1 ? 64 : (nch == 2 ? 80 : 128));
 }
 
 struct SegArgs {
@@ -552,6 +553,9 @@ int dev_tune() {
         if (v == "8x64") return 5;
         if (v == "8x128") return 6;
         if (v == "2x48") return 7;
+        if (v == "4x56") return 8;
+        if (v == "4x64") return 9;
+        if (v == "6x64") return 10;
         return 0;
     }();
     return t;
@@ -568,6 +572,9 @@ void launch_tuned(const SegArgs& a, unsigned blocks, unsigned threads, cudaStrea
             case 5: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 8, 64><<<blocks, threads, 0, s>>>(a); return;
             case 6: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 8, 128><<<blocks, threads, 0, s>>>(a); return;
             case 7: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 2, 48><<<blocks, threads, 0, s>>>(a); return;
+            case 8: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 4, 56><<<blocks, threads, 0, s>>>(a); return;
+            case 9: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 4, 64><<<blocks, threads, 0, s>>>(a); return;
+            case 10: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 6, 64><<<blocks, threads, 0, s>>>(a); return;
             default: break;
         }
     }

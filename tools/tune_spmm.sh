@@ -1,7 +1,8 @@
+#!/bin/bash
+# SpMM lane-group kernel sweep: entries in flight (U) x register cap, per config.
 cfg=${1:-reddit}
-for lr in 0 2048 4096; do
-  AUTOSAGE_DEV_LONG_ROW=$lr timeout 120 python tools/profile_kernels.py --config $cfg --reps 3 --spmm spmm:rowparallel:ft=64:rpc=4:vec=1:hubt=256,spmm:hubsplit:ft=64:rpc=4:vec=1:hubt=256 2>&1 | awk -v c=$cfg -v lr=$lr '{print c, "lr="lr, "tune=", $0}'
-done
-for tma in 1 0; do
-AUTOSAGE_DEV_SDDMM_TMA=$tma timeout 120 python tools/profile_kernels.py --config $cfg --reps 3 --sddmm sddmm:rowparallel:ft=64:rpc=4:vec=1:hubt=256,sddmm:rowparallel:ft=64:rpc=1:vec=1:hubt=256,sddmm:rowparallel:ft=64:rpc=16:vec=1:hubt=256,sddmm:rowparallel:ft=64:rpc=4:vec=0:hubt=256 2>&1 | awk -v c=$cfg -v t=$tma '{print c, "tma="t, "tune=", $0}'
+for t in 4x48 4x56 4x64 6x64 8x64 2x40; do
+  AUTOSAGE_DEV_SPMM_TUNE=$t timeout 120 python tools/profile_kernels.py --config $cfg --reps 3 \
+    --spmm spmm:hubsplit:ft=64:rpc=4:vec=1:hubt=256,spmm:rowparallel:ft=64:rpc=4:vec=1:hubt=256 2>&1 \
+    | awk -v c=$cfg -v t=$t '{print c, t, $0}'
 done
