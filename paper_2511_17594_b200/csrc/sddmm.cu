@@ -294,12 +294,13 @@ __global__ void __launch_bounds__(512)
 // and 3 of every float4 carry the 2^896 that widen_scaled() takes out of
 // the matching Y components (widen.cuh).
 __global__ void widen_kernel(const float4* __restrict__ x, double2* __restrict__ xd, std::uint64_t n4,
-                             const unsigned* __restrict__ finite) {
+                             const unsigned* __restrict__ finite, int mix_all) {
     const double up = (finite && *finite) ? kWidenUp : 1.0;
+    const double up01 = mix_all ? up : 1.0;
     for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
          i += std::uint64_t(gridDim.x) * blockDim.x) {
         const float4 v = __ldg(x + i);
-        xd[2 * i] = make_double2(double(v.x), double(v.y));
+        xd[2 * i] = make_double2(double(v.x) * up01, double(v.y) * up01);
         xd[2 * i + 1] = make_double2(double(v.z) * up, double(v.w) * up);
     }
 }
@@ -341,15 +342,16 @@ __device__ __forceinline__ void fixed_pass(const double* __restrict__ xr, const 
         const double2 x01 = ld_x2<XS>(xr + t);
         const double2 x23 = ld_x2<XS>(xr + t + 2);
         if constexpr (ORD == 0) {
-            acc = dfma(x01.x, y4.x, acc);
-            acc = dfma(x01.y, y4.y, acc);
-            acc = __fma_rn(x23.x, widen<MIX>(y4.z), acc);
-            acc = __fma_rn(x23.y, widen<MIX>(y4.w), acc);
+            // MIX 1: components 2,3 re-biased (ALU); MIX 2: all four
+            acc = __fma_rn(x01.x, widen<(MIX >= 2)>(y4.x), acc);
+            acc = __fma_rn(x01.y, widen<(MIX >= 2)>(y4.y), acc);
+            acc = __fma_rn(x23.x, widen<(MIX >= 1)>(y4.z), acc);
+            acc = __fma_rn(x23.y, widen<(MIX >= 1)>(y4.w), acc);
         } else {
-            a0 = dfma(x01.x, y4.x, a0);
-            a1 = dfma(x01.y, y4.y, a1);
-            a2 = __fma_rn(x23.x, widen<MIX>(y4.z), a2);
-            a3 = __fma_rn(x23.y, widen<MIX>(y4.w), a3);
+            a0 = __fma_rn(x01.x, widen<(MIX >= 2)>(y4.x), a0);
+            a1 = __fma_rn(x01.y, widen<(MIX >= 2)>(y4.y), a1);
+            a2 = __fma_rn(x23.x, widen<(MIX >= 1)>(y4.z), a2);
+            a3 = __fma_rn(x23.y, widen<(MIX >= 1)>(y4.w), a3);
             if constexpr (FT != 0 && FT <= FW)
                 if ((t + 4) % FT == 0) fold4(acc, a0, a1, a2, a3);
         }
@@ -454,8 +456,11 @@ __global__ void __launch_bounds__(256, 3)
                        const std::uint32_t* __restrict__ chunk_row, std::uint64_t n_rows,
                        const double* __restrict__ xd, const float* __restrict__ y,
                        float* __restrict__ out, std::uint64_t nnz, std::uint32_t f, std::uint64_t c_begin,
-                       std::uint64_t c_end, const unsigned* __restrict__ finite) {
-    if (finite && *finite)
+                       std::uint64_t c_end, const unsigned* __restrict__ finite, int mix_all) {
+    if (finite && *finite && mix_all)
+        sddmm_fixed_body<FW, ORD, FT, 2, NP>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, f, c_begin,
+                                             c_end);
+    else if (finite && *finite)
         sddmm_fixed_body<FW, ORD, FT, 1, NP>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, f, c_begin,
                                              c_end);
     else
@@ -503,6 +508,9 @@ bool fixed_eligible(const float* x, const float* y, std::uint32_t f, std::uint32
     return int(ft) % fw == 0 || fw % int(ft) == 0;
 }
 
+// all four components re-biased on the ALU pipe (dev knob; default: half)
+int mix_all() { return dev_knob("AUTOSAGE_DEV_SDDMM_MIXALL", 0); }
+
 int sm_count() {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -518,7 +526,8 @@ void widen_x(Graph& g, const float* x, std::uint32_t f, cudaStream_t s, const un
     if (!n4) return;
     const unsigned blocks = unsigned(std::min<std::uint64_t>((n4 + 255) / 256, std::uint64_t(sm_count()) * 8));
     widen_kernel<<<std::max(blocks, 1u), 256, 0, s>>>(reinterpret_cast<const float4*>(x),
-                                                      reinterpret_cast<double2*>(g.xwide.get()), n4, finite);
+                                                      reinterpret_cast<double2*>(g.xwide.get()), n4, finite,
+                                                      mix_all());
     check_launch("widen_kernel");
 }
 
@@ -535,7 +544,8 @@ void launch_sddmm_fixed(Graph& g, const float* y, std::uint32_t f, float* out, s
         const std::uint64_t cap = std::uint64_t(sms) * std::max(per_sm, 1);
         const unsigned blocks = unsigned(std::max<std::uint64_t>(1, std::min(want, cap)));
         kernel<<<blocks, kWarps * 32, smem, s>>>(g.rowptr.get(), g.colind.get(), g.chunk_row.get(), g.n_rows,
-                                                 g.xwide.get(), y, out, g.nnz, f, c_begin, c_end, finite);
+                                                 g.xwide.get(), y, out, g.nnz, f, c_begin, c_end, finite,
+                                                 mix_all());
         check_launch("sddmm_fixed_kernel");
     };
     // FT: 0 = one block over all of F (ft >= f); else the block width
