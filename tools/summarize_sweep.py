@@ -44,6 +44,15 @@ def main():
             for op, e in ops.items():
                 L.append(f"| {f} | {op} | `{e['choice']}` | {f3(e['ms'])} | {e['gbs']:.0f} | "
                          f"{e['frac_hbm']:.2f} | {f3(e['baseline_ms'])} |")
+        cs = r["c2"].get("cusparse")
+        if cs:
+            L += ["", "cuSPARSE on the same graph via torch (fp32 accumulation, so a speed reference only — not the",
+                  "reference's f64 numerics): `torch.sparse.mm` (CSR SpMM) and `torch.sparse.sampled_addmm` (CSR SDDMM).",
+                  "", "| F | cuSPARSE SpMM ms | ours | cuSPARSE SDDMM ms | ours |", "|---|---|---|---|---|"]
+            for f, e in cs.items():
+                o = r["c2"]["by_F"][f]
+                L.append(f"| {f} | {f3(e.get('spmm_ms'))} | {f3(o['spmm']['ms'])} | {f3(e.get('sddmm_ms'))} | "
+                         f"{f3(o['sddmm']['ms'])} |")
         L.append("")
     if "c3" in r:
         c = r["c3"]

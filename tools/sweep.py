@@ -130,12 +130,38 @@ def case_c1(res):
     res["c1"] = {"graph": {"n": m.n_rows, "nnz": m.nnz, "F": f}, "gpu": r, "cpu_reference": cpu}
 
 
+def cusparse_times(m, f, reps=5):
+    """cuSPARSE through torch (fp32 accumulation -- a speed reference only, not
+    the reference numerics): CSR SpMM (torch.sparse.mm) and CSR SDDMM
+    (torch.sparse.sampled_addmm)."""
+    dev = torch.device("cuda")
+    rp = torch.from_numpy(m.rowptr.astype(np.int64)).to(dev)
+    ci = torch.from_numpy(m.colind.astype(np.int64)).to(dev)
+    val = torch.from_numpy(m.val if m.val is not None else np.ones(m.nnz, np.float32)).to(dev)
+    a = torch.sparse_csr_tensor(rp, ci, val, (m.n_rows, m.n_cols))
+    b = torch.from_numpy(asb.fill_uniform(m.n_cols * f, 1 + f, (m.n_cols, f))).to(dev)
+    x = torch.from_numpy(asb.fill_uniform(m.n_rows * f, 1 + f, (m.n_rows, f))).to(dev)
+    out = {}
+    try:
+        out["spmm_ms"] = ev_time(lambda: torch.sparse.mm(a, b), reps)
+    except Exception as e:  # pragma: no cover
+        out["spmm_error"] = str(e)[:200]
+    try:
+        pat = torch.sparse_csr_tensor(rp, ci, torch.ones_like(val), (m.n_rows, m.n_cols))
+        yt = b.t().contiguous()
+        out["sddmm_ms"] = ev_time(lambda: torch.sparse.sampled_addmm(pat, x, yt, beta=0.0, alpha=1.0), reps)
+    except Exception as e:  # pragma: no cover
+        out["sddmm_error"] = str(e)[:200]
+    return out
+
+
 def case_c2(res):
     m, _ = bench.make_graph("reddit", 1)
-    res["c2"] = {"graph": {"n": m.n_rows, "nnz": m.nnz}, "by_F": {}}
+    res["c2"] = {"graph": {"n": m.n_rows, "nnz": m.nnz}, "by_F": {}, "cusparse": {}}
     for f in (32, 64, 128, 256):
         r, _ = run_graph(m, f, reps=5, with_baseline=(f <= 64))
         res["c2"]["by_F"][str(f)] = r
+        res["c2"]["cusparse"][str(f)] = cusparse_times(m, f)
 
 
 def case_c3(res):
