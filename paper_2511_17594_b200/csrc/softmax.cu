@@ -3,8 +3,8 @@
 // Per non-empty row: mx = max over the f32 values; ex_e = f32(exp(f64 v_e -
 // f64 mx)); sum = f64 sum of ex_e in entry order; out_e = f32(f64 ex_e /
 // sum).  Empty rows produce nothing.  The sum is accumulated sequentially
-// in entry order (lane 0 folds each 32-entry chunk via shuffles), so the
-// only difference from the CPU reference can come from exp() itself
+// in entry order (lane 0 folds each 32-entry chunk from shared memory), so
+// the only difference from the CPU reference can come from exp() itself
 // (CUDA's f64 exp vs libm, both within 1 ulp of f64, rounded to f32).
 // The max ignores NaN where std::max would latch it; either way a NaN in a
 // row makes every ex (or the sum) NaN, so all outputs of that row are NaN
@@ -19,39 +19,103 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-__global__ void row_softmax_kernel(const std::uint64_t* __restrict__ rowptr,
-                                   const std::uint32_t* __restrict__ order, std::uint64_t n_rows,
-                                   const float* __restrict__ vin, float* __restrict__ vout) {
+// lane 0 folds 32 staged f64 values into the row's sum, in entry order
+__device__ __forceinline__ double fold_stage(double sum, const double* st, int n) {
+    if (n == 32) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+            const double2 d = *reinterpret_cast<const double2*>(st + j);
+            sum = __dadd_rn(sum, d.x);
+            sum = __dadd_rn(sum, d.y);
+        }
+    } else {
+        for (int j = 0; j < n; ++j) sum = __dadd_rn(sum, st[j]);
+    }
+    return sum;
+}
+
+// Warp per row, rows in degree-descending order.  Rows of at most 32*K
+// entries keep their values in registers (one read of vin, one write of
+// vout); longer rows take three passes over memory.  Both: row max; ex_e =
+// f32(exp(f64 v_e - f64 mx)) for 32 entries at a time, staged as f64 in
+// shared memory and folded into the row's sum by lane 0 in entry order
+// (one DADD per entry on the chain, no shuffles); out_e = f32(f64 ex_e / sum).
+template <int K>
+__global__ void __launch_bounds__(256) row_softmax_kernel(const std::uint64_t* __restrict__ rowptr,
+                                                          const std::uint32_t* __restrict__ order,
+                                                          std::uint64_t n_rows, const float* __restrict__ vin,
+                                                          float* __restrict__ vout) {
+    __shared__ __align__(16) double stage[8][32];
     const int lane = threadIdx.x & 31;
+    double* st = stage[threadIdx.x >> 5];
     const std::uint64_t total_warps = std::uint64_t(gridDim.x) * (blockDim.x >> 5);
     for (std::uint64_t w = (std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n_rows;
          w += total_warps) {
-        const std::uint64_t row = order ? order[w] : w;
+        const std::uint64_t row = order[w];
         const std::uint64_t e0 = rowptr[row], e1 = rowptr[row + 1];
         if (e0 == e1) continue;
+        const std::uint64_t deg = e1 - e0;
+        if (deg <= 32u * K) {
+            // ---- register path
+            float v[K];
+            float mx = -INFINITY;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const std::uint64_t e = e0 + lane + 32u * k;
+                v[k] = e < e1 ? __ldg(vin + e) : -INFINITY;
+                mx = fmaxf(mx, v[k]);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
+            const double dmx = double(mx);
+            double sum = 0.0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const std::uint64_t base = e0 + 32u * k;
+                if (base >= e1) break;
+                const bool ok = base + lane < e1;
+                const float ex = ok ? float(exp(double(v[k]) - dmx)) : 0.f;
+                v[k] = ex;
+                st[lane] = double(ex);
+                __syncwarp();
+                if (lane == 0) sum = fold_stage(sum, st, (e1 - base) < 32 ? int(e1 - base) : 32);
+                __syncwarp();
+            }
+            sum = __shfl_sync(FULL, sum, 0);
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const std::uint64_t e = e0 + lane + 32u * k;
+                if (e < e1) vout[e] = float(__ddiv_rn(double(v[k]), sum));
+            }
+            continue;
+        }
+        // ---- long rows: three passes
         float mx = -INFINITY;
-        for (std::uint64_t e = e0 + lane; e < e1; e += 32) mx = fmaxf(mx, vin[e]);
+#pragma unroll 8
+        for (std::uint64_t e = e0 + lane; e < e1; e += 32) mx = fmaxf(mx, __ldg(vin + e));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
         const double dmx = double(mx);
-        double sum = 0.0;  // meaningful in lane 0
+        double sum = 0.0;  // lane 0
+        float vnext = e0 + lane < e1 ? __ldg(vin + e0 + lane) : 0.f;
         for (std::uint64_t base = e0; base < e1; base += 32) {
             const std::uint64_t e = base + lane;
+            const float v = vnext;
+            vnext = base + 32 + lane < e1 ? __ldg(vin + base + 32 + lane) : 0.f;
             double exd = 0.0;
             if (e < e1) {
-                const float ex = float(exp(double(vin[e]) - dmx));
+                const float ex = float(exp(double(v) - dmx));
                 vout[e] = ex;
                 exd = double(ex);
             }
-            const int n = (e1 - base) < 32 ? int(e1 - base) : 32;
-            for (int j = 0; j < n; ++j) {
-                const double t = __shfl_sync(FULL, exd, j);
-                sum = __dadd_rn(sum, t);
-            }
+            st[lane] = exd;
+            __syncwarp();
+            if (lane == 0) sum = fold_stage(sum, st, (e1 - base) < 32 ? int(e1 - base) : 32);
+            __syncwarp();
         }
         sum = __shfl_sync(FULL, sum, 0);
-        for (std::uint64_t e = e0 + lane; e < e1; e += 32)
-            vout[e] = float(__ddiv_rn(double(vout[e]), sum));
+#pragma unroll 4
+        for (std::uint64_t e = e0 + lane; e < e1; e += 32) vout[e] = float(__ddiv_rn(double(vout[e]), sum));
     }
 }
 
@@ -64,8 +128,8 @@ void launch_row_softmax(Graph& g, const float* vin, float* vout, cudaStream_t s)
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const std::uint64_t want = (g.n_rows * 32 + 255) / 256;
-    const unsigned blocks = unsigned(std::min<std::uint64_t>(want, std::uint64_t(sms) * 16));
-    row_softmax_kernel<<<blocks, 256, 0, s>>>(g.rowptr.get(), g.order.get(), g.n_rows, vin, vout);
+    const unsigned blocks = unsigned(std::min<std::uint64_t>(want, std::uint64_t(sms) * 8));
+    row_softmax_kernel<16><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.order.get(), g.n_rows, vin, vout);
     check_launch("row_softmax_kernel");
 }
 
