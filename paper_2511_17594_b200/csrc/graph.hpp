@@ -96,8 +96,7 @@ struct Graph {
     DevBuf<double> scratch;            // hub partials
     DevBuf<float> tmp;                 // fused-attention scores
     DevBuf<float> att_buf;             // unfused attention: scores | probabilities
-    DevBuf<float> stage_in, stage_out; // host-buffer entry points
-    DevBuf<float> stage_in2;
+    DevBuf<float> stage_in, stage_out; // host-buffer row softmax
     std::map<std::uint64_t, std::uint64_t> ge_count;  // rows with degree >= key
     DevBuf<unsigned> flag;             // finiteness flag of the current dense operand
     DevBuf<double> xwide;              // SDDMM: X widened to f64 (fixed-width path)

@@ -135,15 +135,15 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
 }
 
-// Per-warp shared-memory slice: NB staging buffers of {32 Y rows (f32,
+// Per-warp shared-memory slice of the generic chunk kernel: {32 Y rows (f32,
 // pitch S), kXRows X rows (f32, pitch f)}, then the X rows widened to f64
 // (pitch f+2).
 __host__ __device__ inline std::uint64_t stage_bytes(std::uint32_t f, std::uint32_t S) {
     return (32ull * S * 4 + std::uint64_t(kXRows) * f * 4 + 15) / 16 * 16;
 }
-__host__ __device__ inline std::uint64_t warp_slice_bytes(std::uint32_t f, std::uint32_t S, int nb) {
+__host__ __device__ inline std::uint64_t warp_slice_bytes(std::uint32_t f, std::uint32_t S) {
     const std::uint64_t xd = std::uint64_t(kXRows) * (f + 2) * 8;
-    return std::uint64_t(nb) * stage_bytes(f, S) + ((xd + 15) / 16 * 16);
+    return stage_bytes(f, S) + ((xd + 15) / 16 * 16);
 }
 
 int dev_knob(const char* name, int dflt) {
@@ -156,10 +156,11 @@ struct ChunkMeta {
     bool valid;
 };
 
-// VLOAD: 16-byte copies (vec4 gate passed).  S: smem row pitch in floats
-// (multiple of 4 when VLOAD).  NB: staging buffers per warp (2 = the next
-// chunk's copies overlap this chunk's dots; 1 = twice the resident warps).
-template <bool VLOAD, int ORD, bool VLDS, int MIX, int NB>
+// Generic widths (any F): VLOAD = 16-byte copies (vec4 gate passed); S =
+// smem row pitch in floats (multiple of 4 when VLOAD).  One staging buffer
+// per warp: a second one (copies of the next chunk overlapping this chunk's
+// dots) halved the resident warps and measured slower.
+template <bool VLOAD, int ORD, bool VLDS, int MIX>
 __device__ __forceinline__ void sddmm_chunk_body(
     const std::uint64_t* __restrict__ rowptr, const std::uint32_t* __restrict__ colind,
     const std::uint32_t* __restrict__ chunk_row, std::uint64_t n_rows, const float* __restrict__ x,
@@ -167,7 +168,7 @@ __device__ __forceinline__ void sddmm_chunk_body(
     std::uint64_t c_end, std::uint32_t f, std::uint32_t S, std::uint32_t ft, char* wsm) {
     const int lane = threadIdx.x & 31;
     const std::uint64_t sbytes = stage_bytes(f, S);
-    double* xd = reinterpret_cast<double*>(wsm + NB * sbytes);
+    double* xd = reinterpret_cast<double*>(wsm + sbytes);
     const std::uint32_t xpitch = f + 2;
     const std::uint64_t n_chunks = (nnz + 31) / 32;
     const std::uint64_t stride = std::uint64_t(gridDim.x) * (blockDim.x >> 5);
@@ -188,9 +189,9 @@ __device__ __forceinline__ void sddmm_chunk_body(
         m.r = m.valid ? row_of(rowptr, m.r_first, e) : m.r_first;
         return m;
     };
-    // async copies of chunk c's 32 Y rows and X rows into buffer b
-    auto issue = [&](const ChunkMeta& m, std::uint64_t c, int b) {
-        float* ys = reinterpret_cast<float*>(wsm + b * sbytes);
+    // async copies of chunk c's 32 Y rows and X rows
+    auto issue = [&](const ChunkMeta& m, std::uint64_t c) {
+        float* ys = reinterpret_cast<float*>(wsm);
         float* xs = ys + 32 * S;
         const std::uint64_t e0 = c * 32;
         std::uint32_t j = j_start, q = q_start;
@@ -217,26 +218,13 @@ __device__ __forceinline__ void sddmm_chunk_body(
 
     std::uint64_t c = c_begin + std::uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     ChunkMeta cur = meta(c);
-    ChunkMeta nxt{};
-    if constexpr (NB == 2) {
-        if (c < c_end) issue(cur, c, 0);
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
-        nxt = meta(c + stride);
-    }
-    int b = 0;
     for (; c < c_end; c += stride) {
-        if constexpr (NB == 1) {
-            issue(cur, c, 0);
-            asm volatile("cp.async.commit_group;\n" ::: "memory");
-            nxt = meta(c + stride);  // resolve the next chunk while the copies fly
-            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-        } else {
-            if (c + stride < c_end) issue(nxt, c + stride, b ^ 1);
-            asm volatile("cp.async.commit_group;\n" ::: "memory");
-            asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // chunk c landed
-        }
+        issue(cur, c);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        const ChunkMeta nxt = meta(c + stride);  // resolve the next chunk while the copies fly
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         __syncwarp();
-        const float* ys = reinterpret_cast<const float*>(wsm + b * sbytes);
+        const float* ys = reinterpret_cast<const float*>(wsm);
         const float* xs = ys + 32 * S;
         for (std::uint32_t idx = std::uint32_t(lane); idx < cur.nx * f; idx += 32) {
             const std::uint32_t rr = idx / f;
@@ -253,17 +241,12 @@ __device__ __forceinline__ void sddmm_chunk_body(
         }
         __syncwarp();
         cur = nxt;
-        if constexpr (NB == 2) {
-            nxt = meta(c + 2 * stride);
-            b ^= 1;
-        }
     }
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
 // MIX (re-bias half of the Y widening on the ALU pipe) only when the
 // device-side scan found Y finite and the float4 smem path is in use.
-template <bool VLOAD, int ORD, bool VLDS, int NB>
+template <bool VLOAD, int ORD, bool VLDS>
 __global__ void __launch_bounds__(512)
     sddmm_chunk_kernel(const std::uint64_t* __restrict__ rowptr,
                        const std::uint32_t* __restrict__ colind,
@@ -273,12 +256,12 @@ __global__ void __launch_bounds__(512)
                        std::uint64_t c_end, std::uint32_t f, std::uint32_t S, std::uint32_t ft,
                        const unsigned* __restrict__ finite, int allow_mix) {
     extern __shared__ __align__(16) char smem[];
-    char* wsm = smem + std::uint64_t(threadIdx.x >> 5) * warp_slice_bytes(f, S, NB);
+    char* wsm = smem + std::uint64_t(threadIdx.x >> 5) * warp_slice_bytes(f, S);
     if (VLDS && allow_mix && finite && *finite)
-        sddmm_chunk_body<VLOAD, ORD, VLDS, 1, NB>(rowptr, colind, chunk_row, n_rows, x, y, out, nnz, c_begin,
+        sddmm_chunk_body<VLOAD, ORD, VLDS, 1>(rowptr, colind, chunk_row, n_rows, x, y, out, nnz, c_begin,
                                                   c_end, f, S, ft, wsm);
     else
-        sddmm_chunk_body<VLOAD, ORD, VLDS, 0, NB>(rowptr, colind, chunk_row, n_rows, x, y, out, nnz, c_begin,
+        sddmm_chunk_body<VLOAD, ORD, VLDS, 0>(rowptr, colind, chunk_row, n_rows, x, y, out, nnz, c_begin,
                                                   c_end, f, S, ft, wsm);
 }
 
@@ -631,7 +614,7 @@ void launch_sddmm_chunks(Graph& g, const float* x, const float* y, std::uint32_t
     const bool vlds = vload && (ord == 0 || ft % 4 == 0);
     const std::uint32_t S = vload ? 4 * ((f / 4) | 1u) : (f | 1u);
     const int allow_mix = dev_knob("AUTOSAGE_DEV_SDDMM_MIX", 0);
-    const std::uint64_t per_warp = warp_slice_bytes(f, S, 1);
+    const std::uint64_t per_warp = warp_slice_bytes(f, S);
     constexpr std::uint64_t kSmemMax = 200 * 1024;
     wpb = std::clamp<std::uint32_t>(wpb, 1, 16);
     while (wpb > 1 && per_warp * wpb > kSmemMax) --wpb;
@@ -653,12 +636,12 @@ void launch_sddmm_chunks(Graph& g, const float* x, const float* y, std::uint32_t
         check_launch("sddmm_chunk_kernel");
     };
     if (vload) {
-        if (ord == 0) go(sddmm_chunk_kernel<true, 0, true, 1>);
-        else if (vlds) go(sddmm_chunk_kernel<true, 1, true, 1>);
-        else go(sddmm_chunk_kernel<true, 1, false, 1>);
+        if (ord == 0) go(sddmm_chunk_kernel<true, 0, true>);
+        else if (vlds) go(sddmm_chunk_kernel<true, 1, true>);
+        else go(sddmm_chunk_kernel<true, 1, false>);
     } else {
-        if (ord == 0) go(sddmm_chunk_kernel<false, 0, false, 1>);
-        else go(sddmm_chunk_kernel<false, 1, false, 1>);
+        if (ord == 0) go(sddmm_chunk_kernel<false, 0, false>);
+        else go(sddmm_chunk_kernel<false, 1, false>);
     }
 }
 

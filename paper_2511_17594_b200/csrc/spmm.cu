@@ -50,11 +50,11 @@ __device__ __forceinline__ float comp(const float4& v, int q) {
     return q == 0 ? v.x : (q == 1 ? v.y : (q == 2 ? v.z : v.w));
 }
 
-__host__ __device__ constexpr int unroll_for(int vec, int nch) {
+[[maybe_unused]] __host__ __device__ constexpr int unroll_for(int vec, int nch) {
     return vec == 4 ? (nch == 1 ? 4 : (nch == 2 ? 2 : 1)) : (nch >= 8 ? 1 : 8 / nch);
 }
 
-__host__ __device__ constexpr int maxreg_for(int vec, int nch) {
+[[maybe_unused]] __host__ __device__ constexpr int maxreg_for(int vec, int nch) {
     // float4 single-chunk tiles at 64 registers (32 warps/SM): 48 spilled the
     // 4 in-flight entries and cost Reddit-shape 2.35 -> 2.41 ms (hubsplit) and
     // 3.24 -> 4.01 ms (rowparallel); wider tiles keep their loads in registers

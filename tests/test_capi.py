@@ -323,3 +323,33 @@ def test_device_entry_points_fail_loudly_without_a_gpu():
         pass
     with pytest.raises((asb.CudaError, MemoryError, RuntimeError)):
         asb.Graph.from_csr(identity(4))
+
+
+def _build_c_client(tmp_path):
+    import shutil
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("gcc not available")
+    exe = tmp_path / "c_client"
+    lib_dir = os.path.join(root, "paper_2511_17594_b200")
+    subprocess.run([gcc, "-std=c11", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(root, "include"),
+                    os.path.join(root, "examples", "c_client.c"), "-L", lib_dir, "-lautosage_b200",
+                    f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
+    return exe
+
+
+def test_c_client_compiles_and_links_against_the_abi(tmp_path):
+    """A plain C program builds against include/autosage_b200.h and links the
+    shared library (the drop-in boundary)."""
+    assert _build_c_client(tmp_path).exists()
+
+
+@pytest.mark.gpu
+def test_c_client_runs_the_reference_worked_example(tmp_path):
+    import subprocess
+    exe = _build_c_client(tmp_path)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "OK" in r.stdout
