@@ -362,16 +362,23 @@ void ensure_pipe(Graph& g) {
 }
 
 void ensure_slices(Graph& g, std::size_t k) {
-    while (g.pipe.slice.size() < k) {
-        cudaEvent_t e;
-        ASB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        g.pipe.slice.push_back(e);
-    }
+    for (auto* v : {&g.pipe.slice, &g.pipe.slice_x})
+        while (v->size() < k) {
+            cudaEvent_t e;
+            ASB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            v->push_back(e);
+        }
+}
+
+// row holding entry e (host rowptr mirror)
+std::uint64_t host_row_of(const Graph& g, std::uint64_t e) {
+    const auto it = std::upper_bound(g.h_rowptr.begin(), g.h_rowptr.end(), e);
+    return std::uint64_t(it - g.h_rowptr.begin()) - 1;
 }
 
 std::uint64_t host_slices() {
     const auto k = env::get_int("AUTOSAGE_HOST_SLICES");
-    return k && *k > 0 ? std::uint64_t(*k) : 8;
+    return k && *k > 0 ? std::uint64_t(*k) : 16;
 }
 
 }  // namespace
@@ -431,8 +438,7 @@ KernelResult sddmm_host(const as_variant* v, Graph& g, const float* x_host, std:
     P.y.ensure(std::max<std::uint64_t>(y_rows * f, 1));
     P.v.ensure(std::max<std::uint64_t>(g.nnz, 1));
     ASB_CUDA(cudaStreamWaitEvent(P.h2d, P.sddmm_done, 0));
-    if (x_rows * f)
-        ASB_CUDA(cudaMemcpyAsync(P.x.get(), x_host, x_rows * f * 4, cudaMemcpyHostToDevice, P.h2d));
+    // Y first (every slice gathers from all of it); X follows slice by slice
     if (y_rows * f)
         ASB_CUDA(cudaMemcpyAsync(P.y.get(), y_host, y_rows * f * 4, cudaMemcpyHostToDevice, P.h2d));
     ASB_CUDA(cudaEventRecord(P.sddmm_in, P.h2d));
@@ -450,13 +456,24 @@ KernelResult sddmm_host(const as_variant* v, Graph& g, const float* x_host, std:
     ensure_slices(g, std::size_t(k));
     const unsigned* fin = nullptr;
     const std::uint32_t wpb = std::uint32_t(std::min<std::uint64_t>(r.variant.rows_per_chunk, 16));
-    if (r.variant.mapping != AS_MAP_BASELINE) {
-        fin = finite_flag(g, y, y_rows * f, g.stream);
-        sddmm_chunks_prepare(g, x, y, std::uint32_t(f), r.variant.f_tile, vec, g.stream, fin);
-    }
+    if (r.variant.mapping != AS_MAP_BASELINE) fin = finite_flag(g, y, y_rows * f, g.stream);
+    std::uint64_t x_done = 0;  // X rows [0, x_done) queued
     for (std::uint64_t i = 0; i < k && n_chunks; ++i) {
         const std::uint64_t c0 = i * per, c1 = std::min(n_chunks, c0 + per);
         if (c0 >= c1) break;
+        // X rows of this slice's entries
+        const std::uint64_t ra = host_row_of(g, c0 * 32);
+        const std::uint64_t rb = host_row_of(g, std::min(c1 * 32, g.nnz) - 1) + 1;
+        if (rb > x_done && f) {
+            const std::uint64_t from = std::max(ra, x_done);
+            ASB_CUDA(cudaMemcpyAsync(P.x.get() + from * f, x_host + from * f, (rb - from) * f * 4,
+                                     cudaMemcpyHostToDevice, P.h2d));
+            x_done = rb;
+        }
+        ASB_CUDA(cudaEventRecord(P.slice_x[i], P.h2d));
+        ASB_CUDA(cudaStreamWaitEvent(g.stream, P.slice_x[i], 0));
+        if (r.variant.mapping != AS_MAP_BASELINE)
+            sddmm_chunks_prepare(g, x, y, std::uint32_t(f), r.variant.f_tile, vec, g.stream, fin, ra, rb);
         if (r.variant.mapping == AS_MAP_BASELINE)
             launch_sddmm_baseline(g, x, y, std::uint32_t(f), out, g.stream, c0, c1);
         else
@@ -467,6 +484,9 @@ KernelResult sddmm_host(const as_variant* v, Graph& g, const float* x_host, std:
         const std::uint64_t e0 = c0 * 32, e1 = std::min(c1 * 32, g.nnz);
         ASB_CUDA(cudaMemcpyAsync(out_host + e0, out + e0, (e1 - e0) * 4, cudaMemcpyDeviceToHost, P.d2h));
     }
+    if (x_done < x_rows && f)  // rows after the last entry (empty rows): keep P.x complete
+        ASB_CUDA(cudaMemcpyAsync(P.x.get() + x_done * f, x_host + x_done * f, (x_rows - x_done) * f * 4,
+                                 cudaMemcpyHostToDevice, P.h2d));
     ASB_CUDA(cudaEventRecord(P.sddmm_done, g.stream));
     ASB_CUDA(cudaStreamWaitEvent(P.d2h, P.sddmm_done, 0));
     ASB_CUDA(cudaEventRecord(P.sddmm_out, P.d2h));

@@ -124,6 +124,7 @@ Graph::~Graph() {
                           pipe.sddmm_out})
         if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : pipe.slice) cudaEventDestroy(e);
+    for (cudaEvent_t e : pipe.slice_x) cudaEventDestroy(e);
 }
 
 std::uint64_t rows_with_degree_at_least(Graph& g, std::uint64_t d) {

@@ -113,7 +113,8 @@ struct Graph {
         // outputs copied (staging writable again)
         cudaEvent_t spmm_in = nullptr, spmm_done = nullptr, spmm_out = nullptr;
         cudaEvent_t sddmm_in = nullptr, sddmm_done = nullptr, sddmm_out = nullptr;
-        std::vector<cudaEvent_t> slice;  // SDDMM output slices
+        std::vector<cudaEvent_t> slice;    // SDDMM output slices computed
+        std::vector<cudaEvent_t> slice_x;  // ... and their X rows landed
     } pipe;
 
     ~Graph();

@@ -39,8 +39,10 @@ void launch_sddmm_chunks(Graph& g, const float* x, const float* y, std::uint32_t
                          std::uint64_t f_tile, bool vec, std::uint32_t wpb, cudaStream_t s,
                          const unsigned* finite = nullptr, std::uint64_t c_begin = 0,
                          std::uint64_t c_end = kAllChunks, bool prepare = true);
+// rows [r0, r1) of X only (the host pipeline streams X in row slices)
 void sddmm_chunks_prepare(Graph& g, const float* x, const float* y, std::uint32_t f,
-                          std::uint64_t f_tile, bool vec, cudaStream_t s, const unsigned* finite);
+                          std::uint64_t f_tile, bool vec, cudaStream_t s, const unsigned* finite,
+                          std::uint64_t r0 = 0, std::uint64_t r1 = ~0ull);
 
 // Device flag: 1 iff p[0..n) has no Inf/NaN (gates the re-bias widening,
 // widen.cuh).  Written into g.flag (one flag per graph; a graph handle runs

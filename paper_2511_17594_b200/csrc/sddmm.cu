@@ -502,15 +502,18 @@ int sm_count() {
 }
 
 // X widened to f64 (prepass of the fixed-width path, once per call)
-void widen_x(Graph& g, const float* x, std::uint32_t f, cudaStream_t s, const unsigned* finite) {
-    const std::uint64_t nx = g.n_rows * f;
-    g.xwide.ensure(std::max<std::uint64_t>(nx, 1));
-    const std::uint64_t n4 = nx / 4;
+// rows [r0, r1) of X (the host pipeline widens each slice's rows as they land)
+void widen_x(Graph& g, const float* x, std::uint32_t f, cudaStream_t s, const unsigned* finite,
+             std::uint64_t r0 = 0, std::uint64_t r1 = ~0ull) {
+    g.xwide.ensure(std::max<std::uint64_t>(g.n_rows * f, 1));
+    r1 = std::min(r1, g.n_rows);
+    if (r0 >= r1) return;
+    const std::uint64_t off4 = r0 * f / 4, n4 = (r1 - r0) * f / 4;
     if (!n4) return;
     const unsigned blocks = unsigned(std::min<std::uint64_t>((n4 + 255) / 256, std::uint64_t(sm_count()) * 8));
-    widen_kernel<<<std::max(blocks, 1u), 256, 0, s>>>(reinterpret_cast<const float4*>(x),
-                                                      reinterpret_cast<double2*>(g.xwide.get()), n4, finite,
-                                                      mix_all());
+    widen_kernel<<<std::max(blocks, 1u), 256, 0, s>>>(reinterpret_cast<const float4*>(x) + off4,
+                                                      reinterpret_cast<double2*>(g.xwide.get()) + 2 * off4, n4,
+                                                      finite, mix_all());
     check_launch("widen_kernel");
 }
 
@@ -580,12 +583,13 @@ void launch_sddmm_baseline(Graph& g, const float* x, const float* y, std::uint32
 }
 
 void sddmm_chunks_prepare(Graph& g, const float* x, const float* y, std::uint32_t f,
-                          std::uint64_t f_tile, bool vec, cudaStream_t s, const unsigned* finite) {
+                          std::uint64_t f_tile, bool vec, cudaStream_t s, const unsigned* finite,
+                          std::uint64_t r0, std::uint64_t r1) {
     if (g.nnz == 0 || f == 0) return;
     ensure_chunk_rows(g);
     const std::uint32_t ft = std::uint32_t(effective_tile(f_tile, f));
     if (fixed_eligible(x, y, f, ft, vec ? 1 : 0))
-        widen_x(g, x, f, s, dev_knob("AUTOSAGE_DEV_SDDMM_MIX", 1) ? finite : nullptr);
+        widen_x(g, x, f, s, dev_knob("AUTOSAGE_DEV_SDDMM_MIX", 1) ? finite : nullptr, r0, r1);
 }
 
 void launch_sddmm_chunks(Graph& g, const float* x, const float* y, std::uint32_t f, float* out,
