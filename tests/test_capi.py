@@ -140,6 +140,52 @@ def test_cost_model_reference_properties():
         asb.estimate_cost(v, gf, 64, asb.DeviceProfile.fixed(0.0, 1.0, 1))
 
 
+B200 = asb.DeviceProfile("b200-test|cores=148|x", 6.0e12, 30.0e12, 148, 1)
+
+
+def test_b200_cost_model_refinement():
+    """AS_MODEL_B200: SpMM pays 8 bytes/nnz per extra
+    f_tile pass; SDDMM has no imbalance penalty.  The reference model is
+    untouched for model-0 profiles (test above)."""
+    rng = np.random.default_rng(5)
+    gf = feats_of(hub_graph(rng, 1000, [400], 5, False))
+    ref = asb.DeviceProfile(B200.device_sig, B200.bw_eff, B200.flops_eff, B200.cores, 0)
+
+    def v(op, mapping, ft):
+        return asb.KernelVariant(op, mapping, ft, 4, True, 256)
+    nnz, n, f = gf.nnz, gf.n_rows, 64
+    base = (8.0 * nnz + 4.0 * nnz * f + 4.0 * n * f + 8.0 * (n + 1)) / B200.bw_eff * 1e3
+    assert asb.estimate_cost(v(asb.SPMM, asb.HUBSPLIT, 64), gf, f, B200) == pytest.approx(base, rel=1e-12)
+    assert asb.estimate_cost(v(asb.SPMM, asb.HUBSPLIT, 32), gf, f, B200) == \
+        pytest.approx((8.0 * nnz * 2 + 4.0 * nnz * f + 4.0 * n * f + 8.0 * (n + 1)) / B200.bw_eff * 1e3,
+                      rel=1e-12)
+    # ft beyond F is one pass, like ft == F
+    assert asb.estimate_cost(v(asb.SPMM, asb.HUBSPLIT, 128), gf, f, B200) == \
+        asb.estimate_cost(v(asb.SPMM, asb.HUBSPLIT, 64), gf, f, B200)
+    # SDDMM: both mappings cost the same; the reference model penalises rowparallel
+    sd = [asb.estimate_cost(v(asb.SDDMM, m, 64), gf, f, B200) for m in (asb.ROWPARALLEL, asb.HUBSPLIT)]
+    assert sd[0] == sd[1]
+    assert asb.estimate_cost(v(asb.SDDMM, asb.ROWPARALLEL, 64), gf, f, ref) > \
+        asb.estimate_cost(v(asb.SDDMM, asb.HUBSPLIT, 64), gf, f, ref)
+
+
+def test_b200_probes_compare_distinct_kernels():
+    """Under the B200 model the top_k probes are distinct sm_100a launches:
+    SpMM vec/scalar and rows_per_chunk variants collapse onto one kernel."""
+    rng = np.random.default_rng(6)
+    gf = feats_of(hub_graph(rng, 1000, [400], 5, False))
+    ctx = asb.ScheduleContext(device=B200, timer=FakeTimer([5.0, 4.0, 3.0, 2.0]))
+    d = asb.decide_host(ctx, asb.ProbeConfig(iters=1, cap_ms=1e9, top_k=3), 0x77, gf, 64, asb.SPMM, 64)
+    keys = [(c.variant.mapping, min(c.variant.f_tile, 64)) for c in d.candidates]
+    assert len(keys) == 3 and len(set(keys)) == 3
+    assert keys[0] == (asb.HUBSPLIT, 64)  # one pass, no imbalance penalty
+    sctx = asb.ScheduleContext(device=B200, timer=FakeTimer([5.0, 4.0, 3.0, 2.0]))
+    s = asb.decide_host(sctx, asb.ProbeConfig(iters=1, cap_ms=1e9, top_k=3), 0x78, gf, 64, asb.SDDMM, 64)
+    skeys = [(c.variant.vectorized, min(c.variant.f_tile, 64) if c.variant.vectorized else 0)
+             for c in s.candidates]
+    assert len(set(skeys)) == len(skeys) == 3
+
+
 # ---- time_kernel and the decision procedure (test_scheduler.cpp) -----------------------
 def test_time_kernel_policy_matches_reference():
     for script, iters, cap in (([0.1] * 5, 5, 1.0), ([2.0], 5, 1.0), ([3.0, 1.0, 2.0], 3, 1e9),
