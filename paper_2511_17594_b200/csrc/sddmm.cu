@@ -292,13 +292,26 @@ __global__ void widen_kernel(const float4* __restrict__ x, double2* __restrict__
 template <int FW>
 struct FixedShape {
     static constexpr int NV = FW / 4;                 // 16-byte units per row slice
-    static constexpr int S = 4 * (NV | 1);            // smem pitch in floats (odd # of 16 B)
+    static constexpr int S = FW;                      // smem pitch in floats: rows 16-B aligned,
+                                                      // 16-B chunks XOR-swizzled (see swz)
     static constexpr int kCopies = NV;                // cp.async per lane per pass (32 rows)
     static constexpr int KX = FW >= 64 ? 1 : 64 / FW; // X rows (f64) staged per chunk
     static constexpr int kXUnits = KX * FW / 2;       // their 16-byte units per pass
     static constexpr std::uint64_t kYBytes = 32ull * S * 4;
     static constexpr std::uint64_t kWarpBytes = kYBytes + std::uint64_t(KX) * FW * 8;
 };
+
+// Y rows sit unpadded in shared memory, so each 256-B row is written as two
+// whole 128-B wavefronts; 16-byte chunk c of row j is stored at c ^ swz(j).
+// When lane j then reads chunk c of its own row, any 8 consecutive lanes hit
+// 8 distinct 16-B bank groups (NV >= 8: j & 7 permutes the chunk index
+// within 128 B; NV == 4: rows are 64 B, so alternate lanes already sit in
+// opposite halves of a 128-B segment and (j >> 1) & 3 separates the rest).
+template <int NV>
+__device__ __forceinline__ int swz(int j) {
+    if constexpr (NV >= 8) return j & 7;
+    else return (j >> 1) & 3;
+}
 
 template <bool SMEM>
 __device__ __forceinline__ double2 ld_x2(const double* p) {
@@ -317,11 +330,12 @@ __device__ __forceinline__ void fold4(double& acc, double& a0, double& a1, doubl
 // chain(s).  ORD 0: one sequential chain.  ORD 1: four stride-4 partials per
 // f_tile block; FT = 0 means one block over all F.
 template <int FW, int ORD, int FT, bool XS, int MIX>
-__device__ __forceinline__ void fixed_pass(const double* __restrict__ xr, const float* yr, int p, int npass,
-                                           double& acc, double& a0, double& a1, double& a2, double& a3) {
+__device__ __forceinline__ void fixed_pass(const double* __restrict__ xr, const float* yr, int key, int p,
+                                           int npass, double& acc, double& a0, double& a1, double& a2,
+                                           double& a3) {
 #pragma unroll 8
     for (int t = 0; t < FW; t += 4) {
-        const float4 y4 = *reinterpret_cast<const float4*>(yr + t);
+        const float4 y4 = *reinterpret_cast<const float4*>(yr + 4 * ((t >> 2) ^ key));
         const double2 x01 = ld_x2<XS>(xr + t);
         const double2 x23 = ld_x2<XS>(xr + t + 2);
         if constexpr (ORD == 0) {
@@ -385,7 +399,7 @@ __device__ __forceinline__ void sddmm_fixed_body(const std::uint64_t* __restrict
             const int idx = it * 32 + lane;
             const int j = idx / Sh::NV, q = idx % Sh::NV;
             const std::uint32_t cj = __shfl_sync(FULL, m.col, j);
-            cp_async16(ys + j * Sh::S + 4 * q, y + std::uint64_t(cj) * F + p * FW + 4 * q);
+            cp_async16(ys + j * Sh::S + 4 * (q ^ swz<Sh::NV>(j)), y + std::uint64_t(cj) * F + p * FW + 4 * q);
         }
 #pragma unroll
         for (int u = lane; u < Sh::kXUnits; u += 32) {
@@ -414,6 +428,7 @@ __device__ __forceinline__ void sddmm_fixed_body(const std::uint64_t* __restrict
         }
         const std::uint32_t rel = r - cur.r_first;
         const float* yr = ys + lane * Sh::S;
+        const int key = swz<Sh::NV>(lane);
         double acc = 0.0, a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         for (int p = 0; p < npass; ++p) {
             if (p > 0) issue(cur, p);
@@ -421,9 +436,9 @@ __device__ __forceinline__ void sddmm_fixed_body(const std::uint64_t* __restrict
             __syncwarp();
             if (e < nnz) {
                 if (rel < Sh::KX)
-                    fixed_pass<FW, ORD, FT, true, MIX>(xs + rel * FW, yr, p, npass, acc, a0, a1, a2, a3);
+                    fixed_pass<FW, ORD, FT, true, MIX>(xs + rel * FW, yr, key, p, npass, acc, a0, a1, a2, a3);
                 else
-                    fixed_pass<FW, ORD, FT, false, MIX>(xd + std::uint64_t(r) * F + p * FW, yr, p, npass, acc,
+                    fixed_pass<FW, ORD, FT, false, MIX>(xd + std::uint64_t(r) * F + p * FW, yr, key, p, npass, acc,
                                                         a0, a1, a2, a3);
             }
             __syncwarp();
