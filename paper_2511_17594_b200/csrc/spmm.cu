@@ -556,6 +556,10 @@ int dev_tune() {
         if (v == "4x56") return 8;
         if (v == "4x64") return 9;
         if (v == "6x64") return 10;
+        if (v == "6x80") return 11;
+        if (v == "8x80") return 12;
+        if (v == "8x96") return 13;
+        if (v == "4x72") return 14;
         return 0;
     }();
     return t;
@@ -575,6 +579,10 @@ void launch_tuned(const SegArgs& a, unsigned blocks, unsigned threads, cudaStrea
             case 8: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 4, 56><<<blocks, threads, 0, s>>>(a); return;
             case 9: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 4, 64><<<blocks, threads, 0, s>>>(a); return;
             case 10: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 6, 64><<<blocks, threads, 0, s>>>(a); return;
+            case 11: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 6, 80><<<blocks, threads, 0, s>>>(a); return;
+            case 12: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 8, 80><<<blocks, threads, 0, s>>>(a); return;
+            case 13: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 8, 96><<<blocks, threads, 0, s>>>(a); return;
+            case 14: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 4, 72><<<blocks, threads, 0, s>>>(a); return;
             default: break;
         }
     }
