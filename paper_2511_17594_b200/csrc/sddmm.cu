@@ -466,6 +466,162 @@ __global__ void __launch_bounds__(256, 3)
                                              c_end);
 }
 
+// ---------------------------------------------------------------------------
+// Pair path (single-pass F in {32, 64}): each lane owns two entries, e and
+// e + 32, of a 64-entry chunk.  The broadcast X reads (half of the shared-
+// memory wavefronts of a 32-entry chunk) then serve two dot chains, and each
+// lane has two independent chains in flight.  64 staged Y rows per warp.
+// ---------------------------------------------------------------------------
+template <int F>
+struct PairShape {
+    static constexpr int NV = F / 4;
+    static constexpr int kCopies = 2 * NV;  // cp.async per lane per chunk (64 rows)
+    static constexpr int KX = 2;            // X rows staged
+    static constexpr int kXUnits = KX * F / 2;
+    static constexpr std::uint64_t kYBytes = 64ull * F * 4;
+    static constexpr std::uint64_t kWarpBytes = kYBytes + std::uint64_t(KX) * F * 8;
+};
+
+template <int F, int ORD, int FT, bool XS, int MIX>
+__device__ __forceinline__ void pair_pass(const double* __restrict__ xa, const double* __restrict__ xb, bool same_x,
+                                          const float* ya, const float* yb, int ka, int kb, double (&c)[2][5]) {
+#pragma unroll 4
+    for (int t = 0; t < F; t += 4) {
+        const float4 u = *reinterpret_cast<const float4*>(ya + 4 * ((t >> 2) ^ ka));
+        const float4 w = *reinterpret_cast<const float4*>(yb + 4 * ((t >> 2) ^ kb));
+        const double2 x01 = ld_x2<XS>(xa + t);
+        const double2 x23 = ld_x2<XS>(xa + t + 2);
+        double2 z01 = x01, z23 = x23;
+        if (!same_x) {
+            z01 = ld_x2<XS>(xb + t);
+            z23 = ld_x2<XS>(xb + t + 2);
+        }
+        if constexpr (ORD == 0) {
+            c[0][0] = __fma_rn(x01.x, widen<0>(u.x), c[0][0]);
+            c[1][0] = __fma_rn(z01.x, widen<0>(w.x), c[1][0]);
+            c[0][0] = __fma_rn(x01.y, widen<0>(u.y), c[0][0]);
+            c[1][0] = __fma_rn(z01.y, widen<0>(w.y), c[1][0]);
+            c[0][0] = __fma_rn(x23.x, widen<MIX>(u.z), c[0][0]);
+            c[1][0] = __fma_rn(z23.x, widen<MIX>(w.z), c[1][0]);
+            c[0][0] = __fma_rn(x23.y, widen<MIX>(u.w), c[0][0]);
+            c[1][0] = __fma_rn(z23.y, widen<MIX>(w.w), c[1][0]);
+        } else {
+            c[0][1] = __fma_rn(x01.x, widen<0>(u.x), c[0][1]);
+            c[1][1] = __fma_rn(z01.x, widen<0>(w.x), c[1][1]);
+            c[0][2] = __fma_rn(x01.y, widen<0>(u.y), c[0][2]);
+            c[1][2] = __fma_rn(z01.y, widen<0>(w.y), c[1][2]);
+            c[0][3] = __fma_rn(x23.x, widen<MIX>(u.z), c[0][3]);
+            c[1][3] = __fma_rn(z23.x, widen<MIX>(w.z), c[1][3]);
+            c[0][4] = __fma_rn(x23.y, widen<MIX>(u.w), c[0][4]);
+            c[1][4] = __fma_rn(z23.y, widen<MIX>(w.w), c[1][4]);
+            const bool block_end = FT == 0 ? t + 4 == F : ((t + 4) % FT == 0 || t + 4 == F);
+            if (block_end) {
+                fold4(c[0][0], c[0][1], c[0][2], c[0][3], c[0][4]);
+                fold4(c[1][0], c[1][1], c[1][2], c[1][3], c[1][4]);
+            }
+        }
+    }
+}
+
+template <int F, int ORD, int FT, int MIX>
+__device__ __forceinline__ void sddmm_pair_body(const std::uint64_t* __restrict__ rowptr,
+                                                const std::uint32_t* __restrict__ colind,
+                                                const std::uint32_t* __restrict__ chunk_row, std::uint64_t n_rows,
+                                                const double* __restrict__ xd, const float* __restrict__ y,
+                                                float* __restrict__ out, std::uint64_t nnz, std::uint64_t c_begin,
+                                                std::uint64_t c_end) {
+    using Sh = PairShape<F>;
+    extern __shared__ __align__(16) char smem[];
+    char* wsm = smem + std::uint64_t(threadIdx.x >> 5) * Sh::kWarpBytes;
+    float* ys = reinterpret_cast<float*>(wsm);
+    double* xs = reinterpret_cast<double*>(wsm + Sh::kYBytes);
+    const int lane = threadIdx.x & 31;
+    const std::uint64_t e_end = min(c_end * 32, nnz);
+    const std::uint64_t n_pairs = (c_end - c_begin + 1) / 2;
+    const std::uint64_t stride = std::uint64_t(gridDim.x) * (blockDim.x >> 5);
+
+    struct Meta {
+        std::uint32_t ca, cb, r_first;
+        std::uint64_t bound;
+    };
+    auto meta = [&](std::uint64_t pc) {
+        Meta m{0u, 0u, 0u, ~0ull};
+        if (pc >= n_pairs) return m;
+        const std::uint64_t e0 = (c_begin + 2 * pc) * 32;
+        m.ca = e0 + lane < e_end ? __ldg(colind + e0 + lane) : 0u;
+        m.cb = e0 + 32 + lane < e_end ? __ldg(colind + e0 + 32 + lane) : 0u;
+        m.r_first = __ldg(chunk_row + c_begin + 2 * pc);
+        const std::uint64_t bi = std::uint64_t(m.r_first) + 1 + lane;
+        if (bi <= n_rows) m.bound = __ldg(rowptr + bi);
+        return m;
+    };
+
+    std::uint64_t pc = std::uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    Meta cur = meta(pc);
+    for (; pc < n_pairs; pc += stride) {
+#pragma unroll
+        for (int it = 0; it < Sh::kCopies; ++it) {
+            const int idx = it * 32 + lane;
+            const int j = idx / Sh::NV, q = idx % Sh::NV;
+            const std::uint32_t cj = __shfl_sync(FULL, j < 32 ? cur.ca : cur.cb, j & 31);
+            cp_async16(ys + j * F + 4 * (q ^ swz<Sh::NV>(j)), y + std::uint64_t(cj) * F + 4 * q);
+        }
+#pragma unroll
+        for (int u = lane; u < Sh::kXUnits; u += 32) {
+            const int k = u / (F / 2), uu = u % (F / 2);
+            const std::uint64_t xr = std::uint64_t(cur.r_first) + k;
+            if (xr < n_rows) cp_async16(xs + 2 * u, xd + xr * F + 2 * uu);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        const Meta nxt = meta(pc + stride);
+        const std::uint64_t e0 = (c_begin + 2 * pc) * 32, ea = e0 + lane, eb = ea + 32;
+        std::uint32_t ra = cur.r_first, rb = cur.r_first;
+        const unsigned inside = __ballot_sync(FULL, cur.bound <= e0 + 63);
+        if (inside) {
+            const int k = __popc(inside);
+#pragma unroll 1
+            for (int b = 0; b < k; ++b) {
+                const std::uint64_t bb = __shfl_sync(FULL, cur.bound, b);
+                ra += bb <= ea ? 1u : 0u;
+                rb += bb <= eb ? 1u : 0u;
+            }
+            if (k == 32) {  // more than 32 rows meet in these 64 entries
+                ra = row_of(rowptr, ra, ea);
+                rb = row_of(rowptr, rb, eb);
+            }
+        }
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        __syncwarp();
+        const std::uint32_t rela = ra - cur.r_first, relb = rb - cur.r_first;
+        double c[2][5] = {{0.0, 0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0, 0.0}};
+        const float* ya = ys + lane * F;
+        const float* yb = ys + (lane + 32) * F;
+        const int ka = swz<Sh::NV>(lane), kb = swz<Sh::NV>(lane + 32);
+        if (rela < Sh::KX && relb < Sh::KX)
+            pair_pass<F, ORD, FT, true, MIX>(xs + rela * F, xs + relb * F, rela == relb, ya, yb, ka, kb, c);
+        else
+            pair_pass<F, ORD, FT, false, MIX>(xd + std::uint64_t(ra) * F, xd + std::uint64_t(rb) * F, ra == rb, ya,
+                                              yb, ka, kb, c);
+        if (ea < e_end) out[ea] = float(c[0][0]);
+        if (eb < e_end) out[eb] = float(c[1][0]);
+        __syncwarp();
+        cur = nxt;
+    }
+}
+
+template <int F, int ORD, int FT>
+__global__ void __launch_bounds__(128, 3)
+    sddmm_pair_kernel(const std::uint64_t* __restrict__ rowptr, const std::uint32_t* __restrict__ colind,
+                      const std::uint32_t* __restrict__ chunk_row, std::uint64_t n_rows,
+                      const double* __restrict__ xd, const float* __restrict__ y, float* __restrict__ out,
+                      std::uint64_t nnz, std::uint32_t /*f*/, std::uint64_t c_begin, std::uint64_t c_end,
+                      const unsigned* __restrict__ finite, int /*mix_all*/) {
+    if (finite && *finite)
+        sddmm_pair_body<F, ORD, FT, 1>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin, c_end);
+    else
+        sddmm_pair_body<F, ORD, FT, 0>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin, c_end);
+}
+
 // Guardrail baseline / large-F fallback: lane per entry, both rows read
 // straight from global memory, scalar loads.
 template <int ORD>
@@ -559,6 +715,34 @@ void launch_sddmm_fixed(Graph& g, const float* y, std::uint32_t f, float* out, s
         else if (ft == 64) go(sddmm_fixed_kernel<FW, 1, 64, NP>, wb);
         else go(sddmm_fixed_kernel<FW, 1, 128, NP>, wb);
     };
+    if ((f == 32 || f == 64) && dev_knob("AUTOSAGE_DEV_SDDMM_PAIR", 1)) {
+        auto pair = [&](auto fc) {
+            constexpr int F = decltype(fc)::value;
+            const std::uint64_t wb = PairShape<F>::kWarpBytes;
+            const int kWarps = 4;
+            auto run = [&](auto kernel) {
+                const std::size_t smem = std::size_t(wb * kWarps);
+                ASB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+                int per_sm = 1;
+                ASB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kWarps * 32, smem));
+                const std::uint64_t pairs = (c_end - c_begin + 1) / 2;
+                const std::uint64_t want = (pairs + kWarps - 1) / kWarps;
+                const std::uint64_t cap = std::uint64_t(sms) * std::max(per_sm, 1);
+                const unsigned blocks = unsigned(std::max<std::uint64_t>(1, std::min(want, cap)));
+                kernel<<<blocks, kWarps * 32, smem, s>>>(g.rowptr.get(), g.colind.get(), g.chunk_row.get(),
+                                                         g.n_rows, g.xwide.get(), y, out, g.nnz, f, c_begin, c_end,
+                                                         finite, mix_all());
+                check_launch("sddmm_pair_kernel");
+            };
+            if (ord == 0) run(sddmm_pair_kernel<F, 0, 0>);
+            else if (ft >= f) run(sddmm_pair_kernel<F, 1, 0>);
+            else if (ft == 32) run(sddmm_pair_kernel<F, 1, 32>);
+            else run(sddmm_pair_kernel<F, 1, (F > 64 ? 64 : 0)>);
+        };
+        if (f == 32) pair(std::integral_constant<int, 32>{});
+        else pair(std::integral_constant<int, 64>{});
+        return;
+    }
     using I = std::integral_constant<int, 1>;
     using R = std::integral_constant<int, 0>;
     switch (f) {  // single-pass widths compile F in; the rest loop over passes

@@ -1,8 +1,8 @@
 #!/bin/bash
-# SDDMM development sweep over F (fixed-width pass kernel vs generic chunk kernel).
+# SDDMM fixed kernel: 32-entry chunks vs the pair kernel (64-entry chunks).
 cfg=${1:-reddit}
-for f in 32 64 128 256; do for fixed in 1 0; do
-AUTOSAGE_DEV_SDDMM_FIXED=$fixed timeout 120 python tools/profile_kernels.py --config $cfg --f $f --reps 3 \
+for f in 32 64; do for pair in 0 1; do
+AUTOSAGE_DEV_SDDMM_PAIR=$pair timeout 120 python tools/profile_kernels.py --config $cfg --f $f --reps 3 \
   --sddmm sddmm:rowparallel:ft=64:rpc=4:vec=1:hubt=256,sddmm:rowparallel:ft=32:rpc=4:vec=0:hubt=256 2>&1 \
-  | awk -v c=$cfg -v fx=$fixed -v f=$f '{print c, "F="f, "fixed="fx, $0}'
+  | awk -v c=$cfg -v p=$pair -v f=$f '{print c, "F="f, "pair="p, $0}'
 done; done
