@@ -467,8 +467,23 @@ def run_e2e(args, g, f, n_rows, b_host, x_host, y_host, dec_spmm, dec_sddmm, ste
     dt = statistics.median(times)
     h2d = (b_host.nbytes + x_host.nbytes + y_host.nbytes)
     d2h = n_rows * f * 4 + g.nnz * 4
+    # the link alone: the same D2H bytes copied device -> pinned host with no
+    # kernels (what the pipeline cannot go below)
+    dev_buf = torch.empty(d2h // 4, dtype=torch.float32, device="cuda")
+    host_buf = torch.empty(d2h // 4, dtype=torch.float32).pin_memory()
+    copy_ms = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        host_buf.copy_(dev_buf, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        copy_ms.append(e0.elapsed_time(e1))
+    d2h_floor_ms = min(copy_ms)
+    del dev_buf, host_buf
     return {"value": step_bytes / dt / 1e9, "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": dt * 1e3, "steps": k,
+            "d2h_copy_only_ms": d2h_floor_ms, "d2h_gbs": d2h / (d2h_floor_ms * 1e-3) / 1e9,
             "timing": "host wall clock per step (median), synchronize at the end of each step",
             "api": "as_sddmm_host_async + as_spmm_host_async + as_graph_synchronize "
                    "(decided variants), pinned host buffers"}
