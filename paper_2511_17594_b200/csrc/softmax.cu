@@ -34,59 +34,56 @@ __device__ __forceinline__ double fold_stage(double sum, const double* st, int n
     return sum;
 }
 
-// Warp per row, rows in degree-descending order.  Rows of at most 32*K
-// entries keep their values in registers (one read of vin, one write of
-// vout); longer rows take three passes over memory.  Both: row max; ex_e =
-// f32(exp(f64 v_e - f64 mx)) for 32 entries at a time, staged as f64 in
-// shared memory and folded into the row's sum by lane 0 in entry order
-// (one DADD per entry on the chain, no shuffles); out_e = f32(f64 ex_e / sum).
-template <int K>
+// Warp per row, rows in degree-descending order.  Rows of at most kRowSmem
+// entries stage their ex values in the warp's shared memory (one read of
+// vin, one write of vout); longer rows take three passes over memory.
+// Both: row max; ex_e = f32(exp(f64 v_e - f64 mx)) for 32 entries at a time,
+// staged as f64 and folded into the row's sum by lane 0 in entry order (one
+// DADD per entry on the chain, no shuffles); out_e = f32(f64 ex_e / sum).
+constexpr int kRowSmem = 1024;
 __global__ void __launch_bounds__(256) row_softmax_kernel(const std::uint64_t* __restrict__ rowptr,
                                                           const std::uint32_t* __restrict__ order,
                                                           std::uint64_t n_rows, const float* __restrict__ vin,
                                                           float* __restrict__ vout) {
     __shared__ __align__(16) double stage[8][32];
+    __shared__ __align__(16) float exs_all[8][kRowSmem];
     const int lane = threadIdx.x & 31;
     double* st = stage[threadIdx.x >> 5];
+    float* exs = exs_all[threadIdx.x >> 5];
     const std::uint64_t total_warps = std::uint64_t(gridDim.x) * (blockDim.x >> 5);
     for (std::uint64_t w = (std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n_rows;
          w += total_warps) {
         const std::uint64_t row = order[w];
         const std::uint64_t e0 = rowptr[row], e1 = rowptr[row + 1];
         if (e0 == e1) continue;
-        const std::uint64_t deg = e1 - e0;
-        if (deg <= 32u * K) {
-            // ---- register path
-            float v[K];
+        const std::uint32_t deg = std::uint32_t(e1 - e0);
+        if (deg <= std::uint32_t(kRowSmem)) {
+            // ---- shared-memory path: values land in exs once
+#pragma unroll 4
+            for (std::uint32_t k = lane; k < deg; k += 32) exs[k] = __ldg(vin + e0 + k);
+            __syncwarp();
             float mx = -INFINITY;
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const std::uint64_t e = e0 + lane + 32u * k;
-                v[k] = e < e1 ? __ldg(vin + e) : -INFINITY;
-                mx = fmaxf(mx, v[k]);
-            }
+            for (std::uint32_t k = lane; k < deg; k += 32) mx = fmaxf(mx, exs[k]);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
             const double dmx = double(mx);
-            double sum = 0.0;
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const std::uint64_t base = e0 + 32u * k;
-                if (base >= e1) break;
-                const bool ok = base + lane < e1;
-                const float ex = ok ? float(exp(double(v[k]) - dmx)) : 0.f;
-                v[k] = ex;
-                st[lane] = double(ex);
+            double sum = 0.0;  // lane 0
+            for (std::uint32_t base = 0; base < deg; base += 32) {
+                const std::uint32_t k = base + lane;
+                double exd = 0.0;
+                if (k < deg) {
+                    const float ex = float(exp(double(exs[k]) - dmx));
+                    exs[k] = ex;
+                    exd = double(ex);
+                }
+                st[lane] = exd;
                 __syncwarp();
-                if (lane == 0) sum = fold_stage(sum, st, (e1 - base) < 32 ? int(e1 - base) : 32);
+                if (lane == 0) sum = fold_stage(sum, st, (deg - base) < 32 ? int(deg - base) : 32);
                 __syncwarp();
             }
             sum = __shfl_sync(FULL, sum, 0);
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const std::uint64_t e = e0 + lane + 32u * k;
-                if (e < e1) vout[e] = float(__ddiv_rn(double(v[k]), sum));
-            }
+            for (std::uint32_t k = lane; k < deg; k += 32) vout[e0 + k] = float(__ddiv_rn(double(exs[k]), sum));
+            __syncwarp();
             continue;
         }
         // ---- long rows: three passes
@@ -129,7 +126,7 @@ void launch_row_softmax(Graph& g, const float* vin, float* vout, cudaStream_t s)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const std::uint64_t want = (g.n_rows * 32 + 255) / 256;
     const unsigned blocks = unsigned(std::min<std::uint64_t>(want, std::uint64_t(sms) * 8));
-    row_softmax_kernel<16><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.order.get(), g.n_rows, vin, vout);
+    row_softmax_kernel<<<blocks, 256, 0, s>>>(g.rowptr.get(), g.order.get(), g.n_rows, vin, vout);
     check_launch("row_softmax_kernel");
 }
 
