@@ -379,9 +379,11 @@ def run_ours(args):
 
     # e2e through the reference-facing host-buffer entry points
     e2e = None
-    if world == 1 and not args.no_e2e:
-        e2e = run_e2e(args, g, f, n_rows, b_host, x_host, y_host, dec_spmm, dec_sddmm,
-                      bytes_spmm + bytes_sddmm)
+    if not args.no_e2e:
+        # every rank: full B/Y and its own X rows in, its own C rows and SDDMM
+        # values out, through the host-buffer API; time = max over ranks
+        e2e = run_e2e(args, g, f, r1 - r0, b_host, x_host[r0:r1], y_host, dec_spmm, dec_sddmm,
+                      bytes_spmm + bytes_sddmm, dist)
 
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu:
@@ -427,7 +429,7 @@ def dataclasses_asdict(cfg):
     return dataclasses.asdict(cfg)
 
 
-def run_e2e(args, g, f, n_rows, b_host, x_host, y_host, dec_spmm, dec_sddmm, step_bytes):
+def run_e2e(args, g, f, n_rows, b_host, x_host, y_host, dec_spmm, dec_sddmm, step_bytes, dist=None):
     """Same step through the host-buffer C-ABI: as_spmm_host_async +
     as_sddmm_host_async + as_graph_synchronize, pinned host buffers.  The H2D
     of B/X/Y and the D2H of C and of the SDDMM values are inside the timed
@@ -438,7 +440,7 @@ def run_e2e(args, g, f, n_rows, b_host, x_host, y_host, dec_spmm, dec_sddmm, ste
     import paper_2511_17594_b200 as asb
     from paper_2511_17594_b200 import _capi
     lib = _capi.lib
-    pin = lambda a: torch.from_numpy(a).pin_memory()  # noqa: E731
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
     b, x, y = pin(b_host), pin(x_host), pin(y_host)
     c = torch.empty((n_rows, f), dtype=torch.float32).pin_memory()
     sv = torch.empty(max(g.nnz, 1), dtype=torch.float32).pin_memory()
@@ -461,16 +463,27 @@ def run_e2e(args, g, f, n_rows, b_host, x_host, y_host, dec_spmm, dec_sddmm, ste
     k = max(3, min(args.steps, 10))
     times = []
     for _ in range(k):
+        if dist:
+            dist.barrier()
         t0 = time.perf_counter()
         step()
         times.append(time.perf_counter() - t0)
+    if dist:  # per step, the slowest rank
+        tt = torch.tensor(times, dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        times = tt.tolist()
     dt = statistics.median(times)
     h2d = (b_host.nbytes + x_host.nbytes + y_host.nbytes)
-    d2h = n_rows * f * 4 + g.nnz * 4
-    # the link alone: the same D2H bytes copied device -> pinned host with no
-    # kernels (what the pipeline cannot go below)
-    dev_buf = torch.empty(d2h // 4, dtype=torch.float32, device="cuda")
-    host_buf = torch.empty(d2h // 4, dtype=torch.float32).pin_memory()
+    d2h_local = n_rows * f * 4 + g.nnz * 4
+    d2h = d2h_local
+    if dist:  # whole-job bytes moved
+        bt = torch.tensor([h2d, d2h], dtype=torch.float64, device="cuda")
+        dist.all_reduce(bt)
+        h2d, d2h = int(bt[0].item()), int(bt[1].item())
+    # the link alone: this rank's D2H bytes copied device -> pinned host with
+    # no kernels (what the pipeline cannot go below)
+    dev_buf = torch.empty(d2h_local // 4, dtype=torch.float32, device="cuda")
+    host_buf = torch.empty(d2h_local // 4, dtype=torch.float32).pin_memory()
     copy_ms = []
     for _ in range(3):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -483,7 +496,7 @@ def run_e2e(args, g, f, n_rows, b_host, x_host, y_host, dec_spmm, dec_sddmm, ste
     del dev_buf, host_buf
     return {"value": step_bytes / dt / 1e9, "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": dt * 1e3, "steps": k,
-            "d2h_copy_only_ms": d2h_floor_ms, "d2h_gbs": d2h / (d2h_floor_ms * 1e-3) / 1e9,
+            "d2h_copy_only_ms": d2h_floor_ms, "d2h_gbs": d2h_local / (d2h_floor_ms * 1e-3) / 1e9,
             "timing": "host wall clock per step (median), synchronize at the end of each step",
             "api": "as_sddmm_host_async + as_spmm_host_async + as_graph_synchronize "
                    "(decided variants), pinned host buffers"}
