@@ -410,7 +410,13 @@ def run_ours(args):
             "decide_cold_ms": cold_ms,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": dom,
-                         "bytes_model": "gather model, proj/src/cost.cpp:21-27", "peak_source": peak_src},
+                         "bytes_model": "gather model, proj/src/cost.cpp:21-27", "peak_source": peak_src,
+                         # measured DRAM bytes over the same time: the gathers hit L2,
+                         # so the op is bound on chip, not by HBM
+                         "dram_gbs": (traffic / (dom_ms * 1e-3) / 1e9) if traffic else None,
+                         "dram_frac": (traffic / (dom_ms * 1e-3) / 1e9 / peak) if traffic else None,
+                         "binding_resource": {"sddmm": "shared-memory datapath (Y staging + X broadcast)",
+                                              "spmm": "L2 gather latency (long scoreboard)"}[dom]},
             "gpu_launches": int(launches),
             "clocks": clk,
         }
