@@ -742,6 +742,17 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const float* b, std::uint3
     wpb = warps_per_cta(wpb);
     const TileShape t = tile_shape(f, f_tile, vec);
     if (plan.n_slots) g.scratch.ensure(plan.n_slots * f);
+    // light rows on the forked stream, concurrent with the pieces: their
+    // blocks fill the SMs the pieces kernel's last wave leaves idle
+    static const bool concurrent = [] {
+        const char* e = std::getenv("AUTOSAGE_DEV_SPMM_CONCURRENT");
+        return e ? std::atoi(e) != 0 : true;
+    }();
+    const bool fork_light = concurrent && plan.n_light && plan.n_pieces;
+    if (fork_light) {
+        cudaStream_t aux = graph_fork(g, s);
+        launch_spmm_rows(g, val, plan.n_heavy, plan.n_light, b, f, c, f_tile, vec, wpb, aux, finite);
+    }
     if (plan.n_pieces) {
         SegArgs a{};
         a.rowptr = g.rowptr.get();
@@ -765,7 +776,8 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const float* b, std::uint3
         else if (vec) launch_seg_vec<4>(a, val != nullptr, t.lanes, wpb, s);
         else launch_seg_vec<1>(a, val != nullptr, t.lanes, wpb, s);
     }
-    if (plan.n_light)
+    if (fork_light) graph_join(g, s);
+    else if (plan.n_light)
         launch_spmm_rows(g, val, plan.n_heavy, plan.n_light, b, f, c, f_tile, vec, wpb, s, finite);
     if (plan.n_red) {
         const std::uint64_t total = plan.n_red * f;
