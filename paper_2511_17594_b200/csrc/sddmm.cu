@@ -424,7 +424,9 @@ __device__ __forceinline__ void sddmm_fixed_body(const std::uint64_t* __restrict
             const int k = __popc(inside);
 #pragma unroll 1
             for (int b = 0; b < k; ++b) r += __shfl_sync(FULL, cur.bound, b) <= e ? 1u : 0u;
-            if (k == 32) r = row_of(rowptr, r, e);  // more rows meet in this chunk
+            // more rows meet in this chunk; the tail's idle lanes search
+            // for the last entry's row (rowptr ends at nnz)
+            if (k == 32) r = row_of(rowptr, r, e < nnz ? e : nnz - 1);
         }
         const std::uint32_t rel = r - cur.r_first;
         const float* yr = ys + lane * Sh::S;
@@ -603,8 +605,8 @@ __device__ __forceinline__ void sddmm_pair_body(const std::uint64_t* __restrict_
                 rb += bb <= eb ? 1u : 0u;
             }
             if (k == 32) {  // more than 32 rows meet in these 64 entries
-                ra = row_of(rowptr, ra, ea);
-                rb = row_of(rowptr, rb, eb);
+                ra = row_of(rowptr, ra, ea < e_end ? ea : e_end - 1);
+                rb = row_of(rowptr, rb, eb < e_end ? eb : e_end - 1);
             }
         }
         const std::uint32_t rela = ra - cur.r_first, relb = rb - cur.r_first;
@@ -771,8 +773,8 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
                 rb += bb <= eb ? 1u : 0u;
             }
             if (k == 32) {  // more than 32 rows meet in these 64 entries
-                ra = row_of(rowptr, ra, ea);
-                rb = row_of(rowptr, rb, eb);
+                ra = row_of(rowptr, ra, ea < e_end ? ea : e_end - 1);
+                rb = row_of(rowptr, rb, eb < e_end ? eb : e_end - 1);
             }
         }
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
