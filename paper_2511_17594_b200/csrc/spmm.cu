@@ -17,9 +17,10 @@
 //  * each entry's value is widened once by the lane that loaded it and
 //    shuffled as f64; half of every B float4 is widened by an exact integer
 //    re-bias on the ALU pipe (widen.cuh) when B is known finite;
-//  * rows of degree >= 2048 (whose dependent round trips would dominate a
-//    lane group) go to a CTA-per-row kernel that streams the gathered B rows
-//    through a cp.async shared-memory ring, concurrently on a forked stream.
+//  * on small graphs, long rows (degree >= 256) and hub pieces (whose
+//    dependent round trips would dominate a lane group) go to a CTA-per-item
+//    kernel that streams the gathered B rows through a cp.async
+//    shared-memory ring, concurrently on a forked stream.
 #include "ops.hpp"
 #include "widen.cuh"
 
@@ -237,17 +238,19 @@ __global__ void hub_reduce_kernel(const std::uint32_t* __restrict__ red_row,
 }
 
 // ---------------------------------------------------------------------------
-// K2L: one CTA per long row (degree >= long_row_min) with the row-parallel
-// numerics, warp-specialized around the Blackwell bulk-copy engine:
-//   warp 0 (producer): streams the row's column indices/values into an index
+// K2L: one CTA per long row or hub piece with the group kernel's numerics,
+// warp-specialized around an mbarrier ring:
+//   warp 0 (producer): streams the item's column indices/values into an index
 //     ring with 4-byte cp.async (kIdxAhead chunks ahead, so no dependent
 //     global load sits on its path), widens the values once into a f64 ring,
-//     and issues ONE cp.async.bulk (TMA bulk copy) per gathered B row into a
-//     kLongStages-deep shared-memory ring, completion tracked by a "full"
-//     mbarrier per stage (arrive.expect_tx + complete_tx);
-//   warps 1.. (consumers): one thread per feature runs that feature's f64
-//     chain in CSR order out of shared memory, then releases the stage on its
-//     "empty" mbarrier.
+//     and gathers each stage's B rows with 16-byte cp.async spread over the
+//     warp (whole 128-byte lines per instruction) into a kLongStages-deep
+//     shared-memory ring.  A stage's "full" mbarrier counts, per producer
+//     lane, one release arrive (its value stores) and one
+//     cp.async.mbarrier.arrive.noinc (its copies landed).  One TMA bulk copy
+//     per 256-byte row measured ~10% slower (c1 rowparallel 0.13 ms vs 0.116).
+//   warps 1.. (consumers): F/FPL threads each run FPL f64 chains in CSR order
+//     out of shared memory, then release the stage on its "empty" mbarrier.
 // No __syncthreads in the steady state; a stage holds ch B rows.  Bit-equal
 // to the group kernel.
 constexpr int kLongStages = 8;
@@ -263,6 +266,9 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -274,10 +280,6 @@ __device__ __forceinline__ void mbar_init(std::uint64_t* bar, unsigned count) {
 __device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void mbar_arrive_expect_tx(std::uint64_t* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
 __device__ __forceinline__ void mbar_wait(std::uint64_t* bar, unsigned parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -285,13 +287,6 @@ __device__ __forceinline__ void mbar_wait(std::uint64_t* bar, unsigned parity) {
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
         "@!p bra LONGROW_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, std::uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
 
@@ -375,7 +370,7 @@ __device__ __forceinline__ void longrow_body(const SegArgs& A, std::uint32_t ch,
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
-            mbar_init(&full[s], 32);  // 32 producer-lane arrivals (+ tx bytes)
+            mbar_init(&full[s], 64);  // per producer lane: values written + its copies landed
             mbar_init(&empty[s], n_cons_warps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -384,7 +379,6 @@ __device__ __forceinline__ void longrow_body(const SegArgs& A, std::uint32_t ch,
 
     if (warp == 0) {
         // ---------------- producer warp ----------------
-        const unsigned row_bytes = f * 4;
         auto issue_idx = [&](std::uint32_t k) {
             if (k < nchunks) {
                 const std::uint32_t base = k * ch, n = min(ch, deg - base);
@@ -410,11 +404,18 @@ __device__ __forceinline__ void longrow_body(const SegArgs& A, std::uint32_t ch,
             double* vdst = vd + std::uint64_t(s) * ch;
             for (std::uint32_t j = lane; j < n; j += 32) vdst[j] = HAS_VAL ? double(vs[j]) : 1.0;
             __syncwarp();
-            if (lane == 0) mbar_arrive_expect_tx(&full[s], n * row_bytes);
-            else mbar_arrive(&full[s]);
+            mbar_arrive(&full[s]);  // release: this lane's value stores
+            // the stage's B rows as 16-byte cp.async pieces spread over the
+            // warp (whole 128-byte lines per instruction); each lane's
+            // arrive fires when its own copies have landed
             float* dst = ring + std::uint64_t(s) * ch * f;
-            for (std::uint32_t j = lane; j < n; j += 32)
-                bulk_g2s(dst + std::uint64_t(j) * f, b + std::uint64_t(cs[j]) * f, row_bytes, &full[s]);
+            const std::uint32_t per_row = f / 4, pieces = n * per_row;
+            for (std::uint32_t pidx = lane; pidx < pieces; pidx += 32) {
+                const std::uint32_t j = pidx / per_row, qq = pidx - j * per_row;
+                cp_async16(dst + std::uint64_t(j) * f + 4 * qq, b + std::uint64_t(cs[j]) * f + 4 * qq);
+            }
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full[s]))
+                         : "memory");
         }
         cp_async_wait<0>();
         return;
