@@ -379,6 +379,9 @@ __device__ __forceinline__ void longrow_body(const SegArgs& A, std::uint32_t ch,
 
     if (warp == 0) {
         // ---------------- producer warp ----------------
+        const std::uint32_t per_row = f / 4;  // 16-byte units per B row
+        const std::uint32_t dj = 32 / per_row, dq = 32 % per_row;
+        const std::uint32_t j0 = std::uint32_t(lane) / per_row, q0 = std::uint32_t(lane) % per_row;
         auto issue_idx = [&](std::uint32_t k) {
             if (k < nchunks) {
                 const std::uint32_t base = k * ch, n = min(ch, deg - base);
@@ -409,10 +412,17 @@ __device__ __forceinline__ void longrow_body(const SegArgs& A, std::uint32_t ch,
             // warp (whole 128-byte lines per instruction); each lane's
             // arrive fires when its own copies have landed
             float* dst = ring + std::uint64_t(s) * ch * f;
-            const std::uint32_t per_row = f / 4, pieces = n * per_row;
-            for (std::uint32_t pidx = lane; pidx < pieces; pidx += 32) {
-                const std::uint32_t j = pidx / per_row, qq = pidx - j * per_row;
-                cp_async16(dst + std::uint64_t(j) * f + 4 * qq, b + std::uint64_t(cs[j]) * f + 4 * qq);
+            // piece p = lane + 32 i -> (row j, 16-byte unit qq), stepped
+            // incrementally (no division in the loop)
+            std::uint32_t j = j0, qq = q0;
+            for (std::uint32_t pidx = lane; pidx < n * per_row; pidx += 32) {
+                cp_async16(dst + j * f + 4 * qq, b + std::uint64_t(cs[j]) * f + 4 * qq);
+                j += dj;
+                qq += dq;
+                if (qq >= per_row) {
+                    qq -= per_row;
+                    ++j;
+                }
             }
             asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full[s]))
                          : "memory");
