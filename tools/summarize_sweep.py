@@ -22,6 +22,10 @@ def main():
          "`python tools/sweep.py` (one GPU). Times are CUDA-event medians per launch after the decision is",
          "cached; GB/s is the reference gather model (proj/src/cost.cpp:21-27) over that time, so it can exceed",
          f"HBM when the dense operand is L2-resident. `frac` = GB/s / {peak:.0f} (MEASURED_PEAKS.json).", ""]
+    m = r.get("meta")
+    if m:
+        L += ["Run: " + ", ".join(f"{k} `{v}`" for k, v in m.items() if k != "probe_config"),
+              f"probe config `{m.get('probe_config')}`", ""]
     if "c1" in r:
         c = r["c1"]
         g = c["graph"]

@@ -291,12 +291,44 @@ def case_c5(res):
     g.close()
 
 
+def run_meta():
+    """Reproducibility sidecar (the reference bench's .meta.json fields,
+    proj/tools/autosage_bench.cpp:144-165, re-targeted): device signature as
+    folded into schedule-cache keys, host CPU and cores for the CPU reference,
+    toolchain, driver and library versions."""
+    import platform
+    import subprocess
+    dp = asb.DeviceProfile.gpu()
+    cpu = ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            cpu = next((ln.split(":", 1)[1].strip() for ln in fh if ln.startswith("model name")), "")
+    except OSError:
+        pass
+    try:
+        drv = subprocess.run(["nvidia-smi", "--query-gpu=driver_version,clocks.max.sm", "--format=csv,noheader"],
+                             capture_output=True, text=True, timeout=20).stdout.strip()
+    except Exception:
+        drv = ""
+    return {"device_sig": dp.device_sig, "bw_eff_gbs": dp.bw_eff / 1e9, "flops_eff_gflops": dp.flops_eff / 1e9,
+            "sms": dp.cores, "cost_model": "b200" if dp.model == 1 else "reference",
+            "host_cpu": cpu, "host_cores": os.cpu_count(), "python": platform.python_version(),
+            "torch": torch.__version__, "cuda_runtime": torch.version.cuda, "driver_and_max_sm_clock": drv,
+            "probe_config": dataclasses_asdict(asb.ProbeConfig.from_env()),
+            "toolchain": asb.toolchain_tag() if hasattr(asb, "toolchain_tag") else None}
+
+
+def dataclasses_asdict(x):
+    import dataclasses
+    return dataclasses.asdict(x)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cases", default="c1,c2,c3,c4,c5")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep.json"))
     a = ap.parse_args()
-    res = {"gpu": torch.cuda.get_device_name(), "peak_gbs": PEAK}
+    res = {"gpu": torch.cuda.get_device_name(), "peak_gbs": PEAK, "meta": run_meta()}
     for cs in a.cases.split(","):
         t0 = time.time()
         globals()[f"case_{cs}"](res)
