@@ -228,6 +228,18 @@ void check_sddmm_dims(const Graph& p, std::uint64_t x_rows, std::uint64_t y_rows
     if (y_rows != p.n_cols) throw InvalidArgument("sddmm: y.n_rows != pattern.n_cols");
 }
 
+// Device flag enabling the ALU re-bias half of the f32 -> f64 widening
+// (widen.cuh), or nullptr for the all-F2F path.  The scan costs a full read
+// of the dense operand; it pays only when the gathers are L2-resident and the
+// XU pipe is a limiter.  A gathered operand larger than ~3/4 of L2 streams from
+// DRAM, where the widening is not on the critical path (Products-shape B,
+// 980 MB: the scan alone was 0.15 ms per call).
+const unsigned* mix_flag(Graph& g, const float* p, std::uint64_t n, cudaStream_t s) {
+    constexpr std::uint64_t kMaxBytes = std::uint64_t(96) << 20;
+    if (n * 4 > kMaxBytes) return nullptr;
+    return finite_flag(g, p, n, s);
+}
+
 void run_spmm_variant(const as_variant& v, Graph& a, const float* vals, const float* b,
                       std::uint64_t f, float* c, cudaStream_t s, bool vec) {
     switch (v.mapping) {
@@ -236,13 +248,13 @@ void run_spmm_variant(const as_variant& v, Graph& a, const float* vals, const fl
             break;
         case AS_MAP_ROWPARALLEL: {
             ensure_order(a);
-            const unsigned* fin = finite_flag(a, b, a.n_cols * f, s);
+            const unsigned* fin = mix_flag(a, b, a.n_cols * f, s);
             launch_spmm_rows(a, vals, 0, a.n_rows, b, std::uint32_t(f), c, v.f_tile, vec,
                              std::uint32_t(std::min<std::uint64_t>(v.rows_per_chunk, 16)), s, fin);
             break;
         }
         case AS_MAP_HUBSPLIT: {
-            const unsigned* fin = finite_flag(a, b, a.n_cols * f, s);
+            const unsigned* fin = mix_flag(a, b, a.n_cols * f, s);
             launch_spmm_hubsplit(a, vals, b, std::uint32_t(f), c, v.f_tile, vec,
                                  std::uint32_t(std::min<std::uint64_t>(v.rows_per_chunk, 16)),
                                  v.hub_threshold, s, fin);
@@ -316,7 +328,7 @@ void sddmm_mapped(const as_variant& v, Graph& p, const float* x, std::uint64_t x
     const void* bases[2] = {x, y};
     const bool vec = v.vectorized && vec4_eligible(f, bases, 2);
     DeviceGuard dg(p.device);
-    const unsigned* fin = finite_flag(p, y, y_rows * f, s);
+    const unsigned* fin = mix_flag(p, y, y_rows * f, s);
     launch_sddmm_chunks(p, x, y, std::uint32_t(f), out, v.f_tile, vec,
                         std::uint32_t(std::min<std::uint64_t>(v.rows_per_chunk, 16)), s, fin);
 }
@@ -338,7 +350,7 @@ KernelResult dispatch_sddmm(const as_variant& v, Graph& p, const float* x, std::
     if (r.variant.mapping == AS_MAP_BASELINE) {
         launch_sddmm_baseline(p, x, y, std::uint32_t(f), out, s);
     } else {
-        const unsigned* fin = finite_flag(p, y, y_rows * f, s);
+        const unsigned* fin = mix_flag(p, y, y_rows * f, s);
         launch_sddmm_chunks(p, x, y, std::uint32_t(f), out, r.variant.f_tile, vec,
                             std::uint32_t(std::min<std::uint64_t>(r.variant.rows_per_chunk, 16)), s,
                             fin);
@@ -456,7 +468,7 @@ KernelResult sddmm_host(const as_variant* v, Graph& g, const float* x_host, std:
     ensure_slices(g, std::size_t(k));
     const unsigned* fin = nullptr;
     const std::uint32_t wpb = std::uint32_t(std::min<std::uint64_t>(r.variant.rows_per_chunk, 16));
-    if (r.variant.mapping != AS_MAP_BASELINE) fin = finite_flag(g, y, y_rows * f, g.stream);
+    if (r.variant.mapping != AS_MAP_BASELINE) fin = mix_flag(g, y, y_rows * f, g.stream);
     std::uint64_t x_done = 0;  // X rows [0, x_done) queued
     for (std::uint64_t i = 0; i < k && n_chunks; ++i) {
         const std::uint64_t c0 = i * per, c1 = std::min(n_chunks, c0 + per);

@@ -781,9 +781,16 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const float* b, std::uint3
         a.n_tiles = t.n_tiles;
         a.f = f;
         a.tile_w = t.tile_w;
-        // pieces are up to 2048-entry dependent chains: where long rows go to
-        // the ring kernel (small graphs), so do the pieces
-        if (long_row_min(g) <= kHubNnzChunk && longrow_ok(f, vec)) launch_longrow<true>(a, plan.n_pieces, s);
+        // pieces are up to 2048-entry dependent chains: when there are too
+        // few of them to fill the lane-group kernel (under a wave), the ring
+        // kernel's deep per-piece prefetch wins (c1: 0.163 -> 0.106 ms); with
+        // thousands of pieces the group kernel's throughput wins (Products
+        // 8-way shard: 1.36 ms vs 1.72 ms)
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const bool few = plan.n_pieces <= std::uint64_t(4) * std::uint64_t(sms);
+        if (few && longrow_ok(f, vec)) launch_longrow<true>(a, plan.n_pieces, s);
         else if (vec) launch_seg_vec<4>(a, val != nullptr, t.lanes, wpb, s);
         else launch_seg_vec<1>(a, val != nullptr, t.lanes, wpb, s);
     }
