@@ -240,8 +240,11 @@ const unsigned* mix_flag(Graph& g, const float* p, std::uint64_t n, cudaStream_t
     return finite_flag(g, p, n, s);
 }
 
+// rmax/rsum (softmax mode, fused attention): vals are raw scores and the
+// kernels apply the row softmax on the fly (ops.hpp)
 void run_spmm_variant(const as_variant& v, Graph& a, const float* vals, const float* b,
-                      std::uint64_t f, float* c, cudaStream_t s, bool vec) {
+                      std::uint64_t f, float* c, cudaStream_t s, bool vec,
+                      const float* rmax = nullptr, const double* rsum = nullptr) {
     switch (v.mapping) {
         case AS_MAP_BASELINE:
             launch_spmm_baseline(a, vals, b, std::uint32_t(f), c, s);
@@ -250,14 +253,15 @@ void run_spmm_variant(const as_variant& v, Graph& a, const float* vals, const fl
             ensure_order(a);
             const unsigned* fin = mix_flag(a, b, a.n_cols * f, s);
             launch_spmm_rows(a, vals, 0, a.n_rows, b, std::uint32_t(f), c, v.f_tile, vec,
-                             std::uint32_t(std::min<std::uint64_t>(v.rows_per_chunk, 16)), s, fin);
+                             std::uint32_t(std::min<std::uint64_t>(v.rows_per_chunk, 16)), s, fin, rmax,
+                             rsum);
             break;
         }
         case AS_MAP_HUBSPLIT: {
             const unsigned* fin = mix_flag(a, b, a.n_cols * f, s);
             launch_spmm_hubsplit(a, vals, b, std::uint32_t(f), c, v.f_tile, vec,
                                  std::uint32_t(std::min<std::uint64_t>(v.rows_per_chunk, 16)),
-                                 v.hub_threshold, s, fin);
+                                 v.hub_threshold, s, fin, rmax, rsum);
             break;
         }
     }
@@ -686,24 +690,21 @@ void attention_forward(const Context& ctx, const as_probe_config& cfg, Graph& pa
     }
 
     bool done = false;
-    if (fused && !p_ready) {
-        // numerics the decided unfused pipeline would produce
-        const void* qk[2] = {q, k};
+    if (fused && !p_ready && pd.has_choice) {
+        // SDDMM -> per-row (max, sum) -> SpMM that turns each score into its
+        // probability as it loads it: p never touches memory, and the bits are
+        // those of the staged pipeline (same softmax.cuh arithmetic)
+        const as_variant pv = apply_env_overrides(pd.choice);
+        check_variant(pv);
         const void* vv[1] = {v};
-        as_variant sv = sd.has_choice ? apply_env_overrides(sd.choice) : default_variant();
-        const bool svec = sd.has_choice && sv.mapping != AS_MAP_BASELINE && sv.vectorized &&
-                          vec4_eligible(f, qk, 2);
-        const std::uint64_t sft = effective_tile(sv.f_tile, f);
-        std::uint64_t hub_t = 0;
-        if (pd.has_choice) {
-            const as_variant pv = apply_env_overrides(pd.choice);
-            if (pv.mapping == AS_MAP_HUBSPLIT) hub_t = pv.hub_threshold;
-        }
-        const bool ok = f > 0 && f % 4 == 0 && vec4_eligible(f, qk, 2) && fv > 0 && fv % 4 == 0 &&
-                        fv <= 512 && vec4_eligible(fv, vv, 1) && (!svec || sft % 4 == 0);
-        if (ok) {
-            launch_attention_fused(pattern, q, k, v, std::uint32_t(f), std::uint32_t(fv), out, sft,
-                                   svec, hub_t, s);
+        if (pv.mapping != AS_MAP_BASELINE && fv % 4 == 0 && vec4_eligible(fv, vv, 1)) {
+            if (sd.has_choice) dispatch_sddmm(sd.choice, pattern, q, q_rows, k, k_rows, f, scores, s, false);
+            else sddmm_baseline(pattern, q, q_rows, k, k_rows, f, scores, s);
+            pattern.att_max.ensure(std::max<std::uint64_t>(pattern.n_rows, 1));
+            pattern.att_sum.ensure(std::max<std::uint64_t>(pattern.n_rows, 1));
+            launch_row_softmax_stats(pattern, scores, pattern.att_max.get(), pattern.att_sum.get(), s);
+            run_spmm_variant(pv, pattern, scores, v, fv, out, s, true, pattern.att_max.get(),
+                             pattern.att_sum.get());
             done = true;
         }
     }

@@ -94,8 +94,9 @@ struct Graph {
     std::map<std::uint64_t, std::unique_ptr<HubPlan>> hub_plans;
     std::map<std::uint64_t, as_features> features;
     DevBuf<double> scratch;            // hub partials
-    DevBuf<float> tmp;                 // fused-attention scores
-    DevBuf<float> att_buf;             // unfused attention: scores | probabilities
+    DevBuf<float> att_buf;             // attention: scores | probabilities (staged)
+    DevBuf<float> att_max;             // fused attention: per-row score max ...
+    DevBuf<double> att_sum;            // ... and softmax denominator
     DevBuf<float> stage_in, stage_out; // host-buffer row softmax
     std::map<std::uint64_t, std::uint64_t> ge_count;  // rows with degree >= key
     DevBuf<unsigned> flag;             // finiteness flag of the current dense operand

@@ -16,13 +16,19 @@ void launch_spmm_baseline(Graph& g, const float* val, const float* b, std::uint3
 // forked stream (same numerics).
 void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uint64_t n_list,
                       const float* b, std::uint32_t f, float* c, std::uint64_t f_tile, bool vec,
-                      std::uint32_t wpb, cudaStream_t s, const unsigned* finite = nullptr);
+                      std::uint32_t wpb, cudaStream_t s, const unsigned* finite = nullptr,
+                      const float* rmax = nullptr, const double* rsum = nullptr);
 // K3: hub split -- light rows via K2 plus 2048-nnz pieces with ordered
 // fp64 partial reduction.
 void launch_spmm_hubsplit(Graph& g, const float* val, const float* b, std::uint32_t f, float* c,
                           std::uint64_t f_tile, bool vec, std::uint32_t wpb,
                           std::uint64_t hub_threshold, cudaStream_t s,
-                          const unsigned* finite = nullptr);
+                          const unsigned* finite = nullptr, const float* rmax = nullptr,
+                          const double* rsum = nullptr);
+// Softmax mode of K2/K3 (rmax != nullptr): `val` holds raw scores and each
+// entry's value is p_e = softmax of its row from (rmax[row], rsum[row])
+// (softmax.cuh), computed by the loading lane -- the SpMM half of the fused
+// attention, bit-equal to SpMM over row_softmax's output.
 
 // ---- SDDMM (src/kernels.cpp:336-429) -----------------------------------
 // order: 0 = sequential (scalar variants and the baseline), 1 = per-f_tile
@@ -51,14 +57,8 @@ const unsigned* finite_flag(Graph& g, const float* p, std::uint64_t n, cudaStrea
 
 // ---- row softmax (src/kernels.cpp:431-461) ----------------------------
 void launch_row_softmax(Graph& g, const float* vin, float* vout, cudaStream_t s);
-
-// ---- fused attention (src/attention.cpp:9-40 in one pass) --------------
-// scores kept on chip per row; sddmm order/ft as for launch_sddmm_chunks;
-// SpMM part in CSR order (bit-equal to the row-parallel mapping), or with
-// 2048-nnz piece partials on rows of degree >= spmm_hub_t (hubsplit; 0 = off).
-void launch_attention_fused(Graph& g, const float* q, const float* k, const float* v,
-                            std::uint32_t f, std::uint32_t fv, float* out, std::uint64_t sddmm_ft,
-                            bool sddmm_vec, std::uint64_t spmm_hub_t, cudaStream_t s);
+// per-row (max, sum) only (fused attention); rows of degree 0 are not written
+void launch_row_softmax_stats(Graph& g, const float* vin, float* rmax, double* rsum, cudaStream_t s);
 
 // ---- calibration (src/device.cpp:42-95 analogue) ------------------------
 double measure_gpu_bandwidth(int device);

@@ -2,132 +2,375 @@
 //
 // Per non-empty row: mx = max over the f32 values; ex_e = f32(exp(f64 v_e -
 // f64 mx)); sum = f64 sum of ex_e in entry order; out_e = f32(f64 ex_e /
-// sum).  Empty rows produce nothing.  The sum is accumulated sequentially
-// in entry order (lane 0 folds each 32-entry chunk from shared memory), so
-// the only difference from the CPU reference can come from exp() itself
-// (CUDA's f64 exp vs libm, both within 1 ulp of f64, rounded to f32).
-// The max ignores NaN where std::max would latch it; either way a NaN in a
-// row makes every ex (or the sum) NaN, so all outputs of that row are NaN
-// exactly as in the reference.
+// sum).  Empty rows produce nothing.  The arithmetic lives in softmax.cuh
+// (shared with the SpMM that applies probabilities on the fly); the sum is
+// reduced in parallel and is bit-equal to the reference's sequential chain
+// whenever the exactness certificate of softmax.cuh holds, else the row
+// re-runs the chain in entry order.  The only difference from the CPU
+// reference can therefore come from exp() itself (CUDA's f64 exp vs libm,
+// both within 1 ulp of f64, rounded to f32).
+// The max ignores NaN where std::max would latch a leading NaN; either way a
+// NaN in a row makes every ex (or the sum) NaN, so all outputs of that row
+// are NaN exactly as in the reference.
+//
+// Mapping: rows in degree-descending order.  Rows longer than kRowSmem
+// entries get a CTA each (staged in shared memory up to kCtaSmem entries,
+// else three passes); the rest get a warp each, software-pipelined so the
+// next row's values stream in (cp.async) while the current one computes.
+// Either way one global read and one write per entry.  The CTA kernel runs
+// on a forked stream, concurrently with the warp kernel.
+//
+// Stats mode (OUT = false) writes only (mx, sum) per row: the fused
+// attention SpMM recomputes p_e from the raw scores with the same code.
 #include "ops.hpp"
+#include "softmax.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace asb {
 
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
+constexpr int kRowSmem = 512;        // warp kernel: rows up to this many entries
+constexpr int kCtaSmem = 8192;       // CTA kernel: rows staged in shared memory
+constexpr int kWarpsPerCta = 8;
 
-// lane 0 folds 32 staged f64 values into the row's sum, in entry order
-__device__ __forceinline__ double fold_stage(double sum, const double* st, int n) {
-    if (n == 32) {
-#pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-            const double2 d = *reinterpret_cast<const double2*>(st + j);
-            sum = __dadd_rn(sum, d.x);
-            sum = __dadd_rn(sum, d.y);
-        }
-    } else {
-        for (int j = 0; j < n; ++j) sum = __dadd_rn(sum, st[j]);
-    }
-    return sum;
+struct SoftmaxArgs {
+    const std::uint64_t* rowptr;
+    const std::uint32_t* order;  // rows of this launch: order[0, n)
+    std::uint64_t n;
+    const float* vin;
+    float* vout;    // OUT
+    float* rmax;    // !OUT
+    double* rsum;   // !OUT
+    int force_seq;  // developer/test knob: always run the sequential chain
+};
+
+// LIB: exp() itself instead of the written-out sm_exp (test knob
+// AUTOSAGE_DEV_SOFTMAX_LIBEXP; the two must agree bit for bit)
+template <bool LIB>
+__device__ __forceinline__ float ex_of(float v, double dmx) {
+    if constexpr (LIB) return float(exp(double(v) - dmx));
+    else return sm_ex(v, dmx);
 }
 
-// Warp per row, rows in degree-descending order.  Rows of at most kRowSmem
-// entries stage their ex values in the warp's shared memory (one read of
-// vin, one write of vout); longer rows take three passes over memory.
-// Both: row max; ex_e = f32(exp(f64 v_e - f64 mx)) for 32 entries at a time,
-// staged as f64 and folded into the row's sum by lane 0 in entry order (one
-// DADD per entry on the chain, no shuffles); out_e = f32(f64 ex_e / sum).
-constexpr int kRowSmem = 1024;
-__global__ void __launch_bounds__(256) row_softmax_kernel(const std::uint64_t* __restrict__ rowptr,
-                                                          const std::uint32_t* __restrict__ order,
-                                                          std::uint64_t n_rows, const float* __restrict__ vin,
-                                                          float* __restrict__ vout) {
-    __shared__ __align__(16) double stage[8][32];
-    __shared__ __align__(16) float exs_all[8][kRowSmem];
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return unsigned(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+// Warp per row (rows of at most kRowSmem entries).  Software pipeline: while
+// a warp works on its row out of shared memory, the next row's values are
+// already in flight (cp.async into the other buffer) and the row after
+// that has its (row, e0, deg) loads issued, so neither global latency sits
+// on the path of a row.
+template <bool OUT, bool LIB>
+__global__ void __launch_bounds__(256, 3) softmax_warp_kernel(SoftmaxArgs a) {
+    __shared__ __align__(16) float buf_all[kWarpsPerCta][2][kRowSmem];
     const int lane = threadIdx.x & 31;
-    double* st = stage[threadIdx.x >> 5];
-    float* exs = exs_all[threadIdx.x >> 5];
-    const std::uint64_t total_warps = std::uint64_t(gridDim.x) * (blockDim.x >> 5);
-    for (std::uint64_t w = (std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n_rows;
-         w += total_warps) {
-        const std::uint64_t row = order[w];
-        const std::uint64_t e0 = rowptr[row], e1 = rowptr[row + 1];
-        if (e0 == e1) continue;
-        const std::uint32_t deg = std::uint32_t(e1 - e0);
-        if (deg <= std::uint32_t(kRowSmem)) {
-            // ---- shared-memory path: values land in exs once
-#pragma unroll 4
-            for (std::uint32_t k = lane; k < deg; k += 32) exs[k] = __ldg(vin + e0 + k);
-            __syncwarp();
+    float (*buf)[kRowSmem] = buf_all[threadIdx.x >> 5];
+    const std::uint64_t tw = std::uint64_t(gridDim.x) * (blockDim.x >> 5);
+    std::uint64_t w = (std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+
+    struct RowRef {
+        std::uint32_t row, deg;
+        std::uint64_t e0;
+    };
+    auto fetch = [&](std::uint64_t wi) {  // index loads (not waited on here)
+        RowRef r{0, 0, 0};
+        if (wi < a.n) {
+            r.row = a.order[wi];
+            r.e0 = a.rowptr[r.row];
+            r.deg = std::uint32_t(a.rowptr[r.row + 1] - r.e0);
+        }
+        return r;
+    };
+    auto issue = [&](const RowRef& r, int slot) {
+        const float* src = a.vin + r.e0;
+        for (std::uint32_t k = lane; k < r.deg; k += 32) cp_async4(&buf[slot][k], src + k);
+        cp_async_commit();
+    };
+    RowRef cur = fetch(w);
+    RowRef nxt = fetch(w + tw);
+    issue(cur, 0);
+    for (int it = 0; w < a.n; w += tw, ++it) {
+        const int slot = it & 1;
+        const RowRef nn = fetch(w + 2 * tw);
+        issue(nxt, slot ^ 1);
+        cp_async_wait1();  // this lane's copies of `cur` landed
+        __syncwarp();      // ... and everyone's
+        const float* exs_in = buf[slot];
+        float* exs = buf[slot];
+        const std::uint32_t deg = cur.deg;
+        if (deg) {
             float mx = -INFINITY;
-            for (std::uint32_t k = lane; k < deg; k += 32) mx = fmaxf(mx, exs[k]);
+            for (std::uint32_t k = lane; k < deg; k += 32) mx = fmaxf(mx, exs_in[k]);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
             const double dmx = double(mx);
-            double sum = 0.0;  // lane 0
-            for (std::uint32_t base = 0; base < deg; base += 32) {
-                const std::uint32_t k = base + lane;
-                double exd = 0.0;
-                if (k < deg) {
-                    const float ex = float(exp(double(exs[k]) - dmx));
-                    exs[k] = ex;
-                    exd = double(ex);
-                }
-                st[lane] = exd;
-                __syncwarp();
-                if (lane == 0) sum = fold_stage(sum, st, (deg - base) < 32 ? int(deg - base) : 32);
-                __syncwarp();
+            double sum = 0.0;
+            unsigned mn = 0xffffffffu;
+#pragma unroll 2
+            for (std::uint32_t k = lane; k < deg; k += 32) {
+                const float ex = ex_of<LIB>(exs[k], dmx);
+                exs[k] = ex;
+                sum += double(ex);
+                mn = sm_cert_acc(mn, ex);
             }
-            sum = __shfl_sync(FULL, sum, 0);
-            for (std::uint32_t k = lane; k < deg; k += 32) vout[e0 + k] = float(__ddiv_rn(double(exs[k]), sum));
-            __syncwarp();
-            continue;
-        }
-        // ---- long rows: three passes
-        float mx = -INFINITY;
-#pragma unroll 8
-        for (std::uint64_t e = e0 + lane; e < e1; e += 32) mx = fmaxf(mx, __ldg(vin + e));
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
-        const double dmx = double(mx);
-        double sum = 0.0;  // lane 0
-        float vnext = e0 + lane < e1 ? __ldg(vin + e0 + lane) : 0.f;
-        for (std::uint64_t base = e0; base < e1; base += 32) {
-            const std::uint64_t e = base + lane;
-            const float v = vnext;
-            vnext = base + 32 + lane < e1 ? __ldg(vin + base + 32 + lane) : 0.f;
-            double exd = 0.0;
-            if (e < e1) {
-                const float ex = float(exp(double(v) - dmx));
-                vout[e] = ex;
-                exd = double(ex);
+            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
+            mn = __reduce_min_sync(FULL, mn);
+            __syncwarp();
+            if (a.force_seq || !__all_sync(FULL, sm_sum_exact(sum, mn))) {
+                // the reference's chain, in entry order
+                if (lane == 0) {
+                    sum = 0.0;
+                    for (std::uint32_t k = 0; k < deg; ++k) sum = __dadd_rn(sum, double(exs[k]));
+                }
+                sum = __shfl_sync(FULL, sum, 0);
             }
-            st[lane] = exd;
-            __syncwarp();
-            if (lane == 0) sum = fold_stage(sum, st, (e1 - base) < 32 ? int(e1 - base) : 32);
-            __syncwarp();
-        }
-        sum = __shfl_sync(FULL, sum, 0);
+            if constexpr (OUT) {
+                const double rcp = sm_rcp(sum);
+                float* vout = a.vout + cur.e0;
 #pragma unroll 4
-        for (std::uint64_t e = e0 + lane; e < e1; e += 32) vout[e] = float(__ddiv_rn(double(vout[e]), sum));
+                for (std::uint32_t k = lane; k < deg; k += 32) vout[k] = sm_prob(exs[k], sum, rcp);
+            } else if (lane == 0) {
+                a.rmax[cur.row] = mx;
+                a.rsum[cur.row] = sum;
+            }
+        }
+        __syncwarp();  // buffer `slot` is refilled by the next iteration's issue
+        cur = nxt;
+        nxt = nn;
     }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+// block-wide reductions over the 8 warps (every thread gets the result)
+struct CtaRed {
+    float f[kWarpsPerCta];
+    double d[kWarpsPerCta];
+    unsigned u[kWarpsPerCta];
+    double seq;
+};
+__device__ __forceinline__ float cta_max(CtaRed& r, float v) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(FULL, v, o));
+    if (lane == 0) r.f[warp] = v;
+    __syncthreads();
+    v = r.f[0];
+#pragma unroll
+    for (int i = 1; i < kWarpsPerCta; ++i) v = fmaxf(v, r.f[i]);
+    return v;
+}
+// sum (exact under the certificate, so any order) and certificate minimum
+__device__ __forceinline__ void cta_sum(CtaRed& r, double& sum, unsigned& mn) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
+    mn = __reduce_min_sync(FULL, mn);
+    if (lane == 0) {
+        r.d[warp] = sum;
+        r.u[warp] = mn;
+    }
+    __syncthreads();
+    sum = r.d[0];
+    mn = r.u[0];
+#pragma unroll
+    for (int i = 1; i < kWarpsPerCta; ++i) {
+        sum += r.d[i];
+        mn = min(mn, r.u[i]);
+    }
+}
+
+// CTA per long row, persistent over rows order[blockIdx.x + k*gridDim.x]
+// with the same software pipeline as the warp kernel: rows of at most
+// kCtaSmem entries stream into one of two shared-memory buffers (cp.async)
+// while the CTA works on the other, so the global read of a row overlaps
+// the previous row's compute; ex is computed once and kept there for the
+// output pass.  Longer rows take three passes over global memory (max; ex
+// and sum; output with ex recomputed).  A failed certificate re-runs the
+// sum as the entry-order chain (thread 0 over 256-entry blocks of ex).
+template <bool OUT, bool LIB>
+__global__ void __launch_bounds__(256, 3) softmax_cta_kernel(SoftmaxArgs a) {
+    extern __shared__ __align__(16) float cbuf[];  // 2 x kCtaSmem floats
+    __shared__ CtaRed red;
+    __shared__ double chunk[256];
+    const int tid = threadIdx.x;
+    struct RowRef {
+        std::uint32_t row, deg;
+        std::uint64_t e0;
+    };
+    auto fetch = [&](std::uint64_t i) {
+        RowRef r{0, 0, 0};
+        if (i < a.n) {
+            r.row = a.order[i];
+            r.e0 = a.rowptr[r.row];
+            r.deg = std::uint32_t(a.rowptr[r.row + 1] - r.e0);
+        }
+        return r;
+    };
+    auto issue = [&](const RowRef& r, int slot) {
+        if (r.deg <= std::uint32_t(kCtaSmem)) {
+            const float* src = a.vin + r.e0;
+            float* dst = cbuf + slot * kCtaSmem;
+            for (std::uint32_t k = tid; k < r.deg; k += 256) cp_async4(dst + k, src + k);
+        }
+        cp_async_commit();
+    };
+    const std::uint64_t G = gridDim.x;
+    std::uint64_t i = blockIdx.x;
+    RowRef cur = fetch(i);
+    RowRef nxt = fetch(i + G);
+    issue(cur, 0);
+    for (int it = 0; i < a.n; i += G, ++it) {
+        const int slot = it & 1;
+        const RowRef nn = fetch(i + 2 * G);
+        issue(nxt, slot ^ 1);
+        cp_async_wait1();
+        __syncthreads();
+        const std::uint32_t deg = cur.deg;
+        const bool staged = deg <= std::uint32_t(kCtaSmem);
+        float* cexs = cbuf + slot * kCtaSmem;
+        const float* vin = a.vin + cur.e0;
+
+        float mx = -INFINITY;
+        if (staged) {
+#pragma unroll 8
+            for (std::uint32_t k = tid; k < deg; k += 256) mx = fmaxf(mx, cexs[k]);
+        } else {
+#pragma unroll 8
+            for (std::uint32_t k = tid; k < deg; k += 256) mx = fmaxf(mx, __ldg(vin + k));
+        }
+        mx = cta_max(red, mx);
+        const double dmx = double(mx);
+
+        double sum = 0.0;
+        unsigned mn = 0xffffffffu;
+        if (staged) {
+#pragma unroll 2
+            for (std::uint32_t k = tid; k < deg; k += 256) {
+                const float ex = ex_of<LIB>(cexs[k], dmx);
+                cexs[k] = ex;
+                sum += double(ex);
+                mn = sm_cert_acc(mn, ex);
+            }
+        } else {
+#pragma unroll 2
+            for (std::uint32_t k = tid; k < deg; k += 256) {
+                const float ex = ex_of<LIB>(__ldg(vin + k), dmx);
+                sum += double(ex);
+                mn = sm_cert_acc(mn, ex);
+            }
+        }
+        cta_sum(red, sum, mn);
+        if (a.force_seq || !sm_sum_exact(sum, mn)) {  // block-uniform
+            double sq = 0.0;
+            for (std::uint32_t base = 0; base < deg; base += 256) {
+                const std::uint32_t k = base + tid;
+                if (k < deg) chunk[tid] = double(staged ? cexs[k] : ex_of<LIB>(__ldg(vin + k), dmx));
+                __syncthreads();
+                if (tid == 0) {
+                    const std::uint32_t n = deg - base < 256 ? deg - base : 256;
+                    for (std::uint32_t j = 0; j < n; ++j) sq = __dadd_rn(sq, chunk[j]);
+                }
+                __syncthreads();
+            }
+            if (tid == 0) red.seq = sq;
+            __syncthreads();
+            sum = red.seq;
+        }
+        if constexpr (OUT) {
+            const double rcp = sm_rcp(sum);
+            float* vout = a.vout + cur.e0;
+            if (staged) {
+#pragma unroll 4
+                for (std::uint32_t k = tid; k < deg; k += 256) vout[k] = sm_prob(cexs[k], sum, rcp);
+            } else {
+                // plain loads: vout may alias vin (each entry is read, then
+                // written, by the same thread)
+#pragma unroll 4
+                for (std::uint32_t k = tid; k < deg; k += 256)
+                    vout[k] = sm_prob(ex_of<LIB>(vin[k], dmx), sum, rcp);
+            }
+        } else if (tid == 0) {
+            a.rmax[cur.row] = mx;
+            a.rsum[cur.row] = sum;
+        }
+        __syncthreads();  // buffer `slot` and `red` are reused next iteration
+        cur = nxt;
+        nxt = nn;
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+bool env_flag(const char* name) {
+    const char* e = std::getenv(name);
+    return e && std::atoi(e) != 0;
+}
+
+template <bool OUT>
+void launch_softmax(Graph& g, const float* vin, float* vout, float* rmax, double* rsum, cudaStream_t s) {
+    if (g.n_rows == 0 || g.nnz == 0) return;
+    ensure_order(g);
+    SoftmaxArgs a{};
+    a.rowptr = g.rowptr.get();
+    a.vin = vin;
+    a.vout = vout;
+    a.rmax = rmax;
+    a.rsum = rsum;
+    a.force_seq = env_flag("AUTOSAGE_DEV_SOFTMAX_SEQ") ? 1 : 0;
+    const bool lib = env_flag("AUTOSAGE_DEV_SOFTMAX_LIBEXP");
+    const std::uint64_t n_long = rows_with_degree_at_least(g, kRowSmem + 1);
+    const std::uint64_t n_short = g.n_rows - n_long;
+    if (n_long) {
+        SoftmaxArgs al = a;
+        al.order = g.order.get();
+        al.n = n_long;
+        cudaStream_t aux = n_short ? graph_fork(g, s) : s;
+        constexpr int smem = 2 * kCtaSmem * 4;
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const unsigned grid = unsigned(std::min<std::uint64_t>(n_long, std::uint64_t(sms) * 3));
+        auto go = [&](auto kern) {
+            ASB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            kern<<<grid, 256, smem, aux>>>(al);
+        };
+        if (lib) go(softmax_cta_kernel<OUT, true>);
+        else go(softmax_cta_kernel<OUT, false>);
+        check_launch("softmax_cta_kernel");
+    }
+    if (n_short) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        a.order = g.order.get() + n_long;
+        a.n = n_short;
+        const std::uint64_t want = (n_short + kWarpsPerCta - 1) / kWarpsPerCta;
+        const unsigned blocks = unsigned(std::min<std::uint64_t>(want, std::uint64_t(sms) * 6));
+        if (lib) softmax_warp_kernel<OUT, true><<<blocks, 32 * kWarpsPerCta, 0, s>>>(a);
+        else softmax_warp_kernel<OUT, false><<<blocks, 32 * kWarpsPerCta, 0, s>>>(a);
+        check_launch("softmax_warp_kernel");
+    }
+    if (n_long && n_short) graph_join(g, s);
 }
 
 } // namespace
 
 void launch_row_softmax(Graph& g, const float* vin, float* vout, cudaStream_t s) {
-    if (g.n_rows == 0 || g.nnz == 0) return;
-    ensure_order(g);
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const std::uint64_t want = (g.n_rows * 32 + 255) / 256;
-    const unsigned blocks = unsigned(std::min<std::uint64_t>(want, std::uint64_t(sms) * 8));
-    row_softmax_kernel<<<blocks, 256, 0, s>>>(g.rowptr.get(), g.order.get(), g.n_rows, vin, vout);
-    check_launch("row_softmax_kernel");
+    launch_softmax<true>(g, vin, vout, nullptr, nullptr, s);
+}
+
+void launch_row_softmax_stats(Graph& g, const float* vin, float* rmax, double* rsum, cudaStream_t s) {
+    launch_softmax<false>(g, vin, nullptr, rmax, rsum, s);
 }
 
 } // namespace asb

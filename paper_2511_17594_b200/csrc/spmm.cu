@@ -22,6 +22,7 @@
 //    kernel that streams the gathered B rows through a cp.async
 //    shared-memory ring, concurrently on a forked stream.
 #include "ops.hpp"
+#include "softmax.cuh"
 #include "widen.cuh"
 
 #include <algorithm>
@@ -75,6 +76,8 @@ struct SegArgs {
     const std::uint32_t* piece_len;
     const std::uint32_t* piece_slot;
     const unsigned* finite;           // device flag: B has no Inf/NaN (nullable)
+    const float* rmax;                // softmax mode: val holds raw scores, and
+    const double* rsum;               // p_e = softmax of the row (softmax.cuh)
     std::uint64_t n_items;
     std::uint32_t n_tiles;
     std::uint32_t f;
@@ -84,8 +87,10 @@ struct SegArgs {
 // One group of LPR lanes owns one (segment, feature tile) item; segment =
 // a whole row (row mode) or a hub piece (PIECES).  MIX selects the widening
 // of B: 0 = F2F only, 1 = components 2,3 of each float4 (or every scalar)
-// re-biased on the ALU pipe.
-template <int VEC, int LPR, int NCH, bool HAS_VAL, bool PIECES, int U, int MIX>
+// re-biased on the ALU pipe.  SMX: the entry values are softmax
+// probabilities computed from raw scores and the row's (max, sum) by the lane
+// that loads them (fused attention), instead of stored values.
+template <int VEC, int LPR, int NCH, bool HAS_VAL, bool PIECES, int U, int MIX, bool SMX>
 __device__ __forceinline__ void seg_body(const SegArgs& a) {
     using VT = typename VecT<VEC>::T;
     constexpr int GPW = 32 / LPR;
@@ -119,6 +124,15 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
     }
     std::uint32_t maxdeg = deg;
     if constexpr (GPW > 1) maxdeg = __reduce_max_sync(FULL, deg);
+    float rmx = 0.f;
+    double rsm = 1.0, rrc = 1.0;
+    if constexpr (SMX) {
+        if (active && deg) {
+            rmx = a.rmax[row];
+            rsm = a.rsum[row];
+            rrc = sm_rcp(rsm);
+        }
+    }
 
     const std::uint32_t f0 = tile * a.tile_w;
     const std::uint32_t fend = min(a.f, f0 + a.tile_w);
@@ -148,7 +162,8 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
             const std::uint32_t k = base + std::uint32_t(s * LPR + gl);
             const bool ok = k < deg;
             cs[s] = ok ? __ldg(colp + k) : 0u;
-            if constexpr (HAS_VAL) vs[s] = ok ? double(__ldg(valp + k)) : 0.0;
+            if constexpr (SMX) vs[s] = ok ? double(sm_prob_of(__ldg(valp + k), rmx, rsm, rrc)) : 0.0;
+            else if constexpr (HAS_VAL) vs[s] = ok ? double(__ldg(valp + k)) : 0.0;
             else vs[s] = 1.0;
         }
 #pragma unroll
@@ -213,10 +228,10 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
 }
 
 template <int VEC, int LPR, int NCH, bool HAS_VAL, bool PIECES, int U = unroll_for(VEC, NCH),
-          int MAXR = maxreg_for(VEC, NCH)>
+          int MAXR = maxreg_for(VEC, NCH), bool SMX = false>
 __global__ void __launch_bounds__(512) __maxnreg__(MAXR) spmm_seg_kernel(SegArgs a) {
-    if (a.finite && *a.finite) seg_body<VEC, LPR, NCH, HAS_VAL, PIECES, U, 1>(a);
-    else seg_body<VEC, LPR, NCH, HAS_VAL, PIECES, U, 0>(a);
+    if (a.finite && *a.finite) seg_body<VEC, LPR, NCH, HAS_VAL, PIECES, U, 1, SMX>(a);
+    else seg_body<VEC, LPR, NCH, HAS_VAL, PIECES, U, 0, SMX>(a);
 }
 
 // K3 epilogue: s = 0.0; s += partial[p] in piece order; C = f32(s)
@@ -335,7 +350,7 @@ __device__ __forceinline__ float long_comp(float4 v, int i) {
 // Row mode: item = a.rowlist[blockIdx.x]; piece mode: hub piece blockIdx.x,
 // written to its f64 partial slot (or straight to C when it is the row's
 // only piece) exactly like the lane-group piece path.
-template <int MIX, bool HAS_VAL, int FPL, bool PIECES>
+template <int MIX, bool HAS_VAL, int FPL, bool PIECES, bool SMX>
 __device__ __forceinline__ void longrow_body(const SegArgs& A, std::uint32_t ch, char* smem) {
     const std::uint64_t* __restrict__ rowptr = A.rowptr;
     const std::uint32_t* __restrict__ colind = A.colind;
@@ -367,6 +382,13 @@ __device__ __forceinline__ void longrow_body(const SegArgs& A, std::uint32_t ch,
     }
     const std::uint32_t nchunks = (deg + ch - 1) / ch;
     const int warp = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
+    float rmx = 0.f;
+    double rsm = 1.0, rrc = 1.0;
+    if constexpr (SMX) {
+        rmx = A.rmax[row];
+        rsm = A.rsum[row];
+        rrc = sm_rcp(rsm);
+    }
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
@@ -405,7 +427,8 @@ __device__ __forceinline__ void longrow_body(const SegArgs& A, std::uint32_t ch,
             const std::uint32_t* cs = cidx + (k % kIdxRing) * ch;
             const float* vs = vidx + (k % kIdxRing) * ch;
             double* vdst = vd + std::uint64_t(s) * ch;
-            for (std::uint32_t j = lane; j < n; j += 32) vdst[j] = HAS_VAL ? double(vs[j]) : 1.0;
+            for (std::uint32_t j = lane; j < n; j += 32)
+                vdst[j] = SMX ? double(sm_prob_of(vs[j], rmx, rsm, rrc)) : (HAS_VAL ? double(vs[j]) : 1.0);
             __syncwarp();
             mbar_arrive(&full[s]);  // release: this lane's value stores
             // the stage's B rows as 16-byte cp.async pieces spread over the
@@ -479,11 +502,11 @@ __device__ __forceinline__ void longrow_body(const SegArgs& A, std::uint32_t ch,
     }
 }
 
-template <bool HAS_VAL, int FPL, bool PIECES>
+template <bool HAS_VAL, int FPL, bool PIECES, bool SMX = false>
 __global__ void __launch_bounds__(32 + kLongMaxConsumers) spmm_longrow_kernel(SegArgs a, std::uint32_t ch) {
     extern __shared__ __align__(16) char lsmem[];
-    if (a.finite && *a.finite) longrow_body<1, HAS_VAL, FPL, PIECES>(a, ch, lsmem);
-    else longrow_body<0, HAS_VAL, FPL, PIECES>(a, ch, lsmem);
+    if (a.finite && *a.finite) longrow_body<1, HAS_VAL, FPL, PIECES, SMX>(a, ch, lsmem);
+    else longrow_body<0, HAS_VAL, FPL, PIECES, SMX>(a, ch, lsmem);
 }
 
 // Launch the ring kernel over n items (rows of a.rowlist, or hub pieces).
@@ -502,7 +525,8 @@ void launch_longrow(const SegArgs& a, std::uint64_t n, cudaStream_t s) {
     };
     auto by_val = [&](auto fc) {
         constexpr int FPL = decltype(fc)::value;
-        if (a.val) go(spmm_longrow_kernel<true, FPL, PIECES>);
+        if (a.rmax) go(spmm_longrow_kernel<true, FPL, PIECES, true>);
+        else if (a.val) go(spmm_longrow_kernel<true, FPL, PIECES>);
         else go(spmm_longrow_kernel<false, FPL, PIECES>);
     };
     if (fpl == 1) by_val(std::integral_constant<int, 1>{});
@@ -621,7 +645,14 @@ void launch_seg(const SegArgs& a, bool has_val, std::uint32_t wpb, cudaStream_t 
     if (blocks == 0) return;
     const bool pieces = a.piece_row != nullptr;
     const unsigned nb = unsigned(blocks), nt = wpb * 32;
-    if (has_val) {
+    if (a.rmax) {  // softmax mode (fused attention): float4 tiles only
+        if constexpr (VEC == 4) {
+            if (pieces) spmm_seg_kernel<VEC, LPR, NCH, true, true, unroll_for(VEC, NCH), maxreg_for(VEC, NCH), true><<<nb, nt, 0, s>>>(a);
+            else spmm_seg_kernel<VEC, LPR, NCH, true, false, unroll_for(VEC, NCH), maxreg_for(VEC, NCH), true><<<nb, nt, 0, s>>>(a);
+        } else {
+            throw LogicError("spmm softmax mode needs float4 tiles");
+        }
+    } else if (has_val) {
         if (pieces) launch_tuned<VEC, LPR, NCH, true, true>(a, nb, nt, s);
         else launch_tuned<VEC, LPR, NCH, true, false>(a, nb, nt, s);
     } else {
@@ -699,7 +730,9 @@ void launch_spmm_baseline(Graph& g, const float* val, const float* b, std::uint3
 
 void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uint64_t n_list,
                       const float* b, std::uint32_t f, float* c, std::uint64_t f_tile, bool vec,
-                      std::uint32_t wpb, cudaStream_t s, const unsigned* finite) {
+                      std::uint32_t wpb, cudaStream_t s, const unsigned* finite, const float* rmax,
+                      const double* rsum) {
+    if (rmax) vec = true;  // softmax mode runs float4 tiles (same numerics, engine gates f % 4)
     if (n_list == 0 || f == 0) return;
     ensure_order(g);
     // long rows (a prefix of the degree-descending order) -> CTA-per-row ring
@@ -719,6 +752,8 @@ void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uin
         a.c = c;
         a.rowlist = g.order.get() + offset;
         a.finite = finite;
+        a.rmax = rmax;
+        a.rsum = rsum;
         a.f = f;
         launch_longrow<false>(a, n_long, graph_fork(g, s));
         offset += n_long;
@@ -734,6 +769,8 @@ void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uin
         a.c = c;
         a.rowlist = g.order.get() + offset;
         a.finite = finite;
+        a.rmax = rmax;
+        a.rsum = rsum;
         a.n_items = n_list * t.n_tiles;
         a.n_tiles = t.n_tiles;
         a.f = f;
@@ -747,8 +784,10 @@ void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uin
 
 void launch_spmm_hubsplit(Graph& g, const float* val, const float* b, std::uint32_t f, float* c,
                           std::uint64_t f_tile, bool vec, std::uint32_t wpb,
-                          std::uint64_t hub_threshold, cudaStream_t s, const unsigned* finite) {
+                          std::uint64_t hub_threshold, cudaStream_t s, const unsigned* finite,
+                          const float* rmax, const double* rsum) {
     if (g.n_rows == 0 || f == 0) return;
+    if (rmax) vec = true;
     const HubPlan& plan = ensure_hub_plan(g, hub_threshold);
     wpb = warps_per_cta(wpb);
     const TileShape t = tile_shape(f, f_tile, vec);
@@ -762,7 +801,7 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const float* b, std::uint3
     const bool fork_light = concurrent && plan.n_light && plan.n_pieces;
     if (fork_light) {
         cudaStream_t aux = graph_fork(g, s);
-        launch_spmm_rows(g, val, plan.n_heavy, plan.n_light, b, f, c, f_tile, vec, wpb, aux, finite);
+        launch_spmm_rows(g, val, plan.n_heavy, plan.n_light, b, f, c, f_tile, vec, wpb, aux, finite, rmax, rsum);
     }
     if (plan.n_pieces) {
         SegArgs a{};
@@ -777,6 +816,8 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const float* b, std::uint3
         a.piece_len = plan.piece_len.get();
         a.piece_slot = plan.piece_slot.get();
         a.finite = finite;
+        a.rmax = rmax;
+        a.rsum = rsum;
         a.n_items = plan.n_pieces * t.n_tiles;
         a.n_tiles = t.n_tiles;
         a.f = f;
@@ -796,7 +837,7 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const float* b, std::uint3
     }
     if (fork_light) graph_join(g, s);
     else if (plan.n_light)
-        launch_spmm_rows(g, val, plan.n_heavy, plan.n_light, b, f, c, f_tile, vec, wpb, s, finite);
+        launch_spmm_rows(g, val, plan.n_heavy, plan.n_light, b, f, c, f_tile, vec, wpb, s, finite, rmax, rsum);
     if (plan.n_red) {
         const std::uint64_t total = plan.n_red * f;
         const unsigned blocks = unsigned(std::min<std::uint64_t>((total + 255) / 256, 148 * 32));

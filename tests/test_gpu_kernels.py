@@ -301,6 +301,78 @@ def test_row_softmax_vs_oracle(hub):
     assert ulp_diff(got, want) <= 1
 
 
+def _softmax_stress_graph(rng):
+    """Warp-path rows (<= 1024 entries) and CTA-path rows (> 1024) whose
+    values make the parallel-sum certificate hold (narrow range), fail
+    (tiny ex next to 1.0: very wide range, subnormal ex) or see NaN/Inf."""
+    m = hub_graph(rng, 6000, [5000, 3000, 1500, 1025, 1024, 600], 40, with_values=False)
+    vals = rng.uniform(-1, 1, size=m.nnz).astype(np.float32)
+    rp = m.rowptr.astype(np.int64)
+    wide = [1, 3, 5, 10, 11]  # rows whose sums need the sequential chain
+    for r in wide:
+        vals[rp[r]:rp[r + 1]] = rng.uniform(-110, 0, size=rp[r + 1] - rp[r]).astype(np.float32)
+    vals[rp[12]] = np.nan                 # short row with a NaN
+    vals[rp[2] + 7] = np.nan              # long row with a NaN
+    vals[rp[13]:rp[14]] = np.float32(-np.inf)
+    vals[rp[13]] = np.float32(3.0)        # -inf entries give ex = 0
+    return m, vals, wide
+
+
+def test_row_softmax_parallel_sum_equals_sequential_chain(monkeypatch):
+    """The certificate path (parallel f64 sum) and the reference's sequential
+    chain (AUTOSAGE_DEV_SOFTMAX_SEQ=1) give the same bits on every row, on
+    both the warp (<= 1024) and the CTA (> 1024 entries) kernels."""
+    rng = np.random.default_rng(61)
+    m, vals, _ = _softmax_stress_graph(rng)
+    fast = asb.row_softmax(m.with_values(vals)).val
+    monkeypatch.setenv("AUTOSAGE_DEV_SOFTMAX_SEQ", "1")
+    seq = asb.row_softmax(m.with_values(vals)).val
+    assert bit_equal(fast, seq)
+
+
+def test_row_softmax_written_out_exp_equals_cuda_exp(monkeypatch):
+    """sm_exp (softmax.cuh) is CUDA's f64 exp instruction sequence written
+    out; AUTOSAGE_DEV_SOFTMAX_LIBEXP=1 runs exp() itself.  Same bits over
+    arguments from 0 down past the f32 underflow and the fast-path edge
+    (-120), including exact ties, zeros, subnormal results and NaN."""
+    rng = np.random.default_rng(64)
+    m = hub_graph(rng, 3000, [2500, 1100], 200, with_values=False)
+    vals = rng.uniform(-130, 0, size=m.nnz).astype(np.float32)
+    vals[::97] = rng.uniform(-1e-3, 0, size=vals[::97].size).astype(np.float32)
+    edge = np.array([-120.0, -119.99999, -103.97208, -103.27893, -87.33655, -0.0, 0.0, -1e-30,
+                     -np.inf, np.nan, -126.5], np.float32)
+    vals[1:1 + edge.size] = edge            # inside the long row: max(row) stays 0-ish
+    rp = m.rowptr.astype(np.int64)
+    for r in range(2, 3000):                # every row's max is 0, so d = v exactly
+        vals[rp[r]] = 0.0
+    vals[rp[0]] = 0.0
+    vals[rp[1]] = 0.0
+    fast = asb.row_softmax(m.with_values(vals)).val
+    monkeypatch.setenv("AUTOSAGE_DEV_SOFTMAX_LIBEXP", "1")
+    lib = asb.row_softmax(m.with_values(vals)).val
+    assert bit_equal(np.nan_to_num(fast), np.nan_to_num(lib))
+    assert np.array_equal(np.isnan(fast), np.isnan(lib))
+    # the division fast path (q = ex * RN(1/sum), midpoint check) vs the
+    # oracle's correctly rounded division
+    want = oracle.row_softmax(m, vals)
+    ok = ~np.isnan(want)
+    assert ulp_diff(fast[ok], want[ok]) <= 1
+
+
+def test_row_softmax_long_and_wide_rows_vs_oracle():
+    rng = np.random.default_rng(62)
+    m, vals, wide = _softmax_stress_graph(rng)
+    got = asb.row_softmax(m.with_values(vals)).val
+    want = oracle.row_softmax(m, vals)
+    nan = np.isnan(want)
+    assert np.array_equal(np.isnan(got), nan)
+    rp = m.rowptr.astype(np.int64)
+    assert np.all(nan[rp[12]:rp[13]]) and np.all(nan[rp[2]:rp[3]])
+    assert max_err(got[~nan], want[~nan]) <= 1.0
+    assert ulp_diff(got[~nan], want[~nan]) <= 1
+    assert np.all(got[rp[13] + 1:rp[14]] == 0.0) and got[rp[13]] == 1.0
+
+
 # ---- dispatch (proj/tests/test_kernels.cpp:299-363) ------------------------------
 def test_dispatch_vec4_gate_and_path_marker():
     rng = np.random.default_rng(16)
@@ -393,6 +465,27 @@ def test_fused_attention_equals_unfused_bitwise():
     warm = asb.attention_probe_breakdown(p, q, k, v, asb.ProbeConfig(iters=2), ctx, fused=True)
     assert warm.sddmm_decision.source == asb.CACHED
     assert bit_equal(cold.output, warm.output)
+
+
+@pytest.mark.parametrize("force", [("AUTOSAGE_WPB", "4"), ("AUTOSAGE_HUB_T", "256"),
+                                   ("AUTOSAGE_HUB_T", "1"), ("AUTOSAGE_FTILE", "32")])
+@pytest.mark.parametrize("scale", [1.0, 40.0])
+def test_fused_attention_softmax_on_the_fly_bitwise(monkeypatch, force, scale):
+    """Fused path = SDDMM -> per-row (max, sum) -> SpMM computing each
+    probability as it loads the score.  Same bits as the staged pipeline for
+    row-parallel and hub-split SpMM (pieces, long rows, light rows), and for
+    score ranges wide enough that row sums take the sequential chain."""
+    monkeypatch.setenv(*force)  # a mapped SpMM variant (the fused path needs one)
+    rng = np.random.default_rng(63)
+    p = hub_graph(rng, 4000, [3900, 2049, 1500, 300], 25, with_values=False)
+    q = random_dense(rng, 4000, 64) * np.float32(scale)
+    k, v = random_dense(rng, 4000, 64), random_dense(rng, 4000, 32)
+    cache = asb.ScheduleCache()
+    ctx = asb.ScheduleContext(device=asb.DeviceProfile.fixed(20e9, 40e9, 2, "test"), cache=cache)
+    staged = asb.attention_probe_breakdown(p, q, k, v, asb.ProbeConfig(iters=2), ctx, fused=False)
+    fused = asb.attention_probe_breakdown(p, q, k, v, asb.ProbeConfig(iters=2), ctx, fused=True)
+    assert fused.spmm_decision.choice is not None
+    assert bit_equal(staged.output, fused.output)
 
 
 # ---- host-buffer pipeline (as_*_host, as_*_host_async) ------------------------------
