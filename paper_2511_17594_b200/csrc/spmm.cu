@@ -78,11 +78,27 @@ struct SegArgs {
     const unsigned* finite;           // device flag: B has no Inf/NaN (nullable)
     const float* rmax;                // softmax mode: val holds raw scores, and
     const double* rsum;               // p_e = softmax of the row (softmax.cuh)
+    int off32;                        // n_cols * f < 2^32: 32-bit element offsets
     std::uint64_t n_items;
     std::uint32_t n_tiles;
     std::uint32_t f;
     std::uint32_t tile_w;
 };
+
+// acc[ch][q] += v * B component, one DFMA each, with MIX's widening split
+template <int VEC, int NCH, int MIX, class VT>
+__device__ __forceinline__ void seg_accumulate(double (&acc)[NCH][VEC], double v, const VT (&bv)[NCH]) {
+    const double vu = MIX ? v * kWidenUp : v;
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) {
+            if (MIX && (VEC == 1 || q >= 2))
+                acc[ch][q] = __fma_rn(vu, widen_scaled(comp(bv[ch], q)), acc[ch][q]);
+            else
+                acc[ch][q] = __fma_rn(v, double(comp(bv[ch], q)), acc[ch][q]);
+        }
+}
 
 // One group of LPR lanes owns one (segment, feature tile) item; segment =
 // a whole row (row mode) or a hub piece (PIECES).  MIX selects the widening
@@ -154,7 +170,61 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
     const float* valp = HAS_VAL ? a.val + e0 : nullptr;
     const float* __restrict__ bmat = a.b;
 
-    for (std::uint32_t base = 0; base < maxdeg; base += W) {
+    // Fast path: while every group of the warp still has W whole entries
+    // left and every lane's features are in range, no predicates at all (a
+    // lane-constant feature predicate measured 25% slower: the compiler
+    // branches around each entry again); the loading lane pre-multiplies the
+    // column by f so each gather address is one IMAD off a per-lane row base.
+    // Same entries, same order.
+    std::uint32_t base = 0;
+    {
+        std::uint32_t mindeg = deg;
+        if constexpr (GPW > 1) mindeg = __reduce_min_sync(FULL, deg);
+        bool lane_full = true;
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) lane_full = lane_full && fok[ch];
+        const std::uint32_t fast_end = mindeg / W * W;
+        if (a.off32 && fast_end && __all_sync(FULL, lane_full)) {
+            const float* bl[NCH];
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch) bl[ch] = bmat + fidx[ch];
+            const std::uint32_t f = a.f;
+            for (; base < fast_end; base += W) {
+                std::uint32_t os[S];
+                double vs[S];
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    const std::uint32_t k = base + std::uint32_t(s * LPR + gl);
+                    os[s] = __ldg(colp + k) * f;
+                    if constexpr (SMX) vs[s] = double(sm_prob_of(__ldg(valp + k), rmx, rsm, rrc));
+                    else if constexpr (HAS_VAL) vs[s] = double(__ldg(valp + k));
+                    else vs[s] = 1.0;
+                }
+#pragma unroll
+                for (int j0 = 0; j0 < W; j0 += U) {
+                    std::uint32_t oj[U];
+                    double vj[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int j = j0 + u;
+                        oj[u] = __shfl_sync(FULL, os[j / LPR], int(gbase) + (j % LPR));
+                        if constexpr (HAS_VAL) vj[u] = __shfl_sync(FULL, vs[j / LPR], int(gbase) + (j % LPR));
+                        else vj[u] = 1.0;
+                    }
+                    VT bv[U][NCH];
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+#pragma unroll
+                        for (int ch = 0; ch < NCH; ++ch)
+                            bv[u][ch] = __ldg(reinterpret_cast<const VT*>(bl[ch] + oj[u]));
+#pragma unroll
+                    for (int u = 0; u < U; ++u) seg_accumulate<VEC, NCH, MIX>(acc, vj[u], bv[u]);
+                }
+            }
+        }
+    }
+
+    for (; base < maxdeg; base += W) {
         std::uint32_t cs[S];
         double vs[S];  // widened once here, by the lane that loaded it
 #pragma unroll
@@ -695,6 +765,16 @@ TileShape tile_shape(std::uint32_t f, std::uint64_t f_tile, bool vec) {
     return t;
 }
 
+// 32-bit gather offsets (col * f) fit; AUTOSAGE_DEV_SPMM_NOFAST=1 disables
+// the predicate-free fast loop (developer A/B knob)
+int fast_gather_ok(const Graph& g, std::uint32_t f) {
+    static const bool off = [] {
+        const char* e = std::getenv("AUTOSAGE_DEV_SPMM_NOFAST");
+        return e && std::atoi(e) != 0;
+    }();
+    return !off && std::uint64_t(g.n_cols) * f < (std::uint64_t(1) << 32);
+}
+
 // Rows at least this long go to the CTA-per-row ring kernel.  In the
 // lane-group kernel a row is a chain of dependent L2 round trips (U entries
 // in flight), so on a small graph its longest rows set the kernel time; on
@@ -755,6 +835,7 @@ void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uin
         a.rmax = rmax;
         a.rsum = rsum;
         a.f = f;
+        a.off32 = fast_gather_ok(g, f);
         launch_longrow<false>(a, n_long, graph_fork(g, s));
         offset += n_long;
         n_list -= n_long;
@@ -774,6 +855,7 @@ void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uin
         a.n_items = n_list * t.n_tiles;
         a.n_tiles = t.n_tiles;
         a.f = f;
+        a.off32 = fast_gather_ok(g, f);
         a.tile_w = t.tile_w;
         wpb = warps_per_cta(wpb);
         if (vec) launch_seg_vec<4>(a, val != nullptr, t.lanes, wpb, s);
@@ -821,6 +903,7 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const float* b, std::uint3
         a.n_items = plan.n_pieces * t.n_tiles;
         a.n_tiles = t.n_tiles;
         a.f = f;
+        a.off32 = fast_gather_ok(g, f);
         a.tile_w = t.tile_w;
         // pieces are up to 2048-entry dependent chains: when there are too
         // few of them to fill the lane-group kernel (under a wave), the ring
