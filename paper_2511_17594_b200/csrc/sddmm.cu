@@ -487,8 +487,10 @@ struct PairShape {
 
 // One pass (features [p*FW, (p+1)*FW)) of both chains.  FT = 0: one f_tile
 // block over all of F.
-template <int FW, int ORD, int FT, bool XS, int MIX>
-__device__ __forceinline__ void pair_pass(const double* __restrict__ xa, const double* __restrict__ xb, bool same_x,
+// SAME: both entries of every lane sit in one row (warp-uniform), so the
+// second X read is skipped without a per-step branch
+template <int FW, int ORD, int FT, bool XS, int MIX, bool SAME>
+__device__ __forceinline__ void pair_pass(const double* __restrict__ xa, const double* __restrict__ xb,
                                           const float* ya, const float* yb, int ka, int kb, int p, int npass,
                                           double (&c)[2][5]) {
 #pragma unroll 4
@@ -498,7 +500,7 @@ __device__ __forceinline__ void pair_pass(const double* __restrict__ xa, const d
         const double2 x01 = ld_x2<XS>(xa + t);
         const double2 x23 = ld_x2<XS>(xa + t + 2);
         double2 z01 = x01, z23 = x23;
-        if (!same_x) {
+        if constexpr (!SAME) {
             z01 = ld_x2<XS>(xb + t);
             z23 = ld_x2<XS>(xb + t + 2);
         }
@@ -615,16 +617,23 @@ __device__ __forceinline__ void sddmm_pair_body(const std::uint64_t* __restrict_
         const float* ya = ys + lane * FW;
         const float* yb = ys + (lane + 32) * FW;
         const int ka = swz<Sh::NV>(lane), kb = swz<Sh::NV>(lane + 32);
+        // warp-uniform, taken before the per-lane staged/unstaged split
+        const bool all_same = __all_sync(FULL, rela == relb);
         auto run_pass = [&](int p) {
             asm volatile("cp.async.wait_group 0;\n" ::: "memory");
             __syncwarp();
-            if (staged)
-                pair_pass<FW, ORD, FT, true, MIX>(xs + rela * FW, xs + relb * FW, rela == relb, ya, yb, ka, kb, p,
-                                                  npass, c);
-            else
-                pair_pass<FW, ORD, FT, false, MIX>(xd + std::uint64_t(ra) * F + p * FW,
-                                                   xd + std::uint64_t(rb) * F + p * FW, ra == rb, ya, yb, ka, kb,
-                                                   p, npass, c);
+            if (staged) {
+                if (all_same)
+                    pair_pass<FW, ORD, FT, true, MIX, true>(xs + rela * FW, xs + relb * FW, ya, yb, ka, kb, p,
+                                                            npass, c);
+                else
+                    pair_pass<FW, ORD, FT, true, MIX, false>(xs + rela * FW, xs + relb * FW, ya, yb, ka, kb, p,
+                                                             npass, c);
+            } else {
+                pair_pass<FW, ORD, FT, false, MIX, false>(xd + std::uint64_t(ra) * F + p * FW,
+                                                          xd + std::uint64_t(rb) * F + p * FW, ya, yb, ka, kb, p,
+                                                          npass, c);
+            }
         };
         if constexpr (NP == 1) {
             run_pass(0);
@@ -669,8 +678,8 @@ struct Pair1Shape {
     static constexpr std::uint64_t kWarpBytes = kYBytes + std::uint64_t(KX) * F * 8;
 };
 
-template <int F, int ORD, int FT, bool XS, int MIX>
-__device__ __forceinline__ void pair1_pass(const double* __restrict__ xa, const double* __restrict__ xb, bool same_x,
+template <int F, int ORD, int FT, bool XS, int MIX, bool SAME>
+__device__ __forceinline__ void pair1_pass(const double* __restrict__ xa, const double* __restrict__ xb,
                                           const float* ya, const float* yb, int ka, int kb, double (&c)[2][5]) {
 #pragma unroll 4
     for (int t = 0; t < F; t += 4) {
@@ -679,7 +688,7 @@ __device__ __forceinline__ void pair1_pass(const double* __restrict__ xa, const 
         const double2 x01 = ld_x2<XS>(xa + t);
         const double2 x23 = ld_x2<XS>(xa + t + 2);
         double2 z01 = x01, z23 = x23;
-        if (!same_x) {
+        if constexpr (!SAME) {
             z01 = ld_x2<XS>(xb + t);
             z23 = ld_x2<XS>(xb + t + 2);
         }
@@ -784,11 +793,16 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
         const float* ya = ys + lane * F;
         const float* yb = ys + (lane + 32) * F;
         const int ka = swz<Sh::NV>(lane), kb = swz<Sh::NV>(lane + 32);
-        if (rela < Sh::KX && relb < Sh::KX)
-            pair1_pass<F, ORD, FT, true, MIX>(xs + rela * F, xs + relb * F, rela == relb, ya, yb, ka, kb, c);
-        else
-            pair1_pass<F, ORD, FT, false, MIX>(xd + std::uint64_t(ra) * F, xd + std::uint64_t(rb) * F, ra == rb, ya,
-                                              yb, ka, kb, c);
+        const bool all_same = __all_sync(FULL, rela == relb);  // warp-uniform, before the split
+        if (rela < Sh::KX && relb < Sh::KX) {
+            if (all_same)
+                pair1_pass<F, ORD, FT, true, MIX, true>(xs + rela * F, xs + relb * F, ya, yb, ka, kb, c);
+            else
+                pair1_pass<F, ORD, FT, true, MIX, false>(xs + rela * F, xs + relb * F, ya, yb, ka, kb, c);
+        } else {
+            pair1_pass<F, ORD, FT, false, MIX, false>(xd + std::uint64_t(ra) * F, xd + std::uint64_t(rb) * F, ya,
+                                                     yb, ka, kb, c);
+        }
         if (ea < e_end) out[ea] = float(c[0][0]);
         if (eb < e_end) out[eb] = float(c[1][0]);
         __syncwarp();
