@@ -35,6 +35,7 @@ namespace asb {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
+constexpr int kSegMaxS = 8;  // max entries per lane per fast-loop block (seg_smem)
 
 template <int VEC>
 struct VecT;
@@ -189,17 +190,26 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
 #pragma unroll
             for (int ch = 0; ch < NCH; ++ch) bl[ch] = bmat + fidx[ch];
             const std::uint32_t f = a.f;
+            // (value, offset) of the warp's W*GPW entries go through shared
+            // memory: one STS.128 per lane per block and one broadcast
+            // LDS.128 per entry, instead of three shuffles per entry (the
+            // shuffles held ~40% of the LSU data pipe)
+            extern __shared__ __align__(16) double2 seg_ent[];
+            static_assert(S <= kSegMaxS, "seg_smem too small");
+            double2* ent = seg_ent + (threadIdx.x >> 5) * (32 * S);
             for (; base < fast_end; base += W) {
-                std::uint32_t os[S];
-                double vs[S];
+                __syncwarp();  // the previous block's readers are done
 #pragma unroll
                 for (int s = 0; s < S; ++s) {
                     const std::uint32_t k = base + std::uint32_t(s * LPR + gl);
-                    os[s] = __ldg(colp + k) * f;
-                    if constexpr (SMX) vs[s] = double(sm_prob_of(__ldg(valp + k), rmx, rsm, rrc));
-                    else if constexpr (HAS_VAL) vs[s] = double(__ldg(valp + k));
-                    else vs[s] = 1.0;
+                    const std::uint32_t o = __ldg(colp + k) * f;
+                    double v;
+                    if constexpr (SMX) v = double(sm_prob_of(__ldg(valp + k), rmx, rsm, rrc));
+                    else if constexpr (HAS_VAL) v = double(__ldg(valp + k));
+                    else v = 1.0;
+                    ent[s * 32 + lane] = make_double2(v, __hiloint2double(0, int(o)));
                 }
+                __syncwarp();
 #pragma unroll
                 for (int j0 = 0; j0 < W; j0 += U) {
                     std::uint32_t oj[U];
@@ -207,9 +217,9 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         const int j = j0 + u;
-                        oj[u] = __shfl_sync(FULL, os[j / LPR], int(gbase) + (j % LPR));
-                        if constexpr (HAS_VAL) vj[u] = __shfl_sync(FULL, vs[j / LPR], int(gbase) + (j % LPR));
-                        else vj[u] = 1.0;
+                        const double2 e = ent[(j / LPR) * 32 + int(gbase) + (j % LPR)];
+                        oj[u] = unsigned(__double2loint(e.y));
+                        vj[u] = e.x;
                     }
                     VT bv[U][NCH];
 #pragma unroll
@@ -644,6 +654,11 @@ __global__ void spmm_baseline_kernel(const std::uint64_t* __restrict__ rowptr,
     }
 }
 
+// dynamic shared memory of the lane-group kernels: the fast loop's
+// (value, offset) staging, 32 x S double2 per warp (S = max(LPR, U) / LPR
+// <= 8, reached by scalar single-lane groups)
+std::size_t seg_smem(unsigned threads) { return std::size_t(threads / 32) * 32 * kSegMaxS * sizeof(double2); }
+
 // developer tuning knob (AUTOSAGE_DEV_SPMM_TUNE=<U>x<MAXR>) for the F=64
 // shapes; default = the tuned constants above
 int dev_tune() {
@@ -674,24 +689,24 @@ template <int VEC, int LPR, int NCH, bool HV, bool PC>
 void launch_tuned(const SegArgs& a, unsigned blocks, unsigned threads, cudaStream_t s) {
     if constexpr (VEC == 4 && NCH == 1 && (LPR == 16 || LPR == 8) && HV) {
         switch (dev_tune()) {
-            case 1: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 2, 40><<<blocks, threads, 0, s>>>(a); return;
-            case 2: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 4, 40><<<blocks, threads, 0, s>>>(a); return;
-            case 3: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 4, 48><<<blocks, threads, 0, s>>>(a); return;
-            case 4: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 8, 48><<<blocks, threads, 0, s>>>(a); return;
-            case 5: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 8, 64><<<blocks, threads, 0, s>>>(a); return;
-            case 6: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 8, 128><<<blocks, threads, 0, s>>>(a); return;
-            case 7: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 2, 48><<<blocks, threads, 0, s>>>(a); return;
-            case 8: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 4, 56><<<blocks, threads, 0, s>>>(a); return;
-            case 9: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 4, 64><<<blocks, threads, 0, s>>>(a); return;
-            case 10: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 6, 64><<<blocks, threads, 0, s>>>(a); return;
-            case 11: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 6, 80><<<blocks, threads, 0, s>>>(a); return;
-            case 12: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 8, 80><<<blocks, threads, 0, s>>>(a); return;
-            case 13: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 8, 96><<<blocks, threads, 0, s>>>(a); return;
-            case 14: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 4, 72><<<blocks, threads, 0, s>>>(a); return;
+            case 1: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 2, 40><<<blocks, threads, seg_smem(threads), s>>>(a); return;
+            case 2: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 4, 40><<<blocks, threads, seg_smem(threads), s>>>(a); return;
+            case 3: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 4, 48><<<blocks, threads, seg_smem(threads), s>>>(a); return;
+            case 4: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 8, 48><<<blocks, threads, seg_smem(threads), s>>>(a); return;
+            case 5: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 8, 64><<<blocks, threads, seg_smem(threads), s>>>(a); return;
+            case 6: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 8, 128><<<blocks, threads, seg_smem(threads), s>>>(a); return;
+            case 7: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 2, 48><<<blocks, threads, seg_smem(threads), s>>>(a); return;
+            case 8: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 4, 56><<<blocks, threads, seg_smem(threads), s>>>(a); return;
+            case 9: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 4, 64><<<blocks, threads, seg_smem(threads), s>>>(a); return;
+            case 10: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 6, 64><<<blocks, threads, seg_smem(threads), s>>>(a); return;
+            case 11: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 6, 80><<<blocks, threads, seg_smem(threads), s>>>(a); return;
+            case 12: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 8, 80><<<blocks, threads, seg_smem(threads), s>>>(a); return;
+            case 13: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 8, 96><<<blocks, threads, seg_smem(threads), s>>>(a); return;
+            case 14: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 4, 72><<<blocks, threads, seg_smem(threads), s>>>(a); return;
             default: break;
         }
     }
-    spmm_seg_kernel<VEC, LPR, NCH, HV, PC><<<blocks, threads, 0, s>>>(a);
+    spmm_seg_kernel<VEC, LPR, NCH, HV, PC><<<blocks, threads, seg_smem(threads), s>>>(a);
 }
 
 // Warps per CTA of the lane-group kernels.  The reference's rows_per_chunk
@@ -717,8 +732,8 @@ void launch_seg(const SegArgs& a, bool has_val, std::uint32_t wpb, cudaStream_t 
     const unsigned nb = unsigned(blocks), nt = wpb * 32;
     if (a.rmax) {  // softmax mode (fused attention): float4 tiles only
         if constexpr (VEC == 4) {
-            if (pieces) spmm_seg_kernel<VEC, LPR, NCH, true, true, unroll_for(VEC, NCH), maxreg_for(VEC, NCH), true><<<nb, nt, 0, s>>>(a);
-            else spmm_seg_kernel<VEC, LPR, NCH, true, false, unroll_for(VEC, NCH), maxreg_for(VEC, NCH), true><<<nb, nt, 0, s>>>(a);
+            if (pieces) spmm_seg_kernel<VEC, LPR, NCH, true, true, unroll_for(VEC, NCH), maxreg_for(VEC, NCH), true><<<nb, nt, seg_smem(nt), s>>>(a);
+            else spmm_seg_kernel<VEC, LPR, NCH, true, false, unroll_for(VEC, NCH), maxreg_for(VEC, NCH), true><<<nb, nt, seg_smem(nt), s>>>(a);
         } else {
             throw LogicError("spmm softmax mode needs float4 tiles");
         }
