@@ -21,6 +21,8 @@ def main():
     ap.add_argument("--f", type=int, default=64)
     ap.add_argument("--fused", type=int, default=1)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--cache", default="", help="schedule cache: load if present, store after the run")
+    ap.add_argument("--replay-only", action="store_true", help="decisions must come from --cache")
     a = ap.parse_args()
     m, _ = bench.make_graph(a.config, 1)
     f = a.f
@@ -30,7 +32,11 @@ def main():
     k = torch.from_numpy(asb.fill_uniform(m.n_cols * f, 2, (m.n_cols, f))).to(dev)
     v = torch.from_numpy(asb.fill_uniform(m.n_cols * f, 3, (m.n_cols, f))).to(dev)
     out = torch.empty((m.n_rows, f), dtype=torch.float32, device=dev)
-    ctx = asb.ScheduleContext(cache=asb.ScheduleCache(), stream=asb.torch_stream_handle())
+    cache = asb.ScheduleCache()
+    if a.cache and os.path.exists(a.cache):
+        cache.load(a.cache)
+    ctx = asb.ScheduleContext(cache=cache, stream=asb.torch_stream_handle(),
+                              replay=asb.ReplayPolicy(replay_only=a.replay_only, strict=a.replay_only))
     cctx, keep = ctx.to_c()
     ccfg = asb.ProbeConfig.from_env().to_c()
     sd, pd = _capi.as_decision(), _capi.as_decision()
@@ -44,6 +50,9 @@ def main():
         e1.record()
         e1.synchronize()
         print("attention fused=%d" % a.fused, e0.elapsed_time(e1), flush=True)
+    print("choices", asb.ScheduleDecision.from_c(sd).choice_string(), asb.ScheduleDecision.from_c(pd).choice_string())
+    if a.cache and not a.replay_only:
+        cache.store(a.cache)
     del keep
 
 
