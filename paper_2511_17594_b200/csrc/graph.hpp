@@ -97,6 +97,9 @@ struct Graph {
     DevBuf<float> att_buf;             // attention: scores | probabilities (staged)
     DevBuf<float> att_max;             // fused attention: per-row score max ...
     DevBuf<double> att_sum;            // ... and softmax denominator
+    DevBuf<std::uint32_t> sm_chain_row; // row softmax: long rows whose sum needs
+    DevBuf<float> sm_chain_mx;          // the entry-order chain (row, max) ...
+    DevBuf<unsigned> sm_chain_n;        // ... and their count
     DevBuf<float> stage_in, stage_out; // host-buffer row softmax
     std::map<std::uint64_t, std::uint64_t> ge_count;  // rows with degree >= key
     DevBuf<unsigned> flag;             // finiteness flag of the current dense operand

@@ -46,6 +46,11 @@ struct SoftmaxArgs {
     float* rmax;    // !OUT
     double* rsum;   // !OUT
     int force_seq;  // developer/test knob: always run the sequential chain
+    // CTA kernel: rows whose certificate failed are handed to the chain
+    // kernel (row, max) instead of serialising the CTA on one sum chain
+    std::uint32_t* chain_row;
+    float* chain_mx;
+    unsigned* chain_n;
 };
 
 // LIB: exp() itself instead of the written-out sm_exp (test knob
@@ -202,7 +207,6 @@ template <bool OUT, bool LIB>
 __global__ void __launch_bounds__(256, 3) softmax_cta_kernel(SoftmaxArgs a) {
     extern __shared__ __align__(16) float cbuf[];  // 2 x kCtaSmem floats
     __shared__ CtaRed red;
-    __shared__ double chunk[256];
     const int tid = threadIdx.x;
     struct RowRef {
         std::uint32_t row, deg;
@@ -272,20 +276,17 @@ __global__ void __launch_bounds__(256, 3) softmax_cta_kernel(SoftmaxArgs a) {
         }
         cta_sum(red, sum, mn);
         if (a.force_seq || !sm_sum_exact(sum, mn)) {  // block-uniform
-            double sq = 0.0;
-            for (std::uint32_t base = 0; base < deg; base += 256) {
-                const std::uint32_t k = base + tid;
-                if (k < deg) chunk[tid] = double(staged ? cexs[k] : ex_of<LIB>(__ldg(vin + k), dmx));
-                __syncthreads();
-                if (tid == 0) {
-                    const std::uint32_t n = deg - base < 256 ? deg - base : 256;
-                    for (std::uint32_t j = 0; j < n; ++j) sq = __dadd_rn(sq, chunk[j]);
-                }
-                __syncthreads();
+            // the sum needs the entry-order chain: defer the row to the
+            // chain kernel (one lane per row there, many rows in flight)
+            if (tid == 0) {
+                const unsigned i = atomicAdd(a.chain_n, 1u);
+                a.chain_row[i] = cur.row;
+                a.chain_mx[i] = mx;
             }
-            if (tid == 0) red.seq = sq;
-            __syncthreads();
-            sum = red.seq;
+            __syncthreads();  // buffer `slot` / `red` reuse
+            cur = nxt;
+            nxt = nn;
+            continue;
         }
         if constexpr (OUT) {
             const double rcp = sm_rcp(sum);
@@ -309,6 +310,62 @@ __global__ void __launch_bounds__(256, 3) softmax_cta_kernel(SoftmaxArgs a) {
         nxt = nn;
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+// Rows deferred by the CTA kernel: warp per row, many warps per SM so many
+// chains are in flight.  32 entries at a time the lanes recompute ex in
+// parallel (next chunk's values already loaded) and stage it as f64; lane 0
+// folds them into the row's sum in entry order (the reference's chain, one
+// DADD per entry, two entries per LDS.128).  Then the output pass (ex
+// recomputed, coalesced) or the stats write.  (Lane per row -- 32 chains per
+// warp, each lane walking its own row -- measured 10x slower: the
+// uncoalesced per-lane streams thrash L1.)
+template <bool OUT, bool LIB>
+__global__ void __launch_bounds__(256, 4) softmax_chain_kernel(SoftmaxArgs a) {
+    __shared__ __align__(16) double stage_all[kWarpsPerCta][32];
+    const int lane = threadIdx.x & 31;
+    double* st = stage_all[threadIdx.x >> 5];
+    const unsigned n = *a.chain_n;
+    const std::uint64_t tw = std::uint64_t(gridDim.x) * (blockDim.x >> 5);
+    for (std::uint64_t w = (std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n; w += tw) {
+        const std::uint32_t row = a.chain_row[w];
+        const float mx = a.chain_mx[w];
+        const double dmx = double(mx);
+        const std::uint64_t e0 = a.rowptr[row];
+        const std::uint32_t deg = std::uint32_t(a.rowptr[row + 1] - e0);
+        const float* vin = a.vin + e0;
+        double sum = 0.0;
+        float vnext = lane < int(deg) ? __ldg(vin + lane) : 0.f;
+        for (std::uint32_t base = 0; base < deg; base += 32) {
+            const float v = vnext;
+            const std::uint32_t kn = base + 32 + lane;
+            vnext = kn < deg ? __ldg(vin + kn) : 0.f;
+            st[lane] = base + lane < deg ? double(ex_of<LIB>(v, dmx)) : 0.0;
+            __syncwarp();
+            if (lane == 0) {
+                const std::uint32_t m = deg - base < 32 ? deg - base : 32;
+                std::uint32_t j = 0;
+                for (; j + 2 <= m; j += 2) {
+                    const double2 d = *reinterpret_cast<const double2*>(st + j);
+                    sum = __dadd_rn(sum, d.x);
+                    sum = __dadd_rn(sum, d.y);
+                }
+                if (j < m) sum = __dadd_rn(sum, st[j]);
+            }
+            __syncwarp();
+        }
+        sum = __shfl_sync(FULL, sum, 0);
+        if constexpr (OUT) {
+            const double rcp = sm_rcp(sum);
+            float* vout = a.vout + e0;
+            // plain loads: vout may alias vin (read, then written, by one lane)
+#pragma unroll 4
+            for (std::uint32_t k = lane; k < deg; k += 32) vout[k] = sm_prob(ex_of<LIB>(vin[k], dmx), sum, rcp);
+        } else if (lane == 0) {
+            a.rmax[row] = mx;
+            a.rsum[row] = sum;
+        }
+    }
 }
 
 bool env_flag(const char* name) {
@@ -344,9 +401,21 @@ void launch_softmax(Graph& g, const float* vin, float* vout, float* rmax, double
             ASB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             kern<<<grid, 256, smem, aux>>>(al);
         };
+        g.sm_chain_row.ensure(n_long);
+        g.sm_chain_mx.ensure(n_long);
+        g.sm_chain_n.ensure(1);
+        al.chain_row = g.sm_chain_row.get();
+        al.chain_mx = g.sm_chain_mx.get();
+        al.chain_n = g.sm_chain_n.get();
+        ASB_CUDA(cudaMemsetAsync(al.chain_n, 0, sizeof(unsigned), aux));
         if (lib) go(softmax_cta_kernel<OUT, true>);
         else go(softmax_cta_kernel<OUT, false>);
         check_launch("softmax_cta_kernel");
+        const unsigned cgrid = unsigned(std::min<std::uint64_t>((n_long + kWarpsPerCta - 1) / kWarpsPerCta,
+                                                                std::uint64_t(sms) * 4));
+        if (lib) softmax_chain_kernel<OUT, true><<<cgrid, 32 * kWarpsPerCta, 0, aux>>>(al);
+        else softmax_chain_kernel<OUT, false><<<cgrid, 32 * kWarpsPerCta, 0, aux>>>(al);
+        check_launch("softmax_chain_kernel");
     }
     if (n_short) {
         int dev = 0, sms = 148;
