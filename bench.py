@@ -406,6 +406,10 @@ def run_ours(args):
                                            "sddmm": dec_sddmm.source_name},
                        "probe": dataclasses_asdict(cfg)},
             "ms_per_op": {"spmm": t_spmm / K, "sddmm": t_sddmm / K, "allgather": t_gather / K},
+            # 2*nnz*F flops per op (proj/src/cost.cpp:28), whole job
+            "gflops_per_s": {"spmm": 2.0 * nnz * f / (t_spmm / K * 1e-3) / 1e9,
+                             "sddmm": 2.0 * nnz * f / (t_sddmm / K * 1e-3) / 1e9,
+                             "step": 4.0 * nnz * f / (total / K * 1e-3) / 1e9},
             "pct_of_8TBs": value / 8000.0 * 100.0,
             "decide_cold_ms": cold_ms,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -43,11 +43,13 @@ def main():
     if "c2" in r:
         g = r["c2"]["graph"]
         L += [f"## c2 — Reddit-shape N={g['n']}, nnz={g['nnz']}", "",
-              "| F | op | choice | ms | GB/s | frac | baseline ms |", "|---|---|---|---|---|---|---|"]
+              "| F | op | choice | ms | GB/s | frac | GFLOP/s | baseline ms |",
+              "|---|---|---|---|---|---|---|---|"]
         for f, ops in r["c2"]["by_F"].items():
             for op, e in ops.items():
+                gf = 2.0 * g["nnz"] * int(f) / (e["ms"] * 1e-3) / 1e9  # 2*nnz*F, proj/src/cost.cpp:28
                 L.append(f"| {f} | {op} | `{e['choice']}` | {f3(e['ms'])} | {e['gbs']:.0f} | "
-                         f"{e['frac_hbm']:.2f} | {f3(e['baseline_ms'])} |")
+                         f"{e['frac_hbm']:.2f} | {gf:.0f} | {f3(e['baseline_ms'])} |")
         cs = r["c2"].get("cusparse")
         if cs:
             L += ["", "cuSPARSE on the same graph via torch (fp32 accumulation, so a speed reference only — not the",
