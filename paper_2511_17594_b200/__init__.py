@@ -1018,8 +1018,9 @@ class AttentionRun:
 def attention_probe_breakdown(pattern, q, k, v, cfg: Optional[ProbeConfig] = None,
                               ctx: Optional[ScheduleContext] = None,
                               fused: bool = False) -> AttentionRun:
-    """src/attention.cpp:9-40; fused=True runs the one-pass kernel with the
-    decided variants' numerics."""
+    """src/attention.cpp:9-40.  fused=True: SDDMM -> per-row (max, sum) -> SpMM
+    that applies the softmax to each score as it loads it (no probability
+    array); the same bits as the staged pipeline (fused=False)."""
     import torch
     cfg = cfg or ProbeConfig()
     ctx = ctx or ScheduleContext()
