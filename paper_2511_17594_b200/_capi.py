@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libautosage_b200.so")
+# AUTOSAGE_DEV_LIB: an alternative in-tree build for developer A/B runs
+LIB_PATH = os.environ.get("AUTOSAGE_DEV_LIB") or os.path.join(_HERE, "libautosage_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

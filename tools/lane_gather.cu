@@ -3,6 +3,8 @@
 //   A: lane per row, 16 LDG.128 per lane (32 distinct rows per instruction)
 //   B: 16 lanes per row, one LDG.128 per lane (2 rows per instruction)
 //   C: lane per row via cp.async into shared memory + LDS.128 (SDDMM today)
+//   D: lane per row via one TMA bulk copy per row (cp.async.bulk, mbarrier
+//      completion) + LDS.128 -- does the async proxy relieve the LSU pipe?
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/lane_gather tools/lane_gather.cu
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -79,6 +81,39 @@ __global__ void __launch_bounds__(128) smem_row(const float* __restrict__ b, uns
     if (acc == 12345.f) out[blockIdx.x * 128 + threadIdx.x] = acc;
 }
 
+__global__ void __launch_bounds__(128) tma_row(const float* __restrict__ b, unsigned n, unsigned long long m,
+                                               float* __restrict__ out) {
+    extern __shared__ __align__(16) float smt[];
+    __shared__ __align__(8) unsigned long long bar[4];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    float* ys = smt + w * 32 * F;
+    const unsigned bs = unsigned(__cvta_generic_to_shared(&bar[w]));
+    if (lane == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bs));
+    __syncwarp();
+    const unsigned long long wid = blockIdx.x * 4ull + w, nw = gridDim.x * 4ull;
+    float acc = 0.f;
+    unsigned phase = 0;
+    for (unsigned long long c = wid * 32; c < m; c += nw * 32) {
+        const unsigned myrow = hsh(unsigned(c + lane)) % n;
+        if (lane == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bs), "r"(32u * F * 4) : "memory");
+        __syncwarp();
+        const unsigned dst = unsigned(__cvta_generic_to_shared(ys + lane * F));
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                     ::"r"(dst), "l"(b + std::uint64_t(myrow) * F), "r"(F * 4), "r"(bs) : "memory");
+        asm volatile("{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n}\n"
+                     ::"r"(bs), "r"(phase) : "memory");
+        phase ^= 1;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const float4 v = *reinterpret_cast<const float4*>(ys + lane * F + 4 * q);
+            acc += v.x + v.y + v.z + v.w;
+        }
+        __syncwarp();
+    }
+    if (acc == 12345.f) out[blockIdx.x * 128 + threadIdx.x] = acc;
+}
+
 int main() {
     const unsigned n = 232965;
     const unsigned long long m = 114615892ull;
@@ -91,20 +126,23 @@ int main() {
     cudaEventCreate(&e1);
     const double bytes = double(m) * F * 4;
     cudaFuncSetAttribute(smem_row, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 32 * F * 4);
+    cudaFuncSetAttribute(tma_row, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 32 * F * 4);
     for (int blocks_per_sm : {4, 8, 16}) {
         const int grid = 148 * blocks_per_sm;
-        for (int k = 0; k < 3; ++k) {
+        for (int k = 0; k < 4; ++k) {
             float t[3];
             for (int rep = 0; rep < 3; ++rep) {
                 cudaEventRecord(e0);
                 if (k == 0) lane_row<<<grid, 128>>>(b, n, m, out);
                 if (k == 1) group_row<<<grid, 128>>>(b, n, m, out);
                 if (k == 2) smem_row<<<grid, 128, 4 * 32 * F * 4>>>(b, n, m, out);
+                if (k == 3) tma_row<<<grid, 128, 4 * 32 * F * 4>>>(b, n, m, out);
                 cudaEventRecord(e1);
                 cudaEventSynchronize(e1);
                 cudaEventElapsedTime(&t[rep], e0, e1);
             }
-            const char* nm[] = {"lane-per-row LDG.128", "16-lanes-per-row LDG.128", "cp.async smem + LDS.128"};
+            const char* nm[] = {"lane-per-row LDG.128", "16-lanes-per-row LDG.128", "cp.async smem + LDS.128",
+                                "TMA bulk row + LDS.128"};
             std::printf("%-28s blocks/SM %2d: %.3f ms  %.1f TB/s\n", nm[k], blocks_per_sm, t[2], bytes / (t[2] * 1e-3) / 1e12);
         }
     }
