@@ -8,8 +8,15 @@ to the single-GPU result (every output row is computed by exactly one rank
 with the same arithmetic).  The only exchange is an all-gather of the dense
 operand's row shards (B for SpMM, Y for SDDMM, K/V for attention): for a
 square graph rank r owns rows [cut_r, cut_{r+1}) of every node-feature
-matrix.  Shards are padded to the largest shard for all_gather_into_tensor
-and un-padded with one index_select.
+matrix.  Shards are padded to the largest shard for all_gather_into_tensor.
+
+Padded-native layout (what bench.py runs): each rank's shard graph has its
+column indices remapped once, c -> owner(c) * shard + (c - cut[owner(c)]),
+so the kernels gather straight from the padded all-gather buffer -- no
+per-step un-pad copy, and the rank's own rows are the all-gather input
+in place.  The remap is monotone in c, so every row keeps its entry order
+and the results stay bit-identical.  allgather_rows (un-padded, global row
+order) remains for callers that need the plain matrix.
 """
 from __future__ import annotations
 
@@ -40,6 +47,32 @@ class RowSharding:
         self.perm = np.concatenate([r * self.shard + np.arange(self.sizes[r])
                                     for r in range(world)]).astype(np.int64)
         self._perm_t = {}
+
+    def remap_cols(self, colind) -> np.ndarray:
+        """Global column -> position in the padded all-gather buffer."""
+        c = np.asarray(colind, dtype=np.int64)
+        owner = np.searchsorted(self.cuts.astype(np.int64), c, side="right") - 1
+        return (owner * self.shard + (c - self.cuts.astype(np.int64)[owner])).astype(np.uint32)
+
+    @property
+    def padded_rows(self) -> int:
+        return self.world * self.shard
+
+    def shard_graph_host(self, m: CsrMatrix) -> CsrMatrix:
+        """This rank's rows with columns remapped into the padded layout."""
+        part = row_range_host(m, self.r0, self.r1)
+        if self.world == 1:
+            return part
+        return CsrMatrix(part.n_rows, self.padded_rows, part.rowptr, self.remap_cols(part.colind), part.val)
+
+    def allgather_padded(self, local_padded, out_padded, group=None, async_op=False):
+        """All-gather (shard x F) padded row blocks into (world*shard x F);
+        returns the work handle when async_op."""
+        import torch.distributed as dist
+        if dist.get_backend(group) == "nccl":
+            return dist.all_gather_into_tensor(out_padded, local_padded, group=group, async_op=async_op)
+        return dist.all_gather(list(out_padded.split(self.shard)), local_padded, group=group,
+                               async_op=async_op)
 
     @property
     def local_rows(self) -> int:

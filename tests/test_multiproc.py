@@ -54,9 +54,24 @@ def _worker(rank, world, port, results):
         parts = [torch.empty(pad) for _ in range(world)]
         dist.all_gather(parts, sp)
         s_full = np.concatenate([p[:n].numpy() for p, n in zip(parts, lens)])
+        # padded-native layout (bench.py): remapped shard graph over the padded
+        # all-gather buffer, no un-pad copy -- same bits
+        loc_pad = torch.zeros((sh.shard, f))
+        loc_pad[: sh.local_rows] = local_b
+        out_pad = torch.empty((sh.padded_rows, f))
+        sh.allgather_padded(loc_pad, out_pad)
+        pg = sh.shard_graph_host(m)
+        assert pg.n_cols == world * sh.shard and asb.validate(pg) is None
+        c_pad = oracle.spmm_baseline(pg, out_pad.numpy())
+        s_pad = oracle.sddmm(pg, x[sh.r0:sh.r1], out_pad.numpy(), 64, True)
+        same_pad = (np.array_equal(c_pad.view(np.uint32), c_local.numpy().view(np.uint32)) and
+                    np.array_equal(s_pad.view(np.uint32), s_local.numpy().view(np.uint32)))
+        flags = torch.tensor([1 if same_pad else 0])
+        dist.all_reduce(flags, op=dist.ReduceOp.MIN)
         if rank == 0:
             want_c = oracle.spmm_baseline(m, b)
             want_s = oracle.sddmm(m, x, b, 64, True)
+            results["padded"] = bool(flags.item() == 1)
             results["spmm"] = bool(np.array_equal(c_full.view(np.uint32), want_c.view(np.uint32)))
             results["sddmm"] = bool(np.array_equal(s_full.view(np.uint32), want_s.view(np.uint32)))
             results["balanced"] = max(lens) - m.nnz / world <= int(m.degrees().max())
@@ -77,3 +92,4 @@ def test_row_sharded_spmm_sddmm_concatenate_bit_exact(world):
         p.join(timeout=240)
         assert p.exitcode == 0
     assert results.get("spmm") and results.get("sddmm") and results.get("balanced")
+    assert results.get("padded")
