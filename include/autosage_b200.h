@@ -375,8 +375,10 @@ as_status as_decide_host(const as_context* ctx, const as_probe_config* cfg, uint
 /* attention_probe_breakdown, src/attention.cpp:9-40: sddmm_auto ->
  * row_softmax -> spmm_auto, each decided under its own key.  q: n_rows x f,
  * k: n_cols x f, v: n_cols x fv, out: n_rows x fv (device).  Decisions are
- * optional outputs.  fused != 0 runs the single-pass fused kernel with the
- * decided variants' numerics. */
+ * optional outputs.  fused != 0: SDDMM -> per-row (max, sum) -> SpMM that
+ * turns each score into its probability as it loads it (no probability
+ * array, the same bits as fused == 0); it needs a mapped SpMM decision and
+ * fv % 4 == 0 with 16-byte aligned v, else the staged pipeline runs. */
 as_status as_csr_attention_forward(const as_context* ctx, const as_probe_config* cfg,
                                    as_graph pattern, const float* q_dev, uint64_t q_rows,
                                    const float* k_dev, uint64_t k_rows, const float* v_dev,
