@@ -191,23 +191,30 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
             for (int ch = 0; ch < NCH; ++ch) bl[ch] = bmat + fidx[ch];
             const std::uint32_t f = a.f;
             // (value, offset) of the warp's W*GPW entries go through shared
-            // memory: one STS.128 per lane per block and one broadcast
-            // LDS.128 per entry, instead of three shuffles per entry (the
-            // shuffles held ~40% of the LSU data pipe)
+            // memory: one STS per lane per block and one broadcast LDS per
+            // entry, instead of three shuffles per entry (the shuffles held
+            // ~40% of the LSU data pipe).  With several groups per warp
+            // (LPR <= 16) the entry is 8 bytes (f32 value + offset, LDS.64)
+            // and every lane widens the value itself: F=64 rowparallel 2.59 ->
+            // 2.29 ms, F=32 1.07 -> 0.97; one group per warp (F >= 128) keeps
+            // the 16-byte pre-widened entry (F=128: 4.19 vs 4.37 ms).
+            constexpr bool E64 = LPR <= 16;
+            using Ent = typename std::conditional<E64, uint2, double2>::type;
             extern __shared__ __align__(16) double2 seg_ent[];
             static_assert(S <= kSegMaxS, "seg_smem too small");
-            double2* ent = seg_ent + (threadIdx.x >> 5) * (32 * S);
+            Ent* ent = reinterpret_cast<Ent*>(seg_ent) + (threadIdx.x >> 5) * (32 * S);
             for (; base < fast_end; base += W) {
                 __syncwarp();  // the previous block's readers are done
 #pragma unroll
                 for (int s = 0; s < S; ++s) {
                     const std::uint32_t k = base + std::uint32_t(s * LPR + gl);
                     const std::uint32_t o = __ldg(colp + k) * f;
-                    double v;
-                    if constexpr (SMX) v = double(sm_prob_of(__ldg(valp + k), rmx, rsm, rrc));
-                    else if constexpr (HAS_VAL) v = double(__ldg(valp + k));
-                    else v = 1.0;
-                    ent[s * 32 + lane] = make_double2(v, __hiloint2double(0, int(o)));
+                    float v;
+                    if constexpr (SMX) v = sm_prob_of(__ldg(valp + k), rmx, rsm, rrc);
+                    else if constexpr (HAS_VAL) v = __ldg(valp + k);
+                    else v = 1.f;
+                    if constexpr (E64) ent[s * 32 + lane] = make_uint2(__float_as_uint(v), o);
+                    else ent[s * 32 + lane] = make_double2(double(v), __hiloint2double(0, int(o)));
                 }
                 __syncwarp();
 #pragma unroll
@@ -217,9 +224,14 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         const int j = j0 + u;
-                        const double2 e = ent[(j / LPR) * 32 + int(gbase) + (j % LPR)];
-                        oj[u] = unsigned(__double2loint(e.y));
-                        vj[u] = e.x;
+                        const Ent e = ent[(j / LPR) * 32 + int(gbase) + (j % LPR)];
+                        if constexpr (E64) {
+                            oj[u] = e.y;
+                            vj[u] = double(__uint_as_float(e.x));
+                        } else {
+                            oj[u] = unsigned(__double2loint(e.y));
+                            vj[u] = e.x;
+                        }
                     }
                     VT bv[U][NCH];
 #pragma unroll
