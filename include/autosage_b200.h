@@ -397,6 +397,33 @@ as_status as_partition_rows(const uint64_t* rowptr_host, uint64_t n_rows, uint32
 as_status as_graph_row_range(as_graph g, uint64_t r0, uint64_t r1, as_graph* out);
 
 /* ------------------------------------------------------------------ */
+/* Backward pass (new, PAPER.md:334 -- the reference has  */
+/* no gradients).  C = A B gives dB = A^T dC (as_spmm_values on the      */
+/* transpose, values permuted) and dval = SDDMM(A, dC, B); out =          */
+/* SDDMM(A, X, Y) gives dX = A[dout] Y and dY = A^T[dout] X.              */
+/* ------------------------------------------------------------------ */
+/* CSR transpose on device (n_cols x n_rows; entries of each new row in
+ * source row order, so canonical, csr.hpp:24-45).  Values are permuted when
+ * g has them; the entry permutation is kept on the new handle. */
+as_status as_graph_transpose(as_graph g, as_graph* out);
+/* Device view of a transpose's permutation: perm[k] = source entry of entry
+ * k (nnz u32).  Not a transpose -> AS_INVALID_ARGUMENT. */
+as_status as_graph_transpose_perm(as_graph gt, const uint32_t** perm);
+/* dst_dev[k] = src_dev[perm[k]] for a transpose's nnz entries (a source
+ * value array carried into the transposed order). */
+as_status as_permute_values(as_graph gt, const float* src_dev, float* dst_dev, void* stream);
+/* as_spmm with an explicit value array (nnz floats, device) in place of the
+ * graph's own: the same kernels and numerics (dispatch, src/kernels.cpp:485-510). */
+as_status as_spmm_values(const as_variant* v, as_graph a, const float* vals_dev, const float* b_dev,
+                         uint64_t b_rows, uint64_t f, float* c_dev, void* stream,
+                         as_kernel_result* res);
+/* Gradient of row_softmax (src/kernels.cpp:431-461): ds = p * (g - dot),
+ * dot = sum_row p*g in f64 (32 strided partials, fixed pairwise fold;
+ * oracle/oracle.c orc_row_softmax_backward). */
+as_status as_row_softmax_backward(as_graph m, const float* p_dev, const float* grad_dev,
+                                  float* ds_dev, void* stream);
+
+/* ------------------------------------------------------------------ */
 /* Synthetic inputs + ASCR I/O (include/autosage/generate.hpp, io.hpp)  */
 /* ------------------------------------------------------------------ */
 /* Heavy-tailed degree CSR: degrees d_i = clamp(floor(d_min * u^(-1/(a-1))),

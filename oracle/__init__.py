@@ -76,6 +76,8 @@ def port():
             "orc_attention": [vp, vp, u64, vp, vp, u64, vp, u64, u64, C.c_int, u64, vp],
             "orc_extract_features": [vp, u64, u64, u64, C.POINTER(orc_features)],
             "orc_partition_rows": [vp, u64, C.c_uint32, vp],
+            "orc_transpose": [vp, vp, u64, u64, vp, vp, vp],
+            "orc_row_softmax_backward": [vp, u64, vp, vp, vp],
         }.items():
             fn = getattr(lib, name)
             fn.restype = None
@@ -176,6 +178,27 @@ def row_softmax(m, vals: Optional[np.ndarray] = None) -> np.ndarray:
     out = vin.copy()
     port().orc_row_softmax(_ptr(m.rowptr), m.n_rows, _ptr(vin), _ptr(out))
     return out
+
+
+def transpose(m):
+    """(A^T as (rowptr, colind, val-or-None), perm): stable counting sort by
+    column; perm[k] = source entry of transposed entry k."""
+    rp = np.zeros(m.n_cols + 1, dtype=np.uint64)
+    ci = np.zeros(max(m.nnz, 1), dtype=np.uint32)
+    perm = np.zeros(max(m.nnz, 1), dtype=np.uint32)
+    port().orc_transpose(_ptr(m.rowptr), _ptr(m.colind), m.n_rows, m.n_cols, _ptr(rp), _ptr(ci),
+                         _ptr(perm))
+    perm = perm[:m.nnz]
+    val = m.val[perm] if m.has_values() else None
+    return (rp, ci[:m.nnz], val), perm
+
+
+def row_softmax_backward(m, p: np.ndarray, g: np.ndarray) -> np.ndarray:
+    p = np.ascontiguousarray(p, dtype=np.float32)
+    g = np.ascontiguousarray(g, dtype=np.float32)
+    out = np.zeros(max(m.nnz, 1), dtype=np.float32)
+    port().orc_row_softmax_backward(_ptr(m.rowptr), m.n_rows, _ptr(p), _ptr(g), _ptr(out))
+    return out[:m.nnz]
 
 
 def attention(m, q, k, v, sddmm_ft=64, sddmm_vec=False, spmm_hub_t=0) -> np.ndarray:

@@ -421,3 +421,52 @@ void orc_partition_rows(const uint64_t* rowptr, uint64_t n_rows, uint32_t g, uin
     }
     cuts[g] = n_rows;
 }
+
+/* ------------------------------------------------ backward (new; N4) -- */
+/* The reference has no backward pass (PAPER.md:334 lists it
+ * as an extension).  These restate the gradients of the forward operators
+ * above with the same accumulation rules, so the device backward can be
+ * held to the same bar: structure bit-exact, SpMM/SDDMM gradients bit-exact
+ * (they ARE SpMM/SDDMM calls), softmax backward bit-exact (f64 sum in entry
+ * order). */
+
+/* Transpose of a canonical CSR (csr.hpp:24-45 invariants): counting sort by
+ * column, entries of a column kept in row order (so the result is canonical
+ * too).  perm[k] = source entry of transposed entry k. */
+void orc_transpose(const uint64_t* rowptr, const uint32_t* colind, uint64_t n_rows,
+                   uint64_t n_cols, uint64_t* rowptr_t, uint32_t* colind_t, uint32_t* perm) {
+    const uint64_t nnz = rowptr[n_rows];
+    for (uint64_t j = 0; j <= n_cols; ++j) rowptr_t[j] = 0;
+    for (uint64_t e = 0; e < nnz; ++e) rowptr_t[colind[e] + 1]++;
+    for (uint64_t j = 0; j < n_cols; ++j) rowptr_t[j + 1] += rowptr_t[j];
+    uint64_t* next = (uint64_t*)malloc((n_cols ? n_cols : 1) * sizeof(uint64_t));
+    for (uint64_t j = 0; j < n_cols; ++j) next[j] = rowptr_t[j];
+    for (uint64_t i = 0; i < n_rows; ++i)
+        for (uint64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) {
+            const uint64_t k = next[colind[e]]++;
+            colind_t[k] = (uint32_t)i;
+            perm[k] = (uint32_t)e;
+        }
+    free(next);
+}
+
+/* Gradient of row_softmax (src/kernels.cpp:431-461): with p = softmax(s) and
+ * upstream g, ds[e] = p[e] * (g[e] - sum_row p*g).  The products f64(p)*f64(g)
+ * are exact; they are summed in a fixed order chosen for a warp per row (the
+ * reference defines none): 32 strided partials (partial l takes the row's
+ * entries l, l+32, l+64, ... in order), folded pairwise part[l] += part[l+o]
+ * for o = 16, 8, 4, 2, 1.  ds = f32(f64(p) * (f64(g) - dot)).  Empty rows
+ * untouched. */
+void orc_row_softmax_backward(const uint64_t* rowptr, uint64_t n_rows, const float* p,
+                              const float* g, float* ds) {
+    for (uint64_t i = 0; i < n_rows; ++i) {
+        const uint64_t e0 = rowptr[i], e1 = rowptr[i + 1];
+        double part[32];
+        for (int l = 0; l < 32; ++l) part[l] = 0.0;
+        for (uint64_t e = e0; e < e1; ++e) part[(e - e0) & 31] += (double)p[e] * (double)g[e];
+        for (int o = 16; o > 0; o >>= 1)
+            for (int l = 0; l < o; ++l) part[l] += part[l + o];
+        const double dot = part[0];
+        for (uint64_t e = e0; e < e1; ++e) ds[e] = (float)((double)p[e] * ((double)g[e] - dot));
+    }
+}

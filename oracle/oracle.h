@@ -117,6 +117,17 @@ int orc_time_kernel_policy(const double* script, int script_len, int iters, doub
  * cuts[g]=n_rows. */
 void orc_partition_rows(const uint64_t* rowptr, uint64_t n_rows, uint32_t g, uint64_t* cuts);
 
+
+/* ---- backward (new; SURVEY 8(f) N4 -- the reference has none) ---- */
+/* CSR transpose by stable counting sort on the column (csr.hpp:24-45
+ * invariants preserved); perm[k] = source entry of transposed entry k. */
+void orc_transpose(const uint64_t* rowptr, const uint32_t* colind, uint64_t n_rows,
+                   uint64_t n_cols, uint64_t* rowptr_t, uint32_t* colind_t, uint32_t* perm);
+/* d row_softmax (src/kernels.cpp:431-461): ds = f32(p * (g - dot)), dot =
+ * 32 strided f64 partials of f64(p)*f64(g) folded in a fixed pairwise tree. */
+void orc_row_softmax_backward(const uint64_t* rowptr, uint64_t n_rows, const float* p,
+                              const float* g, float* ds);
+
 #ifdef __cplusplus
 }
 #endif

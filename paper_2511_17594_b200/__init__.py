@@ -300,6 +300,20 @@ class Graph:
         _check(_lib.as_graph_row_range(self._h, r0, r1, C.byref(h)))
         return Graph(h.value, self.device)
 
+    def transpose(self) -> "Graph":
+        """A^T on device (as_graph_transpose; backward pass):
+        entries of each new row in source row order, values permuted, the
+        entry permutation kept on the new handle."""
+        h = C.c_void_p()
+        _check(_lib.as_graph_transpose(self._h, C.byref(h)))
+        return Graph(h.value, self.device)
+
+    def transpose_perm_ptr(self) -> int:
+        """Device address of a transpose's u32[nnz] permutation (perm[k] = source entry)."""
+        p = C.c_void_p()
+        _check(_lib.as_graph_transpose_perm(self._h, C.byref(p)))
+        return p.value or 0
+
     def download(self) -> CsrMatrix:
         rp = np.zeros(self.n_rows + 1, dtype=np.uint64)
         ci = np.zeros(max(self.nnz, 1), dtype=np.uint32)

@@ -1,0 +1,191 @@
+// backward.cu -- the pieces the operators' gradients need beyond SpMM and
+// SDDMM themselves (the reference has no backward pass,
+// PAPER.md:334).  With C = A B and out = SDDMM(A, X, Y):
+//   dB   = A^T dC          SpMM on the transposed graph, values permuted
+//   dval = SDDMM(A, dC, B)
+//   dX   = A[dout] Y       SpMM with the SDDMM gradient as values
+//   dY   = A^T[dout] X
+// and the row softmax's gradient ds = p * (g - sum_row p*g).
+//
+// Transpose: stable CUB radix sort of (column, entry) pairs over the column
+// bits only, so entries of one column keep source (= row) order and the
+// result is canonical CSR; counts -> exclusive scan give rowptr.  It runs once
+// per graph (the torch ops cache the transposed handle), so it is built from
+// library passes rather than a hand-fused kernel: every pass is a coalesced
+// stream except the sort's scatter and the fill's two gathers.
+//
+// Softmax backward: HBM-bound (12 B per entry + 8 B per row).  Warp per row
+// in degree-descending order (hub rows start first); each lane keeps a
+// strided f64 partial of the exact products f64(p)*f64(g), the 32 partials
+// fold in a fixed xor tree, so the sum is deterministic and equals
+// oracle/oracle.c orc_row_softmax_backward bit for bit.
+#include "graph.hpp"
+#include "ops.hpp"
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+
+namespace asb {
+
+namespace {
+
+unsigned grid_for(std::uint64_t n, unsigned block, unsigned cap = 148u * 16u) {
+    std::uint64_t g = (n + block - 1) / block;
+    if (g == 0) g = 1;
+    return unsigned(std::min<std::uint64_t>(g, cap));
+}
+
+__global__ void col_count_kernel(const std::uint32_t* __restrict__ colind, std::uint64_t nnz,
+                                 unsigned long long* __restrict__ cnt) {
+    for (std::uint64_t e = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; e < nnz;
+         e += std::uint64_t(gridDim.x) * blockDim.x)
+        atomicAdd(&cnt[colind[e]], 1ull);
+}
+
+__global__ void iota_u32_kernel(std::uint32_t* __restrict__ p, std::uint64_t n) {
+    for (std::uint64_t i = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += std::uint64_t(gridDim.x) * blockDim.x)
+        p[i] = std::uint32_t(i);
+}
+
+// erow[e] = row of entry e (warp per row, lanes stride the row)
+__global__ void entry_row_kernel(const std::uint64_t* __restrict__ rowptr, std::uint64_t n_rows,
+                                 std::uint32_t* __restrict__ erow) {
+    const int lane = threadIdx.x & 31;
+    for (std::uint64_t w = (blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x) >> 5; w < n_rows;
+         w += (std::uint64_t(gridDim.x) * blockDim.x) >> 5) {
+        const std::uint64_t e1 = rowptr[w + 1];
+        for (std::uint64_t e = rowptr[w] + lane; e < e1; e += 32) erow[e] = std::uint32_t(w);
+    }
+}
+
+__global__ void transpose_fill_kernel(const std::uint32_t* __restrict__ perm,
+                                      const std::uint32_t* __restrict__ erow,
+                                      const float* __restrict__ val, std::uint64_t nnz,
+                                      std::uint32_t* __restrict__ colind_t, float* __restrict__ val_t) {
+    for (std::uint64_t k = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; k < nnz;
+         k += std::uint64_t(gridDim.x) * blockDim.x) {
+        const std::uint32_t e = perm[k];
+        colind_t[k] = erow[e];
+        if (val) val_t[k] = val[e];
+    }
+}
+
+__global__ void permute_kernel(const float* __restrict__ src, const std::uint32_t* __restrict__ perm,
+                               std::uint64_t n, float* __restrict__ dst) {
+    for (std::uint64_t k = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; k < n;
+         k += std::uint64_t(gridDim.x) * blockDim.x)
+        dst[k] = src[perm[k]];
+}
+
+// ds[e] = f32(f64(p) * (f64(g) - dot)), dot = xor-tree fold of 32 strided
+// partials (lane l sums entries e0 + l, e0 + l + 32, ... in order).
+__global__ void __launch_bounds__(256)
+softmax_backward_kernel(const std::uint64_t* __restrict__ rowptr, const std::uint32_t* __restrict__ order,
+                        std::uint64_t n_rows, const float* __restrict__ p, const float* __restrict__ g,
+                        float* __restrict__ ds) {
+    const int lane = threadIdx.x & 31;
+    for (std::uint64_t w = (blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x) >> 5; w < n_rows;
+         w += (std::uint64_t(gridDim.x) * blockDim.x) >> 5) {
+        const std::uint32_t row = order[w];
+        const std::uint64_t e0 = rowptr[row], e1 = rowptr[row + 1];
+        if (e0 == e1) continue;
+        double part = 0.0;
+        std::uint64_t e = e0 + lane;
+        // two loads in flight per lane; the chain order stays e, e+32, e+64, ...
+        for (; e + 32 < e1; e += 64) {
+            const float pa = __ldg(p + e), ga = __ldg(g + e);
+            const float pb = __ldg(p + e + 32), gb = __ldg(g + e + 32);
+            part = __dadd_rn(part, __dmul_rn(double(pa), double(ga)));
+            part = __dadd_rn(part, __dmul_rn(double(pb), double(gb)));
+        }
+        if (e < e1) part = __dadd_rn(part, __dmul_rn(double(__ldg(p + e)), double(__ldg(g + e))));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
+        // every lane holds lane 0's fold only if the tree is symmetric; take
+        // lane 0's value explicitly so the result is the oracle's fold.
+        const double dot = __shfl_sync(0xffffffffu, part, 0);
+        for (std::uint64_t k = e0 + lane; k < e1; k += 32) {
+            const double pk = double(p[k]), gk = double(g[k]);
+            ds[k] = float(__dmul_rn(pk, __dsub_rn(gk, dot)));
+        }
+    }
+}
+
+} // namespace
+
+std::unique_ptr<Graph> transpose_graph(Graph& g) {
+    DeviceGuard dg(g.device);
+    if (g.nnz >= (1ull << 31)) throw InvalidArgument("transpose: nnz must be < 2^31");
+    auto t = std::make_unique<Graph>();
+    t->device = g.device;
+    t->n_rows = g.n_cols;
+    t->n_cols = g.n_rows;
+    t->nnz = g.nnz;
+    t->has_val = g.has_val;
+    ASB_CUDA(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
+    t->rowptr.alloc(t->n_rows + 1);
+    t->colind.alloc(g.nnz);
+    if (t->has_val) t->val.alloc(g.nnz);
+    t->src_perm.alloc(std::max<std::uint64_t>(g.nnz, 1));
+    cudaStream_t s = g.stream;
+    const std::uint64_t nnz = g.nnz, nc = g.n_cols;
+    {
+        DevBuf<unsigned long long> cnt(nc + 1);
+        ASB_CUDA(cudaMemsetAsync(cnt.get(), 0, (nc + 1) * 8, s));
+        if (nnz) {
+            col_count_kernel<<<grid_for(nnz, 256), 256, 0, s>>>(g.colind.get(), nnz, cnt.get());
+            check_launch("col_count_kernel");
+        }
+        std::size_t tb = 0;
+        ASB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.get(), t->rowptr.get(), int(nc + 1), s));
+        DevBuf<unsigned char> tmp(std::max<std::size_t>(tb, 1));
+        ASB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, cnt.get(), t->rowptr.get(), int(nc + 1), s));
+        count_launch(2);
+    }
+    if (nnz) {
+        DevBuf<std::uint32_t> keys_out(nnz), iota(nnz), erow(nnz);
+        iota_u32_kernel<<<grid_for(nnz, 256), 256, 0, s>>>(iota.get(), nnz);
+        check_launch("iota_u32_kernel");
+        entry_row_kernel<<<grid_for(g.n_rows * 32, 256), 256, 0, s>>>(g.rowptr.get(), g.n_rows, erow.get());
+        check_launch("entry_row_kernel");
+        int end_bit = 1;
+        while (end_bit < 32 && (1ull << end_bit) < nc) ++end_bit;
+        std::size_t tb = 0;
+        ASB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, g.colind.get(), keys_out.get(), iota.get(),
+                                                 t->src_perm.get(), int(nnz), 0, end_bit, s));
+        DevBuf<unsigned char> tmp(std::max<std::size_t>(tb, 1));
+        ASB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, g.colind.get(), keys_out.get(), iota.get(),
+                                                 t->src_perm.get(), int(nnz), 0, end_bit, s));
+        count_launch(4);
+        transpose_fill_kernel<<<grid_for(nnz, 256), 256, 0, s>>>(
+            t->src_perm.get(), erow.get(), g.has_val ? g.val.get() : nullptr, nnz, t->colind.get(),
+            t->has_val ? t->val.get() : nullptr);
+        check_launch("transpose_fill_kernel");
+    }
+    t->h_rowptr.resize(t->n_rows + 1);
+    ASB_CUDA(cudaMemcpyAsync(t->h_rowptr.data(), t->rowptr.get(), (t->n_rows + 1) * 8,
+                             cudaMemcpyDeviceToHost, s));
+    ASB_CUDA(cudaStreamSynchronize(s));
+    t->is_transpose = true;
+    return t;
+}
+
+void launch_permute(const float* src, const std::uint32_t* perm, std::uint64_t n, float* dst,
+                    cudaStream_t s) {
+    if (n == 0) return;
+    permute_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, perm, n, dst);
+    check_launch("permute_kernel");
+}
+
+void launch_row_softmax_backward(Graph& g, const float* p, const float* grad, float* ds, cudaStream_t s) {
+    if (g.n_rows == 0 || g.nnz == 0) return;
+    ensure_order(g);
+    softmax_backward_kernel<<<grid_for(g.n_rows * 32, 256, 148u * 8u), 256, 0, s>>>(
+        g.rowptr.get(), g.order.get(), g.n_rows, p, grad, ds);
+    check_launch("softmax_backward_kernel");
+}
+
+} // namespace asb

@@ -285,8 +285,8 @@ as_status as_graph_download(as_graph g, uint64_t* rowptr, uint32_t* colind, floa
 }
 
 // ---- operators -------------------------------------------------------------------
-as_status as_spmm(const as_variant* v, as_graph a, const float* b_dev, uint64_t b_rows, uint64_t f,
-                  float* c_dev, void* stream, as_kernel_result* res) {
+static as_status spmm_entry(const as_variant* v, as_graph a, const float* vals_dev, const float* b_dev,
+                            uint64_t b_rows, uint64_t f, float* c_dev, void* stream, as_kernel_result* res) {
     return guard([&] {
         Graph& g = G(a);
         cudaStream_t s = resolve_stream(g, stream);
@@ -302,7 +302,7 @@ as_status as_spmm(const as_variant* v, as_graph a, const float* b_dev, uint64_t 
                 ASB_CUDA(cudaEventCreate(&e1));
                 ASB_CUDA(cudaEventRecord(e0, s));
             }
-            spmm_baseline(g, graph_values(g, nullptr), b_dev, b_rows, f, c_dev, s);
+            spmm_baseline(g, graph_values(g, vals_dev), b_dev, b_rows, f, c_dev, s);
             if (res) {
                 ASB_CUDA(cudaEventRecord(e1, s));
                 ASB_CUDA(cudaEventSynchronize(e1));
@@ -315,9 +315,23 @@ as_status as_spmm(const as_variant* v, as_graph a, const float* b_dev, uint64_t 
             fill_result(res, r);
             return;
         }
-        const KernelResult r = dispatch_spmm(*v, g, nullptr, b_dev, b_rows, f, c_dev, s, res != nullptr);
+        const KernelResult r = dispatch_spmm(*v, g, vals_dev, b_dev, b_rows, f, c_dev, s, res != nullptr);
         fill_result(res, r);
     });
+}
+
+as_status as_spmm(const as_variant* v, as_graph a, const float* b_dev, uint64_t b_rows, uint64_t f,
+                  float* c_dev, void* stream, as_kernel_result* res) {
+    return spmm_entry(v, a, nullptr, b_dev, b_rows, f, c_dev, stream, res);
+}
+
+as_status as_spmm_values(const as_variant* v, as_graph a, const float* vals_dev, const float* b_dev,
+                         uint64_t b_rows, uint64_t f, float* c_dev, void* stream, as_kernel_result* res) {
+    if (!vals_dev && a && G(a).nnz) {
+        t_err = "spmm_values: values required";
+        return AS_INVALID_ARGUMENT;
+    }
+    return spmm_entry(v, a, vals_dev, b_dev, b_rows, f, c_dev, stream, res);
 }
 
 as_status as_spmm_rowparallel(const as_variant* v, as_graph a, const float* b_dev, uint64_t b_rows,
@@ -633,6 +647,43 @@ as_status as_partition_rows(const uint64_t* rowptr_host, uint64_t n_rows, uint32
 
 as_status as_graph_row_range(as_graph g, uint64_t r0, uint64_t r1, as_graph* out) {
     return guard([&] { *out = reinterpret_cast<as_graph>(row_range(G(g), r0, r1).release()); });
+}
+
+// ---- backward (backward.cu) -----------------------------------------------------------
+as_status as_graph_transpose(as_graph g, as_graph* out) {
+    return guard([&] {
+        if (!out) throw InvalidArgument("transpose: null output");
+        *out = reinterpret_cast<as_graph>(transpose_graph(G(g)).release());
+    });
+}
+
+as_status as_graph_transpose_perm(as_graph gt, const uint32_t** perm) {
+    return guard([&] {
+        Graph& g = G(gt);
+        if (!g.is_transpose) throw InvalidArgument("transpose_perm: graph is not a transpose");
+        *perm = g.src_perm.get();
+    });
+}
+
+as_status as_permute_values(as_graph gt, const float* src_dev, float* dst_dev, void* stream) {
+    return guard([&] {
+        Graph& g = G(gt);
+        if (!g.is_transpose) throw InvalidArgument("permute_values: graph is not a transpose");
+        if (g.nnz && (!src_dev || !dst_dev)) throw InvalidArgument("permute_values: null array");
+        DeviceGuard dg(g.device);
+        launch_permute(src_dev, g.src_perm.get(), g.nnz, dst_dev, resolve_stream(g, stream));
+    });
+}
+
+as_status as_row_softmax_backward(as_graph m, const float* p_dev, const float* grad_dev, float* ds_dev,
+                                  void* stream) {
+    return guard([&] {
+        Graph& g = G(m);
+        if (g.nnz && (!p_dev || !grad_dev || !ds_dev))
+            throw InvalidArgument("row_softmax_backward: null array");
+        DeviceGuard dg(g.device);
+        launch_row_softmax_backward(g, p_dev, grad_dev, ds_dev, resolve_stream(g, stream));
+    });
 }
 
 // ---- synthetic inputs / io ------------------------------------------------------------

@@ -104,6 +104,8 @@ struct Graph {
     std::map<std::uint64_t, std::uint64_t> ge_count;  // rows with degree >= key
     DevBuf<unsigned> flag;             // finiteness flag of the current dense operand
     DevBuf<double> xwide;              // SDDMM: X widened to f64 (fixed-width path)
+    bool is_transpose = false;         // built by transpose_graph (backward.cu) ...
+    DevBuf<std::uint32_t> src_perm;    // ... entry k came from source entry src_perm[k]
     cudaStream_t aux = nullptr;        // fork/join stream for concurrent kernels
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
@@ -165,6 +167,9 @@ std::unique_ptr<Graph> slice_rows(Graph& g, const std::vector<std::uint64_t>& ro
 std::unique_ptr<Graph> row_range(Graph& g, std::uint64_t r0, std::uint64_t r1);
 // Gathers rows of a dense n x f device matrix (SDDMM probe x-sample,
 // src/scheduler.cpp:214-220).
+// CSR transpose (backward.cu): rows = source columns, entries in source row
+// order, values permuted, src_perm kept for permuting later value arrays.
+std::unique_ptr<Graph> transpose_graph(Graph& g);
 void gather_dense_rows(const float* src, std::uint64_t f, const std::vector<std::uint64_t>& rows,
                        float* dst, cudaStream_t s);
 

@@ -60,6 +60,13 @@ void launch_row_softmax(Graph& g, const float* vin, float* vout, cudaStream_t s)
 // per-row (max, sum) only (fused attention); rows of degree 0 are not written
 void launch_row_softmax_stats(Graph& g, const float* vin, float* rmax, double* rsum, cudaStream_t s);
 
+// ---- backward (backward.cu) ----------------------------
+// dst[k] = src[perm[k]]
+void launch_permute(const float* src, const std::uint32_t* perm, std::uint64_t n, float* dst,
+                    cudaStream_t s);
+// ds = p * (g - sum_row p*g), f64 dot in a fixed strided/tree order
+void launch_row_softmax_backward(Graph& g, const float* p, const float* grad, float* ds, cudaStream_t s);
+
 // ---- calibration (src/device.cpp:42-95 analogue) ------------------------
 double measure_gpu_bandwidth(int device);
 double measure_gpu_flops(int device);

@@ -6,6 +6,7 @@ integration surface).
     c = torch.ops.autosage.spmm_csr_auto(crow, col, val, b)       # decide (cached) + run
     s = torch.ops.autosage.sddmm_csr(crow, col, x, y, "")          # "" = baseline
     o = torch.ops.autosage.csr_attention(crow, col, q, k, v, False)
+    p = torch.ops.autosage.row_softmax_csr(crow, col, s, n_cols)
 
 CSR arrays are CUDA tensors: crow int64 [n_rows + 1], col int32 [nnz],
 values float32 [nnz] (optional: pass an empty tensor for pattern-only).  The
@@ -13,7 +14,16 @@ number of columns is the dense operand's row count.  Results are computed on
 torch's current stream by the sm_100a kernels, with the same numerics as the
 reference (bit-exact SpMM/SDDMM).  Device graph handles (upload, degree
 order, hub plans) are cached per CSR storage, so repeated calls on a static
-graph pay the setup once.  Forward only (backward kernels are SURVEY 8(f) N4).
+graph pay the setup once.
+
+Backward (the reference has no gradients): every op has a
+registered autograd formula built from the same kernels -- A^T products run
+the SpMM on a cached device transpose (as_graph_transpose) with the values
+carried through its entry permutation, value gradients are SDDMMs, and the
+softmax gradient is as_row_softmax_backward.  SpMM mappings are bit-identical
+to each other, so the backward SpMMs use the hub-split mapping (`_BWD_SPMM`)
+whatever the forward variant was.  csr_attention's backward recomputes the
+scores and probabilities (staged) rather than keeping them from the forward.
 """
 from __future__ import annotations
 
@@ -27,6 +37,7 @@ from . import (Graph, ProbeConfig, ScheduleCache, ScheduleContext, _check, _lib,
 from . import _capi as _c
 
 _GRAPHS: "OrderedDict[tuple, Graph]" = OrderedDict()
+_TRANSPOSES: "OrderedDict[tuple, Graph]" = OrderedDict()
 _MAX_GRAPHS = 8
 _CACHE = None
 
@@ -58,6 +69,21 @@ def _graph(crow: torch.Tensor, col: torch.Tensor, val: torch.Tensor, n_cols: int
     _GRAPHS[k] = g
     while len(_GRAPHS) > _MAX_GRAPHS:
         _GRAPHS.popitem(last=False)[1].close()
+    return g
+
+
+def _transpose(crow: torch.Tensor, col: torch.Tensor, n_cols: int) -> Graph:
+    """Pattern-only A^T (device), cached per CSR storage like _graph."""
+    empty = torch.empty(0, dtype=torch.float32, device=crow.device)
+    k = _key(crow, col, empty, n_cols)
+    g = _TRANSPOSES.get(k)
+    if g is not None:
+        _TRANSPOSES.move_to_end(k)
+        return g
+    g = _graph(crow, col, empty, n_cols).transpose()
+    _TRANSPOSES[k] = g
+    while len(_TRANSPOSES) > _MAX_GRAPHS:
+        _TRANSPOSES.popitem(last=False)[1].close()
     return g
 
 
@@ -155,3 +181,157 @@ def csr_attention(crow: torch.Tensor, col: torch.Tensor, q: torch.Tensor, k: tor
 @csr_attention.register_fake
 def _(crow, col, q, k, v, fused):
     return q.new_empty((crow.shape[0] - 1, v.shape[1]))
+
+
+# ---------------------------------------------------------------------------
+# Backward
+# ---------------------------------------------------------------------------
+_BWD_SPMM = "spmm:hubsplit:ft=64:rpc=1:vec=1:hubt=256"
+
+
+def _spmm_vals(g: Graph, vals, b: torch.Tensor) -> torch.Tensor:
+    """C = G[vals] B on torch's stream (vals None: G's own values / implicit 1)."""
+    b = b.contiguous().float()
+    c = torch.empty((g.n_rows, b.shape[1]), dtype=torch.float32, device=b.device)
+    if vals is None:
+        _check(_lib.as_spmm(_variant(_BWD_SPMM), g.handle, C.c_void_p(b.data_ptr()), b.shape[0],
+                            b.shape[1], C.c_void_p(c.data_ptr()), _stream(b), None))
+    else:
+        vals = vals.contiguous().float()
+        _check(_lib.as_spmm_values(_variant(_BWD_SPMM), g.handle,
+                                   C.c_void_p(vals.data_ptr()) if vals.numel() else None,
+                                   C.c_void_p(b.data_ptr()), b.shape[0], b.shape[1],
+                                   C.c_void_p(c.data_ptr()), _stream(b), None))
+    return c
+
+
+def _spmm_t(crow, col, vals, n_cols: int, dc: torch.Tensor) -> torch.Tensor:
+    """A^T[vals] dC: SpMM on the cached transpose, vals (source order) permuted."""
+    gt = _transpose(crow, col, n_cols)
+    if vals is None or vals.numel() == 0:
+        return _spmm_vals(gt, None, dc)
+    vt = torch.empty_like(vals, dtype=torch.float32)
+    _check(_lib.as_permute_values(gt.handle, C.c_void_p(vals.contiguous().float().data_ptr()),
+                                  C.c_void_p(vt.data_ptr()), _stream(dc)))
+    return _spmm_vals(gt, vt, dc)
+
+
+@torch.library.custom_op("autosage::row_softmax_csr", mutates_args=())
+def row_softmax_csr(crow: torch.Tensor, col: torch.Tensor, s: torch.Tensor, n_cols: int) -> torch.Tensor:
+    """row_softmax over explicit values (src/kernels.cpp:431-461)."""
+    s = s.contiguous().float()
+    empty = torch.empty(0, dtype=torch.float32, device=s.device)
+    g = _graph(crow, col, empty, n_cols)
+    out = torch.empty_like(s)
+    if s.numel():
+        _check(_lib.as_row_softmax(g.handle, C.c_void_p(s.data_ptr()), C.c_void_p(out.data_ptr()),
+                                   _stream(s)))
+    return out
+
+
+@row_softmax_csr.register_fake
+def _(crow, col, s, n_cols):
+    return torch.empty_like(s)
+
+
+@torch.library.custom_op("autosage::row_softmax_csr_backward", mutates_args=())
+def row_softmax_csr_backward(crow: torch.Tensor, col: torch.Tensor, p: torch.Tensor,
+                             grad: torch.Tensor, n_cols: int) -> torch.Tensor:
+    """ds = p * (grad - sum_row p*grad) (as_row_softmax_backward)."""
+    p, grad = p.contiguous().float(), grad.contiguous().float()
+    empty = torch.empty(0, dtype=torch.float32, device=p.device)
+    g = _graph(crow, col, empty, n_cols)
+    ds = torch.zeros_like(p)
+    if p.numel():
+        _check(_lib.as_row_softmax_backward(g.handle, C.c_void_p(p.data_ptr()), C.c_void_p(grad.data_ptr()),
+                                            C.c_void_p(ds.data_ptr()), _stream(p)))
+    return ds
+
+
+@row_softmax_csr_backward.register_fake
+def _(crow, col, p, grad, n_cols):
+    return torch.empty_like(p)
+
+
+def _softmax_setup(ctx, inputs, output):
+    crow, col, _, n_cols = inputs
+    ctx.n_cols = n_cols
+    ctx.save_for_backward(crow, col, output)
+
+
+def _softmax_bwd(ctx, grad):
+    crow, col, p = ctx.saved_tensors
+    return None, None, row_softmax_csr_backward(crow, col, p, grad, ctx.n_cols), None
+
+
+row_softmax_csr.register_autograd(_softmax_bwd, setup_context=_softmax_setup)
+
+
+def _spmm_setup(ctx, inputs, output):
+    crow, col, val, b = inputs[:4]
+    ctx.save_for_backward(crow, col, val, b)
+
+
+def _spmm_bwd(ctx, dc):
+    crow, col, val, b = ctx.saved_tensors
+    dval = db = None
+    if ctx.needs_input_grad[2] and val.numel():
+        dval = sddmm_csr(crow, col, dc, b, "")
+    if ctx.needs_input_grad[3]:
+        db = _spmm_t(crow, col, val if val.numel() else None, b.shape[0], dc)
+    return (None, None, dval, db) + (None,) * (ctx.n_extra)
+
+
+def _spmm_setup_v(ctx, inputs, output):
+    _spmm_setup(ctx, inputs, output)
+    ctx.n_extra = 1
+
+
+def _spmm_setup_auto(ctx, inputs, output):
+    _spmm_setup(ctx, inputs, output)
+    ctx.n_extra = 0
+
+
+spmm_csr.register_autograd(_spmm_bwd, setup_context=_spmm_setup_v)
+spmm_csr_auto.register_autograd(_spmm_bwd, setup_context=_spmm_setup_auto)
+
+
+def _sddmm_setup(ctx, inputs, output):
+    crow, col, x, y, _ = inputs
+    ctx.save_for_backward(crow, col, x, y)
+
+
+def _sddmm_bwd(ctx, dout):
+    crow, col, x, y = ctx.saved_tensors
+    dx = dy = None
+    if ctx.needs_input_grad[2]:
+        dx = _spmm_vals(_graph(crow, col, torch.empty(0, device=x.device), y.shape[0]), dout, y)
+    if ctx.needs_input_grad[3]:
+        dy = _spmm_t(crow, col, dout, y.shape[0], x)
+    return None, None, dx, dy, None
+
+
+sddmm_csr.register_autograd(_sddmm_bwd, setup_context=_sddmm_setup)
+
+
+def _attention_setup(ctx, inputs, output):
+    crow, col, q, k, v, _ = inputs
+    ctx.save_for_backward(crow, col, q, k, v)
+
+
+def _attention_bwd(ctx, do):
+    """Staged recompute: s = SDDMM(q, k), p = softmax(s); then dv = A^T[p] dO,
+    dp = SDDMM(dO, v), ds = softmax'(p, dp), dq = A[ds] k, dk = A^T[ds] q."""
+    crow, col, q, k, v = ctx.saved_tensors
+    s = sddmm_csr(crow, col, q, k, "")
+    p = row_softmax_csr(crow, col, s, k.shape[0])
+    dv = _spmm_t(crow, col, p, k.shape[0], do) if ctx.needs_input_grad[4] else None
+    dp = sddmm_csr(crow, col, do, v, "")
+    ds = row_softmax_csr_backward(crow, col, p, dp, k.shape[0])
+    pat = _graph(crow, col, torch.empty(0, device=q.device), k.shape[0])
+    dq = _spmm_vals(pat, ds, k) if ctx.needs_input_grad[2] else None
+    dk = _spmm_t(crow, col, ds, k.shape[0], q) if ctx.needs_input_grad[3] else None
+    return None, None, dq, dk, dv, None
+
+
+csr_attention.register_autograd(_attention_bwd, setup_context=_attention_setup)

@@ -1,0 +1,274 @@
+"""Backward pass (the reference has no gradients):
+device CSR transpose, value permutation, SpMM with explicit values, the row
+softmax gradient, and torch autograd through torch.ops.autosage.*.
+
+Parity bar: structure and permutation bit-exact vs oracle.transpose; SpMM /
+SDDMM gradients bit-exact vs the oracle's SpMM / SDDMM on the transposed or
+re-valued CSR (they are the same kernels); softmax gradient bit-exact vs
+oracle.row_softmax_backward (fixed summation order, oracle/oracle.c).
+Float64 torch autograd on a dense copy checks the formulas themselves
+(tolerance 1e-5 relative, the north-star value bar)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2511_17594_b200 as asb
+import paper_2511_17594_b200.torch_ops  # noqa: F401
+from tests.util import bit_equal, csr_from_degrees, empty_rows, hub_graph, random_csr, random_dense
+
+
+def _dense(m):
+    d = np.zeros((m.n_rows, m.n_cols), dtype=np.float64)
+    for i in range(m.n_rows):
+        for e in range(int(m.rowptr[i]), int(m.rowptr[i + 1])):
+            d[i, m.colind[e]] = m.val[e] if m.has_values() else 1.0
+    return d
+
+
+# ---------------------------------------------------------------- CPU: oracle
+
+def test_oracle_transpose_matches_dense_and_is_canonical():
+    rng = np.random.default_rng(3)
+    m = random_csr(rng, 40, 55, 12)
+    (rp, ci, val), perm = oracle.transpose(m)
+    t = asb.CsrMatrix(m.n_cols, m.n_rows, rp, ci, val)
+    assert asb.validate(t) is None
+    assert np.array_equal(_dense(t), _dense(m).T)
+    # perm maps every transposed entry to its source entry
+    assert sorted(perm.tolist()) == list(range(m.nnz))
+    assert np.array_equal(m.colind[perm], np.repeat(np.arange(m.n_cols), np.diff(rp.astype(np.int64))))
+    # transpose of the transpose is the original
+    (rp2, ci2, val2), _ = oracle.transpose(t)
+    assert np.array_equal(rp2, m.rowptr) and np.array_equal(ci2, m.colind)
+    assert bit_equal(val2, m.val)
+
+
+def test_oracle_transpose_edge_cases():
+    m = empty_rows(5, 7)
+    (rp, ci, _), perm = oracle.transpose(m)
+    assert rp.tolist() == [0] * 8 and ci.size == 0 and perm.size == 0
+    m = asb.CsrMatrix(0, 3, np.zeros(1, dtype=np.uint64), np.zeros(0, dtype=np.uint32))
+    (rp, _, _), _ = oracle.transpose(m)
+    assert rp.tolist() == [0, 0, 0, 0]
+
+
+def _softmax_bwd_py(m, p, g):
+    """Pure-Python statement of the fixed order (32 strided partials, pairwise fold)."""
+    out = np.zeros(m.nnz, dtype=np.float32)
+    for i in range(m.n_rows):
+        e0, e1 = int(m.rowptr[i]), int(m.rowptr[i + 1])
+        part = [0.0] * 32
+        for e in range(e0, e1):
+            part[(e - e0) & 31] += float(p[e]) * float(g[e])
+        o = 16
+        while o:
+            for l in range(o):
+                part[l] += part[l + o]
+            o >>= 1
+        for e in range(e0, e1):
+            out[e] = np.float32(float(p[e]) * (float(g[e]) - part[0]))
+    return out
+
+
+def test_oracle_softmax_backward_order_and_formula():
+    rng = np.random.default_rng(4)
+    m = csr_from_degrees(rng, 6, 200, [0, 1, 31, 32, 33, 150])
+    s = rng.standard_normal(m.nnz).astype(np.float32) * 4
+    p = oracle.row_softmax(m, s)
+    g = rng.standard_normal(m.nnz).astype(np.float32)
+    got = oracle.row_softmax_backward(m, p, g)
+    assert bit_equal(got, _softmax_bwd_py(m, p, g))
+    # the Jacobian-vector product of softmax, in f64 on a dense row
+    for i in range(m.n_rows):
+        e0, e1 = int(m.rowptr[i]), int(m.rowptr[i + 1])
+        if e0 == e1:
+            continue
+        pp, gg = p[e0:e1].astype(np.float64), g[e0:e1].astype(np.float64)
+        want = pp * (gg - (pp * gg).sum())
+        assert np.allclose(got[e0:e1], want, rtol=1e-5, atol=1e-6)
+
+
+def test_backward_ops_registered_with_fake_shapes():
+    from torch._subclasses.fake_tensor import FakeTensorMode
+    for name in ("row_softmax_csr", "row_softmax_csr_backward"):
+        assert hasattr(torch.ops.autosage, name)
+    with FakeTensorMode():
+        crow = torch.empty(11, dtype=torch.int64)
+        col = torch.empty(30, dtype=torch.int32)
+        s = torch.empty(30)
+        assert torch.ops.autosage.row_softmax_csr(crow, col, s, 7).shape == (30,)
+        assert torch.ops.autosage.row_softmax_csr_backward(crow, col, s, s, 7).shape == (30,)
+
+
+# ---------------------------------------------------------------- GPU: kernels
+
+def _graphs():
+    rng = np.random.default_rng(11)
+    yield random_csr(rng, 300, 420, 25)
+    yield hub_graph(rng, 1200, [1100, 700, 300], 9)
+    yield csr_from_degrees(rng, 64, 5000, [0] * 10 + [4999] + [1] * 53)
+    yield empty_rows(9, 4)
+
+
+@pytest.mark.gpu
+def test_device_transpose_bit_exact_vs_oracle():
+    for m in _graphs():
+        g = asb.Graph.from_csr(m)
+        gt = g.transpose()
+        t = gt.download()
+        (rp, ci, val), perm = oracle.transpose(m)
+        assert (gt.n_rows, gt.n_cols, gt.nnz) == (m.n_cols, m.n_rows, m.nnz)
+        assert np.array_equal(t.rowptr, rp) and np.array_equal(t.colind, ci)
+        if m.nnz:
+            assert bit_equal(t.val, val)
+            # the kept permutation, read through as_permute_values of iota (< 2^24: exact in f32)
+            import ctypes as C
+            from paper_2511_17594_b200 import _lib
+            iota = torch.arange(m.nnz, dtype=torch.float32, device="cuda")
+            out = torch.empty_like(iota)
+            asb._check(_lib.as_permute_values(gt.handle, C.c_void_p(iota.data_ptr()),
+                                              C.c_void_p(out.data_ptr()), None))
+            torch.cuda.synchronize()
+            assert np.array_equal(out.cpu().numpy().astype(np.uint32), perm)
+            assert gt.transpose_perm_ptr() != 0
+        gt.close()
+        g.close()
+
+
+@pytest.mark.gpu
+def test_transpose_perm_rejects_non_transpose():
+    m = random_csr(np.random.default_rng(1), 10, 10, 3)
+    g = asb.Graph.from_csr(m)
+    with pytest.raises(asb.InvalidArgument):
+        g.transpose_perm_ptr()
+
+
+@pytest.mark.gpu
+def test_spmm_values_and_permute_match_oracle():
+    import ctypes as C
+    from paper_2511_17594_b200 import _lib
+    rng = np.random.default_rng(12)
+    m = hub_graph(rng, 1500, [1400, 500], 11)
+    g = asb.Graph.from_csr(m.with_values(None))
+    gt = g.transpose()
+    (rp, ci, _), perm = oracle.transpose(m)
+    w = rng.standard_normal(m.nnz).astype(np.float32)
+    wd = torch.from_numpy(w).cuda()
+    wt = torch.empty_like(wd)
+    asb._check(_lib.as_permute_values(gt.handle, C.c_void_p(wd.data_ptr()), C.c_void_p(wt.data_ptr()), None))
+    torch.cuda.synchronize()
+    assert bit_equal(wt.cpu().numpy(), w[perm])
+    for f in (1, 7, 64, 100):
+        b = random_dense(rng, m.n_rows, f)
+        bd = torch.from_numpy(b).cuda()
+        c = torch.empty((m.n_cols, f), device="cuda")
+        for v in (None, "spmm:rowparallel:ft=32:rpc=4:vec=1:hubt=256", "spmm:hubsplit:ft=64:rpc=1:vec=1:hubt=64"):
+            va = None if v is None else C.byref(asb.variant_from_string(v).to_c())
+            asb._check(_lib.as_spmm_values(va, gt.handle, C.c_void_p(wt.data_ptr()), C.c_void_p(bd.data_ptr()),
+                                           m.n_rows, f, C.c_void_p(c.data_ptr()), None, None))
+            torch.cuda.synchronize()
+            want = oracle.spmm_baseline(asb.CsrMatrix(m.n_cols, m.n_rows, rp, ci, w[perm]), b)
+            assert bit_equal(c.cpu().numpy(), want), (f, v)
+    with pytest.raises(asb.InvalidArgument):
+        asb._check(_lib.as_spmm_values(None, gt.handle, None, C.c_void_p(bd.data_ptr()), m.n_rows, f,
+                                       C.c_void_p(c.data_ptr()), None, None))
+
+
+@pytest.mark.gpu
+def test_softmax_backward_bit_exact_vs_oracle():
+    rng = np.random.default_rng(13)
+    for m in (csr_from_degrees(rng, 8, 3000, [0, 1, 2, 31, 32, 33, 64, 2999]),
+              hub_graph(rng, 2000, [1900, 1000], 40, with_values=False)):
+        crow = torch.from_numpy(m.rowptr.astype(np.int64)).cuda()
+        col = torch.from_numpy(m.colind.astype(np.int32)).cuda()
+        s = (rng.standard_normal(m.nnz) * 5).astype(np.float32)
+        p = oracle.row_softmax(m, s)
+        gr = rng.standard_normal(m.nnz).astype(np.float32)
+        got = torch.ops.autosage.row_softmax_csr_backward(crow, col, torch.from_numpy(p).cuda(),
+                                                          torch.from_numpy(gr).cuda(), m.n_cols)
+        assert bit_equal(got.cpu().numpy(), oracle.row_softmax_backward(m, p, gr))
+        pd = torch.ops.autosage.row_softmax_csr(crow, col, torch.from_numpy(s).cuda(), m.n_cols)
+        assert bit_equal(pd.cpu().numpy(), p)
+
+
+# ---------------------------------------------------------------- GPU: autograd
+
+def _t(a, grad=False):
+    t = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    return t.requires_grad_(grad)
+
+
+@pytest.mark.gpu
+def test_spmm_autograd_bit_exact_vs_oracle():
+    rng = np.random.default_rng(21)
+    m = hub_graph(rng, 900, [850, 400], 8)
+    crow, col = _t(m.rowptr.astype(np.int64)), _t(m.colind.astype(np.int32))
+    for f in (16, 64):
+        b = random_dense(rng, m.n_cols, f)
+        dc = random_dense(rng, m.n_rows, f)
+        val, bt = _t(m.val, True), _t(b, True)
+        for v in ("", "spmm:hubsplit:ft=32:rpc=4:vec=1:hubt=128"):
+            val.grad = bt.grad = None
+            out = torch.ops.autosage.spmm_csr(crow, col, val, bt, v)
+            out.backward(_t(dc))
+            (rp, ci, vt), perm = oracle.transpose(m)
+            want_db = oracle.spmm_baseline(asb.CsrMatrix(m.n_cols, m.n_rows, rp, ci, vt), dc)
+            want_dval = oracle.sddmm(m, dc, b)
+            assert bit_equal(bt.grad.cpu().numpy(), want_db)
+            assert bit_equal(val.grad.cpu().numpy(), want_dval)
+    # formula check against dense f64 autograd
+    bd = torch.from_numpy(b).double().requires_grad_(True)
+    A = torch.from_numpy(_dense(m))
+    (A @ bd).backward(torch.from_numpy(dc).double())
+    assert np.allclose(bt.grad.cpu().numpy(), bd.grad.numpy(), rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.gpu
+def test_sddmm_autograd_bit_exact_vs_oracle():
+    rng = np.random.default_rng(22)
+    m = hub_graph(rng, 800, [790, 300], 10, with_values=False)
+    crow, col = _t(m.rowptr.astype(np.int64)), _t(m.colind.astype(np.int32))
+    x, y = random_dense(rng, m.n_rows, 32), random_dense(rng, m.n_cols, 32)
+    dout = rng.standard_normal(m.nnz).astype(np.float32)
+    xt, yt = _t(x, True), _t(y, True)
+    torch.ops.autosage.sddmm_csr(crow, col, xt, yt, "").backward(_t(dout))
+    want_dx = oracle.spmm_baseline(m.with_values(dout), y)
+    (rp, ci, _), perm = oracle.transpose(m)
+    want_dy = oracle.spmm_baseline(asb.CsrMatrix(m.n_cols, m.n_rows, rp, ci, dout[perm]), x)
+    assert bit_equal(xt.grad.cpu().numpy(), want_dx)
+    assert bit_equal(yt.grad.cpu().numpy(), want_dy)
+
+
+@pytest.mark.gpu
+def test_attention_autograd_matches_composed_oracle_and_f64():
+    rng = np.random.default_rng(23)
+    m = hub_graph(rng, 600, [590, 200], 7, with_values=False)
+    crow, col = _t(m.rowptr.astype(np.int64)), _t(m.colind.astype(np.int32))
+    q, k, v = (random_dense(rng, 600, 16) for _ in range(3))
+    do = random_dense(rng, 600, 16)
+    qt, kt, vt = _t(q, True), _t(k, True), _t(v, True)
+    for fused in (False, True):
+        qt.grad = kt.grad = vt.grad = None
+        torch.ops.autosage.csr_attention(crow, col, qt, kt, vt, fused).backward(_t(do))
+        # composed oracle: the same staged recompute
+        s = oracle.sddmm(m, q, k)
+        p = oracle.row_softmax(m, s)
+        (rp, ci, _), perm = oracle.transpose(m)
+        mt = lambda w: asb.CsrMatrix(m.n_cols, m.n_rows, rp, ci, w[perm])  # noqa: E731
+        want_dv = oracle.spmm_baseline(mt(p), do)
+        dp = oracle.sddmm(m, do, v)
+        ds = oracle.row_softmax_backward(m, p, dp)
+        want_dq = oracle.spmm_baseline(m.with_values(ds), k)
+        want_dk = oracle.spmm_baseline(mt(ds), q)
+        assert bit_equal(vt.grad.cpu().numpy(), want_dv)
+        assert bit_equal(qt.grad.cpu().numpy(), want_dq)
+        assert bit_equal(kt.grad.cpu().numpy(), want_dk)
+    # formulas vs dense f64 autograd (masked softmax attention)
+    mask = torch.from_numpy(_dense(m) != 0)
+    Q, K, V = (torch.from_numpy(a).double().requires_grad_(True) for a in (q, k, v))
+    S = (Q @ K.T).masked_fill(~mask, float("-inf"))
+    P = torch.softmax(S, dim=1).nan_to_num(0.0)
+    (P @ V).backward(torch.from_numpy(do).double())
+    for got, want in ((qt, Q), (kt, K), (vt, V)):
+        assert np.allclose(got.grad.cpu().numpy(), want.grad.numpy(), rtol=1e-4, atol=1e-5)
