@@ -417,6 +417,13 @@ as_status as_permute_values(as_graph gt, const float* src_dev, float* dst_dev, v
 as_status as_spmm_values(const as_variant* v, as_graph a, const float* vals_dev, const float* b_dev,
                          uint64_t b_rows, uint64_t f, float* c_dev, void* stream,
                          as_kernel_result* res);
+/* SpMM with a bf16 dense operand (new):
+ * b_dev holds b_rows x f bf16 values (raw 16-bit words), vals_dev f32 or
+ * NULL (graph's own values), f64 accumulation, f32 C.  bf16 -> f32 is exact,
+ * so C equals as_spmm on the f32 copy of B bit for bit, with half the gather
+ * bytes.  v == NULL -> baseline kernel; env overrides as in dispatch. */
+as_status as_spmm_bf16(const as_variant* v, as_graph a, const float* vals_dev, const uint16_t* b_dev,
+                       uint64_t b_rows, uint64_t f, float* c_dev, void* stream, as_kernel_result* res);
 /* Gradient of row_softmax (src/kernels.cpp:431-461): ds = p * (g - dot),
  * dot = sum_row p*g in f64 (32 strided partials, fixed pairwise fold;
  * oracle/oracle.c orc_row_softmax_backward). */

@@ -94,23 +94,38 @@ softmax_backward_kernel(const std::uint64_t* __restrict__ rowptr, const std::uin
         if (e0 == e1) continue;
         double part = 0.0;
         std::uint64_t e = e0 + lane;
-        // two loads in flight per lane; the chain order stays e, e+32, e+64, ...
-        for (; e + 32 < e1; e += 64) {
-            const float pa = __ldg(p + e), ga = __ldg(g + e);
-            const float pb = __ldg(p + e + 32), gb = __ldg(g + e + 32);
-            part = __dadd_rn(part, __dmul_rn(double(pa), double(ga)));
-            part = __dadd_rn(part, __dmul_rn(double(pb), double(gb)));
+        // four entries (eight loads) in flight per lane; the chain order stays
+        // e, e+32, e+64, ...
+        for (; e + 96 < e1; e += 128) {
+            float pv[4], gv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                pv[u] = __ldg(p + e + 32 * u);
+                gv[u] = __ldg(g + e + 32 * u);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) part = __dadd_rn(part, __dmul_rn(double(pv[u]), double(gv[u])));
         }
-        if (e < e1) part = __dadd_rn(part, __dmul_rn(double(__ldg(p + e)), double(__ldg(g + e))));
+        for (; e < e1; e += 32) part = __dadd_rn(part, __dmul_rn(double(__ldg(p + e)), double(__ldg(g + e))));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
-        // every lane holds lane 0's fold only if the tree is symmetric; take
-        // lane 0's value explicitly so the result is the oracle's fold.
+        // lanes other than 0 may associate the fold differently; lane 0 holds
+        // the oracle's order
         const double dot = __shfl_sync(0xffffffffu, part, 0);
-        for (std::uint64_t k = e0 + lane; k < e1; k += 32) {
-            const double pk = double(p[k]), gk = double(g[k]);
-            ds[k] = float(__dmul_rn(pk, __dsub_rn(gk, dot)));
+        // second pass: the row was just read, so these are L2 hits
+        std::uint64_t k = e0 + lane;
+        for (; k + 96 < e1; k += 128) {
+            float pv[4], gv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                pv[u] = p[k + 32 * u];
+                gv[u] = g[k + 32 * u];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                ds[k + 32 * u] = float(__dmul_rn(double(pv[u]), __dsub_rn(double(gv[u]), dot)));
         }
+        for (; k < e1; k += 32) ds[k] = float(__dmul_rn(double(p[k]), __dsub_rn(double(g[k]), dot)));
     }
 }
 

@@ -675,6 +675,17 @@ as_status as_permute_values(as_graph gt, const float* src_dev, float* dst_dev, v
     });
 }
 
+as_status as_spmm_bf16(const as_variant* v, as_graph a, const float* vals_dev, const uint16_t* b_dev,
+                       uint64_t b_rows, uint64_t f, float* c_dev, void* stream, as_kernel_result* res) {
+    return guard([&] {
+        Graph& g = G(a);
+        if (g.n_rows && f && (!b_dev || !c_dev)) throw InvalidArgument("spmm_bf16: null operand");
+        const KernelResult r = dispatch_spmm_bf16(v, g, vals_dev, b_dev, b_rows, f, c_dev,
+                                                  resolve_stream(g, stream), res != nullptr);
+        fill_result(res, r);
+    });
+}
+
 as_status as_row_softmax_backward(as_graph m, const float* p_dev, const float* grad_dev, float* ds_dev,
                                   void* stream) {
     return guard([&] {

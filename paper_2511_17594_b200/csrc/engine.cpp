@@ -315,6 +315,52 @@ KernelResult dispatch_spmm(const as_variant& v, Graph& a, const float* vals, con
     return r;
 }
 
+// SpMM with a bf16 B: the same kernels reading
+// half the gather bytes.  bf16 -> f32 is exact, so the result equals the f32
+// SpMM on float(B) bit for bit.  v == nullptr: baseline.  The 4-wide path
+// (8-byte loads) needs f % 4 == 0 and an 8-byte aligned base; the ring
+// kernel and the softmax mode stay f32-only.
+KernelResult dispatch_spmm_bf16(const as_variant* v, Graph& a, const float* vals, const std::uint16_t* b,
+                                std::uint64_t b_rows, std::uint64_t f, float* c, cudaStream_t s, bool timed) {
+    check_spmm_dims(a, b_rows);
+    KernelResult r;
+    if (v) {
+        if (v->op != AS_OP_SPMM) throw InvalidArgument("dispatch: spmm operands given to a non-spmm variant");
+        r.variant = apply_env_overrides(*v);
+        check_variant(r.variant);
+    } else {
+        r.variant = default_variant();
+        r.variant.mapping = AS_MAP_BASELINE;
+    }
+    const bool vec_ok = f > 0 && f % 4 == 0 && (reinterpret_cast<std::uintptr_t>(b) & 7) == 0;
+    DeviceGuard dg(a.device);
+    const float* va = graph_values(a, vals);
+    const std::uint32_t wpb = std::uint32_t(std::min<std::uint64_t>(r.variant.rows_per_chunk, 16));
+    const unsigned* fin = nullptr;
+    if (r.variant.mapping != AS_MAP_BASELINE) {
+        if (r.variant.mapping == AS_MAP_ROWPARALLEL) ensure_order(a);
+        else ensure_hub_plan(a, r.variant.hub_threshold);
+        if (a.n_cols * f * 2 <= (std::uint64_t(96) << 20)) fin = finite_flag_bf16(a, b, a.n_cols * f, s);
+    }
+    TimedRegion tr(s, timed);
+    switch (r.variant.mapping) {
+        case AS_MAP_BASELINE:
+            launch_spmm_baseline(a, va, b, std::uint32_t(f), c, s, true);
+            break;
+        case AS_MAP_ROWPARALLEL:
+            launch_spmm_rows(a, va, 0, a.n_rows, b, std::uint32_t(f), c, r.variant.f_tile, vec_ok, wpb, s, fin,
+                             nullptr, nullptr, true);
+            break;
+        case AS_MAP_HUBSPLIT:
+            launch_spmm_hubsplit(a, va, b, std::uint32_t(f), c, r.variant.f_tile, vec_ok, wpb,
+                                 r.variant.hub_threshold, s, fin, nullptr, nullptr, true);
+            break;
+    }
+    r.elapsed_ms = tr.stop();
+    r.vectorized_path = r.variant.vectorized && vec_ok && r.variant.mapping != AS_MAP_BASELINE;
+    return r;
+}
+
 void sddmm_baseline(Graph& p, const float* x, std::uint64_t x_rows, const float* y,
                     std::uint64_t y_rows, std::uint64_t f, float* out, cudaStream_t s) {
     check_sddmm_dims(p, x_rows, y_rows);

@@ -33,6 +33,9 @@ void spmm_mapped(const as_variant& v, int expect_mapping, Graph& a, const float*
 KernelResult dispatch_spmm(const as_variant& v, Graph& a, const float* vals, const float* b,
                            std::uint64_t b_rows, std::uint64_t f, float* c, cudaStream_t s,
                            bool timed);
+// SpMM with bf16 B words (v == nullptr: baseline); the f32 result on float(B).
+KernelResult dispatch_spmm_bf16(const as_variant* v, Graph& a, const float* vals, const std::uint16_t* b,
+                                std::uint64_t b_rows, std::uint64_t f, float* c, cudaStream_t s, bool timed);
 void sddmm_baseline(Graph& p, const float* x, std::uint64_t x_rows, const float* y,
                     std::uint64_t y_rows, std::uint64_t f, float* out, cudaStream_t s);
 // sddmm_rowparallel (src/kernels.cpp:357-429): variant as given, no env.

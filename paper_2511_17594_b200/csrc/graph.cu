@@ -554,7 +554,43 @@ __global__ void finite_check_kernel(const float* __restrict__ p, std::uint64_t n
     }
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *flag = 0u;
 }
+
+// bf16 words: exponent field 0x7F80 all ones = Inf/NaN
+__global__ void finite_check_bf16_kernel(const unsigned short* __restrict__ p, std::uint64_t n,
+                                         unsigned* __restrict__ flag) {
+    bool bad = false;
+    const std::uint64_t stride = std::uint64_t(gridDim.x) * blockDim.x;
+    const std::uint64_t i = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
+    if ((reinterpret_cast<std::uintptr_t>(p) & 15) == 0) {
+        const std::uint64_t n8 = n / 8;
+        const uint4* p8 = reinterpret_cast<const uint4*>(p);
+        for (std::uint64_t k = i; k < n8; k += stride) {
+            const uint4 v = __ldg(p8 + k);
+            for (unsigned w : {v.x, v.y, v.z, v.w})
+                bad |= ((w & 0x7F80u) == 0x7F80u) | ((w & 0x7F800000u) == 0x7F800000u);
+        }
+        for (std::uint64_t k = n8 * 8 + i; k < n; k += stride) bad |= (p[k] & 0x7F80u) == 0x7F80u;
+    } else {
+        for (std::uint64_t k = i; k < n; k += stride) bad |= (p[k] & 0x7F80u) == 0x7F80u;
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *flag = 0u;
+}
 }  // namespace
+
+const unsigned* finite_flag_bf16(Graph& g, const unsigned short* p, std::uint64_t n, cudaStream_t s) {
+    g.flag.ensure(1);
+    ASB_CUDA(cudaMemsetAsync(g.flag.get(), 0, 4, s));
+    if (n == 0 || p == nullptr) return g.flag.get();
+    ASB_CUDA(cudaMemsetAsync(g.flag.get(), 1, 1, s));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const std::uint64_t want = (n / 8 + 255) / 256 + 1;
+    const unsigned blocks = unsigned(std::min<std::uint64_t>(want, std::uint64_t(sms) * 8));
+    finite_check_bf16_kernel<<<blocks, 256, 0, s>>>(p, n, g.flag.get());
+    check_launch("finite_check_bf16_kernel");
+    return g.flag.get();
+}
 
 const unsigned* finite_flag(Graph& g, const float* p, std::uint64_t n, cudaStream_t s) {
     g.flag.ensure(1);

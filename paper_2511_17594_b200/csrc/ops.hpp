@@ -8,23 +8,26 @@ namespace asb {
 
 // ---- SpMM (src/kernels.cpp:210-334) ------------------------------------
 // K1: warp per row, lane per feature, scalar loads, natural row order.
-void launch_spmm_baseline(Graph& g, const float* val, const float* b, std::uint32_t f, float* c, cudaStream_t s);
+// b: f32, or bf16 words when bf16 (every kernel reads B through an exact
+// bf16 -> f32 step, so a bf16 B gives the f32 result on float(B) bit for bit)
+void launch_spmm_baseline(Graph& g, const float* val, const void* b, std::uint32_t f, float* c, cudaStream_t s,
+                          bool bf16 = false);
 // K2: row groups over rows in degree-descending order; f_tile splits the
 // feature dimension into independent work items; wpb warps per CTA.
 // Rows order[offset, offset+n_list) of the degree-descending order; rows of
 // degree >= 2048 among them go to the CTA-per-row cp.async ring kernel on a
 // forked stream (same numerics).
 void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uint64_t n_list,
-                      const float* b, std::uint32_t f, float* c, std::uint64_t f_tile, bool vec,
+                      const void* b, std::uint32_t f, float* c, std::uint64_t f_tile, bool vec,
                       std::uint32_t wpb, cudaStream_t s, const unsigned* finite = nullptr,
-                      const float* rmax = nullptr, const double* rsum = nullptr);
+                      const float* rmax = nullptr, const double* rsum = nullptr, bool bf16 = false);
 // K3: hub split -- light rows via K2 plus 2048-nnz pieces with ordered
 // fp64 partial reduction.
-void launch_spmm_hubsplit(Graph& g, const float* val, const float* b, std::uint32_t f, float* c,
+void launch_spmm_hubsplit(Graph& g, const float* val, const void* b, std::uint32_t f, float* c,
                           std::uint64_t f_tile, bool vec, std::uint32_t wpb,
                           std::uint64_t hub_threshold, cudaStream_t s,
                           const unsigned* finite = nullptr, const float* rmax = nullptr,
-                          const double* rsum = nullptr);
+                          const double* rsum = nullptr, bool bf16 = false);
 // Softmax mode of K2/K3 (rmax != nullptr): `val` holds raw scores and each
 // entry's value is p_e = softmax of its row from (rmax[row], rsum[row])
 // (softmax.cuh), computed by the loading lane -- the SpMM half of the fused
@@ -54,6 +57,8 @@ void sddmm_chunks_prepare(Graph& g, const float* x, const float* y, std::uint32_
 // widen.cuh).  Written into g.flag (one flag per graph; a graph handle runs
 // one operator at a time).
 const unsigned* finite_flag(Graph& g, const float* p, std::uint64_t n, cudaStream_t s);
+// the same over n bf16 words
+const unsigned* finite_flag_bf16(Graph& g, const unsigned short* p, std::uint64_t n, cudaStream_t s);
 
 // ---- row softmax (src/kernels.cpp:431-461) ----------------------------
 void launch_row_softmax(Graph& g, const float* vin, float* vout, cudaStream_t s);

@@ -37,38 +37,65 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int kSegMaxS = 8;  // max entries per lane per fast-loop block (seg_smem)
 
-template <int VEC>
+// Load type of VEC consecutive B elements: f32 (float / float4) or, with BF,
+// bf16 (as raw 16-bit words: ushort / uint2 -- 8-byte loads for 4 features).
+template <int VEC, bool BF = false>
 struct VecT;
 template <>
-struct VecT<1> {
+struct VecT<1, false> {
     using T = float;
 };
 template <>
-struct VecT<4> {
+struct VecT<4, false> {
     using T = float4;
+};
+template <>
+struct VecT<1, true> {
+    using T = unsigned short;
+};
+template <>
+struct VecT<4, true> {
+    using T = uint2;
+};
+template <>
+struct VecT<8, true> {
+    using T = uint4;
 };
 
 __device__ __forceinline__ float comp(const float& v, int) { return v; }
 __device__ __forceinline__ float comp(const float4& v, int q) {
     return q == 0 ? v.x : (q == 1 ? v.y : (q == 2 ? v.z : v.w));
 }
+// bf16 -> f32 is exact (the f32 with the same top 16 bits), so every later
+// widening and product is the f32 path's on float(B)
+__device__ __forceinline__ float comp(const unsigned short& h, int) { return __uint_as_float(unsigned(h) << 16); }
+__device__ __forceinline__ float comp(const uint2& w, int q) {
+    const unsigned x = q < 2 ? w.x : w.y;
+    return __uint_as_float((q & 1) ? (x & 0xffff0000u) : (x << 16));
+}
+__device__ __forceinline__ float comp(const uint4& w, int q) {
+    const unsigned x = q < 2 ? w.x : (q < 4 ? w.y : (q < 6 ? w.z : w.w));
+    return __uint_as_float((q & 1) ? (x & 0xffff0000u) : (x << 16));
+}
 
 [[maybe_unused]] __host__ __device__ constexpr int unroll_for(int vec, int nch) {
-    return vec == 4 ? (nch == 1 ? 4 : (nch == 2 ? 2 : 1)) : (nch >= 8 ? 1 : 8 / nch);
+    return vec >= 4 ? (nch == 1 ? 4 : (nch == 2 ? 2 : 1)) : (nch >= 8 ? 1 : 8 / nch);
 }
 
 [[maybe_unused]] __host__ __device__ constexpr int maxreg_for(int vec, int nch) {
     // float4 single-chunk tiles at 64 registers (32 warps/SM): 48 spilled the
     // 4 in-flight entries and cost Reddit-shape 2.35 -> 2.41 ms (hubsplit) and
     // 3.24 -> 4.01 ms (rowparallel); wider tiles keep their loads in registers
-    return vec == 1 ? (nch == 1 ? 64 : (nch == 2 ? 96 : 128)) : (nch == 1 ? 64 : (nch == 2 ? 80 : 128));
+    // bf16 8-wide tiles (uint4 = 8 features per lane) carry 8 f64 accumulators per chunk
+    return vec == 1 ? (nch == 1 ? 64 : (nch == 2 ? 96 : 128))
+                    : (vec == 8 ? (nch == 1 ? 96 : 128) : (nch == 1 ? 64 : (nch == 2 ? 80 : 128)));
 }
 
 struct SegArgs {
     const std::uint64_t* rowptr;
     const std::uint32_t* colind;
     const float* val;
-    const float* b;
+    const void* b;                    // f32, or bf16 words when BF
     float* c;
     double* scratch;
     const std::uint32_t* rowlist;     // row mode: row ids (nullptr: identity)
@@ -80,6 +107,7 @@ struct SegArgs {
     const float* rmax;                // softmax mode: val holds raw scores, and
     const double* rsum;               // p_e = softmax of the row (softmax.cuh)
     int off32;                        // n_cols * f < 2^32: 32-bit element offsets
+    int bf16;                         // B holds bf16 (seg kernels' BF instantiation)
     std::uint64_t n_items;
     std::uint32_t n_tiles;
     std::uint32_t f;
@@ -87,14 +115,20 @@ struct SegArgs {
 };
 
 // acc[ch][q] += v * B component, one DFMA each, with MIX's widening split
-template <int VEC, int NCH, int MIX, class VT>
+// first component of a VEC-wide load re-biased on the ALU (MIX): f32 float4
+// splits half/half with the XU's F2F; a bf16 component's re-bias is two ALU
+// ops (its low mantissa word is zero), so bf16 loads put 3/4 on the ALU
+template <int VEC, bool BF>
+__host__ __device__ constexpr int mix_from() { return VEC == 1 ? 0 : (BF ? VEC / 4 : 2); }
+
+template <int VEC, int NCH, int MIX, class VT, int MQ = mix_from<VEC, false>()>
 __device__ __forceinline__ void seg_accumulate(double (&acc)[NCH][VEC], double v, const VT (&bv)[NCH]) {
     const double vu = MIX ? v * kWidenUp : v;
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll
         for (int q = 0; q < VEC; ++q) {
-            if (MIX && (VEC == 1 || q >= 2))
+            if (MIX && q >= MQ)
                 acc[ch][q] = __fma_rn(vu, widen_scaled(comp(bv[ch], q)), acc[ch][q]);
             else
                 acc[ch][q] = __fma_rn(v, double(comp(bv[ch], q)), acc[ch][q]);
@@ -107,9 +141,10 @@ __device__ __forceinline__ void seg_accumulate(double (&acc)[NCH][VEC], double v
 // re-biased on the ALU pipe.  SMX: the entry values are softmax
 // probabilities computed from raw scores and the row's (max, sum) by the lane
 // that loads them (fused attention), instead of stored values.
-template <int VEC, int LPR, int NCH, bool HAS_VAL, bool PIECES, int U, int MIX, bool SMX>
+template <int VEC, int LPR, int NCH, bool HAS_VAL, bool PIECES, int U, int MIX, bool SMX, bool BF>
 __device__ __forceinline__ void seg_body(const SegArgs& a) {
-    using VT = typename VecT<VEC>::T;
+    using VT = typename VecT<VEC, BF>::T;
+    using BT = typename std::conditional<BF, unsigned short, float>::type;
     constexpr int GPW = 32 / LPR;
     constexpr int W = LPR > U ? LPR : U;
     constexpr int S = W / LPR;
@@ -169,7 +204,7 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
     const unsigned gbase = unsigned(grp * LPR);
     const std::uint32_t* colp = a.colind + e0;
     const float* valp = HAS_VAL ? a.val + e0 : nullptr;
-    const float* __restrict__ bmat = a.b;
+    const BT* __restrict__ bmat = static_cast<const BT*>(a.b);
 
     // Fast path: while every group of the warp still has W whole entries
     // left and every lane's features are in range, no predicates at all (a
@@ -186,7 +221,7 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
         for (int ch = 0; ch < NCH; ++ch) lane_full = lane_full && fok[ch];
         const std::uint32_t fast_end = mindeg / W * W;
         if (a.off32 && fast_end && __all_sync(FULL, lane_full)) {
-            const float* bl[NCH];
+            const BT* bl[NCH];
 #pragma unroll
             for (int ch = 0; ch < NCH; ++ch) bl[ch] = bmat + fidx[ch];
             const std::uint32_t f = a.f;
@@ -240,7 +275,8 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
                         for (int ch = 0; ch < NCH; ++ch)
                             bv[u][ch] = __ldg(reinterpret_cast<const VT*>(bl[ch] + oj[u]));
 #pragma unroll
-                    for (int u = 0; u < U; ++u) seg_accumulate<VEC, NCH, MIX>(acc, vj[u], bv[u]);
+                    for (int u = 0; u < U; ++u)
+                        seg_accumulate<VEC, NCH, MIX, VT, mix_from<VEC, BF>()>(acc, vj[u], bv[u]);
                 }
             }
         }
@@ -291,7 +327,7 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
                     if (okj && fok[ch]) {
 #pragma unroll
                         for (int q = 0; q < VEC; ++q) {
-                            const bool rebias = MIX && (VEC == 1 || q >= 2);
+                            const bool rebias = MIX && q >= mix_from<VEC, BF>();
                             if (rebias)
                                 acc[ch][q] = __fma_rn(vu, widen_scaled(comp(bv[u][ch], q)), acc[ch][q]);
                             else
@@ -320,10 +356,10 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
 }
 
 template <int VEC, int LPR, int NCH, bool HAS_VAL, bool PIECES, int U = unroll_for(VEC, NCH),
-          int MAXR = maxreg_for(VEC, NCH), bool SMX = false>
+          int MAXR = maxreg_for(VEC, NCH), bool SMX = false, bool BF = false>
 __global__ void __launch_bounds__(512) __maxnreg__(MAXR) spmm_seg_kernel(SegArgs a) {
-    if (a.finite && *a.finite) seg_body<VEC, LPR, NCH, HAS_VAL, PIECES, U, 1, SMX>(a);
-    else seg_body<VEC, LPR, NCH, HAS_VAL, PIECES, U, 0, SMX>(a);
+    if (a.finite && *a.finite) seg_body<VEC, LPR, NCH, HAS_VAL, PIECES, U, 1, SMX, BF>(a);
+    else seg_body<VEC, LPR, NCH, HAS_VAL, PIECES, U, 0, SMX, BF>(a);
 }
 
 // K3 epilogue: s = 0.0; s += partial[p] in piece order; C = f32(s)
@@ -447,7 +483,7 @@ __device__ __forceinline__ void longrow_body(const SegArgs& A, std::uint32_t ch,
     const std::uint64_t* __restrict__ rowptr = A.rowptr;
     const std::uint32_t* __restrict__ colind = A.colind;
     const float* __restrict__ val = A.val;
-    const float* __restrict__ b = A.b;
+    const float* __restrict__ b = static_cast<const float*>(A.b);
     float* __restrict__ c = A.c;
     const std::uint32_t f = A.f;
     constexpr int S = kLongStages;
@@ -636,10 +672,10 @@ bool longrow_ok(std::uint32_t f, bool vec) {
 // ---------------------------------------------------------------------------
 // K1: the guardrail baseline.  Warp per row in natural order, lane per
 // feature (NF features per lane per pass), scalar loads, no prefetch.
-template <int NF>
+template <int NF, class BT = float>
 __global__ void spmm_baseline_kernel(const std::uint64_t* __restrict__ rowptr,
                                      const std::uint32_t* __restrict__ colind,
-                                     const float* __restrict__ val, const float* __restrict__ b,
+                                     const float* __restrict__ val, const BT* __restrict__ b,
                                      float* __restrict__ c, std::uint64_t n_rows, std::uint32_t f) {
     const std::uint64_t row = (std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (row >= n_rows) return;
@@ -650,12 +686,12 @@ __global__ void spmm_baseline_kernel(const std::uint64_t* __restrict__ rowptr,
 #pragma unroll
         for (int q = 0; q < NF; ++q) acc[q] = 0.0;
         for (std::uint64_t e = e0; e < e1; ++e) {
-            const float* brow = b + std::uint64_t(colind[e]) * f + f0;
+            const BT* brow = b + std::uint64_t(colind[e]) * f + f0;
             const double v = val ? double(val[e]) : 1.0;
 #pragma unroll
             for (int q = 0; q < NF; ++q) {
                 const std::uint32_t t = std::uint32_t(lane + 32 * q);
-                if (f0 + t < f) acc[q] = __fma_rn(v, double(brow[t]), acc[q]);
+                if (f0 + t < f) acc[q] = __fma_rn(v, double(comp(brow[t], 0)), acc[q]);
             }
         }
 #pragma unroll
@@ -742,7 +778,21 @@ void launch_seg(const SegArgs& a, bool has_val, std::uint32_t wpb, cudaStream_t 
     if (blocks == 0) return;
     const bool pieces = a.piece_row != nullptr;
     const unsigned nb = unsigned(blocks), nt = wpb * 32;
-    if (a.rmax) {  // softmax mode (fused attention): float4 tiles only
+    if constexpr (VEC == 8) {
+        if (!a.bf16) throw LogicError("8-wide SpMM tiles are bf16-only");
+    }
+    if (VEC == 8 || a.bf16) {  // bf16 B: default tuning, no softmax mode
+        constexpr int U = unroll_for(VEC, NCH), R = maxreg_for(VEC, NCH);
+        if (a.rmax) throw LogicError("spmm softmax mode takes f32 operands");
+        if (has_val) {
+            if (pieces) spmm_seg_kernel<VEC, LPR, NCH, true, true, U, R, false, true><<<nb, nt, seg_smem(nt), s>>>(a);
+            else spmm_seg_kernel<VEC, LPR, NCH, true, false, U, R, false, true><<<nb, nt, seg_smem(nt), s>>>(a);
+        } else {
+            if (pieces) spmm_seg_kernel<VEC, LPR, NCH, false, true, U, R, false, true><<<nb, nt, seg_smem(nt), s>>>(a);
+            else spmm_seg_kernel<VEC, LPR, NCH, false, false, U, R, false, true><<<nb, nt, seg_smem(nt), s>>>(a);
+        }
+    } else if constexpr (VEC == 8) {
+    } else if (a.rmax) {  // softmax mode (fused attention): float4 tiles only
         if constexpr (VEC == 4) {
             if (pieces) spmm_seg_kernel<VEC, LPR, NCH, true, true, unroll_for(VEC, NCH), maxreg_for(VEC, NCH), true><<<nb, nt, seg_smem(nt), s>>>(a);
             else spmm_seg_kernel<VEC, LPR, NCH, true, false, unroll_for(VEC, NCH), maxreg_for(VEC, NCH), true><<<nb, nt, seg_smem(nt), s>>>(a);
@@ -770,6 +820,7 @@ void launch_seg_vec(const SegArgs& a, bool has_val, std::uint32_t lanes, std::ui
     else if (lanes <= 32) launch_seg<VEC, 32, 1>(a, has_val, wpb, s);
     else if (lanes <= 64) launch_seg<VEC, 32, 2>(a, has_val, wpb, s);
     else if (lanes <= 128) launch_seg<VEC, 32, 4>(a, has_val, wpb, s);
+    else if constexpr (VEC == 8) throw LogicError("8-wide tiles take at most 4 chunks per lane");
     else launch_seg<VEC, 32, 8>(a, has_val, wpb, s);
 }
 
@@ -780,11 +831,20 @@ struct TileShape {
 // GPU meaning of (f_tile, vec): a work item covers tile_w features; tiles
 // are independent items.  Any tiling gives the same bits (per-feature
 // accumulation order is always CSR order).
-TileShape tile_shape(std::uint32_t f, std::uint64_t f_tile, bool vec) {
-    const int v = vec ? 4 : 1;
+// vec8: bf16 B with f % 8 == 0 and a 16-byte base (uint4 = 8 features per
+// lane).  Below f = 64 the 4-wide tiles keep more lanes per row in flight
+// (Reddit-shape F=32: 0.90 ms 4-wide vs 1.10 ms 8-wide; F=64: 1.72 vs 1.56;
+// F=128: 3.80 vs 3.29).
+bool vec8_ok(const void* b, std::uint32_t f, bool vec, bool bf16) {
+    return bf16 && vec && f >= 64 && f % 8 == 0 && (reinterpret_cast<std::uintptr_t>(b) & 15) == 0;
+}
+
+TileShape tile_shape(std::uint32_t f, std::uint64_t f_tile, bool vec, bool vec8 = false) {
+    const int v = vec8 ? 8 : (vec ? 4 : 1);
     std::uint64_t tw = effective_tile(f_tile, f);
-    if (vec) tw = (tw + 3) / 4 * 4;                                 // keep float4 alignment
-    tw = std::min<std::uint64_t>(tw, std::uint64_t(32 * 8 * v));  // at most 8 chunks / lane
+    if (vec) tw = (tw + v - 1) / v * v;                             // keep the vector alignment
+    // at most 8 chunks per lane (4 for the 8-wide tiles: 8 f64 accumulators each)
+    tw = std::min<std::uint64_t>(tw, std::uint64_t(32 * (v == 8 ? 4 : 8) * v));
     TileShape t;
     t.tile_w = std::uint32_t(std::max<std::uint64_t>(tw, 1));
     t.n_tiles = (f + t.tile_w - 1) / t.tile_w;
@@ -819,11 +879,23 @@ std::uint64_t long_row_min(const Graph& g) {
 
 } // namespace
 
-void launch_spmm_baseline(Graph& g, const float* val, const float* b, std::uint32_t f, float* c,
-                          cudaStream_t s) {
+void launch_spmm_baseline(Graph& g, const float* val, const void* bv, std::uint32_t f, float* c,
+                          cudaStream_t s, bool bf16) {
     if (g.n_rows == 0 || f == 0) return;
     const std::uint64_t threads = g.n_rows * 32;
     const unsigned blocks = unsigned((threads + 255) / 256);
+    if (bf16) {
+        const auto* b = static_cast<const unsigned short*>(bv);
+        if (f <= 32)
+            spmm_baseline_kernel<1><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f);
+        else if (f <= 64)
+            spmm_baseline_kernel<2><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f);
+        else
+            spmm_baseline_kernel<4><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f);
+        check_launch("spmm_baseline_kernel");
+        return;
+    }
+    const auto* b = static_cast<const float*>(bv);
     if (f <= 32)
         spmm_baseline_kernel<1><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f);
     else if (f <= 64)
@@ -836,9 +908,9 @@ void launch_spmm_baseline(Graph& g, const float* val, const float* b, std::uint3
 }
 
 void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uint64_t n_list,
-                      const float* b, std::uint32_t f, float* c, std::uint64_t f_tile, bool vec,
+                      const void* b, std::uint32_t f, float* c, std::uint64_t f_tile, bool vec,
                       std::uint32_t wpb, cudaStream_t s, const unsigned* finite, const float* rmax,
-                      const double* rsum) {
+                      const double* rsum, bool bf16) {
     if (rmax) vec = true;  // softmax mode runs float4 tiles (same numerics, engine gates f % 4)
     if (n_list == 0 || f == 0) return;
     ensure_order(g);
@@ -846,7 +918,7 @@ void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uin
     // kernel on a forked stream, concurrent with the group kernel
     const std::uint64_t lmin = long_row_min(g);
     std::uint64_t n_long = 0;
-    if (lmin > 0 && longrow_ok(f, vec)) {
+    if (lmin > 0 && !bf16 && longrow_ok(f, vec)) {
         const std::uint64_t ge = rows_with_degree_at_least(g, lmin);
         n_long = ge > offset ? std::min(ge - offset, n_list) : 0;
     }
@@ -868,7 +940,8 @@ void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uin
         n_list -= n_long;
     }
     if (n_list) {
-        const TileShape t = tile_shape(f, f_tile, vec);
+        const bool v8 = vec8_ok(b, f, vec, bf16);
+        const TileShape t = tile_shape(f, f_tile, vec, v8);
         SegArgs a{};
         a.rowptr = g.rowptr.get();
         a.colind = g.colind.get();
@@ -883,23 +956,26 @@ void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uin
         a.n_tiles = t.n_tiles;
         a.f = f;
         a.off32 = fast_gather_ok(g, f);
+        a.bf16 = bf16;
         a.tile_w = t.tile_w;
         wpb = warps_per_cta(wpb);
-        if (vec) launch_seg_vec<4>(a, val != nullptr, t.lanes, wpb, s);
+        if (v8) launch_seg_vec<8>(a, val != nullptr, t.lanes, wpb, s);
+        else if (vec) launch_seg_vec<4>(a, val != nullptr, t.lanes, wpb, s);
         else launch_seg_vec<1>(a, val != nullptr, t.lanes, wpb, s);
     }
     if (n_long) graph_join(g, s);
 }
 
-void launch_spmm_hubsplit(Graph& g, const float* val, const float* b, std::uint32_t f, float* c,
+void launch_spmm_hubsplit(Graph& g, const float* val, const void* b, std::uint32_t f, float* c,
                           std::uint64_t f_tile, bool vec, std::uint32_t wpb,
                           std::uint64_t hub_threshold, cudaStream_t s, const unsigned* finite,
-                          const float* rmax, const double* rsum) {
+                          const float* rmax, const double* rsum, bool bf16) {
     if (g.n_rows == 0 || f == 0) return;
     if (rmax) vec = true;
     const HubPlan& plan = ensure_hub_plan(g, hub_threshold);
     wpb = warps_per_cta(wpb);
-    const TileShape t = tile_shape(f, f_tile, vec);
+    const bool v8 = vec8_ok(b, f, vec, bf16);
+    const TileShape t = tile_shape(f, f_tile, vec, v8);
     if (plan.n_slots) g.scratch.ensure(plan.n_slots * f);
     // light rows on the forked stream, concurrent with the pieces: their
     // blocks fill the SMs the pieces kernel's last wave leaves idle
@@ -910,7 +986,8 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const float* b, std::uint3
     const bool fork_light = concurrent && plan.n_light && plan.n_pieces;
     if (fork_light) {
         cudaStream_t aux = graph_fork(g, s);
-        launch_spmm_rows(g, val, plan.n_heavy, plan.n_light, b, f, c, f_tile, vec, wpb, aux, finite, rmax, rsum);
+        launch_spmm_rows(g, val, plan.n_heavy, plan.n_light, b, f, c, f_tile, vec, wpb, aux, finite, rmax, rsum,
+                         bf16);
     }
     if (plan.n_pieces) {
         SegArgs a{};
@@ -931,6 +1008,7 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const float* b, std::uint3
         a.n_tiles = t.n_tiles;
         a.f = f;
         a.off32 = fast_gather_ok(g, f);
+        a.bf16 = bf16;
         a.tile_w = t.tile_w;
         // pieces are up to 2048-entry dependent chains: when there are too
         // few of them to fill the lane-group kernel (under a wave), the ring
@@ -941,13 +1019,15 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const float* b, std::uint3
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const bool few = plan.n_pieces <= std::uint64_t(4) * std::uint64_t(sms);
-        if (few && longrow_ok(f, vec)) launch_longrow<true>(a, plan.n_pieces, s);
+        if (few && !bf16 && longrow_ok(f, vec)) launch_longrow<true>(a, plan.n_pieces, s);
+        else if (v8) launch_seg_vec<8>(a, val != nullptr, t.lanes, wpb, s);
         else if (vec) launch_seg_vec<4>(a, val != nullptr, t.lanes, wpb, s);
         else launch_seg_vec<1>(a, val != nullptr, t.lanes, wpb, s);
     }
     if (fork_light) graph_join(g, s);
     else if (plan.n_light)
-        launch_spmm_rows(g, val, plan.n_heavy, plan.n_light, b, f, c, f_tile, vec, wpb, s, finite, rmax, rsum);
+        launch_spmm_rows(g, val, plan.n_heavy, plan.n_light, b, f, c, f_tile, vec, wpb, s, finite, rmax, rsum,
+                         bf16);
     if (plan.n_red) {
         const std::uint64_t total = plan.n_red * f;
         const unsigned blocks = unsigned(std::min<std::uint64_t>((total + 255) / 256, 148 * 32));

@@ -22,7 +22,8 @@ the SpMM on a cached device transpose (as_graph_transpose) with the values
 carried through its entry permutation, value gradients are SDDMMs, and the
 softmax gradient is as_row_softmax_backward.  SpMM mappings are bit-identical
 to each other, so the backward SpMMs use the hub-split mapping (`_BWD_SPMM`)
-whatever the forward variant was.  csr_attention's backward recomputes the
+whatever the forward variant was; the SDDMMs use a scalar (sequential-order)
+mapped variant (`_BWD_SDDMM`), the same bits as the baseline.  csr_attention's backward recomputes the
 scores and probabilities (staged) rather than keeping them from the forward.
 """
 from __future__ import annotations
@@ -105,7 +106,16 @@ def _ctx(t: torch.Tensor):
 @torch.library.custom_op("autosage::spmm_csr", mutates_args=())
 def spmm_csr(crow: torch.Tensor, col: torch.Tensor, val: torch.Tensor, b: torch.Tensor,
              variant: str) -> torch.Tensor:
-    """C = A B (dispatch(variant, A, B), src/kernels.cpp:485-506; "" = baseline)."""
+    """C = A B (dispatch(variant, A, B), src/kernels.cpp:485-506; "" = baseline).
+    A bfloat16 B is read as bf16 (as_spmm_bf16: half the gather bytes, the
+    f32 result on float(B) bit for bit); C is float32 either way."""
+    if b.dtype == torch.bfloat16:
+        b = b.contiguous()
+        g = _graph(crow, col, val, b.shape[0])
+        c = torch.empty((g.n_rows, b.shape[1]), dtype=torch.float32, device=b.device)
+        _check(_lib.as_spmm_bf16(_variant(variant), g.handle, None, C.c_void_p(b.data_ptr()), b.shape[0],
+                                 b.shape[1], C.c_void_p(c.data_ptr()), _stream(b), None))
+        return c
     b = b.contiguous().float()
     g = _graph(crow, col, val, b.shape[0])
     c = torch.empty((g.n_rows, b.shape[1]), dtype=torch.float32, device=b.device)
@@ -116,7 +126,7 @@ def spmm_csr(crow: torch.Tensor, col: torch.Tensor, val: torch.Tensor, b: torch.
 
 @spmm_csr.register_fake
 def _(crow, col, val, b, variant):
-    return b.new_empty((crow.shape[0] - 1, b.shape[1]))
+    return b.new_empty((crow.shape[0] - 1, b.shape[1]), dtype=torch.float32)
 
 
 @torch.library.custom_op("autosage::spmm_csr_auto", mutates_args=())
@@ -187,6 +197,8 @@ def _(crow, col, q, k, v, fused):
 # Backward
 # ---------------------------------------------------------------------------
 _BWD_SPMM = "spmm:hubsplit:ft=64:rpc=1:vec=1:hubt=256"
+# sequential-order SDDMM (scalar variant: the same bits as the baseline, src/kernels.cpp:103-127)
+_BWD_SDDMM = "sddmm:rowparallel:ft=32:rpc=1:vec=0:hubt=256"
 
 
 def _spmm_vals(g: Graph, vals, b: torch.Tensor) -> torch.Tensor:
@@ -276,9 +288,9 @@ def _spmm_bwd(ctx, dc):
     crow, col, val, b = ctx.saved_tensors
     dval = db = None
     if ctx.needs_input_grad[2] and val.numel():
-        dval = sddmm_csr(crow, col, dc, b, "")
+        dval = sddmm_csr(crow, col, dc, b.float(), _BWD_SDDMM)
     if ctx.needs_input_grad[3]:
-        db = _spmm_t(crow, col, val if val.numel() else None, b.shape[0], dc)
+        db = _spmm_t(crow, col, val if val.numel() else None, b.shape[0], dc).to(b.dtype)
     return (None, None, dval, db) + (None,) * (ctx.n_extra)
 
 
@@ -323,10 +335,10 @@ def _attention_bwd(ctx, do):
     """Staged recompute: s = SDDMM(q, k), p = softmax(s); then dv = A^T[p] dO,
     dp = SDDMM(dO, v), ds = softmax'(p, dp), dq = A[ds] k, dk = A^T[ds] q."""
     crow, col, q, k, v = ctx.saved_tensors
-    s = sddmm_csr(crow, col, q, k, "")
+    s = sddmm_csr(crow, col, q, k, _BWD_SDDMM)
     p = row_softmax_csr(crow, col, s, k.shape[0])
     dv = _spmm_t(crow, col, p, k.shape[0], do) if ctx.needs_input_grad[4] else None
-    dp = sddmm_csr(crow, col, do, v, "")
+    dp = sddmm_csr(crow, col, do, v, _BWD_SDDMM)
     ds = row_softmax_csr_backward(crow, col, p, dp, k.shape[0])
     pat = _graph(crow, col, torch.empty(0, device=q.device), k.shape[0])
     dq = _spmm_vals(pat, ds, k) if ctx.needs_input_grad[2] else None

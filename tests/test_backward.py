@@ -272,3 +272,68 @@ def test_attention_autograd_matches_composed_oracle_and_f64():
     (P @ V).backward(torch.from_numpy(do).double())
     for got, want in ((qt, Q), (kt, K), (vt, V)):
         assert np.allclose(got.grad.cpu().numpy(), want.grad.numpy(), rtol=1e-4, atol=1e-5)
+
+
+# ---------------------------------------------------------------- GPU: bf16 B
+
+def _bf16_words(rng, rows, f):
+    """bf16 bit patterns of U(-1,1) values, and their exact f32 values."""
+    x = (rng.random((rows, f), dtype=np.float32) * 2 - 1).astype(np.float32)
+    w = (x.view(np.uint32) >> 16).astype(np.uint16)
+    return w, (w.astype(np.uint32) << 16).view(np.float32)
+
+
+@pytest.mark.gpu
+def test_spmm_bf16_bit_exact_vs_oracle_on_widened_b():
+    import ctypes as C
+    from paper_2511_17594_b200 import _lib
+    rng = np.random.default_rng(31)
+    for m in (hub_graph(rng, 1300, [1250, 600, 300], 9), hub_graph(rng, 700, [650], 5, with_values=False)):
+        g = asb.Graph.from_csr(m)
+        for f in (1, 6, 16, 64, 100, 132):
+            w, bf = _bf16_words(rng, m.n_cols, f)
+            if f == 16:
+                w[3, 2] = 0x7F80     # +Inf: the finite scan must route to the F2F widening
+                bf = (w.astype(np.uint32) << 16).view(np.float32)
+            wd = torch.from_numpy(w.view(np.int16)).cuda()
+            c = torch.empty((m.n_rows, f), device="cuda")
+            want = oracle.spmm_baseline(m, bf)
+            for v in (None, "spmm:rowparallel:ft=64:rpc=4:vec=1:hubt=256", "spmm:rowparallel:ft=32:rpc=1:vec=0:hubt=256",
+                      "spmm:hubsplit:ft=64:rpc=1:vec=1:hubt=64", "spmm:hubsplit:ft=128:rpc=4:vec=1:hubt=400"):
+                va = None if v is None else C.byref(asb.variant_from_string(v).to_c())
+                res = asb._capi.as_kernel_result()
+                asb._check(_lib.as_spmm_bf16(va, g.handle, None, C.c_void_p(wd.data_ptr()), m.n_cols, f,
+                                             C.c_void_p(c.data_ptr()), None, C.byref(res)))
+                torch.cuda.synchronize()
+                got = c.cpu().numpy()
+                if v is not None and "hubsplit" in v:
+                    hubt = int(v.rsplit("=", 1)[1])
+                    ref = oracle.spmm_hubsplit(m, bf, hubt)
+                else:
+                    ref = want
+                assert bit_equal(got, ref), (f, v)
+        # misaligned base (2-byte offset): the scalar path
+        w, bf = _bf16_words(rng, m.n_cols + 1, 8)
+        wd = torch.from_numpy(w.view(np.int16).reshape(-1)).cuda()
+        c = torch.empty((m.n_rows, 8), device="cuda")
+        va = C.byref(asb.variant_from_string("spmm:rowparallel:ft=64:rpc=4:vec=1:hubt=256").to_c())
+        asb._check(_lib.as_spmm_bf16(va, g.handle, None, C.c_void_p(wd.data_ptr() + 2), m.n_cols, 8,
+                                     C.c_void_p(c.data_ptr()), None, None))
+        torch.cuda.synchronize()
+        shifted = bf.reshape(-1)[1:1 + m.n_cols * 8].reshape(m.n_cols, 8)
+        assert bit_equal(c.cpu().numpy(), oracle.spmm_baseline(m, shifted))
+        g.close()
+
+
+@pytest.mark.gpu
+def test_spmm_op_bf16_forward_and_grad():
+    rng = np.random.default_rng(32)
+    m = hub_graph(rng, 600, [560], 6)
+    crow, col = _t(m.rowptr.astype(np.int64)), _t(m.colind.astype(np.int32))
+    w, bf = _bf16_words(rng, m.n_cols, 64)
+    b16 = torch.from_numpy(w.view(np.int16)).cuda().view(torch.bfloat16).requires_grad_(True)
+    out = torch.ops.autosage.spmm_csr(crow, col, _t(m.val), b16, "spmm:hubsplit:ft=64:rpc=1:vec=1:hubt=256")
+    assert out.dtype == torch.float32
+    assert bit_equal(out.detach().cpu().numpy(), oracle.spmm_hubsplit(m, bf, 256))
+    out.sum().backward()
+    assert b16.grad.dtype == torch.bfloat16

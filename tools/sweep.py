@@ -13,6 +13,9 @@ c4  skew stressor: Zipf exponents 1.5 / 2.0 / 2.5 / 3.0, hubs up to 1M nnz,
     F = 16 / 64 / 128: decision, guardrail (chosen vs baseline on the full
     graph) and cache replay (a fresh context replaying the stored decisions)
 c5  CSR attention on Reddit-shape, 8 heads x F=64: fused vs unfused per head
+bwd backward pieces on Reddit-shape F=64: transpose build, dB = A^T dC, dval = SDDMM(dC, B),
+    row-softmax gradient, torch autograd of spmm_csr / csr_attention
+bf16 SpMM with a bf16 B (as_spmm_bf16) beside f32 on Reddit F=32/64/128 and Products F=100
 
 Every GPU time is CUDA events on the launching stream around `reps` launches
 (median per launch), decisions made once before timing.  Bytes are the
@@ -289,6 +292,95 @@ def case_c5(res):
                  "fused_gbs": 8 * by / (fused_ms * 1e-3) / 1e9, "heads": heads}
     del keep
     g.close()
+
+
+def case_bwd(res):
+    """Backward pass on the Reddit-shape graph at F=64."""
+    import paper_2511_17594_b200.torch_ops  # noqa: F401
+    m, _ = bench.make_graph("reddit", 1)
+    f = 64
+    dev = torch.device("cuda")
+    g = asb.Graph.from_csr(m)
+    t0 = time.perf_counter()
+    gt = g.transpose()
+    torch.cuda.synchronize()
+    t_transpose = (time.perf_counter() - t0) * 1e3
+    t1 = time.perf_counter()
+    gt2 = g.transpose()
+    torch.cuda.synchronize()
+    t_transpose_warm = (time.perf_counter() - t1) * 1e3
+    gt2.close()
+    dc = torch.from_numpy(asb.fill_uniform(m.n_rows * f, 7, (m.n_rows, f))).to(dev)
+    b = torch.from_numpy(asb.fill_uniform(m.n_cols * f, 8, (m.n_cols, f))).to(dev)
+    db = torch.empty((m.n_cols, f), dtype=torch.float32, device=dev)
+    vals = torch.from_numpy(m.val).to(dev)
+    vt = torch.empty_like(vals)
+    stream = C.c_void_p(asb.torch_stream_handle())
+    hub = asb.variant_from_string("spmm:hubsplit:ft=64:rpc=1:vec=1:hubt=256").to_c()
+    asb._check(lib.as_permute_values(gt.handle, P(vals), P(vt), stream))
+    t_perm = ev_time(lambda: asb._check(lib.as_permute_values(gt.handle, P(vals), P(vt), stream)))
+    t_db = ev_time(lambda: asb._check(lib.as_spmm_values(C.byref(hub), gt.handle, P(vt), P(dc), m.n_rows, f,
+                                                         P(db), stream, None)))
+    # softmax gradient on probabilities of the graph's own values
+    p = torch.empty_like(vals)
+    asb._check(lib.as_row_softmax(g.handle, P(vals), P(p), stream))
+    gr = torch.from_numpy(asb.fill_uniform(m.nnz, 9, (m.nnz,))).to(dev)
+    ds = torch.empty_like(vals)
+    t_sm = ev_time(lambda: asb._check(lib.as_row_softmax_backward(g.handle, P(p), P(gr), P(ds), stream)))
+    # whole autograd steps through torch.ops (graph + transpose handles cached after the first call)
+    crow = torch.from_numpy(m.rowptr.astype(np.int64)).to(dev)
+    col = torch.from_numpy(m.colind.astype(np.int32)).to(dev)
+    vg, bg = vals.clone().requires_grad_(True), b.clone().requires_grad_(True)
+    hv = "spmm:hubsplit:ft=64:rpc=1:vec=1:hubt=256"
+
+    def spmm_step():
+        vg.grad = bg.grad = None
+        torch.ops.autosage.spmm_csr(crow, col, vg, bg, hv).backward(dc)
+    t_spmm_step = ev_time(spmm_step, 3, 1)
+    q, k, v = (torch.from_numpy(asb.fill_uniform(m.n_rows * f, 20 + i, (m.n_rows, f))).to(dev).requires_grad_(True)
+               for i in range(3))
+
+    def att_step():
+        q.grad = k.grad = v.grad = None
+        torch.ops.autosage.csr_attention(crow, col, q, k, v, True).backward(dc)
+    t_att_step = ev_time(att_step, 3, 1)
+    n, nnz = m.n_rows, m.nnz
+    res["bwd"] = {"graph": {"n": n, "nnz": nnz, "F": f},
+                  "transpose_first_ms": t_transpose, "transpose_ms": t_transpose_warm,
+                  "permute_ms": t_perm, "permute_gbs": 12 * nnz / (t_perm * 1e-3) / 1e9,
+                  "spmm_t_ms": t_db, "spmm_t_gbs": gbs("spmm", n, nnz, f, t_db),
+                  "softmax_bwd_ms": t_sm, "softmax_bwd_gbs": (8 * (n + 1) + 12 * nnz) / (t_sm * 1e-3) / 1e9,
+                  "spmm_autograd_step_ms": t_spmm_step, "attention_autograd_step_ms": t_att_step}
+    gt.close()
+    g.close()
+
+
+def case_bf16(res):
+    """bf16 dense operand: the same variant on f32 and bf16 B."""
+    out = {}
+    for cfg, fs, variant in (("reddit", (32, 64, 128), "spmm:hubsplit:ft=64:rpc=1:vec=1:hubt=256"),
+                             ("products", (100,), "spmm:hubsplit:ft=64:rpc=1:vec=1:hubt=256")):
+        m, _ = bench.make_graph(cfg, 1)
+        g = asb.Graph.from_csr(m)
+        dev = torch.device("cuda")
+        stream = C.c_void_p(asb.torch_stream_handle())
+        cv = asb.variant_from_string(variant).to_c()
+        for f in fs:
+            b = torch.from_numpy(asb.fill_uniform(m.n_cols * f, 1 + f, (m.n_cols, f))).to(dev)
+            b16 = b.to(torch.bfloat16)
+            c = torch.empty((m.n_rows, f), dtype=torch.float32, device=dev)
+            t32 = ev_time(lambda: asb._check(lib.as_spmm(C.byref(cv), g.handle, P(b), m.n_cols, f, P(c), stream,
+                                                         None)))
+            t16 = ev_time(lambda: asb._check(lib.as_spmm_bf16(C.byref(cv), g.handle, None, P(b16), m.n_cols, f,
+                                                              P(c), stream, None)))
+            # bf16 gather-model bytes: the B gather term at 2 bytes per element
+            by16 = 8 * m.nnz + 2 * m.nnz * f + 4 * m.n_rows * f + 8 * (m.n_rows + 1)
+            out[f"{cfg}_F{f}"] = {"variant": variant, "f32_ms": t32, "bf16_ms": t16, "speedup": t32 / t16,
+                                  "f32_gbs": gbs("spmm", m.n_rows, m.nnz, f, t32),
+                                  "bf16_gbs": by16 / (t16 * 1e-3) / 1e9}
+            del b, b16, c
+        g.close()
+    res["bf16"] = out
 
 
 def run_meta():
