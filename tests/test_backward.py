@@ -290,7 +290,7 @@ def test_spmm_bf16_bit_exact_vs_oracle_on_widened_b():
     rng = np.random.default_rng(31)
     for m in (hub_graph(rng, 1300, [1250, 600, 300], 9), hub_graph(rng, 700, [650], 5, with_values=False)):
         g = asb.Graph.from_csr(m)
-        for f in (1, 6, 16, 64, 100, 132):
+        for f in (1, 6, 16, 64, 100, 132, 512):
             w, bf = _bf16_words(rng, m.n_cols, f)
             if f == 16:
                 w[3, 2] = 0x7F80     # +Inf: the finite scan must route to the F2F widening
@@ -299,7 +299,8 @@ def test_spmm_bf16_bit_exact_vs_oracle_on_widened_b():
             c = torch.empty((m.n_rows, f), device="cuda")
             want = oracle.spmm_baseline(m, bf)
             for v in (None, "spmm:rowparallel:ft=64:rpc=4:vec=1:hubt=256", "spmm:rowparallel:ft=32:rpc=1:vec=0:hubt=256",
-                      "spmm:hubsplit:ft=64:rpc=1:vec=1:hubt=64", "spmm:hubsplit:ft=128:rpc=4:vec=1:hubt=400"):
+                      "spmm:hubsplit:ft=64:rpc=1:vec=1:hubt=64", "spmm:hubsplit:ft=128:rpc=4:vec=1:hubt=400",
+                      "spmm:rowparallel:ft=1024:rpc=4:vec=1:hubt=256"):
                 va = None if v is None else C.byref(asb.variant_from_string(v).to_c())
                 res = asb._capi.as_kernel_result()
                 asb._check(_lib.as_spmm_bf16(va, g.handle, None, C.c_void_p(wd.data_ptr()), m.n_cols, f,
