@@ -424,6 +424,12 @@ as_status as_spmm_values(const as_variant* v, as_graph a, const float* vals_dev,
  * bytes.  v == NULL -> baseline kernel; env overrides as in dispatch. */
 as_status as_spmm_bf16(const as_variant* v, as_graph a, const float* vals_dev, const uint16_t* b_dev,
                        uint64_t b_rows, uint64_t f, float* c_dev, void* stream, as_kernel_result* res);
+/* SDDMM on bf16 X (x_rows x f) and Y (y_rows x f) words, f64 accumulation,
+ * f32 out: as_sddmm on the f32 copies of X and Y with the same variant, bit
+ * for bit (the vec order applies whenever f % 4 == 0).  v == NULL -> baseline. */
+as_status as_sddmm_bf16(const as_variant* v, as_graph pattern, const uint16_t* x_dev, uint64_t x_rows,
+                        const uint16_t* y_dev, uint64_t y_rows, uint64_t f, float* out_dev, void* stream,
+                        as_kernel_result* res);
 /* Gradient of row_softmax (src/kernels.cpp:431-461): ds = p * (g - dot),
  * dot = sum_row p*g in f64 (32 strided partials, fixed pairwise fold;
  * oracle/oracle.c orc_row_softmax_backward). */

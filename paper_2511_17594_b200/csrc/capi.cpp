@@ -686,6 +686,18 @@ as_status as_spmm_bf16(const as_variant* v, as_graph a, const float* vals_dev, c
     });
 }
 
+as_status as_sddmm_bf16(const as_variant* v, as_graph pattern, const uint16_t* x_dev, uint64_t x_rows,
+                        const uint16_t* y_dev, uint64_t y_rows, uint64_t f, float* out_dev, void* stream,
+                        as_kernel_result* res) {
+    return guard([&] {
+        Graph& g = G(pattern);
+        if (g.nnz && f && (!x_dev || !y_dev || !out_dev)) throw InvalidArgument("sddmm_bf16: null operand");
+        const KernelResult r = dispatch_sddmm_bf16(v, g, x_dev, x_rows, y_dev, y_rows, f, out_dev,
+                                                   resolve_stream(g, stream), res != nullptr);
+        fill_result(res, r);
+    });
+}
+
 as_status as_row_softmax_backward(as_graph m, const float* p_dev, const float* grad_dev, float* ds_dev,
                                   void* stream) {
     return guard([&] {

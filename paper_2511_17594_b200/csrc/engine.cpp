@@ -361,6 +361,35 @@ KernelResult dispatch_spmm_bf16(const as_variant* v, Graph& a, const float* vals
     return r;
 }
 
+// SDDMM on bf16 X and Y (raw words).  The vec flag selects the reference's
+// four-way block order (src/kernels.cpp:103-127) whenever f % 4 == 0 -- the
+// gate the f32 copies of X and Y would pass -- so the result is as_sddmm on
+// float(X), float(Y) with the same variant, bit for bit.
+KernelResult dispatch_sddmm_bf16(const as_variant* v, Graph& p, const std::uint16_t* x, std::uint64_t x_rows,
+                                 const std::uint16_t* y, std::uint64_t y_rows, std::uint64_t f, float* out,
+                                 cudaStream_t s, bool timed) {
+    check_sddmm_dims(p, x_rows, y_rows);
+    KernelResult r;
+    if (v) {
+        if (v->op != AS_OP_SDDMM) throw InvalidArgument("dispatch: sddmm operands given to a non-sddmm variant");
+        r.variant = apply_env_overrides(*v);
+        check_variant(r.variant);
+    } else {
+        r.variant = default_variant();
+        r.variant.op = AS_OP_SDDMM;
+        r.variant.mapping = AS_MAP_BASELINE;
+    }
+    const bool baseline = r.variant.mapping == AS_MAP_BASELINE;
+    const int ord = !baseline && r.variant.vectorized && f > 0 && f % 4 == 0 ? 1 : 0;
+    const std::uint32_t ft = std::uint32_t(baseline ? std::max<std::uint64_t>(f, 1) : effective_tile(r.variant.f_tile, f));
+    DeviceGuard dg(p.device);
+    TimedRegion tr(s, timed);
+    launch_sddmm_bf16(p, x, y, std::uint32_t(f), out, ft, ord, baseline, s);
+    r.elapsed_ms = tr.stop();
+    r.vectorized_path = ord == 1;
+    return r;
+}
+
 void sddmm_baseline(Graph& p, const float* x, std::uint64_t x_rows, const float* y,
                     std::uint64_t y_rows, std::uint64_t f, float* out, cudaStream_t s) {
     check_sddmm_dims(p, x_rows, y_rows);

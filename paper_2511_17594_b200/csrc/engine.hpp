@@ -36,6 +36,10 @@ KernelResult dispatch_spmm(const as_variant& v, Graph& a, const float* vals, con
 // SpMM with bf16 B words (v == nullptr: baseline); the f32 result on float(B).
 KernelResult dispatch_spmm_bf16(const as_variant* v, Graph& a, const float* vals, const std::uint16_t* b,
                                 std::uint64_t b_rows, std::uint64_t f, float* c, cudaStream_t s, bool timed);
+// SDDMM on bf16 X, Y words (v == nullptr: baseline); the f32 result on float(X), float(Y).
+KernelResult dispatch_sddmm_bf16(const as_variant* v, Graph& p, const std::uint16_t* x, std::uint64_t x_rows,
+                                 const std::uint16_t* y, std::uint64_t y_rows, std::uint64_t f, float* out,
+                                 cudaStream_t s, bool timed);
 void sddmm_baseline(Graph& p, const float* x, std::uint64_t x_rows, const float* y,
                     std::uint64_t y_rows, std::uint64_t f, float* out, cudaStream_t s);
 // sddmm_rowparallel (src/kernels.cpp:357-429): variant as given, no env.

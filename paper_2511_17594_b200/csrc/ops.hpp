@@ -53,6 +53,11 @@ void sddmm_chunks_prepare(Graph& g, const float* x, const float* y, std::uint32_
                           std::uint64_t f_tile, bool vec, cudaStream_t s, const unsigned* finite,
                           std::uint64_t r0 = 0, std::uint64_t r1 = ~0ull);
 
+// SDDMM on bf16 X, Y (raw words): ord 0 sequential, 1 the four-way vec blocks
+// of width ft; baseline = the direct kernel (guardrail mapping)
+void launch_sddmm_bf16(Graph& g, const std::uint16_t* x, const std::uint16_t* y, std::uint32_t f, float* out,
+                       std::uint32_t ft, int ord, bool baseline, cudaStream_t s);
+
 // Device flag: 1 iff p[0..n) has no Inf/NaN (gates the re-bias widening,
 // widen.cuh).  Written into g.flag (one flag per graph; a graph handle runs
 // one operator at a time).

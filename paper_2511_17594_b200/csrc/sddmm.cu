@@ -56,11 +56,17 @@ __device__ __forceinline__ X4 load_x4(const double* p) {
 }
 __device__ __forceinline__ double x_at(const float* p, std::uint32_t t) { return double(p[t]); }
 __device__ __forceinline__ double x_at(const double* p, std::uint32_t t) { return p[t]; }
+// bf16 operands (raw 16-bit words): bf16 -> f32 is exact, so every product
+// is the f32 path's on float(X), float(Y)
+__device__ __forceinline__ float bf16f(unsigned short h) { return __uint_as_float(unsigned(h) << 16); }
+__device__ __forceinline__ double x_at(const unsigned short* p, std::uint32_t t) { return double(bf16f(p[t])); }
+__device__ __forceinline__ float y_at(const float* p, std::uint32_t t) { return p[t]; }
+__device__ __forceinline__ float y_at(const unsigned short* p, std::uint32_t t) { return bf16f(p[t]); }
 
 // Sequential dot over [0, f): VLDS uses 16-byte reads (f % 4 == 0, both
 // pointers 16-byte aligned).
-template <bool VLDS, int MIX, class XT>
-__device__ __forceinline__ double dot_seq(const XT* xr, const float* yr, std::uint32_t f) {
+template <bool VLDS, int MIX, class XT, class YT>
+__device__ __forceinline__ double dot_seq(const XT* xr, const YT* yr, std::uint32_t f) {
     double acc = 0.0;
     if constexpr (VLDS) {
 #pragma unroll 4
@@ -74,14 +80,14 @@ __device__ __forceinline__ double dot_seq(const XT* xr, const float* yr, std::ui
         }
     } else {
 #pragma unroll 4
-        for (std::uint32_t t = 0; t < f; ++t) acc = dfma(x_at(xr, t), yr[t], acc);
+        for (std::uint32_t t = 0; t < f; ++t) acc = dfma(x_at(xr, t), y_at(yr, t), acc);
     }
     return acc;
 }
 
 // src/kernels.cpp:103-127 vec path.  VLDS requires ft % 4 == 0 too.
-template <bool VLDS, int MIX, class XT>
-__device__ __forceinline__ double dot_vec4blk(const XT* xr, const float* yr, std::uint32_t f,
+template <bool VLDS, int MIX, class XT, class YT>
+__device__ __forceinline__ double dot_vec4blk(const XT* xr, const YT* yr, std::uint32_t f,
                                               std::uint32_t ft) {
     double acc = 0.0;
     for (std::uint32_t b0 = 0; b0 < f; b0 += ft) {
@@ -98,7 +104,8 @@ __device__ __forceinline__ double dot_vec4blk(const XT* xr, const float* yr, std
                 y = *reinterpret_cast<const float4*>(yr + b0 + t);
             } else {
                 x = {x_at(xr, b0 + t), x_at(xr, b0 + t + 1), x_at(xr, b0 + t + 2), x_at(xr, b0 + t + 3)};
-                y = make_float4(yr[b0 + t], yr[b0 + t + 1], yr[b0 + t + 2], yr[b0 + t + 3]);
+                y = make_float4(y_at(yr, b0 + t), y_at(yr, b0 + t + 1), y_at(yr, b0 + t + 2),
+                                y_at(yr, b0 + t + 3));
             }
             a0 = dfma(x.a, y.x, a0);
             a1 = dfma(x.b, y.y, a1);
@@ -106,14 +113,14 @@ __device__ __forceinline__ double dot_vec4blk(const XT* xr, const float* yr, std
             a3 = dfma_r<MIX>(x.d, y.w, a3);
         }
         double tail = 0.0;
-        for (; t < fw; ++t) tail = dfma(x_at(xr, b0 + t), yr[b0 + t], tail);
+        for (; t < fw; ++t) tail = dfma(x_at(xr, b0 + t), y_at(yr, b0 + t), tail);
         acc = __dadd_rn(acc, __dadd_rn(__dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3)), tail));
     }
     return acc;
 }
 
-template <int ORD, bool VLDS, int MIX, class XT>
-__device__ __forceinline__ double dot_ord(const XT* xr, const float* yr, std::uint32_t f,
+template <int ORD, bool VLDS, int MIX, class XT, class YT>
+__device__ __forceinline__ double dot_ord(const XT* xr, const YT* yr, std::uint32_t f,
                                           std::uint32_t ft) {
     if constexpr (ORD == 0) return dot_seq<VLDS, MIX>(xr, yr, f);
     else return dot_vec4blk<VLDS, MIX>(xr, yr, f, ft);
@@ -285,6 +292,21 @@ __global__ void widen_kernel(const float4* __restrict__ x, double2* __restrict__
         const float4 v = __ldg(x + i);
         xd[2 * i] = make_double2(double(v.x) * up01, double(v.y) * up01);
         xd[2 * i + 1] = make_double2(double(v.z) * up, double(v.w) * up);
+    }
+}
+
+// bf16 X (4 words per uint2) -> f64, the same layout and scaling
+__global__ void widen_bf16_kernel(const uint2* __restrict__ x, double2* __restrict__ xd, std::uint64_t n4,
+                                  const unsigned* __restrict__ finite, int mix_all) {
+    const double up = (finite && *finite) ? kWidenUp : 1.0;
+    const double up01 = mix_all ? up : 1.0;
+    for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+         i += std::uint64_t(gridDim.x) * blockDim.x) {
+        const uint2 v = __ldg(x + i);
+        const float a = __uint_as_float(v.x << 16), b = __uint_as_float(v.x & 0xffff0000u);
+        const float c = __uint_as_float(v.y << 16), d = __uint_as_float(v.y & 0xffff0000u);
+        xd[2 * i] = make_double2(double(a) * up01, double(b) * up01);
+        xd[2 * i + 1] = make_double2(double(c) * up, double(d) * up);
     }
 }
 
@@ -668,23 +690,45 @@ __global__ void __launch_bounds__(128, 3)
 
 // Single-pass F in {32, 64}: the same pair mapping with F compiled in (this
 // specialisation measured 6% faster than the pass loop at F = 64).
-template <int F>
+// BF: Y rows staged as bf16 (half the cp.async and LDS wavefronts; one
+// 16-byte unit holds 8 features)
+template <int F, bool BF = false>
 struct Pair1Shape {
-    static constexpr int NV = F / 4;
-    static constexpr int kCopies = 2 * NV;  // cp.async per lane per chunk (64 rows)
-    static constexpr int KX = 2;            // X rows staged
+    static constexpr int kYElem = BF ? 2 : 4;
+    static constexpr int NV = F * kYElem / 16;  // 16-byte units per Y row
+    static constexpr int kCopies = 2 * NV;      // cp.async per lane per chunk (64 rows)
+    static constexpr int KX = 2;                // X rows staged
     static constexpr int kXUnits = KX * F / 2;
-    static constexpr std::uint64_t kYBytes = 64ull * F * 4;
+    static constexpr std::uint64_t kYBytes = 64ull * F * kYElem;
     static constexpr std::uint64_t kWarpBytes = kYBytes + std::uint64_t(KX) * F * 8;
 };
 
-template <int F, int ORD, int FT, bool XS, int MIX, bool SAME>
+// Y features [t, t+4) of the lane's two rows as f32 (u for entry a, w for b)
+template <int F, bool BF>
+__device__ __forceinline__ void pair1_y4(const void* ya, const void* yb, int ka, int kb, int t, float4& u,
+                                         float4& w) {
+    if constexpr (BF) {
+        const unsigned short* pa = static_cast<const unsigned short*>(ya);
+        const unsigned short* pb = static_cast<const unsigned short*>(yb);
+        const uint2 ua = *reinterpret_cast<const uint2*>(pa + 8 * ((t >> 3) ^ ka) + (t & 4));
+        const uint2 wb = *reinterpret_cast<const uint2*>(pb + 8 * ((t >> 3) ^ kb) + (t & 4));
+        u = make_float4(__uint_as_float(ua.x << 16), __uint_as_float(ua.x & 0xffff0000u),
+                        __uint_as_float(ua.y << 16), __uint_as_float(ua.y & 0xffff0000u));
+        w = make_float4(__uint_as_float(wb.x << 16), __uint_as_float(wb.x & 0xffff0000u),
+                        __uint_as_float(wb.y << 16), __uint_as_float(wb.y & 0xffff0000u));
+    } else {
+        u = *reinterpret_cast<const float4*>(static_cast<const float*>(ya) + 4 * ((t >> 2) ^ ka));
+        w = *reinterpret_cast<const float4*>(static_cast<const float*>(yb) + 4 * ((t >> 2) ^ kb));
+    }
+}
+
+template <int F, int ORD, int FT, bool XS, int MIX, bool SAME, bool BF = false>
 __device__ __forceinline__ void pair1_pass(const double* __restrict__ xa, const double* __restrict__ xb,
-                                          const float* ya, const float* yb, int ka, int kb, double (&c)[2][5]) {
+                                          const void* ya, const void* yb, int ka, int kb, double (&c)[2][5]) {
 #pragma unroll 4
     for (int t = 0; t < F; t += 4) {
-        const float4 u = *reinterpret_cast<const float4*>(ya + 4 * ((t >> 2) ^ ka));
-        const float4 w = *reinterpret_cast<const float4*>(yb + 4 * ((t >> 2) ^ kb));
+        float4 u, w;
+        pair1_y4<F, BF>(ya, yb, ka, kb, t, u, w);
         const double2 x01 = ld_x2<XS>(xa + t);
         const double2 x23 = ld_x2<XS>(xa + t + 2);
         double2 z01 = x01, z23 = x23;
@@ -719,17 +763,20 @@ __device__ __forceinline__ void pair1_pass(const double* __restrict__ xa, const 
     }
 }
 
-template <int F, int ORD, int FT, int MIX>
+template <int F, int ORD, int FT, int MIX, bool BF = false>
 __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict__ rowptr,
                                                 const std::uint32_t* __restrict__ colind,
                                                 const std::uint32_t* __restrict__ chunk_row, std::uint64_t n_rows,
-                                                const double* __restrict__ xd, const float* __restrict__ y,
+                                                const double* __restrict__ xd, const void* __restrict__ yv,
                                                 float* __restrict__ out, std::uint64_t nnz, std::uint64_t c_begin,
                                                 std::uint64_t c_end) {
-    using Sh = Pair1Shape<F>;
+    using Sh = Pair1Shape<F, BF>;
+    using YT = typename std::conditional<BF, unsigned short, float>::type;
+    constexpr int kUnitElems = 16 / Sh::kYElem;  // Y elements per 16-byte unit
+    const YT* __restrict__ y = static_cast<const YT*>(yv);
     extern __shared__ __align__(16) char smem[];
     char* wsm = smem + std::uint64_t(threadIdx.x >> 5) * Sh::kWarpBytes;
-    float* ys = reinterpret_cast<float*>(wsm);
+    YT* ys = reinterpret_cast<YT*>(wsm);
     double* xs = reinterpret_cast<double*>(wsm + Sh::kYBytes);
     const int lane = threadIdx.x & 31;
     const std::uint64_t e_end = min(c_end * 32, nnz);
@@ -760,7 +807,7 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
             const int idx = it * 32 + lane;
             const int j = idx / Sh::NV, q = idx % Sh::NV;
             const std::uint32_t cj = __shfl_sync(FULL, j < 32 ? cur.ca : cur.cb, j & 31);
-            cp_async16(ys + j * F + 4 * (q ^ swz<Sh::NV>(j)), y + std::uint64_t(cj) * F + 4 * q);
+            cp_async16(ys + j * F + kUnitElems * (q ^ swz<Sh::NV>(j)), y + std::uint64_t(cj) * F + kUnitElems * q);
         }
 #pragma unroll
         for (int u = lane; u < Sh::kXUnits; u += 32) {
@@ -790,18 +837,18 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
         __syncwarp();
         const std::uint32_t rela = ra - cur.r_first, relb = rb - cur.r_first;
         double c[2][5] = {{0.0, 0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0, 0.0}};
-        const float* ya = ys + lane * F;
-        const float* yb = ys + (lane + 32) * F;
+        const YT* ya = ys + lane * F;
+        const YT* yb = ys + (lane + 32) * F;
         const int ka = swz<Sh::NV>(lane), kb = swz<Sh::NV>(lane + 32);
         const bool all_same = __all_sync(FULL, rela == relb);  // warp-uniform, before the split
         if (rela < Sh::KX && relb < Sh::KX) {
             if (all_same)
-                pair1_pass<F, ORD, FT, true, MIX, true>(xs + rela * F, xs + relb * F, ya, yb, ka, kb, c);
+                pair1_pass<F, ORD, FT, true, MIX, true, BF>(xs + rela * F, xs + relb * F, ya, yb, ka, kb, c);
             else
-                pair1_pass<F, ORD, FT, true, MIX, false>(xs + rela * F, xs + relb * F, ya, yb, ka, kb, c);
+                pair1_pass<F, ORD, FT, true, MIX, false, BF>(xs + rela * F, xs + relb * F, ya, yb, ka, kb, c);
         } else {
-            pair1_pass<F, ORD, FT, false, MIX, false>(xd + std::uint64_t(ra) * F, xd + std::uint64_t(rb) * F, ya,
-                                                     yb, ka, kb, c);
+            pair1_pass<F, ORD, FT, false, MIX, false, BF>(xd + std::uint64_t(ra) * F, xd + std::uint64_t(rb) * F,
+                                                         ya, yb, ka, kb, c);
         }
         if (ea < e_end) out[ea] = float(c[0][0]);
         if (eb < e_end) out[eb] = float(c[1][0]);
@@ -810,34 +857,34 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
     }
 }
 
-template <int F, int ORD, int FT>
+template <int F, int ORD, int FT, bool BF = false>
 __global__ void __launch_bounds__(128, 3)
     sddmm_pair1_kernel(const std::uint64_t* __restrict__ rowptr, const std::uint32_t* __restrict__ colind,
                       const std::uint32_t* __restrict__ chunk_row, std::uint64_t n_rows,
-                      const double* __restrict__ xd, const float* __restrict__ y, float* __restrict__ out,
+                      const double* __restrict__ xd, const void* __restrict__ y, float* __restrict__ out,
                       std::uint64_t nnz, std::uint32_t /*f*/, std::uint64_t c_begin, std::uint64_t c_end,
                       const unsigned* __restrict__ finite, int /*mix_all*/) {
     if (finite && *finite)
-        sddmm_pair1_body<F, ORD, FT, 1>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin, c_end);
+        sddmm_pair1_body<F, ORD, FT, 1, BF>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin, c_end);
     else
-        sddmm_pair1_body<F, ORD, FT, 0>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin, c_end);
+        sddmm_pair1_body<F, ORD, FT, 0, BF>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin, c_end);
 }
 
 // Guardrail baseline / large-F fallback: lane per entry, both rows read
 // straight from global memory, scalar loads.
-template <int ORD>
+template <int ORD, class T = float>
 __global__ void sddmm_direct_kernel(const std::uint64_t* __restrict__ rowptr,
                                     const std::uint32_t* __restrict__ colind,
                                     const std::uint32_t* __restrict__ chunk_row,
-                                    const float* __restrict__ x, const float* __restrict__ y,
+                                    const T* __restrict__ x, const T* __restrict__ y,
                                     float* __restrict__ out, std::uint64_t nnz, std::uint64_t c_begin,
                                     std::uint64_t c_end, std::uint32_t f, std::uint32_t ft) {
     const std::uint64_t ch = c_begin + ((std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
     const std::uint64_t e = ch * 32 + (threadIdx.x & 31);
     if (ch >= c_end || e >= nnz) return;
     const std::uint32_t r = row_of(rowptr, chunk_row[ch], e);
-    const float* xr = x + std::uint64_t(r) * f;
-    const float* yr = y + std::uint64_t(colind[e]) * f;
+    const T* xr = x + std::uint64_t(r) * f;
+    const T* yr = y + std::uint64_t(colind[e]) * f;
     out[e] = float(dot_ord<ORD, false, 0>(xr, yr, f, ft));
 }
 
@@ -1077,6 +1124,72 @@ void launch_sddmm_chunks(Graph& g, const float* x, const float* y, std::uint32_t
         if (ord == 0) go(sddmm_chunk_kernel<false, 0, false>);
         else go(sddmm_chunk_kernel<false, 1, false>);
     }
+}
+
+// SDDMM on bf16 X and Y: the pair kernel with bf16 Y staging
+// for F in {32, 64} (16-byte aligned operands, blocks that line up), the
+// direct kernel otherwise.  ord/ft as in launch_sddmm_chunks; the result is
+// the f32 SDDMM on float(X), float(Y) bit for bit.
+void launch_sddmm_bf16(Graph& g, const std::uint16_t* x, const std::uint16_t* y, std::uint32_t f, float* out,
+                       std::uint32_t ft, int ord, bool baseline, cudaStream_t s) {
+    if (g.nnz == 0) return;
+    ensure_chunk_rows(g);
+    const std::uint64_t c_end = (g.nnz + 31) / 32;
+    if (f == 0) {
+        ASB_CUDA(cudaMemsetAsync(out, 0, g.nnz * 4, s));
+        return;
+    }
+    const auto* xs = reinterpret_cast<const unsigned short*>(x);
+    const auto* ys = reinterpret_cast<const unsigned short*>(y);
+    const bool pair_ok = !baseline && (f == 32 || f == 64) && aligned16(x) && aligned16(y) &&
+                         (ord == 0 || ft >= f || ft == 32) && dev_knob("AUTOSAGE_DEV_SDDMM_PAIR", 1);
+    if (!pair_ok) {
+        const unsigned blocks = unsigned((c_end * 32 + 255) / 256);
+        if (ord == 0)
+            sddmm_direct_kernel<0><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), g.chunk_row.get(), xs, ys,
+                                                          out, g.nnz, 0, c_end, f, ft);
+        else
+            sddmm_direct_kernel<1><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), g.chunk_row.get(), xs, ys,
+                                                          out, g.nnz, 0, c_end, f, ft);
+        check_launch("sddmm_direct_kernel");
+        return;
+    }
+    const unsigned* fin = nullptr;
+    if (dev_knob("AUTOSAGE_DEV_SDDMM_MIX", 1) && g.n_cols * f * 2 <= (std::uint64_t(96) << 20))
+        fin = finite_flag_bf16(g, ys, g.n_cols * f, s);
+    g.xwide.ensure(std::max<std::uint64_t>(g.n_rows * f, 1));
+    const std::uint64_t n4 = g.n_rows * f / 4;
+    if (n4) {
+        const unsigned wb = unsigned(std::min<std::uint64_t>((n4 + 255) / 256, std::uint64_t(sm_count()) * 8));
+        widen_bf16_kernel<<<std::max(wb, 1u), 256, 0, s>>>(reinterpret_cast<const uint2*>(x),
+                                                           reinterpret_cast<double2*>(g.xwide.get()), n4, fin,
+                                                           mix_all());
+        check_launch("widen_bf16_kernel");
+    }
+    const int sms = sm_count();
+    auto pair1 = [&](auto fc) {
+        constexpr int F = decltype(fc)::value;
+        const std::uint64_t wbytes = Pair1Shape<F, true>::kWarpBytes;
+        const int kWarps = 4;
+        auto run = [&](auto kernel) {
+            const std::size_t smem = std::size_t(wbytes * kWarps);
+            ASB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            int per_sm = 1;
+            ASB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kWarps * 32, smem));
+            const std::uint64_t pairs = (c_end + 1) / 2;
+            const std::uint64_t want = (pairs + kWarps - 1) / kWarps;
+            const std::uint64_t cap = std::uint64_t(sms) * std::max(per_sm, 1);
+            const unsigned blocks = unsigned(std::max<std::uint64_t>(1, std::min(want, cap)));
+            kernel<<<blocks, kWarps * 32, smem, s>>>(g.rowptr.get(), g.colind.get(), g.chunk_row.get(), g.n_rows,
+                                                     g.xwide.get(), y, out, g.nnz, f, 0, c_end, fin, mix_all());
+            check_launch("sddmm_pair_kernel");
+        };
+        if (ord == 0) run(sddmm_pair1_kernel<F, 0, 0, true>);
+        else if (ft >= f) run(sddmm_pair1_kernel<F, 1, 0, true>);
+        else run(sddmm_pair1_kernel<F, 1, 32, true>);
+    };
+    if (f == 32) pair1(std::integral_constant<int, 32>{});
+    else pair1(std::integral_constant<int, 64>{});
 }
 
 } // namespace asb

@@ -338,3 +338,38 @@ def test_spmm_op_bf16_forward_and_grad():
     assert bit_equal(out.detach().cpu().numpy(), oracle.spmm_hubsplit(m, bf, 256))
     out.sum().backward()
     assert b16.grad.dtype == torch.bfloat16
+
+
+@pytest.mark.gpu
+def test_sddmm_bf16_bit_exact_vs_oracle_on_widened_operands():
+    import ctypes as C
+    from paper_2511_17594_b200 import _lib
+    rng = np.random.default_rng(33)
+    for m in (hub_graph(rng, 1100, [1000, 400], 9, with_values=False), random_csr(rng, 500, 700, 40)):
+        g = asb.Graph.from_csr(m.with_values(None))
+        for f in (1, 12, 32, 64, 80):
+            wx, bx = _bf16_words(rng, m.n_rows, f)
+            wy, by = _bf16_words(rng, m.n_cols, f)
+            if f == 64:
+                wy[5, 7] = 0x7FC0    # NaN in Y: the F2F widening path, NaN propagates
+                by = (wy.astype(np.uint32) << 16).view(np.float32)
+            xd = torch.from_numpy(wx.view(np.int16)).cuda()
+            yd = torch.from_numpy(wy.view(np.int16)).cuda()
+            out = torch.empty(max(m.nnz, 1), device="cuda")
+            for v in (None, "sddmm:rowparallel:ft=32:rpc=1:vec=0:hubt=256", "sddmm:rowparallel:ft=32:rpc=4:vec=1:hubt=256",
+                      "sddmm:hubsplit:ft=64:rpc=4:vec=1:hubt=256", "sddmm:rowparallel:ft=128:rpc=1:vec=1:hubt=256"):
+                va = None if v is None else C.byref(asb.variant_from_string(v).to_c())
+                asb._check(_lib.as_sddmm_bf16(va, g.handle, C.c_void_p(xd.data_ptr()), m.n_rows,
+                                              C.c_void_p(yd.data_ptr()), m.n_cols, f, C.c_void_p(out.data_ptr()),
+                                              None, None))
+                torch.cuda.synchronize()
+                if v is None:
+                    want = oracle.sddmm(m, bx, by, f, False)
+                else:
+                    var = asb.variant_from_string(v)
+                    want = oracle.sddmm(m, bx, by, var.f_tile, var.vectorized and f % 4 == 0)
+                got = out.cpu().numpy()[:m.nnz]
+                nan = np.isnan(want)
+                assert np.array_equal(np.isnan(got), nan), (f, v)   # NaN payloads are not compared
+                assert bit_equal(got[~nan], want[~nan]), (f, v)
+        g.close()

@@ -90,6 +90,23 @@ def main():
               f"| fused kernel | {c['fused_ms_8_heads']:.2f} | {c['fused_ms_8_heads'] / 8:.2f} |",
               f"| unfused (SDDMM → softmax → SpMM) | {c['unfused_ms_8_heads']:.2f} | "
               f"{c['unfused_ms_8_heads'] / 8:.2f} |", ""]
+    if "bwd" in r:
+        b = r["bwd"]
+        g = b["graph"]
+        L += [f"## bwd — backward pieces, Reddit-shape N={g['n']} nnz={g['nnz']}, F={g['F']}", "",
+              "| piece | ms | note |", "|---|---|---|",
+              f"| transpose (first / repeat, one-time setup) | {b['transpose_first_ms']:.1f} / {b['transpose_ms']:.1f} | host wall clock |",
+              f"| permute values into Aᵀ order | {f3(b['permute_ms'])} | {b['permute_gbs']:.0f} GB/s (12 B/entry) |",
+              f"| Aᵀ·dC SpMM (hubsplit ft=64) | {f3(b['spmm_t_ms'])} | {b['spmm_t_gbs']:.0f} GB/s gather-model |",
+              f"| row-softmax gradient | {f3(b['softmax_bwd_ms'])} | {b['softmax_bwd_gbs']:.0f} GB/s (8(N+1) + 12·nnz) |",
+              f"| spmm_csr forward + backward (torch) | {b['spmm_autograd_step_ms']:.2f} | |",
+              f"| csr_attention fused forward + backward (torch) | {b['attention_autograd_step_ms']:.2f} | |", ""]
+    if "bf16" in r:
+        L += ["## bf16 — SpMM with a bf16 B (as_spmm_bf16) vs f32 B, same variant", "",
+              "| case | variant | f32 ms | bf16 ms | speed-up |", "|---|---|---|---|---|"]
+        for k, e in r["bf16"].items():
+            L.append(f"| {k} | `{e['variant']}` | {f3(e['f32_ms'])} | {f3(e['bf16_ms'])} | {e['speedup']:.2f} |")
+        L.append("")
     out = os.path.join(ROOT, "profiles", f"{tag}_sweep.md")
     with open(out, "w") as fh:
         fh.write("\n".join(L) + "\n")
