@@ -452,19 +452,19 @@ void orc_transpose(const uint64_t* rowptr, const uint32_t* colind, uint64_t n_ro
 
 /* Gradient of row_softmax (src/kernels.cpp:431-461): with p = softmax(s) and
  * upstream g, ds[e] = p[e] * (g[e] - sum_row p*g).  The products f64(p)*f64(g)
- * are exact; they are summed in a fixed order chosen for a warp per row (the
- * reference defines none): 32 strided partials (partial l takes the row's
- * entries l, l+32, l+64, ... in order), folded pairwise part[l] += part[l+o]
- * for o = 16, 8, 4, 2, 1.  ds = f32(f64(p) * (f64(g) - dot)).  Empty rows
+ * are exact; they are summed in a fixed order chosen for the GPU (the
+ * reference defines none): 256 strided partials (partial l takes the row's
+ * entries l, l+256, l+512, ... in order), folded pairwise part[l] += part[l+o]
+ * for o = 128, 64, ..., 1.  ds = f32(f64(p) * (f64(g) - dot)).  Empty rows
  * untouched. */
 void orc_row_softmax_backward(const uint64_t* rowptr, uint64_t n_rows, const float* p,
                               const float* g, float* ds) {
     for (uint64_t i = 0; i < n_rows; ++i) {
         const uint64_t e0 = rowptr[i], e1 = rowptr[i + 1];
-        double part[32];
-        for (int l = 0; l < 32; ++l) part[l] = 0.0;
-        for (uint64_t e = e0; e < e1; ++e) part[(e - e0) & 31] += (double)p[e] * (double)g[e];
-        for (int o = 16; o > 0; o >>= 1)
+        double part[256];
+        for (int l = 0; l < 256; ++l) part[l] = 0.0;
+        for (uint64_t e = e0; e < e1; ++e) part[(e - e0) & 255] += (double)p[e] * (double)g[e];
+        for (int o = 128; o > 0; o >>= 1)
             for (int l = 0; l < o; ++l) part[l] += part[l + o];
         const double dot = part[0];
         for (uint64_t e = e0; e < e1; ++e) ds[e] = (float)((double)p[e] * ((double)g[e] - dot));

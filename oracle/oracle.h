@@ -124,7 +124,7 @@ void orc_partition_rows(const uint64_t* rowptr, uint64_t n_rows, uint32_t g, uin
 void orc_transpose(const uint64_t* rowptr, const uint32_t* colind, uint64_t n_rows,
                    uint64_t n_cols, uint64_t* rowptr_t, uint32_t* colind_t, uint32_t* perm);
 /* d row_softmax (src/kernels.cpp:431-461): ds = f32(p * (g - dot)), dot =
- * 32 strided f64 partials of f64(p)*f64(g) folded in a fixed pairwise tree. */
+ * 256 strided f64 partials of f64(p)*f64(g) folded in a fixed pairwise tree. */
 void orc_row_softmax_backward(const uint64_t* rowptr, uint64_t n_rows, const float* p,
                               const float* g, float* ds);
 

@@ -14,11 +14,11 @@
 // library passes rather than a hand-fused kernel: every pass is a coalesced
 // stream except the sort's scatter and the fill's two gathers.
 //
-// Softmax backward: HBM-bound (12 B per entry + 8 B per row).  Warp per row
-// in degree-descending order (hub rows start first); each lane keeps a
-// strided f64 partial of the exact products f64(p)*f64(g), the 32 partials
-// fold in a fixed xor tree, so the sum is deterministic and equals
-// oracle/oracle.c orc_row_softmax_backward bit for bit.
+// Softmax backward: HBM-bound (12 B per entry + 8 B per row).  The exact
+// products f64(p)*f64(g) are summed as 256 strided partials folded in a fixed
+// tree, so the sum is deterministic and equals oracle/oracle.c
+// orc_row_softmax_backward bit for bit; a warp per row (eight chains per lane)
+// or, for rows of >= 4096 entries, a CTA per row (one chain per thread).
 #include "graph.hpp"
 #include "ops.hpp"
 
@@ -80,8 +80,36 @@ __global__ void permute_kernel(const float* __restrict__ src, const std::uint32_
         dst[k] = src[perm[k]];
 }
 
-// ds[e] = f32(f64(p) * (f64(g) - dot)), dot = xor-tree fold of 32 strided
-// partials (lane l sums entries e0 + l, e0 + l + 32, ... in order).
+// Softmax gradient.  dot = the fixed fold of 256 strided partials (partial
+// l sums entries e0 + l, e0 + l + 256, ... in order; then part[l] +=
+// part[l + o] for o = 128 .. 1), the order oracle/oracle.c restates.
+//
+// Warp kernel: lane l owns partials l + 32j, j = 0..7 -- eight independent
+// f64 chains and 16 loads in flight per lane; the o = 128, 64, 32 steps of
+// the fold are inside the lane, o = 16 .. 1 are xor shuffles (lane 0 then
+// holds the oracle's association).
+__device__ __forceinline__ void sbw_fma(double& part, float p, float g) {
+    part = __dadd_rn(part, __dmul_rn(double(p), double(g)));
+}
+
+__device__ __forceinline__ void sbw_write(const float* __restrict__ p, const float* __restrict__ g,
+                                          float* __restrict__ ds, std::uint64_t k0, std::uint64_t e1,
+                                          std::uint64_t step, double dot) {
+    std::uint64_t k = k0;
+    for (; k + 3 * step < e1; k += 4 * step) {
+        float pv[4], gv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            pv[u] = p[k + u * step];
+            gv[u] = g[k + u * step];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            ds[k + u * step] = float(__dmul_rn(double(pv[u]), __dsub_rn(double(gv[u]), dot)));
+    }
+    for (; k < e1; k += step) ds[k] = float(__dmul_rn(double(p[k]), __dsub_rn(double(g[k]), dot)));
+}
+
 __global__ void __launch_bounds__(256)
 softmax_backward_kernel(const std::uint64_t* __restrict__ rowptr, const std::uint32_t* __restrict__ order,
                         std::uint64_t n_rows, const float* __restrict__ p, const float* __restrict__ g,
@@ -92,40 +120,78 @@ softmax_backward_kernel(const std::uint64_t* __restrict__ rowptr, const std::uin
         const std::uint32_t row = order[w];
         const std::uint64_t e0 = rowptr[row], e1 = rowptr[row + 1];
         if (e0 == e1) continue;
-        double part = 0.0;
-        std::uint64_t e = e0 + lane;
-        // four entries (eight loads) in flight per lane; the chain order stays
-        // e, e+32, e+64, ...
-        for (; e + 96 < e1; e += 128) {
+        double part[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        std::uint64_t base = e0;
+        for (; base + 256 <= e1; base += 256) {
+            float pv[8], gv[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                pv[j] = __ldg(p + base + 32 * j + lane);
+                gv[j] = __ldg(g + base + 32 * j + lane);
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) sbw_fma(part[j], pv[j], gv[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const std::uint64_t k = base + 32 * j + lane;
+            if (k < e1) sbw_fma(part[j], __ldg(p + k), __ldg(g + k));
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) part[j] = __dadd_rn(part[j], part[j + 4]);  // o = 128
+#pragma unroll
+        for (int j = 0; j < 2; ++j) part[j] = __dadd_rn(part[j], part[j + 2]);  // o = 64
+        double v = __dadd_rn(part[0], part[1]);                                // o = 32
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+        const double dot = __shfl_sync(0xffffffffu, v, 0);
+        sbw_write(p, g, ds, e0 + lane, e1, 32, dot);  // the row was just read: L2 hits
+    }
+}
+
+// CTA kernel for long rows (the first rows of the degree-descending order):
+// warp w of 8 owns partials 32w + lane, so each chain has deg/256 terms; the
+// o = 128, 64, 32 steps combine warps through shared memory in the same
+// tree, o = 16 .. 1 are shuffles in warp 0.
+__global__ void __launch_bounds__(256)
+softmax_backward_cta_kernel(const std::uint64_t* __restrict__ rowptr, const std::uint32_t* __restrict__ order,
+                            std::uint64_t n_long, const float* __restrict__ p, const float* __restrict__ g,
+                            float* __restrict__ ds) {
+    __shared__ double sp[256];
+    __shared__ double sdot;
+    const int t = threadIdx.x;
+    for (std::uint64_t r = blockIdx.x; r < n_long; r += gridDim.x) {
+        const std::uint32_t row = order[r];
+        const std::uint64_t e0 = rowptr[row], e1 = rowptr[row + 1];
+        double a = 0.0;  // partial t: one chain per thread, loads unrolled ahead of it
+        std::uint64_t k = e0 + t;
+        for (; k + 3 * 256 < e1; k += 4 * 256) {
             float pv[4], gv[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                pv[u] = __ldg(p + e + 32 * u);
-                gv[u] = __ldg(g + e + 32 * u);
+                pv[u] = __ldg(p + k + 256 * u);
+                gv[u] = __ldg(g + k + 256 * u);
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) part = __dadd_rn(part, __dmul_rn(double(pv[u]), double(gv[u])));
+            for (int u = 0; u < 4; ++u) sbw_fma(a, pv[u], gv[u]);
         }
-        for (; e < e1; e += 32) part = __dadd_rn(part, __dmul_rn(double(__ldg(p + e)), double(__ldg(g + e))));
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
-        // lanes other than 0 may associate the fold differently; lane 0 holds
-        // the oracle's order
-        const double dot = __shfl_sync(0xffffffffu, part, 0);
-        // second pass: the row was just read, so these are L2 hits
-        std::uint64_t k = e0 + lane;
-        for (; k + 96 < e1; k += 128) {
-            float pv[4], gv[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                pv[u] = p[k + 32 * u];
-                gv[u] = g[k + 32 * u];
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                ds[k + 32 * u] = float(__dmul_rn(double(pv[u]), __dsub_rn(double(gv[u]), dot)));
+        for (; k < e1; k += 256) sbw_fma(a, __ldg(p + k), __ldg(g + k));
+        sp[t] = a;
+        __syncthreads();
+        for (int o = 128; o >= 32; o >>= 1) {
+            if (t < o) sp[t] = __dadd_rn(sp[t], sp[t + o]);
+            __syncthreads();
         }
-        for (; k < e1; k += 32) ds[k] = float(__dmul_rn(double(p[k]), __dsub_rn(double(g[k]), dot)));
+        if (t < 32) {
+            double v = sp[t];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+            if (t == 0) sdot = v;
+        }
+        __syncthreads();
+        const double dot = sdot;
+        sbw_write(p, g, ds, e0 + t, e1, 256, dot);
+        __syncthreads();  // sp / sdot reused by the next row
     }
 }
 
@@ -195,12 +261,26 @@ void launch_permute(const float* src, const std::uint32_t* perm, std::uint64_t n
     check_launch("permute_kernel");
 }
 
+// Rows of at least kSbwLongRow entries (a prefix of the degree order) take
+// the CTA kernel: one warp would run their 256 partials as deg/256-term chains
+// eight at a time and set the kernel's tail (Reddit-shape's 21,657-entry hub).
+constexpr std::uint64_t kSbwLongRow = 4096;
+
 void launch_row_softmax_backward(Graph& g, const float* p, const float* grad, float* ds, cudaStream_t s) {
     if (g.n_rows == 0 || g.nnz == 0) return;
     ensure_order(g);
-    softmax_backward_kernel<<<grid_for(g.n_rows * 32, 256, 148u * 8u), 256, 0, s>>>(
-        g.rowptr.get(), g.order.get(), g.n_rows, p, grad, ds);
-    check_launch("softmax_backward_kernel");
+    const std::uint64_t n_long = rows_with_degree_at_least(g, kSbwLongRow);
+    if (n_long) {
+        softmax_backward_cta_kernel<<<unsigned(std::min<std::uint64_t>(n_long, 148u * 8u)), 256, 0, s>>>(
+            g.rowptr.get(), g.order.get(), n_long, p, grad, ds);
+        check_launch("softmax_backward_cta_kernel");
+    }
+    const std::uint64_t n_rest = g.n_rows - n_long;
+    if (n_rest) {
+        softmax_backward_kernel<<<grid_for(n_rest * 32, 256, 148u * 8u), 256, 0, s>>>(
+            g.rowptr.get(), g.order.get() + n_long, n_rest, p, grad, ds);
+        check_launch("softmax_backward_kernel");
+    }
 }
 
 } // namespace asb

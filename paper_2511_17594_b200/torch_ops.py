@@ -152,7 +152,18 @@ def _(crow, col, val, b):
 @torch.library.custom_op("autosage::sddmm_csr", mutates_args=())
 def sddmm_csr(crow: torch.Tensor, col: torch.Tensor, x: torch.Tensor, y: torch.Tensor,
               variant: str) -> torch.Tensor:
-    """out[e] = <x[i], y[col[e]]> on A's pattern (src/kernels.cpp:336-429)."""
+    """out[e] = <x[i], y[col[e]]> on A's pattern (src/kernels.cpp:336-429).
+    bfloat16 x and y are read as bf16 (as_sddmm_bf16; the f32 result on the
+    widened operands, bit for bit); out is float32 either way."""
+    if x.dtype == torch.bfloat16 and y.dtype == torch.bfloat16:
+        x, y = x.contiguous(), y.contiguous()
+        empty = torch.empty(0, dtype=torch.float32, device=x.device)
+        g = _graph(crow, col, empty, y.shape[0])
+        out = torch.empty(col.numel(), dtype=torch.float32, device=x.device)
+        _check(_lib.as_sddmm_bf16(_variant(variant), g.handle, C.c_void_p(x.data_ptr()), x.shape[0],
+                                  C.c_void_p(y.data_ptr()), y.shape[0], x.shape[1],
+                                  C.c_void_p(out.data_ptr()) if out.numel() else None, _stream(x), None))
+        return out
     x, y = x.contiguous().float(), y.contiguous().float()
     empty = torch.empty(0, dtype=torch.float32, device=x.device)
     g = _graph(crow, col, empty, y.shape[0])
@@ -165,7 +176,7 @@ def sddmm_csr(crow: torch.Tensor, col: torch.Tensor, x: torch.Tensor, y: torch.T
 
 @sddmm_csr.register_fake
 def _(crow, col, x, y, variant):
-    return x.new_empty((col.shape[0],))
+    return x.new_empty((col.shape[0],), dtype=torch.float32)
 
 
 @torch.library.custom_op("autosage::csr_attention", mutates_args=())
@@ -317,9 +328,9 @@ def _sddmm_bwd(ctx, dout):
     crow, col, x, y = ctx.saved_tensors
     dx = dy = None
     if ctx.needs_input_grad[2]:
-        dx = _spmm_vals(_graph(crow, col, torch.empty(0, device=x.device), y.shape[0]), dout, y)
+        dx = _spmm_vals(_graph(crow, col, torch.empty(0, device=x.device), y.shape[0]), dout, y).to(x.dtype)
     if ctx.needs_input_grad[3]:
-        dy = _spmm_t(crow, col, dout, y.shape[0], x)
+        dy = _spmm_t(crow, col, dout, y.shape[0], x).to(y.dtype)
     return None, None, dx, dy, None
 
 

@@ -54,14 +54,14 @@ def test_oracle_transpose_edge_cases():
 
 
 def _softmax_bwd_py(m, p, g):
-    """Pure-Python statement of the fixed order (32 strided partials, pairwise fold)."""
+    """Pure-Python statement of the fixed order (256 strided partials, pairwise fold)."""
     out = np.zeros(m.nnz, dtype=np.float32)
     for i in range(m.n_rows):
         e0, e1 = int(m.rowptr[i]), int(m.rowptr[i + 1])
-        part = [0.0] * 32
+        part = [0.0] * 256
         for e in range(e0, e1):
-            part[(e - e0) & 31] += float(p[e]) * float(g[e])
-        o = 16
+            part[(e - e0) & 255] += float(p[e]) * float(g[e])
+        o = 128
         while o:
             for l in range(o):
                 part[l] += part[l + o]
@@ -73,7 +73,7 @@ def _softmax_bwd_py(m, p, g):
 
 def test_oracle_softmax_backward_order_and_formula():
     rng = np.random.default_rng(4)
-    m = csr_from_degrees(rng, 6, 200, [0, 1, 31, 32, 33, 150])
+    m = csr_from_degrees(rng, 8, 1200, [0, 1, 31, 32, 33, 150, 256, 1100])
     s = rng.standard_normal(m.nnz).astype(np.float32) * 4
     p = oracle.row_softmax(m, s)
     g = rng.standard_normal(m.nnz).astype(np.float32)
@@ -178,8 +178,8 @@ def test_spmm_values_and_permute_match_oracle():
 @pytest.mark.gpu
 def test_softmax_backward_bit_exact_vs_oracle():
     rng = np.random.default_rng(13)
-    for m in (csr_from_degrees(rng, 8, 3000, [0, 1, 2, 31, 32, 33, 64, 2999]),
-              hub_graph(rng, 2000, [1900, 1000], 40, with_values=False)):
+    for m in (csr_from_degrees(rng, 10, 9000, [0, 1, 2, 31, 32, 33, 64, 2999, 4096, 8999]),
+              hub_graph(rng, 6000, [5900, 4100, 1000], 40, with_values=False)):
         crow = torch.from_numpy(m.rowptr.astype(np.int64)).cuda()
         col = torch.from_numpy(m.colind.astype(np.int32)).cuda()
         s = (rng.standard_normal(m.nnz) * 5).astype(np.float32)
@@ -373,3 +373,19 @@ def test_sddmm_bf16_bit_exact_vs_oracle_on_widened_operands():
                 assert np.array_equal(np.isnan(got), nan), (f, v)   # NaN payloads are not compared
                 assert bit_equal(got[~nan], want[~nan]), (f, v)
         g.close()
+
+
+@pytest.mark.gpu
+def test_sddmm_op_bf16_forward_and_grad():
+    rng = np.random.default_rng(34)
+    m = hub_graph(rng, 400, [380], 6, with_values=False)
+    crow, col = _t(m.rowptr.astype(np.int64)), _t(m.colind.astype(np.int32))
+    wx, bx = _bf16_words(rng, m.n_rows, 64)
+    wy, by = _bf16_words(rng, m.n_cols, 64)
+    x16 = torch.from_numpy(wx.view(np.int16)).cuda().view(torch.bfloat16).requires_grad_(True)
+    y16 = torch.from_numpy(wy.view(np.int16)).cuda().view(torch.bfloat16).requires_grad_(True)
+    out = torch.ops.autosage.sddmm_csr(crow, col, x16, y16, "sddmm:rowparallel:ft=32:rpc=1:vec=0:hubt=256")
+    assert out.dtype == torch.float32
+    assert bit_equal(out.detach().cpu().numpy(), oracle.sddmm(m, bx, by, 32, False))
+    out.sum().backward()
+    assert x16.grad.dtype == torch.bfloat16 and y16.grad.dtype == torch.bfloat16

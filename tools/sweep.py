@@ -378,6 +378,21 @@ def case_bf16(res):
             out[f"{cfg}_F{f}"] = {"variant": variant, "f32_ms": t32, "bf16_ms": t16, "speedup": t32 / t16,
                                   "f32_gbs": gbs("spmm", m.n_rows, m.nnz, f, t32),
                                   "bf16_gbs": by16 / (t16 * 1e-3) / 1e9}
+            if cfg == "reddit" and f in (32, 64):
+                x = torch.from_numpy(asb.fill_uniform(m.n_rows * f, 2 + f, (m.n_rows, f))).to(dev)
+                y = torch.from_numpy(asb.fill_uniform(m.n_cols * f, 3 + f, (m.n_cols, f))).to(dev)
+                x16, y16 = x.to(torch.bfloat16), y.to(torch.bfloat16)
+                sv = torch.empty(m.nnz, dtype=torch.float32, device=dev)
+                sd = asb.variant_from_string("sddmm:rowparallel:ft=32:rpc=1:vec=0:hubt=256").to_c()
+                s32 = ev_time(lambda: asb._check(lib.as_sddmm(C.byref(sd), g.handle, P(x), m.n_rows, P(y), m.n_cols,
+                                                              f, P(sv), stream, None)))
+                s16 = ev_time(lambda: asb._check(lib.as_sddmm_bf16(C.byref(sd), g.handle, P(x16), m.n_rows, P(y16),
+                                                                   m.n_cols, f, P(sv), stream, None)))
+                out[f"{cfg}_F{f}_sddmm"] = {"variant": "sddmm:rowparallel:ft=32:rpc=1:vec=0:hubt=256",
+                                            "f32_ms": s32, "bf16_ms": s16, "speedup": s32 / s16,
+                                            "f32_gbs": gbs("sddmm", m.n_rows, m.nnz, f, s32),
+                                            "bf16_gbs": (8 * m.nnz + 4 * m.nnz * f + 4 * m.nnz) / (s16 * 1e-3) / 1e9}
+                del x, y, x16, y16, sv
             del b, b16, c
         g.close()
     res["bf16"] = out
