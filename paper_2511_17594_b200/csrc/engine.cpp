@@ -484,7 +484,7 @@ KernelResult spmm_host(const as_variant* v, Graph& g, const float* b_host, std::
     P.c.ensure(std::max<std::uint64_t>(g.n_rows * f, 1));
     // the previous SpMM's kernel must have finished reading the staging B
     ASB_CUDA(cudaStreamWaitEvent(P.h2d, P.spmm_done, 0));
-    if (b_rows * f)
+    if (b_rows && f)
         ASB_CUDA(cudaMemcpyAsync(P.b.get(), b_host, b_rows * f * 4, cudaMemcpyHostToDevice, P.h2d));
     ASB_CUDA(cudaEventRecord(P.spmm_in, P.h2d));
     ASB_CUDA(cudaStreamWaitEvent(g.stream, P.spmm_in, 0));
@@ -499,7 +499,7 @@ KernelResult spmm_host(const as_variant* v, Graph& g, const float* b_host, std::
     }
     ASB_CUDA(cudaEventRecord(P.spmm_done, g.stream));
     ASB_CUDA(cudaStreamWaitEvent(P.d2h, P.spmm_done, 0));
-    if (g.n_rows * f)
+    if (g.n_rows && f)
         ASB_CUDA(cudaMemcpyAsync(c_host, P.c.get(), g.n_rows * f * 4, cudaMemcpyDeviceToHost, P.d2h));
     ASB_CUDA(cudaEventRecord(P.spmm_out, P.d2h));
     if (sync) ASB_CUDA(cudaEventSynchronize(P.spmm_out));
@@ -530,7 +530,7 @@ KernelResult sddmm_host(const as_variant* v, Graph& g, const float* x_host, std:
     P.v.ensure(std::max<std::uint64_t>(g.nnz, 1));
     ASB_CUDA(cudaStreamWaitEvent(P.h2d, P.sddmm_done, 0));
     // Y first (every slice gathers from all of it); X follows slice by slice
-    if (y_rows * f)
+    if (y_rows && f)
         ASB_CUDA(cudaMemcpyAsync(P.y.get(), y_host, y_rows * f * 4, cudaMemcpyHostToDevice, P.h2d));
     ASB_CUDA(cudaEventRecord(P.sddmm_in, P.h2d));
     ASB_CUDA(cudaStreamWaitEvent(g.stream, P.sddmm_in, 0));
