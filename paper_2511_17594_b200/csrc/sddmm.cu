@@ -857,8 +857,12 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
     }
 }
 
-template <int F, int ORD, int FT, bool BF = false>
-__global__ void __launch_bounds__(128, 3)
+// MINB: resident CTAs per SM the register budget is cut for.  f32 Y staging
+// (17.4 KB per warp at F=64) caps residency at 3 CTAs through shared memory
+// anyway; bf16 staging halves that, so its kernels can trade registers for
+// occupancy.
+template <int F, int ORD, int FT, bool BF = false, int MINB = 3>
+__global__ void __launch_bounds__(128, MINB)
     sddmm_pair1_kernel(const std::uint64_t* __restrict__ rowptr, const std::uint32_t* __restrict__ colind,
                       const std::uint32_t* __restrict__ chunk_row, std::uint64_t n_rows,
                       const double* __restrict__ xd, const void* __restrict__ y, float* __restrict__ out,
@@ -1010,8 +1014,19 @@ void launch_sddmm_fixed(Graph& g, const float* y, std::uint32_t f, float* out, s
                                                              c_end, finite, mix_all());
                     check_launch("sddmm_pair_kernel");
                 };
-                if (ord == 0) run(sddmm_pair1_kernel<F, 0, 0>);
-                else if (ft >= f) run(sddmm_pair1_kernel<F, 1, 0>);
+                // F=32 stages 8.7 KB per warp, so shared memory admits more than 3
+                // CTAs; 4 (<= 128 registers) measured 1.378 -> 1.221 ms on Reddit-shape
+                // (5: 1.236).  F=64 (17.4 KB per warp) stays at 3, the shared-memory
+                // limit.  AUTOSAGE_DEV_SDDMM_MINB=3/4/5 overrides at F=32 (A/B knob).
+                const int minb = F == 32 ? dev_knob("AUTOSAGE_DEV_SDDMM_MINB", 4) : 3;
+                if (ord == 0) {
+                    if (minb == 4) run(sddmm_pair1_kernel<F, 0, 0, false, 4>);
+                    else if (minb == 5) run(sddmm_pair1_kernel<F, 0, 0, false, 5>);
+                    else run(sddmm_pair1_kernel<F, 0, 0>);
+                } else if (minb == 4) {
+                    if (ft >= f) run(sddmm_pair1_kernel<F, 1, 0, false, 4>);
+                    else run(sddmm_pair1_kernel<F, 1, 32, false, 4>);
+                } else if (ft >= f) run(sddmm_pair1_kernel<F, 1, 0>);
                 else run(sddmm_pair1_kernel<F, 1, 32>);
             };
             if (f == 32) pair1(std::integral_constant<int, 32>{});
@@ -1184,9 +1199,15 @@ void launch_sddmm_bf16(Graph& g, const std::uint16_t* x, const std::uint16_t* y,
                                                      g.xwide.get(), y, out, g.nnz, f, 0, c_end, fin, mix_all());
             check_launch("sddmm_pair_kernel");
         };
-        if (ord == 0) run(sddmm_pair1_kernel<F, 0, 0, true>);
-        else if (ft >= f) run(sddmm_pair1_kernel<F, 1, 0, true>);
-        else run(sddmm_pair1_kernel<F, 1, 32, true>);
+        // 4 resident CTAs (<= 128 registers): Reddit-shape F=32 1.32 -> 1.16 ms,
+        // F=64 2.03 -> 1.95 ms against 3; 5 (96 registers) is slower at F=64
+        const int minb = dev_knob("AUTOSAGE_DEV_SDDMM_BF16_MINB", 4);
+        if (ord == 0) {
+            if (minb == 3) run(sddmm_pair1_kernel<F, 0, 0, true, 3>);
+            else if (minb == 5) run(sddmm_pair1_kernel<F, 0, 0, true, 5>);
+            else run(sddmm_pair1_kernel<F, 0, 0, true, 4>);
+        } else if (ft >= f) run(sddmm_pair1_kernel<F, 1, 0, true, 4>);
+        else run(sddmm_pair1_kernel<F, 1, 32, true, 4>);
     };
     if (f == 32) pair1(std::integral_constant<int, 32>{});
     else pair1(std::integral_constant<int, 64>{});
