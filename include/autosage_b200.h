@@ -430,6 +430,13 @@ as_status as_spmm_bf16(const as_variant* v, as_graph a, const float* vals_dev, c
 as_status as_sddmm_bf16(const as_variant* v, as_graph pattern, const uint16_t* x_dev, uint64_t x_rows,
                         const uint16_t* y_dev, uint64_t y_rows, uint64_t f, float* out_dev, void* stream,
                         as_kernel_result* res);
+/* A^T[vals] * B on a transpose gt, with vals in the SOURCE graph's entry
+ * order (nnz floats, device): the kernels read val[perm[k]] at the value
+ * load, so no permuted copy is written (as_permute_values + as_spmm_values
+ * in one pass, the same bits).  gt not a transpose -> AS_INVALID_ARGUMENT. */
+as_status as_spmm_transpose_values(const as_variant* v, as_graph gt, const float* vals_src_dev,
+                                   const float* b_dev, uint64_t b_rows, uint64_t f, float* c_dev, void* stream,
+                                   as_kernel_result* res);
 /* Gradient of row_softmax (src/kernels.cpp:431-461): ds = p * (g - dot),
  * dot = sum_row p*g in f64 (32 strided partials, fixed pairwise fold;
  * oracle/oracle.c orc_row_softmax_backward). */

@@ -192,6 +192,7 @@ _proto("as_permute_values", st, vp, vp, vp, vp)
 _proto("as_spmm_values", st, P(as_variant), vp, vp, vp, u64, u64, vp, vp, P(as_kernel_result))
 _proto("as_row_softmax_backward", st, vp, vp, vp, vp, vp)
 _proto("as_spmm_bf16", st, P(as_variant), vp, vp, vp, u64, u64, vp, vp, P(as_kernel_result))
+_proto("as_spmm_transpose_values", st, P(as_variant), vp, vp, vp, u64, u64, vp, vp, P(as_kernel_result))
 _proto("as_sddmm_bf16", st, P(as_variant), vp, vp, u64, vp, u64, u64, vp, vp, P(as_kernel_result))
 _proto("as_gen_powerlaw", st, u64, u64, u64, dbl, u64, u64, u64, C.c_int, P(vp), P(vp), P(vp),
        P(u64))
@@ -224,5 +225,5 @@ EXPORTED = [
     "as_fill_uniform", "as_free", "as_save_csr", "as_load_csr", "as_host_alloc",
     "as_host_free", "as_kernel_launch_count", "as_graph_transpose", "as_graph_transpose_perm",
     "as_permute_values", "as_spmm_values", "as_row_softmax_backward", "as_spmm_bf16",
-    "as_sddmm_bf16",
+    "as_sddmm_bf16", "as_spmm_transpose_values",
 ]

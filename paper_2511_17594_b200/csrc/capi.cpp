@@ -665,6 +665,29 @@ as_status as_graph_transpose_perm(as_graph gt, const uint32_t** perm) {
     });
 }
 
+// ValPermScope: the graph reads its values through its transpose
+// permutation for one call (graph handles run one operator at a time)
+struct ValPermScope {
+    Graph& g;
+    explicit ValPermScope(Graph& gr) : g(gr) { g.val_perm = g.src_perm.get(); }
+    ~ValPermScope() { g.val_perm = nullptr; }
+};
+
+as_status as_spmm_transpose_values(const as_variant* v, as_graph gt, const float* vals_src_dev,
+                                   const float* b_dev, uint64_t b_rows, uint64_t f, float* c_dev, void* stream,
+                                   as_kernel_result* res) {
+    Graph* gp = nullptr;
+    const as_status st = guard([&] {
+        Graph& g = G(gt);
+        if (!g.is_transpose) throw InvalidArgument("spmm_transpose_values: graph is not a transpose");
+        if (g.nnz && !vals_src_dev) throw InvalidArgument("spmm_transpose_values: values required");
+        gp = &g;
+    });
+    if (st != AS_OK) return st;
+    ValPermScope scope(*gp);
+    return spmm_entry(v, gt, vals_src_dev, b_dev, b_rows, f, c_dev, stream, res);
+}
+
 as_status as_permute_values(as_graph gt, const float* src_dev, float* dst_dev, void* stream) {
     return guard([&] {
         Graph& g = G(gt);

@@ -106,6 +106,9 @@ struct Graph {
     DevBuf<double> xwide;              // SDDMM: X widened to f64 (fixed-width path)
     bool is_transpose = false;         // built by transpose_graph (backward.cu) ...
     DevBuf<std::uint32_t> src_perm;    // ... entry k came from source entry src_perm[k]
+    // set for the duration of one SpMM call (ValPermScope, engine.cpp): the
+    // value array is in source order and entry k reads val[val_perm[k]]
+    const std::uint32_t* val_perm = nullptr;
     cudaStream_t aux = nullptr;        // fork/join stream for concurrent kernels
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 

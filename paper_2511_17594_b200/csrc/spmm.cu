@@ -104,6 +104,7 @@ struct SegArgs {
     const std::uint32_t* piece_len;
     const std::uint32_t* piece_slot;
     const unsigned* finite;           // device flag: B has no Inf/NaN (nullable)
+    const std::uint32_t* vperm;       // values in source order: entry e reads val[vperm[e]] (nullable)
     const float* rmax;                // softmax mode: val holds raw scores, and
     const double* rsum;               // p_e = softmax of the row (softmax.cuh)
     int off32;                        // n_cols * f < 2^32: 32-bit element offsets
@@ -141,7 +142,7 @@ __device__ __forceinline__ void seg_accumulate(double (&acc)[NCH][VEC], double v
 // re-biased on the ALU pipe.  SMX: the entry values are softmax
 // probabilities computed from raw scores and the row's (max, sum) by the lane
 // that loads them (fused attention), instead of stored values.
-template <int VEC, int LPR, int NCH, bool HAS_VAL, bool PIECES, int U, int MIX, bool SMX, bool BF>
+template <int VEC, int LPR, int NCH, bool HAS_VAL, bool PIECES, int U, int MIX, bool SMX, bool BF, bool VP>
 __device__ __forceinline__ void seg_body(const SegArgs& a) {
     using VT = typename VecT<VEC, BF>::T;
     using BT = typename std::conditional<BF, unsigned short, float>::type;
@@ -204,6 +205,9 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
     const unsigned gbase = unsigned(grp * LPR);
     const std::uint32_t* colp = a.colind + e0;
     const float* valp = HAS_VAL ? a.val + e0 : nullptr;
+    // VP (A^T products of the backward): entry k's value is val[vperm[e0 + k]]
+    // (a separate instantiation: a runtime branch here cost the forward kernel ~3%)
+    const std::uint32_t* vpp = VP ? a.vperm + e0 : nullptr;
     const BT* __restrict__ bmat = static_cast<const BT*>(a.b);
 
     // Fast path: while every group of the warp still has W whole entries
@@ -246,6 +250,7 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
                     const std::uint32_t o = __ldg(colp + k) * f;
                     float v;
                     if constexpr (SMX) v = sm_prob_of(__ldg(valp + k), rmx, rsm, rrc);
+                    else if constexpr (VP) v = __ldg(a.val + __ldg(vpp + k));
                     else if constexpr (HAS_VAL) v = __ldg(valp + k);
                     else v = 1.f;
                     if constexpr (E64) ent[s * 32 + lane] = make_uint2(__float_as_uint(v), o);
@@ -291,6 +296,7 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
             const bool ok = k < deg;
             cs[s] = ok ? __ldg(colp + k) : 0u;
             if constexpr (SMX) vs[s] = ok ? double(sm_prob_of(__ldg(valp + k), rmx, rsm, rrc)) : 0.0;
+            else if constexpr (VP) vs[s] = ok ? double(__ldg(a.val + __ldg(vpp + k))) : 0.0;
             else if constexpr (HAS_VAL) vs[s] = ok ? double(__ldg(valp + k)) : 0.0;
             else vs[s] = 1.0;
         }
@@ -356,10 +362,10 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
 }
 
 template <int VEC, int LPR, int NCH, bool HAS_VAL, bool PIECES, int U = unroll_for(VEC, NCH),
-          int MAXR = maxreg_for(VEC, NCH), bool SMX = false, bool BF = false>
+          int MAXR = maxreg_for(VEC, NCH), bool SMX = false, bool BF = false, bool VP = false>
 __global__ void __launch_bounds__(512) __maxnreg__(MAXR) spmm_seg_kernel(SegArgs a) {
-    if (a.finite && *a.finite) seg_body<VEC, LPR, NCH, HAS_VAL, PIECES, U, 1, SMX, BF>(a);
-    else seg_body<VEC, LPR, NCH, HAS_VAL, PIECES, U, 0, SMX, BF>(a);
+    if (a.finite && *a.finite) seg_body<VEC, LPR, NCH, HAS_VAL, PIECES, U, 1, SMX, BF, VP>(a);
+    else seg_body<VEC, LPR, NCH, HAS_VAL, PIECES, U, 0, SMX, BF, VP>(a);
 }
 
 // K3 epilogue: s = 0.0; s += partial[p] in piece order; C = f32(s)
@@ -676,7 +682,8 @@ template <int NF, class BT = float>
 __global__ void spmm_baseline_kernel(const std::uint64_t* __restrict__ rowptr,
                                      const std::uint32_t* __restrict__ colind,
                                      const float* __restrict__ val, const BT* __restrict__ b,
-                                     float* __restrict__ c, std::uint64_t n_rows, std::uint32_t f) {
+                                     float* __restrict__ c, std::uint64_t n_rows, std::uint32_t f,
+                                     const std::uint32_t* __restrict__ vperm = nullptr) {
     const std::uint64_t row = (std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (row >= n_rows) return;
     const int lane = threadIdx.x & 31;
@@ -687,7 +694,7 @@ __global__ void spmm_baseline_kernel(const std::uint64_t* __restrict__ rowptr,
         for (int q = 0; q < NF; ++q) acc[q] = 0.0;
         for (std::uint64_t e = e0; e < e1; ++e) {
             const BT* brow = b + std::uint64_t(colind[e]) * f + f0;
-            const double v = val ? double(val[e]) : 1.0;
+            const double v = val ? double(val[vperm ? vperm[e] : e]) : 1.0;
 #pragma unroll
             for (int q = 0; q < NF; ++q) {
                 const std::uint32_t t = std::uint32_t(lane + 32 * q);
@@ -780,6 +787,16 @@ void launch_seg(const SegArgs& a, bool has_val, std::uint32_t wpb, cudaStream_t 
     const unsigned nb = unsigned(blocks), nt = wpb * 32;
     if constexpr (VEC == 8) {
         if (!a.bf16) throw LogicError("8-wide SpMM tiles are bf16-only");
+    }
+    if constexpr (VEC != 8) {
+        if (a.vperm) {  // values read through a transpose permutation (f32 B, values present)
+            constexpr int U = unroll_for(VEC, NCH), R = maxreg_for(VEC, NCH);
+            if (a.bf16 || a.rmax || !has_val) throw LogicError("spmm: permuted values take f32 B and values");
+            if (pieces) spmm_seg_kernel<VEC, LPR, NCH, true, true, U, R, false, false, true><<<nb, nt, seg_smem(nt), s>>>(a);
+            else spmm_seg_kernel<VEC, LPR, NCH, true, false, U, R, false, false, true><<<nb, nt, seg_smem(nt), s>>>(a);
+            check_launch("spmm_seg_kernel");
+            return;
+        }
     }
     if (VEC == 8 || a.bf16) {  // bf16 B: default tuning, no softmax mode
         constexpr int U = unroll_for(VEC, NCH), R = maxreg_for(VEC, NCH);
@@ -887,23 +904,23 @@ void launch_spmm_baseline(Graph& g, const float* val, const void* bv, std::uint3
     if (bf16) {
         const auto* b = static_cast<const unsigned short*>(bv);
         if (f <= 32)
-            spmm_baseline_kernel<1><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f);
+            spmm_baseline_kernel<1><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f, g.val_perm);
         else if (f <= 64)
-            spmm_baseline_kernel<2><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f);
+            spmm_baseline_kernel<2><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f, g.val_perm);
         else
-            spmm_baseline_kernel<4><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f);
+            spmm_baseline_kernel<4><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f, g.val_perm);
         check_launch("spmm_baseline_kernel");
         return;
     }
     const auto* b = static_cast<const float*>(bv);
     if (f <= 32)
-        spmm_baseline_kernel<1><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f);
+        spmm_baseline_kernel<1><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f, g.val_perm);
     else if (f <= 64)
-        spmm_baseline_kernel<2><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f);
+        spmm_baseline_kernel<2><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f, g.val_perm);
     else if (f <= 128)
-        spmm_baseline_kernel<4><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f);
+        spmm_baseline_kernel<4><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f, g.val_perm);
     else
-        spmm_baseline_kernel<8><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f);
+        spmm_baseline_kernel<8><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f, g.val_perm);
     check_launch("spmm_baseline_kernel");
 }
 
@@ -918,7 +935,7 @@ void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uin
     // kernel on a forked stream, concurrent with the group kernel
     const std::uint64_t lmin = long_row_min(g);
     std::uint64_t n_long = 0;
-    if (lmin > 0 && !bf16 && longrow_ok(f, vec)) {
+    if (lmin > 0 && !bf16 && !g.val_perm && longrow_ok(f, vec)) {
         const std::uint64_t ge = rows_with_degree_at_least(g, lmin);
         n_long = ge > offset ? std::min(ge - offset, n_list) : 0;
     }
@@ -927,6 +944,7 @@ void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uin
         a.rowptr = g.rowptr.get();
         a.colind = g.colind.get();
         a.val = val;
+        a.vperm = g.val_perm;
         a.b = b;
         a.c = c;
         a.rowlist = g.order.get() + offset;
@@ -946,6 +964,7 @@ void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uin
         a.rowptr = g.rowptr.get();
         a.colind = g.colind.get();
         a.val = val;
+        a.vperm = g.val_perm;
         a.b = b;
         a.c = c;
         a.rowlist = g.order.get() + offset;
@@ -994,6 +1013,7 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const void* b, std::uint32
         a.rowptr = g.rowptr.get();
         a.colind = g.colind.get();
         a.val = val;
+        a.vperm = g.val_perm;
         a.b = b;
         a.c = c;
         a.scratch = g.scratch.get();
@@ -1019,7 +1039,7 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const void* b, std::uint32
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const bool few = plan.n_pieces <= std::uint64_t(4) * std::uint64_t(sms);
-        if (few && !bf16 && longrow_ok(f, vec)) launch_longrow<true>(a, plan.n_pieces, s);
+        if (few && !bf16 && !g.val_perm && longrow_ok(f, vec)) launch_longrow<true>(a, plan.n_pieces, s);
         else if (v8) launch_seg_vec<8>(a, val != nullptr, t.lanes, wpb, s);
         else if (vec) launch_seg_vec<4>(a, val != nullptr, t.lanes, wpb, s);
         else launch_seg_vec<1>(a, val != nullptr, t.lanes, wpb, s);

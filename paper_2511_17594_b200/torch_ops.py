@@ -233,10 +233,14 @@ def _spmm_t(crow, col, vals, n_cols: int, dc: torch.Tensor) -> torch.Tensor:
     gt = _transpose(crow, col, n_cols)
     if vals is None or vals.numel() == 0:
         return _spmm_vals(gt, None, dc)
-    vt = torch.empty_like(vals, dtype=torch.float32)
-    _check(_lib.as_permute_values(gt.handle, C.c_void_p(vals.contiguous().float().data_ptr()),
-                                  C.c_void_p(vt.data_ptr()), _stream(dc)))
-    return _spmm_vals(gt, vt, dc)
+    vals = vals.contiguous().float()
+    dc = dc.contiguous().float()
+    c = torch.empty((gt.n_rows, dc.shape[1]), dtype=torch.float32, device=dc.device)
+    # the kernels read vals through the transpose's permutation (no permuted copy)
+    _check(_lib.as_spmm_transpose_values(_variant(_BWD_SPMM), gt.handle, C.c_void_p(vals.data_ptr()),
+                                         C.c_void_p(dc.data_ptr()), dc.shape[0], dc.shape[1],
+                                         C.c_void_p(c.data_ptr()), _stream(dc), None))
+    return c
 
 
 @torch.library.custom_op("autosage::row_softmax_csr", mutates_args=())

@@ -389,3 +389,35 @@ def test_sddmm_op_bf16_forward_and_grad():
     assert bit_equal(out.detach().cpu().numpy(), oracle.sddmm(m, bx, by, 32, False))
     out.sum().backward()
     assert x16.grad.dtype == torch.bfloat16 and y16.grad.dtype == torch.bfloat16
+
+
+@pytest.mark.gpu
+def test_spmm_transpose_values_equals_permute_then_spmm():
+    import ctypes as C
+    from paper_2511_17594_b200 import _lib
+    rng = np.random.default_rng(35)
+    for m in (hub_graph(rng, 1500, [1400, 500], 11), random_csr(rng, 300, 300, 30)):
+        g = asb.Graph.from_csr(m.with_values(None))
+        gt = g.transpose()
+        (rp, ci, _), perm = oracle.transpose(m)
+        w = rng.standard_normal(m.nnz).astype(np.float32)
+        wd = torch.from_numpy(w).cuda()
+        for f in (3, 64, 100):
+            b = random_dense(rng, m.n_rows, f)
+            bd = torch.from_numpy(b).cuda()
+            c = torch.empty((m.n_cols, f), device="cuda")
+            want = oracle.spmm_baseline(asb.CsrMatrix(m.n_cols, m.n_rows, rp, ci, w[perm]), b)
+            for v in (None, "spmm:rowparallel:ft=64:rpc=4:vec=1:hubt=256", "spmm:hubsplit:ft=32:rpc=1:vec=0:hubt=64",
+                      "spmm:hubsplit:ft=64:rpc=1:vec=1:hubt=256"):
+                va = None if v is None else C.byref(asb.variant_from_string(v).to_c())
+                asb._check(_lib.as_spmm_transpose_values(va, gt.handle, C.c_void_p(wd.data_ptr()),
+                                                         C.c_void_p(bd.data_ptr()), m.n_rows, f,
+                                                         C.c_void_p(c.data_ptr()), None, None))
+                torch.cuda.synchronize()
+                assert bit_equal(c.cpu().numpy(), want), (f, v)
+        with pytest.raises(asb.InvalidArgument):
+            asb._check(_lib.as_spmm_transpose_values(None, g.handle, C.c_void_p(wd.data_ptr()),
+                                                     C.c_void_p(bd.data_ptr()), m.n_cols, f,
+                                                     C.c_void_p(c.data_ptr()), None, None))
+        gt.close()
+        g.close()
