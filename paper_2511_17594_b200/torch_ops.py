@@ -268,7 +268,7 @@ def row_softmax_csr_backward(crow: torch.Tensor, col: torch.Tensor, p: torch.Ten
     p, grad = p.contiguous().float(), grad.contiguous().float()
     empty = torch.empty(0, dtype=torch.float32, device=p.device)
     g = _graph(crow, col, empty, n_cols)
-    ds = torch.zeros_like(p)
+    ds = torch.empty_like(p)  # every entry is written (empty rows have none)
     if p.numel():
         _check(_lib.as_row_softmax_backward(g.handle, C.c_void_p(p.data_ptr()), C.c_void_p(grad.data_ptr()),
                                             C.c_void_p(ds.data_ptr()), _stream(p)))
