@@ -386,6 +386,17 @@ as_status as_csr_attention_forward(const as_context* ctx, const as_probe_config*
                                    int fused, as_decision* sddmm_decision,
                                    as_decision* spmm_decision);
 
+/* The staged pipeline with the probabilities p = row_softmax(SDDMM(q, k))
+ * also written to p_dev (nnz floats, device): the training forward keeps p
+ * for the backward instead of recomputing it (new).  out is
+ * bit-identical to as_csr_attention_forward. */
+as_status as_csr_attention_forward_p(const as_context* ctx, const as_probe_config* cfg,
+                                     as_graph pattern, const float* q_dev, uint64_t q_rows,
+                                     const float* k_dev, uint64_t k_rows, const float* v_dev,
+                                     uint64_t v_rows, uint64_t f, uint64_t fv, float* out_dev,
+                                     float* p_dev, as_decision* sddmm_decision,
+                                     as_decision* spmm_decision);
+
 /* ------------------------------------------------------------------ */
 /* Multi-GPU row partition (new)                           */
 /* ------------------------------------------------------------------ */

@@ -184,6 +184,8 @@ _proto("as_decide_host", st, P(as_context), P(as_probe_config), u64, P(as_featur
        C.c_int, u64, P(as_decision))
 _proto("as_csr_attention_forward", st, P(as_context), P(as_probe_config), vp, vp, u64, vp, u64,
        vp, u64, u64, u64, vp, C.c_int, P(as_decision), P(as_decision))
+_proto("as_csr_attention_forward_p", st, P(as_context), P(as_probe_config), vp, vp, u64, vp, u64,
+       vp, u64, u64, u64, vp, vp, P(as_decision), P(as_decision))
 _proto("as_partition_rows", st, vp, u64, u32, vp)
 _proto("as_graph_row_range", st, vp, u64, u64, P(vp))
 _proto("as_graph_transpose", st, vp, P(vp))
@@ -225,5 +227,5 @@ EXPORTED = [
     "as_fill_uniform", "as_free", "as_save_csr", "as_load_csr", "as_host_alloc",
     "as_host_free", "as_kernel_launch_count", "as_graph_transpose", "as_graph_transpose_perm",
     "as_permute_values", "as_spmm_values", "as_row_softmax_backward", "as_spmm_bf16",
-    "as_sddmm_bf16", "as_spmm_transpose_values",
+    "as_sddmm_bf16", "as_spmm_transpose_values", "as_csr_attention_forward_p",
 ]

@@ -639,6 +639,18 @@ as_status as_csr_attention_forward(const as_context* ctx, const as_probe_config*
     });
 }
 
+as_status as_csr_attention_forward_p(const as_context* ctx, const as_probe_config* cfg, as_graph pattern,
+                                     const float* q_dev, uint64_t q_rows, const float* k_dev, uint64_t k_rows,
+                                     const float* v_dev, uint64_t v_rows, uint64_t f, uint64_t fv, float* out_dev,
+                                     float* p_dev, as_decision* sd, as_decision* pd) {
+    return guard([&] {
+        Graph& g = G(pattern);
+        if (g.nnz && !p_dev) throw InvalidArgument("attention: p output required");
+        attention_forward(make_ctx(ctx), cfg_or_default(cfg), g, q_dev, q_rows, k_dev, k_rows, v_dev, v_rows, f,
+                          fv, out_dev, false, sd, pd, p_dev);
+    });
+}
+
 // ---- multi-GPU partition ------------------------------------------------------------
 as_status as_partition_rows(const uint64_t* rowptr_host, uint64_t n_rows, uint32_t g,
                             uint64_t* cuts) {

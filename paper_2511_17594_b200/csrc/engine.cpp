@@ -714,7 +714,7 @@ void reset_probe_launch_count() { g_probe_launches.store(0); }
 void attention_forward(const Context& ctx, const as_probe_config& cfg, Graph& pattern,
                        const float* q, std::uint64_t q_rows, const float* k, std::uint64_t k_rows,
                        const float* v, std::uint64_t v_rows, std::uint64_t f, std::uint64_t fv,
-                       float* out, bool fused, as_decision* sd_out, as_decision* pd_out) {
+                       float* out, bool fused, as_decision* sd_out, as_decision* pd_out, float* p_out) {
     if (q_rows != pattern.n_rows || k_rows != pattern.n_cols || v_rows != pattern.n_cols)
         throw InvalidArgument("attention: operand row counts incompatible with pattern");
     DeviceGuard dg(pattern.device);
@@ -723,7 +723,7 @@ void attention_forward(const Context& ctx, const as_probe_config& cfg, Graph& pa
     const as_decision sd = decide_sddmm(ctx, cfg, pattern, q, q_rows, k, k_rows, f);
     pattern.att_buf.ensure(std::max<std::uint64_t>(2 * pattern.nnz, 2));
     float* scores = pattern.att_buf.get();
-    float* p = scores + pattern.nnz;
+    float* p = p_out ? p_out : scores + pattern.nnz;
     bool p_ready = false;
     auto make_p = [&] {
         if (p_ready) return;
@@ -732,7 +732,7 @@ void attention_forward(const Context& ctx, const as_probe_config& cfg, Graph& pa
         row_softmax(pattern, scores, p, s);
         p_ready = true;
     };
-    if (!fused) make_p();
+    if (!fused || p_out) make_p();
 
     // decide_spmm on p = softmax(scores): same structure (same graph_sig), the
     // probe sample slices p's values -- materialized only if a probe runs

@@ -89,9 +89,12 @@ void sddmm_auto(const Context& ctx, const as_probe_config& cfg, Graph& p, const 
 std::uint64_t probe_launch_count();
 void reset_probe_launch_count();
 
+// p_out (nnz floats, nullable): also keep the probabilities there (staged
+// pipeline; the training path saves them for the backward)
 void attention_forward(const Context& ctx, const as_probe_config& cfg, Graph& pattern,
                        const float* q, std::uint64_t q_rows, const float* k, std::uint64_t k_rows,
                        const float* v, std::uint64_t v_rows, std::uint64_t f, std::uint64_t fv,
-                       float* out, bool fused, as_decision* sd, as_decision* pd);
+                       float* out, bool fused, as_decision* sd, as_decision* pd,
+                       float* p_out = nullptr);
 
 } // namespace asb

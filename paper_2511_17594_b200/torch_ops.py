@@ -362,3 +362,69 @@ def _attention_bwd(ctx, do):
 
 
 csr_attention.register_autograd(_attention_bwd, setup_context=_attention_setup)
+
+
+# ---------------------------------------------------------------------------
+# Training form of the attention: keeps p for the backward
+# ---------------------------------------------------------------------------
+@torch.library.custom_op("autosage::csr_attention_with_probs", mutates_args=())
+def csr_attention_with_probs(crow: torch.Tensor, col: torch.Tensor, q: torch.Tensor, k: torch.Tensor,
+                             v: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    """(out, p): the staged pipeline (as_csr_attention_forward_p), p = the row
+    softmax of the scores (nnz floats).  out is bit-identical to csr_attention;
+    its backward reuses p instead of recomputing SDDMM + softmax."""
+    q, k, v = q.contiguous().float(), k.contiguous().float(), v.contiguous().float()
+    empty = torch.empty(0, dtype=torch.float32, device=q.device)
+    g = _graph(crow, col, empty, k.shape[0])
+    out = torch.empty((g.n_rows, v.shape[1]), dtype=torch.float32, device=q.device)
+    p = torch.empty(col.numel(), dtype=torch.float32, device=q.device)
+    cctx, keep = _ctx(q).to_c()
+    ccfg = ProbeConfig.from_env().to_c()
+    sd, pd = _c.as_decision(), _c.as_decision()
+    _check(_lib.as_csr_attention_forward_p(C.byref(cctx), C.byref(ccfg), g.handle, C.c_void_p(q.data_ptr()),
+                                           q.shape[0], C.c_void_p(k.data_ptr()), k.shape[0],
+                                           C.c_void_p(v.data_ptr()), v.shape[0], q.shape[1], v.shape[1],
+                                           C.c_void_p(out.data_ptr()), C.c_void_p(p.data_ptr()) if p.numel() else None,
+                                           C.byref(sd), C.byref(pd)))
+    del keep
+    return out, p
+
+
+@csr_attention_with_probs.register_fake
+def _(crow, col, q, k, v):
+    return q.new_empty((crow.shape[0] - 1, v.shape[1])), q.new_empty((col.shape[0],))
+
+
+def _attention_p_setup(ctx, inputs, output):
+    crow, col, q, k, v = inputs
+    ctx.save_for_backward(crow, col, q, k, v, output[1])
+
+
+def _attention_p_bwd(ctx, do, gp):
+    """dv = A^T[p] dO, dp = SDDMM(dO, v) (+ the gradient reaching p directly),
+    ds = softmax'(p, dp), dq = A[ds] k, dk = A^T[ds] q -- p from the forward."""
+    crow, col, q, k, v, p = ctx.saved_tensors
+    n_cols = k.shape[0]
+    dv = dq = dk = None
+    if do is None:
+        do = torch.zeros((crow.shape[0] - 1, v.shape[1]), dtype=torch.float32, device=q.device)
+    if ctx.needs_input_grad[4]:
+        dv = _spmm_t(crow, col, p, n_cols, do)
+    dp = sddmm_csr(crow, col, do, v, _BWD_SDDMM)
+    if gp is not None:
+        dp = dp + gp
+    ds = row_softmax_csr_backward(crow, col, p, dp, n_cols)
+    if ctx.needs_input_grad[2]:
+        dq = _spmm_vals(_graph(crow, col, torch.empty(0, device=q.device), n_cols), ds, k)
+    if ctx.needs_input_grad[3]:
+        dk = _spmm_t(crow, col, ds, n_cols, q)
+    return None, None, dq, dk, dv
+
+
+csr_attention_with_probs.register_autograd(_attention_p_bwd, setup_context=_attention_p_setup)
+
+
+def csr_attention_train(crow, col, q, k, v) -> torch.Tensor:
+    """CSR attention for training: the forward keeps p (4 bytes per nonzero)
+    so the backward skips the SDDMM + softmax recompute of csr_attention."""
+    return csr_attention_with_probs(crow, col, q, k, v)[0]

@@ -421,3 +421,25 @@ def test_spmm_transpose_values_equals_permute_then_spmm():
                                                      C.c_void_p(c.data_ptr()), None, None))
         gt.close()
         g.close()
+
+
+@pytest.mark.gpu
+def test_attention_with_probs_forward_and_grads_match_recompute_path():
+    from paper_2511_17594_b200.torch_ops import csr_attention_train
+    rng = np.random.default_rng(36)
+    m = hub_graph(rng, 700, [650, 300], 7, with_values=False)
+    crow, col = _t(m.rowptr.astype(np.int64)), _t(m.colind.astype(np.int32))
+    q, k, v = (random_dense(rng, 700, 32) for _ in range(3))
+    do = random_dense(rng, 700, 32)
+    grads = []
+    for fn in (lambda a, b, c: torch.ops.autosage.csr_attention(crow, col, a, b, c, True),
+               lambda a, b, c: csr_attention_train(crow, col, a, b, c)):
+        qt, kt, vt = _t(q, True), _t(k, True), _t(v, True)
+        out = fn(qt, kt, vt)
+        out.backward(_t(do))
+        grads.append((out.detach().cpu().numpy(), qt.grad.cpu().numpy(), kt.grad.cpu().numpy(),
+                      vt.grad.cpu().numpy()))
+    for a, b in zip(*grads):
+        assert bit_equal(a, b)
+    out, p = torch.ops.autosage.csr_attention_with_probs(crow, col, _t(q), _t(k), _t(v))
+    assert bit_equal(p.cpu().numpy(), oracle.row_softmax(m, oracle.sddmm(m, q, k)))

@@ -100,7 +100,10 @@ def main():
               f"| Aᵀ·dC SpMM (hubsplit ft=64) | {f3(b['spmm_t_ms'])} | {b['spmm_t_gbs']:.0f} GB/s gather-model |",
               f"| row-softmax gradient | {f3(b['softmax_bwd_ms'])} | {b['softmax_bwd_gbs']:.0f} GB/s (8(N+1) + 12·nnz) |",
               f"| spmm_csr forward + backward (torch) | {b['spmm_autograd_step_ms']:.2f} | |",
-              f"| csr_attention fused forward + backward (torch) | {b['attention_autograd_step_ms']:.2f} | |", ""]
+              f"| csr_attention fused forward + backward (torch) | {b['attention_autograd_step_ms']:.2f} | recompute of p |"]
+        if "attention_train_step_ms" in b:
+            L.append(f"| csr_attention_train forward + backward (torch) | {b['attention_train_step_ms']:.2f} | p kept from the forward |")
+        L.append("")
     if "bf16" in r:
         L += ["## bf16 — SpMM with a bf16 B (as_spmm_bf16) vs f32 B, same variant", "",
               "| case | variant | f32 ms | bf16 ms | speed-up |", "|---|---|---|---|---|"]

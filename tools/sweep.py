@@ -344,13 +344,20 @@ def case_bwd(res):
         q.grad = k.grad = v.grad = None
         torch.ops.autosage.csr_attention(crow, col, q, k, v, True).backward(dc)
     t_att_step = ev_time(att_step, 3, 1)
+    from paper_2511_17594_b200.torch_ops import csr_attention_train
+
+    def att_train_step():
+        q.grad = k.grad = v.grad = None
+        csr_attention_train(crow, col, q, k, v).backward(dc)
+    t_att_train = ev_time(att_train_step, 3, 1)
     n, nnz = m.n_rows, m.nnz
     res["bwd"] = {"graph": {"n": n, "nnz": nnz, "F": f},
                   "transpose_first_ms": t_transpose, "transpose_ms": t_transpose_warm,
                   "permute_ms": t_perm, "permute_gbs": 12 * nnz / (t_perm * 1e-3) / 1e9,
                   "spmm_t_ms": t_db, "spmm_t_gbs": gbs("spmm", n, nnz, f, t_db),
                   "softmax_bwd_ms": t_sm, "softmax_bwd_gbs": (8 * (n + 1) + 12 * nnz) / (t_sm * 1e-3) / 1e9,
-                  "spmm_autograd_step_ms": t_spmm_step, "attention_autograd_step_ms": t_att_step}
+                  "spmm_autograd_step_ms": t_spmm_step, "attention_autograd_step_ms": t_att_step,
+                  "attention_train_step_ms": t_att_train}
     gt.close()
     g.close()
 
