@@ -182,7 +182,11 @@ def _(crow, col, x, y, variant):
 @torch.library.custom_op("autosage::csr_attention", mutates_args=())
 def csr_attention(crow: torch.Tensor, col: torch.Tensor, q: torch.Tensor, k: torch.Tensor,
                   v: torch.Tensor, fused: bool) -> torch.Tensor:
-    """csr_attention_forward (src/attention.cpp:9-40), decisions cached."""
+    """csr_attention_forward (src/attention.cpp:9-40), decisions cached.
+    bfloat16 q, k and v take the staged bf16 route (_attention_bf16; `fused`
+    does not apply there)."""
+    if _all_bf16(q, k, v):
+        return _attention_bf16(crow, col, q, k, v)[0]
     q, k, v = q.contiguous().float(), k.contiguous().float(), v.contiguous().float()
     empty = torch.empty(0, dtype=torch.float32, device=q.device)
     g = _graph(crow, col, empty, k.shape[0])
@@ -201,7 +205,33 @@ def csr_attention(crow: torch.Tensor, col: torch.Tensor, q: torch.Tensor, k: tor
 
 @csr_attention.register_fake
 def _(crow, col, q, k, v, fused):
-    return q.new_empty((crow.shape[0] - 1, v.shape[1]))
+    return q.new_empty((crow.shape[0] - 1, v.shape[1]), dtype=torch.float32)
+
+
+def _all_bf16(*ts) -> bool:
+    return all(t.dtype == torch.bfloat16 for t in ts)
+
+
+def _attention_bf16(crow, col, q, k, v):
+    """Staged attention on bf16 q, k, v: scores =
+    as_sddmm_bf16(q, k), p = as_row_softmax(scores), out = as_spmm_bf16 with
+    values p over bf16 v.  Fixed variants (_BWD_SDDMM: the sequential dot
+    order, src/kernels.cpp:336-355; _BWD_SPMM), so (out, p) equal the f32
+    pipeline sddmm_csr -> row_softmax_csr -> spmm_csr on q.float(), k.float(),
+    v.float() with the same variants, bit for bit, while the Q/K/V gathers
+    read half the bytes.  out and p are float32."""
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    if k.shape[0] != v.shape[0]:
+        raise ValueError("csr_attention: k and v need the same row count")
+    n_cols = k.shape[0]
+    s = sddmm_csr(crow, col, q, k, _BWD_SDDMM)
+    p = row_softmax_csr(crow, col, s, n_cols)
+    pat = _graph(crow, col, torch.empty(0, dtype=torch.float32, device=q.device), n_cols)
+    out = torch.empty((pat.n_rows, v.shape[1]), dtype=torch.float32, device=q.device)
+    _check(_lib.as_spmm_bf16(_variant(_BWD_SPMM), pat.handle, C.c_void_p(p.data_ptr()) if p.numel() else None,
+                             C.c_void_p(v.data_ptr()), v.shape[0], v.shape[1], C.c_void_p(out.data_ptr()),
+                             _stream(q), None))
+    return out, p
 
 
 # ---------------------------------------------------------------------------
@@ -356,9 +386,9 @@ def _attention_bwd(ctx, do):
     dp = sddmm_csr(crow, col, do, v, _BWD_SDDMM)
     ds = row_softmax_csr_backward(crow, col, p, dp, k.shape[0])
     pat = _graph(crow, col, torch.empty(0, device=q.device), k.shape[0])
-    dq = _spmm_vals(pat, ds, k) if ctx.needs_input_grad[2] else None
-    dk = _spmm_t(crow, col, ds, k.shape[0], q) if ctx.needs_input_grad[3] else None
-    return None, None, dq, dk, dv, None
+    dq = _spmm_vals(pat, ds, k).to(q.dtype) if ctx.needs_input_grad[2] else None
+    dk = _spmm_t(crow, col, ds, k.shape[0], q).to(k.dtype) if ctx.needs_input_grad[3] else None
+    return None, None, dq, dk, None if dv is None else dv.to(v.dtype), None
 
 
 csr_attention.register_autograd(_attention_bwd, setup_context=_attention_setup)
@@ -372,7 +402,10 @@ def csr_attention_with_probs(crow: torch.Tensor, col: torch.Tensor, q: torch.Ten
                              v: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
     """(out, p): the staged pipeline (as_csr_attention_forward_p), p = the row
     softmax of the scores (nnz floats).  out is bit-identical to csr_attention;
-    its backward reuses p instead of recomputing SDDMM + softmax."""
+    its backward reuses p instead of recomputing SDDMM + softmax.  bfloat16
+    q, k and v take the staged bf16 route (_attention_bf16)."""
+    if _all_bf16(q, k, v):
+        return _attention_bf16(crow, col, q, k, v)
     q, k, v = q.contiguous().float(), k.contiguous().float(), v.contiguous().float()
     empty = torch.empty(0, dtype=torch.float32, device=q.device)
     g = _graph(crow, col, empty, k.shape[0])
@@ -392,7 +425,8 @@ def csr_attention_with_probs(crow: torch.Tensor, col: torch.Tensor, q: torch.Ten
 
 @csr_attention_with_probs.register_fake
 def _(crow, col, q, k, v):
-    return q.new_empty((crow.shape[0] - 1, v.shape[1])), q.new_empty((col.shape[0],))
+    return (q.new_empty((crow.shape[0] - 1, v.shape[1]), dtype=torch.float32),
+            q.new_empty((col.shape[0],), dtype=torch.float32))
 
 
 def _attention_p_setup(ctx, inputs, output):
@@ -415,10 +449,10 @@ def _attention_p_bwd(ctx, do, gp):
         dp = dp + gp
     ds = row_softmax_csr_backward(crow, col, p, dp, n_cols)
     if ctx.needs_input_grad[2]:
-        dq = _spmm_vals(_graph(crow, col, torch.empty(0, device=q.device), n_cols), ds, k)
+        dq = _spmm_vals(_graph(crow, col, torch.empty(0, device=q.device), n_cols), ds, k).to(q.dtype)
     if ctx.needs_input_grad[3]:
-        dk = _spmm_t(crow, col, ds, n_cols, q)
-    return None, None, dq, dk, dv
+        dk = _spmm_t(crow, col, ds, n_cols, q).to(k.dtype)
+    return None, None, dq, dk, None if dv is None else dv.to(v.dtype)
 
 
 csr_attention_with_probs.register_autograd(_attention_p_bwd, setup_context=_attention_p_setup)

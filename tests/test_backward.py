@@ -99,6 +99,14 @@ def test_backward_ops_registered_with_fake_shapes():
         s = torch.empty(30)
         assert torch.ops.autosage.row_softmax_csr(crow, col, s, 7).shape == (30,)
         assert torch.ops.autosage.row_softmax_csr_backward(crow, col, s, s, 7).shape == (30,)
+        # bf16 attention: float32 outputs of the f32 shapes
+        q = torch.empty(10, 16, dtype=torch.bfloat16)
+        kv = torch.empty(7, 8, dtype=torch.bfloat16)
+        out = torch.ops.autosage.csr_attention(crow, col, q, torch.empty(7, 16, dtype=torch.bfloat16), kv, False)
+        assert out.shape == (10, 8) and out.dtype == torch.float32
+        out, p = torch.ops.autosage.csr_attention_with_probs(crow, col, q, torch.empty(7, 16, dtype=torch.bfloat16),
+                                                            kv)
+        assert out.dtype == p.dtype == torch.float32 and p.shape == (30,)
 
 
 # ---------------------------------------------------------------- GPU: kernels
@@ -443,3 +451,37 @@ def test_attention_with_probs_forward_and_grads_match_recompute_path():
         assert bit_equal(a, b)
     out, p = torch.ops.autosage.csr_attention_with_probs(crow, col, _t(q), _t(k), _t(v))
     assert bit_equal(p.cpu().numpy(), oracle.row_softmax(m, oracle.sddmm(m, q, k)))
+
+
+@pytest.mark.gpu
+def test_attention_bf16_bit_exact_vs_oracle_on_widened_operands():
+    """bf16 q, k, v: (out, p) equal the oracle's staged attention on the
+    widened f32 operands (sequential SDDMM order, hub-split SpMM at hubT 256),
+    bit for bit; grads come back in bf16 and match the f32 op's on the
+    widened operands."""
+    from paper_2511_17594_b200.torch_ops import csr_attention_train
+    rng = np.random.default_rng(37)
+    for m, f in ((hub_graph(rng, 900, [880, 400], 9, with_values=False), 64),
+                 (random_csr(rng, 300, 300, 20).with_values(None), 32),
+                 (empty_rows(9, 4).with_values(None), 16)):
+        crow, col = _t(m.rowptr.astype(np.int64)), _t(m.colind.astype(np.int32))
+        (wq, bq), (wk, bk), (wv, bv) = (_bf16_words(rng, m.n_rows, f) for _ in range(3))
+        b16 = lambda w: torch.from_numpy(w.view(np.int16)).cuda().view(torch.bfloat16)  # noqa: E731
+        want_p = oracle.row_softmax(m, oracle.sddmm(m, bq, bk, 32, False))
+        want = oracle.attention(m, bq, bk, bv, 32, False, 256)
+        out = torch.ops.autosage.csr_attention(crow, col, b16(wq), b16(wk), b16(wv), True)
+        assert out.dtype == torch.float32
+        assert bit_equal(out.cpu().numpy(), want)
+        out, p = torch.ops.autosage.csr_attention_with_probs(crow, col, b16(wq), b16(wk), b16(wv))
+        assert bit_equal(p.cpu().numpy(), want_p)
+        assert bit_equal(out.cpu().numpy(), want)
+        if m.nnz == 0:
+            continue
+        do = _t(random_dense(rng, m.n_rows, f))
+        q16, k16, v16 = (b16(w).requires_grad_(True) for w in (wq, wk, wv))
+        csr_attention_train(crow, col, q16, k16, v16).backward(do)
+        qf, kf, vf = (_t(a, True) for a in (bq, bk, bv))
+        torch.ops.autosage.csr_attention(crow, col, qf, kf, vf, False).backward(do)
+        for g16, gf in ((q16, qf), (k16, kf), (v16, vf)):
+            assert g16.grad.dtype == torch.bfloat16
+            assert torch.equal(g16.grad, gf.grad.to(torch.bfloat16))

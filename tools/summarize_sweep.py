@@ -108,7 +108,9 @@ def main():
         L += ["## bf16 — SpMM with a bf16 B (as_spmm_bf16) vs f32 B, same variant", "",
               "| case | variant | f32 ms | bf16 ms | speed-up |", "|---|---|---|---|---|"]
         for k, e in r["bf16"].items():
-            L.append(f"| {k} | `{e['variant']}` | {f3(e['f32_ms'])} | {f3(e['bf16_ms'])} | {e['speedup']:.2f} |")
+            f32 = e.get('f32_ms', e.get('f32_staged_ms'))
+            L.append(f"| {k} | `{e.get('variant', 'csr_attention staged (torch op)')}` | {f3(f32)} | "
+                     f"{f3(e['bf16_ms'])} | {e['speedup']:.2f} |")
         L.append("")
     out = os.path.join(ROOT, "profiles", f"{tag}_sweep.md")
     with open(out, "w") as fh:

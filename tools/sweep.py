@@ -399,6 +399,16 @@ def case_bf16(res):
                                             "f32_ms": s32, "bf16_ms": s16, "speedup": s32 / s16,
                                             "f32_gbs": gbs("sddmm", m.n_rows, m.nnz, f, s32),
                                             "bf16_gbs": (8 * m.nnz + 4 * m.nnz * f + 4 * m.nnz) / (s16 * 1e-3) / 1e9}
+                if f == 64:
+                    # one attention head through the torch op: f32 staged vs bf16 q, k, v
+                    import paper_2511_17594_b200.torch_ops  # noqa: F401
+                    crow = torch.from_numpy(m.rowptr.astype(np.int64)).to(dev)
+                    col = torch.from_numpy(m.colind.astype(np.int32)).to(dev)
+                    att = torch.ops.autosage.csr_attention
+                    a32 = ev_time(lambda: att(crow, col, x, y, b, False))
+                    a16 = ev_time(lambda: att(crow, col, x16, y16, b16, False))
+                    out[f"{cfg}_F{f}_attention"] = {"f32_staged_ms": a32, "bf16_ms": a16, "speedup": a32 / a16}
+                    del crow, col
                 del x, y, x16, y16, sv
             del b, b16, c
         g.close()
