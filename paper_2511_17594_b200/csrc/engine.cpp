@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstring>
 #include <limits>
+#include <map>
 #include <mutex>
 
 namespace asb {
@@ -79,11 +80,40 @@ Record to_record(const as_decision& d) {  // src/scheduler.cpp:72-82
     return rec;
 }
 
+// AUTOSAGE_PROBE_FLUSH_L2=<MiB> (default 256, 0 = off): before each timed
+// probe run, overwrite that many MiB on the probe stream, outside the timed
+// events, so candidates are timed from a cold L2 -- the condition of a step
+// whose operands were evicted since the last op (bench.py flushes between
+// steps).  A warm-L2 probe on the small sample ranks mappings whose cold
+// costs differ: c1 (1.6M nnz, F=64) picked rowparallel (0.143-0.147 ms on a
+// cold step) in 3 of 3 runs, the cold probe hub-split (0.105 ms) in 3 of 3;
+// Reddit-shape picks are unchanged.  One scratch buffer per device.
+void probe_flush_l2(cudaStream_t s) {
+    const auto knob = env::get_int("AUTOSAGE_PROBE_FLUSH_L2");
+    const long long mib = knob ? *knob : 256;
+    if (mib <= 0) return;
+    static std::mutex mu;
+    static std::map<int, std::pair<void*, std::size_t>> bufs;
+    int dev = 0;
+    ASB_CUDA(cudaGetDevice(&dev));
+    const std::size_t bytes = std::size_t(mib) << 20;
+    std::lock_guard<std::mutex> lk(mu);
+    auto& b = bufs[dev];
+    if (b.second < bytes) {
+        if (b.first) ASB_CUDA(cudaFree(b.first));
+        b = {nullptr, 0};
+        ASB_CUDA(cudaMalloc(&b.first, bytes));
+        b.second = bytes;
+    }
+    ASB_CUDA(cudaMemsetAsync(b.first, int(b.second >> 20) & 0xff, bytes, s));
+}
+
 TimeOnce event_timer(cudaStream_t s) {
     return [s](const std::string&, const std::function<void()>& run) {
         cudaEvent_t e0, e1;
         ASB_CUDA(cudaEventCreate(&e0));
         ASB_CUDA(cudaEventCreate(&e1));
+        probe_flush_l2(s);
         ASB_CUDA(cudaEventRecord(e0, s));
         run();
         ASB_CUDA(cudaEventRecord(e1, s));

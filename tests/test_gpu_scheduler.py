@@ -210,6 +210,25 @@ def test_default_gpu_profile_and_real_probe():
     assert cache.size() == 1
 
 
+def test_probe_with_cold_l2_knob(monkeypatch):
+    """AUTOSAGE_PROBE_FLUSH_L2 (default 256 MiB, 0 = off) flushes L2 before
+    each timed probe: either way the decide probes every candidate and its
+    choice keeps the guardrail."""
+    for mib in ("32", "0"):
+        _cold_probe(monkeypatch, mib)
+
+
+def _cold_probe(monkeypatch, mib):
+    monkeypatch.setenv("AUTOSAGE_PROBE_FLUSH_L2", mib)
+    rng = np.random.default_rng(4)
+    a = asb.gen_powerlaw(20000, 20000, 300000, 2.2, 4, 2000, 5)
+    b = random_dense(rng, 20000, 64)
+    d = asb.decide_spmm(a, b, asb.ProbeConfig(iters=2), asb.ScheduleContext(cache=asb.ScheduleCache()))
+    assert d.source == asb.PROBED and d.baseline_ms > 0 and len(d.candidates) == 3
+    if d.choice is not None:
+        assert d.t_star <= 0.95 * d.baseline_ms
+
+
 def test_probe_config_validation():
     fx = Fixture()
     ctx = asb.ScheduleContext(device=fx.dev)
