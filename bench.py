@@ -11,15 +11,26 @@ own cost formulas, proj/src/cost.cpp:21-27) over all ranks / max-rank time.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config reddit]
   python bench.py --impl reference ...   # reference CPU library, host cores
 
-Multi-GPU (torchrun): rows are nnz-balanced across ranks (as_partition_rows);
-each step all-gathers the dense B/Y row shards over NCCL, then runs the
-local SpMM/SDDMM on the rank's row range ("strong" scaling).
+--gpus N without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (one per GPU, NCCL).  Rows are
+nnz-balanced across ranks (as_partition_rows); each step all-gathers the
+dense B/Y row shards, Y in column blocks that the SDDMM consumes as they land
+(dist.py), and runs the local SpMM/SDDMM on the rank's row range.
+
+At N=1 the line also carries
+  parity        our full-graph outputs vs the reference library
+                (oracle/_ref) dispatched with the same decided variants,
+                compared bit for bit;
+  cpu_baseline  the reference's own input-aware multicore path
+                (decide once, then 2 warm-ups + 12 timed dispatches,
+                proj/tools/autosage_bench.cpp:132-134) on the full graph.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -41,6 +52,7 @@ CONFIGS = {
 }
 L2_FLUSH_BYTES = 256 << 20
 PEAK_FALLBACK_GBS = 6650.0
+CPU_WARMUP, CPU_ITERS = 2, 12  # proj/tools/autosage_bench.cpp:132-134
 
 
 def gather_bytes(op: str, n_rows: int, nnz: int, f: int) -> float:
@@ -50,6 +62,15 @@ def gather_bytes(op: str, n_rows: int, nnz: int, f: int) -> float:
     return 8.0 * nnz + 8.0 * nnz * f + 4.0 * nnz
 
 
+def compulsory_bytes(op: str, n_rows: int, n_cols: int, nnz: int, f: int, has_val: bool = True) -> float:
+    """Every array crossing HBM once: the floor of an
+    op's DRAM traffic.  SpMM: rowptr, colind, val, B once, C written.
+    SDDMM: rowptr, colind, X once, Y once, values written."""
+    if op == "spmm":
+        return 8.0 * (n_rows + 1) + (8.0 if has_val else 4.0) * nnz + 4.0 * n_cols * f + 4.0 * n_rows * f
+    return 8.0 * (n_rows + 1) + 4.0 * nnz + 4.0 * n_rows * f + 4.0 * n_cols * f + 4.0 * nnz
+
+
 def measured_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -57,6 +78,14 @@ def measured_peak():
             return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return PEAK_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+def profile_json(name):
+    try:
+        with open(os.path.join(ROOT, "profiles", name)) as fh:
+            return json.load(fh)
+    except Exception:
+        return None
 
 
 class ClockSampler:
@@ -125,92 +154,146 @@ class ClockSampler:
 
 
 def make_graph(cfg_name: str, seed: int):
+    """The workload through the package's generator (as_gen_powerlaw)."""
     import paper_2511_17594_b200 as asb
     n, nnz, alpha, dmin, dmax, f = CONFIGS[cfg_name]
-    m = asb.gen_powerlaw(n, n, nnz, alpha, dmin, dmax, seed)
-    return m, f
+    return asb.gen_powerlaw(n, n, nnz, alpha, dmin, dmax, seed), f
 
 
-def host_row_sample(m, step: int):
-    """Every `step`-th row (a systematic sample) as a host CSR."""
-    import paper_2511_17594_b200 as asb
-    rows = np.arange(0, m.n_rows, step)
-    deg = (m.rowptr[rows + 1] - m.rowptr[rows]).astype(np.int64)
-    rp = np.zeros(rows.size + 1, dtype=np.uint64)
-    rp[1:] = np.cumsum(deg)
-    idx = np.concatenate([np.arange(m.rowptr[r], m.rowptr[r + 1], dtype=np.int64) for r in rows])
-    return asb.CsrMatrix(rows.size, m.n_cols, rp, m.colind[idx],
-                         None if m.val is None else m.val[idx]), rows
-
-
-# ---------------------------------------------------------------------------
-# reference CPU arm
-# ---------------------------------------------------------------------------
-def cpu_reference_run(m, f, seed, steps, warmup, sample_step):
-    """Reference library (oracle/_ref, else the C port) on the host cores:
-    decide once with the reference scheduler, then time dispatch(choice)
-    SpMM + SDDMM per step on a systematic row sample of the workload."""
+def make_graph_oracle(cfg_name: str, seed: int):
+    """The same bytes through oracle/gen.c (the reference arm loads nothing
+    from the package; tests/test_oracle.py checks the two generators agree)."""
     import oracle
-    import paper_2511_17594_b200 as asb
-    sm, rows = host_row_sample(m, sample_step)
-    b = asb.fill_uniform(m.n_cols * f, seed + f, (m.n_cols, f))
-    x = asb.fill_uniform(m.n_rows * f, seed + f, (m.n_rows, f))[rows]
-    y = asb.fill_uniform(m.n_cols * f, seed + f + 1, (m.n_cols, f))
-    total = gather_bytes("spmm", sm.n_rows, sm.nnz, f) + gather_bytes("sddmm", sm.n_rows, sm.nnz, f)
-    if oracle.ref_available():
-        kind, cores = "reference", oracle.ref_default_workers()
-        rg, rb, rx, ry = oracle.RefGraph(sm), oracle.RefDense(b), oracle.RefDense(x), oracle.RefDense(y)
-        spmm_choice, _ = oracle.ref_decide(rg, None, rb, 0)
-        sddmm_choice, _ = oracle.ref_decide(rg, rx, ry, 1)
-        out = np.empty((sm.n_rows, f), np.float32)
+    n, nnz, alpha, dmin, dmax, f = CONFIGS[cfg_name]
+    return oracle.gen_powerlaw(n, n, nnz, alpha, dmin, dmax, seed), f
 
-        def step():
-            if spmm_choice == "baseline":
-                oracle.ref_spmm_baseline(rg, rb)
-            else:
-                oracle.ref_spmm_dispatch(spmm_choice, rg, rb, 0, out)
-            if sddmm_choice == "baseline":
-                oracle.ref_sddmm_baseline(rg, rx, ry)
-            else:
-                oracle.ref_sddmm_dispatch(sddmm_choice, rg, rx, ry, 0)
-        choices = {"spmm": spmm_choice, "sddmm": sddmm_choice}
-    else:
-        kind, cores = "port", 1
-        choices = {"spmm": "baseline", "sddmm": "baseline"}
 
-        def step():
-            oracle.spmm_baseline(sm, b)
-            oracle.sddmm(sm, x, y)
-    for _ in range(warmup):
-        step()
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        step()
-    dt = time.perf_counter() - t0
-    gbs = total * steps / dt / 1e9
-    sample = (f"every {sample_step}th row of the workload ({sm.n_rows} rows, {sm.nnz} nnz, F={f}); "
-              f"SpMM {choices['spmm']} + SDDMM {choices['sddmm']}; {steps} timed steps")
-    return {"value": gbs, "unit": "GB/s", "cores": int(cores), "kind": kind, "sample": sample,
-            "ms_per_step": dt / steps * 1e3}
+def dense_inputs(fill, m, f, seed):
+    """Reference bench seeds (proj/tools/autosage_bench.cpp:57-63, :269-270):
+    B seed+F, X seed+F, Y seed+F+1."""
+    b = fill(m.n_cols * f, seed + f, (m.n_cols, f))
+    x = fill(m.n_rows * f, seed + f, (m.n_rows, f))
+    y = fill(m.n_cols * f, seed + f + 1, (m.n_cols, f))
+    return b, x, y
+
+
+# ---------------------------------------------------------------------------
+# reference CPU library (oracle/_ref): the reference arm and cpu_baseline
+# ---------------------------------------------------------------------------
+class RefWorkload:
+    """The full workload inside the reference library (autosage_ref::)."""
+
+    def __init__(self, m, f, seed):
+        import oracle
+        self.oracle = oracle
+        self.m, self.f = m, f
+        b, x, y = dense_inputs(oracle.fill_uniform, m, f, seed)
+        self.kind = "reference" if oracle.ref_available() else "port"
+        if self.kind == "reference":
+            self.rg = oracle.RefGraph(m)
+            self.rb, self.rx, self.ry = oracle.RefDense(b), oracle.RefDense(x), oracle.RefDense(y)
+            self.cores = int(oracle.ref_default_workers())
+        else:
+            self.b, self.x, self.y = b, x, y
+            self.cores = 1
+        self.out = np.empty((m.n_rows, f), np.float32)
+
+    def decide(self):
+        """The reference scheduler (decide_spmm / decide_sddmm, default
+        ProbeConfig, src/scheduler.cpp:195-224) -- the port has none."""
+        if self.kind != "reference":
+            return "baseline", "baseline", 0.0
+        t0 = time.perf_counter()
+        s, _ = self.oracle.ref_decide(self.rg, None, self.rb, 0)
+        d, _ = self.oracle.ref_decide(self.rg, self.rx, self.ry, 1)
+        return s, d, (time.perf_counter() - t0) * 1e3
+
+    def spmm(self, choice):
+        o = self.oracle
+        if self.kind != "reference":
+            return o.spmm_baseline(self.m, self.b)
+        if choice == "baseline":
+            return o.ref_spmm_baseline(self.rg, self.rb)
+        return o.ref_spmm_dispatch(choice, self.rg, self.rb, 0, self.out)[0]
+
+    def sddmm(self, choice):
+        o = self.oracle
+        if self.kind != "reference":
+            return o.sddmm(self.m, self.x, self.y)
+        if choice == "baseline":
+            return o.ref_sddmm_baseline(self.rg, self.rx, self.ry)
+        return o.ref_sddmm_dispatch(choice, self.rg, self.rx, self.ry, 0)
+
+    def time_steps(self, spmm_choice, sddmm_choice, steps, warmup):
+        for _ in range(warmup):
+            self.spmm(spmm_choice)
+            self.sddmm(sddmm_choice)
+        times = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            self.spmm(spmm_choice)
+            self.sddmm(sddmm_choice)
+            times.append(time.perf_counter() - t0)
+        return times
+
+
+def cpu_reference_run(m, f, seed, steps, warmup, cfg_name):
+    """The reference library's own input-aware path on the host cores:
+    decide once with the reference scheduler, then time dispatch(choice)
+    SpMM + SDDMM per step on the full workload."""
+    w = RefWorkload(m, f, seed)
+    spmm_choice, sddmm_choice, decide_ms = w.decide()
+    times = w.time_steps(spmm_choice, sddmm_choice, steps, warmup)
+    step_bytes = gather_bytes("spmm", m.n_rows, m.nnz, f) + gather_bytes("sddmm", m.n_rows, m.nnz, f)
+    mean_s = sum(times) / len(times)
+    sample = (f"full {cfg_name} workload ({m.n_rows} rows, {m.nnz} nnz, F={f}); reference "
+              f"decide once ({decide_ms:.0f} ms, not timed), then SpMM {spmm_choice} + SDDMM "
+              f"{sddmm_choice}: {warmup} warm-up + {steps} timed steps")
+    res = {"value": step_bytes / mean_s / 1e9, "unit": "GB/s", "cores": w.cores, "kind": w.kind,
+           "sample": sample, "ms_per_step": mean_s * 1e3,
+           "ms_per_step_median": statistics.median(times) * 1e3,
+           "choices": {"spmm": spmm_choice, "sddmm": sddmm_choice}, "decide_ms": decide_ms}
+    return res, w
+
+
+def parity_check(w: "RefWorkload", c_dev, sv_dev, spmm_choice, sddmm_choice):
+    """Our full-graph outputs vs the reference library dispatched with our
+    decided variants (bit for bit: the reference accumulates in f64 in the
+    same order); also the relative distance to the reference's
+    own choice (its SDDMM vec order differs from the scalar one)."""
+    c = c_dev.cpu().numpy()
+    s = sv_dev[: w.m.nnz].cpu().numpy()
+    want_c = w.spmm(spmm_choice)
+    want_s = w.sddmm(sddmm_choice)
+    bits = lambda a: np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)  # noqa: E731
+    res = {"against": f"{w.kind} library dispatch(our choice) on the full graph",
+           "rows_checked": int(w.m.n_rows), "nnz_checked": int(w.m.nnz),
+           "spmm_bitdiff": int(np.count_nonzero(bits(c) != bits(want_c))),
+           "sddmm_bitdiff": int(np.count_nonzero(bits(s) != bits(want_s)))}
+    return res
 
 
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    m, f = make_graph(args.config, args.seed)
-    steps, warmup = args.steps, args.warmup
-    cpu = cpu_reference_run(m, f, args.seed, steps, warmup, args.cpu_sample_step)
+    m, f = make_graph_oracle(args.config, args.seed)
+    if args.f:
+        f = args.f
+    cpu, _ = cpu_reference_run(m, f, args.seed, args.steps, args.warmup, args.config)
     line = {
         "impl": "reference", "metric": metric_name(args.config, f), "value": cpu["value"],
-        "unit": "GB/s", "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
+        "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": cpu["ms_per_step"], "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_name(args.config, f), "n_rows": m.n_rows, "nnz": m.nnz,
-                   "F": f, "sample": cpu["sample"]},
+                   "F": f, "sample": cpu["sample"], "inputs": "oracle/gen.c (byte-identical to the "
+                   "package generator; nothing loaded from paper_2511_17594_b200)"},
         "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": cpu["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "choices": cpu["choices"], "decide_ms": cpu["decide_ms"],
+        "ms_per_step_median": cpu["ms_per_step_median"],
     }
     print(json.dumps(line), flush=True)
 
@@ -227,6 +310,34 @@ def workload_name(cfg, f):
 # ---------------------------------------------------------------------------
 # B200 arm
 # ---------------------------------------------------------------------------
+def op_traffic(cfg, f, op):
+    """Per-launch DRAM bytes of one op (sum over its kernels) from the
+    committed ncu launch list (profiles/ncu_traffic.json)."""
+    t = profile_json("ncu_traffic.json") or {}
+    e = t.get(f"{cfg}:F={f}:{op}")
+    if e is None:
+        return None, None
+    if isinstance(e, dict):
+        return float(e["bytes"]), e.get("source")
+    return float(e), None
+
+
+def decision_report(d):
+    """ProbeReport (include/autosage/scheduler.hpp:36-46) + cold phases."""
+    return {"choice": d.choice_string(), "source": d.source_name, "baseline_ms": d.baseline_ms,
+            "t_star": d.t_star, "alpha": d.alpha, "sample_rows": d.sample_rows,
+            "candidates": [{"variant": _vs(c.variant), "median_ms": c.median_ms,
+                            "completed": c.completed} for c in d.candidates],
+            "best_index": d.best_index,
+            "phases_ms": {"graph_sig": d.sig_ms, "features": d.features_ms, "sample": d.sample_ms,
+                          "probes": d.probe_wall_ms, "decide_total": d.decide_wall_ms}}
+
+
+def _vs(v):
+    import paper_2511_17594_b200 as asb
+    return asb.variant_to_string(v)
+
+
 def run_ours(args):
     import torch
     import paper_2511_17594_b200 as asb
@@ -244,9 +355,11 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
 
+    t_gen = time.perf_counter()
     m, f = make_graph(args.config, args.seed)
     if args.f:
         f = args.f
+    gen_s = time.perf_counter() - t_gen
     n_rows, nnz = m.n_rows, m.nnz
     from paper_2511_17594_b200.dist import RowSharding
     sh = RowSharding(m.rowptr, world, rank)  # nnz-balanced contiguous row ranges
@@ -254,10 +367,7 @@ def run_ours(args):
     # N>1: this rank's rows, columns remapped into the padded all-gather layout
     # (dist.py), so the kernels gather straight from the NCCL buffer
     g = asb.Graph.from_csr(m if world == 1 else sh.shard_graph_host(m), device=local)
-    # dense operands (reference bench seeds: B seed+F, X seed+F, Y seed+F+1)
-    b_host = asb.fill_uniform(m.n_cols * f, args.seed + f, (m.n_cols, f))
-    x_host = asb.fill_uniform(n_rows * f, args.seed + f, (n_rows, f))
-    y_host = asb.fill_uniform(m.n_cols * f, args.seed + f + 1, (m.n_cols, f))
+    b_host, x_host, y_host = dense_inputs(asb.fill_uniform, m, f, args.seed)
     # square graph: rank r owns the B/Y rows of its own node range
     b_full = torch.from_numpy(b_host).to(dev)
     y_full = torch.from_numpy(y_host).to(dev)
@@ -378,23 +488,7 @@ def run_ours(args):
     bytes_sddmm = gather_bytes("sddmm", n_rows, nnz, f)
     value = (bytes_spmm + bytes_sddmm) * K / (total * 1e-3) / 1e9
     peak, peak_src = measured_peak()
-
-    # roofline of the dominant op (its algorithmic bytes per launch on this rank)
-    local_nnz = g.nnz
-    lb_spmm = gather_bytes("spmm", r1 - r0, local_nnz, f)
-    lb_sddmm = gather_bytes("sddmm", r1 - r0, local_nnz, f)
-    dom = "sddmm" if t_sddmm >= t_spmm else "spmm"
-    dom_ms = (t_sddmm if dom == "sddmm" else t_spmm) / K
-    dom_bytes = lb_sddmm if dom == "sddmm" else lb_spmm
-    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        try:
-            with open(tp) as fh:
-                traffic = json.load(fh).get(f"{args.config}:F={f}:{dom}")
-        except Exception:
-            traffic = None
+    roof = roofline(args, g, f, r1 - r0, m.n_cols, t_spmm / K, t_sddmm / K, peak, peak_src)
 
     # e2e through the reference-facing host-buffer entry points
     e2e = None
@@ -404,10 +498,16 @@ def run_ours(args):
         e2e = run_e2e(args, g, f, r1 - r0, b_host_e2e, x_host[r0:r1], y_host_e2e, dec_spmm, dec_sddmm,
                       bytes_spmm + bytes_sddmm, dist)
 
-    cpu = None
+    cpu = parity = None
     if world == 1 and rank == 0 and not args.no_cpu:
-        cpu = cpu_reference_run(m, f, args.seed, 2, 1, args.cpu_sample_step)
-        cpu.pop("ms_per_step", None)
+        # the device outputs of the last timed step, checked against the
+        # reference library on the full graph; then the reference timed
+        del b_full, y_full, flush
+        cpu, w = cpu_reference_run(m, f, args.seed, CPU_ITERS, CPU_WARMUP, args.config)
+        parity = parity_check(w, c, sv, dec_spmm.choice_string(), dec_sddmm.choice_string())
+        del w
+        for k in ("ms_per_step_median", "decide_ms"):
+            cpu.pop(k, None)
 
     if rank == 0:
         clk = clocks.summary()
@@ -426,34 +526,70 @@ def run_ours(args):
                        "sddmm_choice": dec_sddmm.choice_string(),
                        "decision_source": {"spmm": dec_spmm.source_name,
                                            "sddmm": dec_sddmm.source_name},
-                       "probe": dataclasses_asdict(cfg)},
+                       "probe": dataclasses_asdict(cfg), "input_gen_s": gen_s},
             "ms_per_op": {"spmm": t_spmm / K, "sddmm": t_sddmm / K, "allgather": t_gather / K},
             # 2*nnz*F flops per op (proj/src/cost.cpp:28), whole job
             "gflops_per_s": {"spmm": 2.0 * nnz * f / (t_spmm / K * 1e-3) / 1e9,
                              "sddmm": 2.0 * nnz * f / (t_sddmm / K * 1e-3) / 1e9,
                              "step": 4.0 * nnz * f / (total / K * 1e-3) / 1e9},
-            "pct_of_8TBs": value / 8000.0 * 100.0,
+            "gather_model_pct_of_8TBs": value / 8000.0 * 100.0,
             "decide_cold_ms": cold_ms,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": dom,
-                         "bytes_model": "gather model, proj/src/cost.cpp:21-27", "peak_source": peak_src,
-                         # measured DRAM bytes over the same time: the gathers hit L2,
-                         # so the op is bound on chip, not by HBM
-                         "dram_gbs": (traffic / (dom_ms * 1e-3) / 1e9) if traffic else None,
-                         "dram_frac": (traffic / (dom_ms * 1e-3) / 1e9 / peak) if traffic else None,
-                         "binding_resource": {"sddmm": "shared-memory datapath (Y staging + X broadcast)",
-                                              "spmm": "L2 gather latency (long scoreboard)"}[dom]},
+            "probe_report": {"spmm": decision_report(dec_spmm), "sddmm": decision_report(dec_sddmm)},
+            "roofline": roof,
             "gpu_launches": int(launches),
             "clocks": clk,
         }
+        if world > 1:
+            line["nccl"] = {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
+                            "nccl_version": ".".join(map(str, torch.cuda.nccl.version()))}
         if e2e:
             line["e2e"] = e2e
         if cpu:
             line["cpu_baseline"] = cpu
+        if parity:
+            line["parity"] = parity
         print(json.dumps(line), flush=True)
     del keep
     if dist:
         dist.destroy_process_group()
+
+
+def roofline(args, g, f, rows, n_cols, spmm_ms, sddmm_ms, peak, peak_src):
+    """Roofline of the dominant op (per launch, this rank).
+
+    achieved / frac: DRAM bytes the op's kernels move per launch (ncu,
+    profiles/ncu_traffic.json) over the live CUDA-event op time, against the
+    measured HBM copy bandwidth -- an honest HBM fraction.  Beside it: the
+    compulsory bytes (each array once, the floor of that traffic), the
+    reference gather model (proj/src/cost.cpp:21-27; its B/Y row gathers are
+    mostly L2 hits, so it can exceed HBM) and that gather rate against the
+    measured on-chip gather roof (tools/gather_roofline.cu, profiles/)."""
+    dom = "sddmm" if sddmm_ms >= spmm_ms else "spmm"
+    dom_ms = sddmm_ms if dom == "sddmm" else spmm_ms
+    comp = compulsory_bytes(dom, rows, n_cols, g.nnz, f, g.has_values())
+    gm = gather_bytes(dom, rows, g.nnz, f)
+    traffic, src = op_traffic(args.config, f, dom)
+    to_gbs = lambda b: b / (dom_ms * 1e-3) / 1e9  # noqa: E731
+    achieved = to_gbs(traffic) if traffic else to_gbs(comp)
+    r = {"bound": "hbm", "kernel": dom, "unit": "GB/s", "peak": peak, "peak_source": peak_src,
+         "achieved": achieved, "frac": achieved / peak, "traffic": traffic,
+         "achieved_basis": ("ncu DRAM bytes per launch (" + (src or "profiles/ncu_traffic.json") + ")"
+                            if traffic else "compulsory bytes (no ncu traffic recorded for this config)"),
+         "op_ms": dom_ms,
+         "compulsory": {"bytes": comp, "gbs": to_gbs(comp), "frac": to_gbs(comp) / peak},
+         "gather_model": {"bytes": gm, "gbs": to_gbs(gm), "model": "proj/src/cost.cpp:21-27"}}
+    if traffic:
+        r["traffic_over_compulsory"] = traffic / comp
+    oc = profile_json("onchip_roofs.json")
+    if oc and dom in oc.get("ops", {}):
+        # the row gathers themselves: one 4F-byte B (SpMM) / Y (SDDMM) row per
+        # nonzero, the traffic the measured gather roof moves
+        rows_b = 4.0 * f * g.nnz
+        roof = float(oc["ops"][dom]["gbs"])
+        r["onchip"] = {"row_gather_bytes": rows_b, "achieved_gbs": to_gbs(rows_b), "roof_gbs": roof,
+                       "frac": to_gbs(rows_b) / roof, "what": oc["ops"][dom]["what"],
+                       "source": oc.get("source")}
+    return r
 
 
 def dataclasses_asdict(cfg):
@@ -534,6 +670,28 @@ def run_e2e(args, g, f, n_rows, b_host, x_host, y_host, dec_spmm, dec_sddmm, ste
                    "(decided variants), pinned host buffers"}
 
 
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch_distributed(n: int) -> None:
+    """`bench.py --gpus N` outside torchrun: re-exec under
+    torch.distributed.run, one rank per GPU (the driver's own launch line),
+    with NCCL's INFO init lines on stderr so the rank count is visible."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)]
+    cmd += sys.argv[1:]
+    os.execvpe(cmd[0], cmd, env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -543,15 +701,16 @@ def main():
     ap.add_argument("--config", default="reddit", choices=sorted(CONFIGS))
     ap.add_argument("--f", type=int, default=0, help="override feature width")
     ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--cpu-sample-step", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip cpu_baseline and parity (N=1)")
     ap.add_argument("--cache", default="", help="schedule cache file: load if present, store after decide")
     ap.add_argument("--replay-only", action="store_true",
                     help="decisions must come from --cache (strict replay, no probes)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_distributed(args.gpus)
     if args.impl == "reference":
         run_reference_arm(args)
     else:

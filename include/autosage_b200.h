@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define AS_ABI_VERSION 1
+#define AS_ABI_VERSION 2
 
 typedef enum {
     AS_OK = 0,
@@ -330,6 +330,13 @@ typedef struct {
     uint64_t sample_rows;
     double probe_wall_ms;
     double max_single_run_ms;
+    /* cold-decide phases (new; host wall clock, ms): graph signature
+     * (memoised per graph: 0 after the first decide), features, the probe
+     * sample (rows + slice), and the whole decide call */
+    double sig_ms;
+    double features_ms;
+    double sample_ms;
+    double decide_wall_ms;
 } as_decision;
 
 /* ScheduleContext, include/autosage/scheduler.hpp:61-69.  Every pointer

@@ -85,6 +85,12 @@ def port():
         lib.orc_shortlist.restype = C.c_int
         lib.orc_shortlist.argtypes = [C.POINTER(orc_features), u64, C.c_int, dbl, dbl, u64,
                                       C.POINTER(orc_variant)]
+        lib.orc_gen_powerlaw_degrees.restype = C.c_int
+        lib.orc_gen_powerlaw_degrees.argtypes = [u64, u64, u64, dbl, u64, u64, u64, vp]
+        lib.orc_gen_powerlaw_columns.restype = None
+        lib.orc_gen_powerlaw_columns.argtypes = [u64, u64, u64, vp, vp, vp]
+        lib.orc_fill_uniform.restype = None
+        lib.orc_fill_uniform.argtypes = [vp, u64, u64]
         lib.orc_time_kernel_policy.restype = C.c_int
         lib.orc_time_kernel_policy.argtypes = [C.POINTER(dbl), C.c_int, C.c_int, dbl, dbl,
                                                C.POINTER(orc_timed_stats)]
@@ -270,6 +276,49 @@ def partition_rows(rowptr: np.ndarray, g: int) -> np.ndarray:
     cuts = np.zeros(g + 1, dtype=np.uint64)
     port().orc_partition_rows(_ptr(rowptr), rowptr.size - 1, g, _ptr(cuts))
     return cuts
+
+
+# ---------------------------------------------------------------------------
+# Input generators (oracle/gen.c): the bench workload without the package
+# ---------------------------------------------------------------------------
+class HostCsr:
+    """A host CSR with the attributes the oracle functions read (the same
+    duck type as the package's CsrMatrix, so the reference arm and the tests
+    can build inputs without importing the B200 package)."""
+
+    def __init__(self, n_rows, n_cols, rowptr, colind, val=None):
+        self.n_rows, self.n_cols = int(n_rows), int(n_cols)
+        self.rowptr = np.ascontiguousarray(rowptr, dtype=np.uint64)
+        self.colind = np.ascontiguousarray(colind, dtype=np.uint32)
+        self.val = None if val is None else np.ascontiguousarray(val, dtype=np.float32)
+
+    @property
+    def nnz(self) -> int:
+        return int(self.colind.size)
+
+    def has_values(self) -> bool:
+        return self.val is not None and self.val.size > 0
+
+
+def gen_powerlaw(n_rows: int, n_cols: int, nnz_target: int, alpha: float, d_min: int, d_max: int,
+                 seed: int, with_values: bool = True) -> HostCsr:
+    """Same bytes as the package's gen_powerlaw (checked in test_oracle)."""
+    rowptr = np.zeros(n_rows + 1, dtype=np.uint64)
+    if port().orc_gen_powerlaw_degrees(n_rows, n_cols, nnz_target, alpha, d_min, d_max, seed,
+                                       _ptr(rowptr)) != 0:
+        raise ValueError("gen_powerlaw: bad arguments")
+    nnz = int(rowptr[-1])
+    colind = np.empty(nnz, dtype=np.uint32)
+    val = np.empty(nnz, dtype=np.float32) if with_values else None
+    port().orc_gen_powerlaw_columns(n_rows, n_cols, seed, _ptr(rowptr), _ptr(colind), _ptr(val))
+    return HostCsr(n_rows, n_cols, rowptr, colind, val)
+
+
+def fill_uniform(n: int, seed: int, shape=None) -> np.ndarray:
+    """U[-1, 1) f32, the same bytes as the package's fill_uniform."""
+    out = np.empty(n, dtype=np.float32)
+    port().orc_fill_uniform(_ptr(out), n, seed)
+    return out.reshape(shape) if shape is not None else out
 
 
 # ---------------------------------------------------------------------------

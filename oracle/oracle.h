@@ -128,6 +128,18 @@ void orc_transpose(const uint64_t* rowptr, const uint32_t* colind, uint64_t n_ro
 void orc_row_softmax_backward(const uint64_t* rowptr, uint64_t n_rows, const float* p,
                               const float* g, float* ds);
 
+/* ---- input generators (gen.c; no reference counterpart -- see gen.c) ---- */
+/* Heavy-tailed degrees: deg_i = min(cap, floor(d_min * u^(-1/(alpha-1)))),
+ * u from row i's own stream, rescaled to nnz_target (0 = keep) and settled
+ * one entry per row; writes rowptr[n_rows+1].  Returns -1 on bad args. */
+int orc_gen_powerlaw_degrees(uint64_t n_rows, uint64_t n_cols, uint64_t nnz_target, double alpha,
+                             uint64_t d_min, uint64_t d_max, uint64_t seed, uint64_t* rowptr);
+/* Distinct ascending columns per row (and U[0,1) values when val != NULL). */
+void orc_gen_powerlaw_columns(uint64_t n_rows, uint64_t n_cols, uint64_t seed, const uint64_t* rowptr,
+                              uint32_t* colind, float* val);
+/* out[i] = U[-1, 1) from splitmix64(seed * 0xA0761D6478BD642F + i). */
+void orc_fill_uniform(float* out, uint64_t n, uint64_t seed);
+
 #ifdef __cplusplus
 }
 #endif

@@ -882,6 +882,10 @@ class ScheduleDecision:
     sample_rows: int
     probe_wall_ms: float
     max_single_run_ms: float
+    sig_ms: float = 0.0
+    features_ms: float = 0.0
+    sample_ms: float = 0.0
+    decide_wall_ms: float = 0.0
 
     def choice_string(self) -> str:
         return variant_to_string(self.choice) if self.choice is not None else "baseline"
@@ -899,7 +903,8 @@ class ScheduleDecision:
                                 d.source, ScheduleKey.from_c(d.key), d.alpha, d.baseline_ms,
                                 d.baseline_completed, bool(d.baseline_capped), cands,
                                 d.best_index, d.t_star, d.sample_rows, d.probe_wall_ms,
-                                d.max_single_run_ms)
+                                d.max_single_run_ms, d.sig_ms, d.features_ms, d.sample_ms,
+                                d.decide_wall_ms)
 
 
 def _to_device(a, device: int):

@@ -92,7 +92,8 @@ class as_decision(C.Structure):
                 ("baseline_capped", i32), ("n_candidates", i32),
                 ("candidates", as_candidate_timing * AS_MAX_CANDIDATES), ("best_index", i32),
                 ("t_star", dbl), ("sample_rows", u64), ("probe_wall_ms", dbl),
-                ("max_single_run_ms", dbl)]
+                ("max_single_run_ms", dbl), ("sig_ms", dbl), ("features_ms", dbl),
+                ("sample_ms", dbl), ("decide_wall_ms", dbl)]
 
 
 RUN_FN = C.CFUNCTYPE(None, vp)

@@ -138,10 +138,21 @@ as_decision decide_common(const Context& ctx, const as_probe_config& cfg,
                           const as_device_profile& dp, const std::function<std::uint64_t()>& sig,
                           std::uint64_t f, int op, ProbeHooks& hooks) {
     check_probe_config(cfg);
+    using clk = std::chrono::steady_clock;
+    auto ms_since = [](clk::time_point t) {
+        return std::chrono::duration<double, std::milli>(clk::now() - t).count();
+    };
+    const auto call0 = clk::now();
     as_decision d{};
     d.best_index = -1;
     set_key(d, dp, sig(), f, op);
+    d.sig_ms = ms_since(call0);
     d.alpha = cfg.alpha;
+    struct WallOnExit {
+        as_decision& d;
+        clk::time_point t0;
+        ~WallOnExit() { d.decide_wall_ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count(); }
+    } wall_on_exit{d, call0};
 
     if (auto forced = forced_env_variant(op)) {
         d.has_choice = 1;
@@ -164,11 +175,15 @@ as_decision decide_common(const Context& ctx, const as_probe_config& cfg,
         return d;
     }
 
+    auto t_phase = clk::now();
     const as_features gf = hooks.features();
+    d.features_ms = ms_since(t_phase);
     auto candidates = shortlist(gf, f, op, dp);
     if (dp.model == AS_MODEL_B200) candidates = distinct_gpu_configs(candidates, f);
     if (candidates.size() > std::size_t(cfg.top_k)) candidates.resize(std::size_t(cfg.top_k));
+    t_phase = clk::now();
     const std::uint64_t sample_rows = hooks.prepare ? hooks.prepare() : 0;
+    d.sample_ms = ms_since(t_phase);
 
     TimeOnce timer = ctx.timer ? ctx.timer : event_timer(hooks.stream);
     std::lock_guard<std::mutex> probe_lock(g_probe_mutex);

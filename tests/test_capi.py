@@ -32,7 +32,7 @@ def test_every_declared_symbol_is_exported():
     missing = [s for s in sorted(declared) if not hasattr(_capi.lib, s)]
     assert not missing, missing
     assert set(_capi.EXPORTED) <= declared
-    assert _capi.lib.as_abi_version() == 1
+    assert _capi.lib.as_abi_version() == 2
     assert _capi.lib.as_artifact_version().decode() == "autosage-b200-0.1.0"
 
 
