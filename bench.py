@@ -168,6 +168,34 @@ def make_graph_oracle(cfg_name: str, seed: int):
     return oracle.gen_powerlaw(n, n, nnz, alpha, dmin, dmax, seed), f
 
 
+def with_hubs(m, hub_degrees, seed, fill_uniform=None):
+    """Replace the first rows by hubs of the given degrees (distinct sorted
+    columns), keeping the rest of the power-law graph."""
+    if fill_uniform is None:
+        import paper_2511_17594_b200 as asb
+        fill_uniform = asb.fill_uniform
+    rng = np.random.default_rng(seed)
+    deg = np.diff(m.rowptr.astype(np.int64))
+    rows = []
+    for i in range(m.n_rows):
+        if i < len(hub_degrees):
+            cols = np.sort(rng.permutation(m.n_cols)[:hub_degrees[i]]).astype(np.uint32)
+        else:
+            break
+        rows.append(cols)
+    k = len(rows)
+    head = np.concatenate(rows)
+    tail = m.colind[int(m.rowptr[k]):]
+    deg2 = np.concatenate([np.array([r.size for r in rows], np.int64), deg[k:]])
+    rp = np.zeros(m.n_rows + 1, np.uint64)
+    rp[1:] = np.cumsum(deg2)
+    val = None
+    if m.val is not None:
+        val = np.concatenate([fill_uniform(head.size, seed, (head.size,)) * 0.5 + 0.5,
+                              m.val[int(m.rowptr[k]):]]).astype(np.float32)
+    return type(m)(m.n_rows, m.n_cols, rp, np.concatenate([head, tail]), val)
+
+
 def dense_inputs(fill, m, f, seed):
     """Reference bench seeds (proj/tools/autosage_bench.cpp:57-63, :269-270):
     B seed+F, X seed+F, Y seed+F+1."""

@@ -97,10 +97,13 @@ typedef struct as_graph_s* as_graph;
 as_status as_graph_create(const uint64_t* rowptr_host, const uint32_t* colind_host,
                           const float* val_host, uint64_t n_rows, uint64_t n_cols,
                           uint64_t nnz, int device, as_graph* out);
-/* Same from device arrays (copied; no validation of colind ordering). */
+/* Same from device arrays (copied).  The copies are ordered after the work
+ * already enqueued on `stream` (the stream that produced the arrays; NULL =
+ * the legacy default stream).  Validated on the device: rowptr as for
+ * as_graph_create; columns < n_cols and strictly increasing in each row. */
 as_status as_graph_create_device(const uint64_t* rowptr_dev, const uint32_t* colind_dev,
                                  const float* val_dev, uint64_t n_rows, uint64_t n_cols,
-                                 uint64_t nnz, int device, as_graph* out);
+                                 uint64_t nnz, int device, void* stream, as_graph* out);
 as_status as_graph_destroy(as_graph g);
 as_status as_graph_shape(as_graph g, uint64_t* n_rows, uint64_t* n_cols, uint64_t* nnz,
                          int* has_values);
@@ -361,6 +364,13 @@ as_status as_decide_sddmm(const as_context* ctx, const as_probe_config* cfg, as_
 as_status as_spmm_auto(const as_context* ctx, const as_probe_config* cfg, as_graph a,
                        const float* b_dev, uint64_t b_rows, uint64_t f, float* c_dev,
                        as_decision* decision);
+/* spmm_auto over explicit values vals_dev (nnz floats, device) instead of
+ * the graph's own: the same decision key (graph_sig excludes values,
+ * src/cache.cpp:66-74), so one cached pattern graph serves any edge
+ * weights (new; the torch ops pass weights per call). */
+as_status as_spmm_auto_values(const as_context* ctx, const as_probe_config* cfg, as_graph a,
+                              const float* vals_dev, const float* b_dev, uint64_t b_rows, uint64_t f,
+                              float* c_dev, as_decision* decision);
 as_status as_sddmm_auto(const as_context* ctx, const as_probe_config* cfg, as_graph pattern,
                         const float* x_dev, uint64_t x_rows, const float* y_dev,
                         uint64_t y_rows, uint64_t f, float* out_dev, as_decision* decision);

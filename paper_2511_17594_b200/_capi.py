@@ -123,7 +123,7 @@ _proto("as_variant_to_string", st, P(as_variant), C.c_char_p, C.c_size_t)
 _proto("as_variant_from_string", st, cp, P(as_variant))
 _proto("as_vec4_eligible", C.c_int, u64, P(vp), C.c_int)
 _proto("as_graph_create", st, vp, vp, vp, u64, u64, u64, C.c_int, P(vp))
-_proto("as_graph_create_device", st, vp, vp, vp, u64, u64, u64, C.c_int, P(vp))
+_proto("as_graph_create_device", st, vp, vp, vp, u64, u64, u64, C.c_int, vp, P(vp))
 _proto("as_graph_destroy", st, vp)
 _proto("as_graph_shape", st, vp, P(u64), P(u64), P(u64), P(C.c_int))
 _proto("as_graph_device_arrays", st, vp, P(vp), P(vp), P(vp))
@@ -176,6 +176,8 @@ _proto("as_decide_spmm", st, P(as_context), P(as_probe_config), vp, vp, u64, u64
 _proto("as_decide_sddmm", st, P(as_context), P(as_probe_config), vp, vp, u64, vp, u64, u64,
        P(as_decision))
 _proto("as_spmm_auto", st, P(as_context), P(as_probe_config), vp, vp, u64, u64, vp,
+       P(as_decision))
+_proto("as_spmm_auto_values", st, P(as_context), P(as_probe_config), vp, vp, vp, u64, u64, vp,
        P(as_decision))
 _proto("as_sddmm_auto", st, P(as_context), P(as_probe_config), vp, vp, u64, vp, u64, u64, vp,
        P(as_decision))

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <exception>
+#include <memory>
 #include <new>
 
 namespace asb {
@@ -174,12 +175,13 @@ as_status as_graph_create(const uint64_t* rowptr, const uint32_t* colind, const 
 }
 
 as_status as_graph_create_device(const uint64_t* rowptr, const uint32_t* colind, const float* val,
-                                 uint64_t n_rows, uint64_t n_cols, uint64_t nnz, int device,
+                                 uint64_t n_rows, uint64_t n_cols, uint64_t nnz, int device, void* stream,
                                  as_graph* out) {
     return guard([&] {
         if (!out) throw InvalidArgument("null output");
-        *out = reinterpret_cast<as_graph>(
-            graph_create_device(rowptr, colind, val, n_rows, n_cols, nnz, device).release());
+        *out = reinterpret_cast<as_graph>(graph_create_device(rowptr, colind, val, n_rows, n_cols, nnz, device,
+                                                              static_cast<cudaStream_t>(stream))
+                                              .release());
     });
 }
 
@@ -290,6 +292,7 @@ static as_status spmm_entry(const as_variant* v, as_graph a, const float* vals_d
     return guard([&] {
         Graph& g = G(a);
         cudaStream_t s = resolve_stream(g, stream);
+        GraphUse use(g, s);
         if (!v) {
             KernelResult r;
             r.variant = default_variant();
@@ -339,6 +342,7 @@ as_status as_spmm_rowparallel(const as_variant* v, as_graph a, const float* b_de
     return guard([&] {
         if (!v) throw InvalidArgument("null variant");
         Graph& g = G(a);
+        GraphUse use(g, resolve_stream(g, stream));
         spmm_mapped(*v, AS_MAP_ROWPARALLEL, g, graph_values(g, nullptr), b_dev, b_rows, f, c_dev,
                     resolve_stream(g, stream));
     });
@@ -349,6 +353,7 @@ as_status as_spmm_hubsplit(const as_variant* v, as_graph a, const float* b_dev, 
     return guard([&] {
         if (!v) throw InvalidArgument("null variant");
         Graph& g = G(a);
+        GraphUse use(g, resolve_stream(g, stream));
         spmm_mapped(*v, AS_MAP_HUBSPLIT, g, graph_values(g, nullptr), b_dev, b_rows, f, c_dev,
                     resolve_stream(g, stream));
     });
@@ -360,6 +365,7 @@ as_status as_sddmm(const as_variant* v, as_graph pattern, const float* x_dev, ui
     return guard([&] {
         Graph& g = G(pattern);
         cudaStream_t s = resolve_stream(g, stream);
+        GraphUse use(g, s);
         if (!v) {
             KernelResult r;
             r.variant = default_variant();
@@ -397,6 +403,7 @@ as_status as_sddmm_rowparallel(const as_variant* v, as_graph pattern, const floa
     return guard([&] {
         if (!v) throw InvalidArgument("null variant");
         Graph& g = G(pattern);
+        GraphUse use(g, resolve_stream(g, stream));
         sddmm_mapped(*v, g, x_dev, x_rows, y_dev, y_rows, f, out_dev, resolve_stream(g, stream));
     });
 }
@@ -404,6 +411,7 @@ as_status as_sddmm_rowparallel(const as_variant* v, as_graph pattern, const floa
 as_status as_row_softmax(as_graph m, const float* vals_dev, float* out_dev, void* stream) {
     return guard([&] {
         Graph& g = G(m);
+        GraphUse use(g, resolve_stream(g, stream));
         row_softmax(g, graph_values(g, vals_dev), out_dev, resolve_stream(g, stream));
     });
 }
@@ -413,26 +421,34 @@ as_status as_row_softmax(as_graph m, const float* vals_dev, float* out_dev, void
 // values come back in slices that overlap the remaining kernels.
 as_status as_spmm_host(const as_variant* v, as_graph a, const float* b_host, uint64_t b_rows,
                        uint64_t f, float* c_host, as_kernel_result* res) {
-    return guard([&] { fill_result(res, spmm_host(v, G(a), b_host, b_rows, f, c_host, true)); });
+    return guard([&] {
+        GraphUse use(G(a), G(a).stream);
+        fill_result(res, spmm_host(v, G(a), b_host, b_rows, f, c_host, true));
+    });
 }
 
 as_status as_sddmm_host(const as_variant* v, as_graph pattern, const float* x_host, uint64_t x_rows,
                         const float* y_host, uint64_t y_rows, uint64_t f, float* out_host,
                         as_kernel_result* res) {
     return guard([&] {
+        GraphUse use(G(pattern), G(pattern).stream);
         fill_result(res, sddmm_host(v, G(pattern), x_host, x_rows, y_host, y_rows, f, out_host, true));
     });
 }
 
 as_status as_spmm_host_async(const as_variant* v, as_graph a, const float* b_host, uint64_t b_rows,
                              uint64_t f, float* c_host, as_kernel_result* res) {
-    return guard([&] { fill_result(res, spmm_host(v, G(a), b_host, b_rows, f, c_host, false)); });
+    return guard([&] {
+        GraphUse use(G(a), G(a).stream);
+        fill_result(res, spmm_host(v, G(a), b_host, b_rows, f, c_host, false));
+    });
 }
 
 as_status as_sddmm_host_async(const as_variant* v, as_graph pattern, const float* x_host,
                               uint64_t x_rows, const float* y_host, uint64_t y_rows, uint64_t f,
                               float* out_host, as_kernel_result* res) {
     return guard([&] {
+        GraphUse use(G(pattern), G(pattern).stream);
         fill_result(res, sddmm_host(v, G(pattern), x_host, x_rows, y_host, y_rows, f, out_host, false));
     });
 }
@@ -445,6 +461,7 @@ as_status as_row_softmax_host(as_graph m, const float* vals_host, float* out_hos
     return guard([&] {
         Graph& g = G(m);
         DeviceGuard dg(g.device);
+        GraphUse use(g, g.stream);
         const float* vin = nullptr;
         if (vals_host) {
             g.stage_in.ensure(std::max<std::uint64_t>(g.nnz, 1));
@@ -587,7 +604,9 @@ void as_replay_policy_from_env(as_replay_policy* out) { *out = replay_policy_fro
 as_status as_decide_spmm(const as_context* ctx, const as_probe_config* cfg, as_graph a,
                          const float* b_dev, uint64_t b_rows, uint64_t f, as_decision* out) {
     return guard([&] {
-        *out = decide_spmm(make_ctx(ctx), cfg_or_default(cfg), G(a), nullptr, b_dev, b_rows, f);
+        const Context c = make_ctx(ctx);
+        GraphUse use(G(a), c.stream ? c.stream : G(a).stream);
+        *out = decide_spmm(c, cfg_or_default(cfg), G(a), nullptr, b_dev, b_rows, f);
     });
 }
 
@@ -595,8 +614,9 @@ as_status as_decide_sddmm(const as_context* ctx, const as_probe_config* cfg, as_
                           const float* x_dev, uint64_t x_rows, const float* y_dev, uint64_t y_rows,
                           uint64_t f, as_decision* out) {
     return guard([&] {
-        *out = decide_sddmm(make_ctx(ctx), cfg_or_default(cfg), G(pattern), x_dev, x_rows, y_dev,
-                            y_rows, f);
+        const Context c = make_ctx(ctx);
+        GraphUse use(G(pattern), c.stream ? c.stream : G(pattern).stream);
+        *out = decide_sddmm(c, cfg_or_default(cfg), G(pattern), x_dev, x_rows, y_dev, y_rows, f);
     });
 }
 
@@ -604,7 +624,21 @@ as_status as_spmm_auto(const as_context* ctx, const as_probe_config* cfg, as_gra
                        const float* b_dev, uint64_t b_rows, uint64_t f, float* c_dev,
                        as_decision* decision) {
     return guard([&] {
-        spmm_auto(make_ctx(ctx), cfg_or_default(cfg), G(a), nullptr, b_dev, b_rows, f, c_dev, decision);
+        const Context c = make_ctx(ctx);
+        GraphUse use(G(a), c.stream ? c.stream : G(a).stream);
+        spmm_auto(c, cfg_or_default(cfg), G(a), nullptr, b_dev, b_rows, f, c_dev, decision);
+    });
+}
+
+as_status as_spmm_auto_values(const as_context* ctx, const as_probe_config* cfg, as_graph a,
+                              const float* vals_dev, const float* b_dev, uint64_t b_rows, uint64_t f,
+                              float* c_dev, as_decision* decision) {
+    return guard([&] {
+        Graph& g = G(a);
+        if (!vals_dev && g.nnz) throw InvalidArgument("spmm_auto_values: values required");
+        const Context c = make_ctx(ctx);
+        GraphUse use(g, c.stream ? c.stream : g.stream);
+        spmm_auto(c, cfg_or_default(cfg), g, vals_dev, b_dev, b_rows, f, c_dev, decision);
     });
 }
 
@@ -612,8 +646,9 @@ as_status as_sddmm_auto(const as_context* ctx, const as_probe_config* cfg, as_gr
                         const float* x_dev, uint64_t x_rows, const float* y_dev, uint64_t y_rows,
                         uint64_t f, float* out_dev, as_decision* decision) {
     return guard([&] {
-        sddmm_auto(make_ctx(ctx), cfg_or_default(cfg), G(pattern), x_dev, x_rows, y_dev, y_rows, f,
-                   out_dev, decision);
+        const Context c = make_ctx(ctx);
+        GraphUse use(G(pattern), c.stream ? c.stream : G(pattern).stream);
+        sddmm_auto(c, cfg_or_default(cfg), G(pattern), x_dev, x_rows, y_dev, y_rows, f, out_dev, decision);
     });
 }
 
@@ -634,8 +669,10 @@ as_status as_csr_attention_forward(const as_context* ctx, const as_probe_config*
                                    uint64_t v_rows, uint64_t f, uint64_t fv, float* out_dev,
                                    int fused, as_decision* sd, as_decision* pd) {
     return guard([&] {
-        attention_forward(make_ctx(ctx), cfg_or_default(cfg), G(pattern), q_dev, q_rows, k_dev, k_rows,
-                          v_dev, v_rows, f, fv, out_dev, fused != 0, sd, pd);
+        const Context c = make_ctx(ctx);
+        GraphUse use(G(pattern), c.stream ? c.stream : G(pattern).stream);
+        attention_forward(c, cfg_or_default(cfg), G(pattern), q_dev, q_rows, k_dev, k_rows, v_dev, v_rows, f,
+                          fv, out_dev, fused != 0, sd, pd);
     });
 }
 
@@ -646,7 +683,9 @@ as_status as_csr_attention_forward_p(const as_context* ctx, const as_probe_confi
     return guard([&] {
         Graph& g = G(pattern);
         if (g.nnz && !p_dev) throw InvalidArgument("attention: p output required");
-        attention_forward(make_ctx(ctx), cfg_or_default(cfg), g, q_dev, q_rows, k_dev, k_rows, v_dev, v_rows, f,
+        const Context c = make_ctx(ctx);
+        GraphUse use(g, c.stream ? c.stream : g.stream);
+        attention_forward(c, cfg_or_default(cfg), g, q_dev, q_rows, k_dev, k_rows, v_dev, v_rows, f,
                           fv, out_dev, false, sd, pd, p_dev);
     });
 }
@@ -678,7 +717,8 @@ as_status as_graph_transpose_perm(as_graph gt, const uint32_t** perm) {
 }
 
 // ValPermScope: the graph reads its values through its transpose
-// permutation for one call (graph handles run one operator at a time)
+// permutation for one call, set and cleared while the caller holds the
+// graph (GraphUse), so no other operator sees it
 struct ValPermScope {
     Graph& g;
     explicit ValPermScope(Graph& gr) : g(gr) { g.val_perm = g.src_perm.get(); }
@@ -696,6 +736,9 @@ as_status as_spmm_transpose_values(const as_variant* v, as_graph gt, const float
         gp = &g;
     });
     if (st != AS_OK) return st;
+    std::unique_ptr<GraphUse> use;
+    const as_status st2 = guard([&] { use = std::make_unique<GraphUse>(*gp, resolve_stream(*gp, stream)); });
+    if (st2 != AS_OK) return st2;
     ValPermScope scope(*gp);
     return spmm_entry(v, gt, vals_src_dev, b_dev, b_rows, f, c_dev, stream, res);
 }
@@ -706,6 +749,7 @@ as_status as_permute_values(as_graph gt, const float* src_dev, float* dst_dev, v
         if (!g.is_transpose) throw InvalidArgument("permute_values: graph is not a transpose");
         if (g.nnz && (!src_dev || !dst_dev)) throw InvalidArgument("permute_values: null array");
         DeviceGuard dg(g.device);
+        GraphUse use(g, resolve_stream(g, stream));
         launch_permute(src_dev, g.src_perm.get(), g.nnz, dst_dev, resolve_stream(g, stream));
     });
 }
@@ -715,6 +759,7 @@ as_status as_spmm_bf16(const as_variant* v, as_graph a, const float* vals_dev, c
     return guard([&] {
         Graph& g = G(a);
         if (g.n_rows && f && (!b_dev || !c_dev)) throw InvalidArgument("spmm_bf16: null operand");
+        GraphUse use(g, resolve_stream(g, stream));
         const KernelResult r = dispatch_spmm_bf16(v, g, vals_dev, b_dev, b_rows, f, c_dev,
                                                   resolve_stream(g, stream), res != nullptr);
         fill_result(res, r);
@@ -727,6 +772,7 @@ as_status as_sddmm_bf16(const as_variant* v, as_graph pattern, const uint16_t* x
     return guard([&] {
         Graph& g = G(pattern);
         if (g.nnz && f && (!x_dev || !y_dev || !out_dev)) throw InvalidArgument("sddmm_bf16: null operand");
+        GraphUse use(g, resolve_stream(g, stream));
         const KernelResult r = dispatch_sddmm_bf16(v, g, x_dev, x_rows, y_dev, y_rows, f, out_dev,
                                                    resolve_stream(g, stream), res != nullptr);
         fill_result(res, r);
@@ -740,6 +786,7 @@ as_status as_row_softmax_backward(as_graph m, const float* p_dev, const float* g
         if (g.nnz && (!p_dev || !grad_dev || !ds_dev))
             throw InvalidArgument("row_softmax_backward: null array");
         DeviceGuard dg(g.device);
+        GraphUse use(g, resolve_stream(g, stream));
         launch_row_softmax_backward(g, p_dev, grad_dev, ds_dev, resolve_stream(g, stream));
     });
 }

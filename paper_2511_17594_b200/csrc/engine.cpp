@@ -80,40 +80,32 @@ Record to_record(const as_decision& d) {  // src/scheduler.cpp:72-82
     return rec;
 }
 
-// AUTOSAGE_PROBE_FLUSH_L2=<MiB> (default 256, 0 = off): before each timed
-// probe run, overwrite that many MiB on the probe stream, outside the timed
-// events, so candidates are timed from a cold L2 -- the condition of a step
-// whose operands were evicted since the last op (bench.py flushes between
-// steps).  A warm-L2 probe on the small sample ranks mappings whose cold
-// costs differ: c1 (1.6M nnz, F=64) picked rowparallel (0.143-0.147 ms on a
-// cold step) in 3 of 3 runs, the cold probe hub-split (0.105 ms) in 3 of 3;
-// Reddit-shape picks are unchanged.  One scratch buffer per device.
-void probe_flush_l2(cudaStream_t s) {
+// AUTOSAGE_PROBE_FLUSH_L2=<MiB> (default: twice the device's L2, 0 = off):
+// before each timed probe run, overwrite that many bytes on the probe
+// stream, outside the timed events, so candidates are timed from a cold L2
+// -- the condition of a step whose operands were evicted since the last op
+// (bench.py flushes between steps).  A warm-L2 probe on the small sample
+// ranks mappings whose cold costs differ: c1 (1.6M nnz, F=64) picked
+// rowparallel (0.143-0.147 ms on a cold step) in 3 of 3 runs, the cold probe
+// hub-split (0.105 ms) in 3 of 3; Reddit-shape picks are unchanged.  The
+// buffer lives for one decide call (allocated only when the CUDA-event timer
+// runs) and is freed with it.
+std::size_t probe_flush_bytes() {
     const auto knob = env::get_int("AUTOSAGE_PROBE_FLUSH_L2");
-    const long long mib = knob ? *knob : 256;
-    if (mib <= 0) return;
-    static std::mutex mu;
-    static std::map<int, std::pair<void*, std::size_t>> bufs;
-    int dev = 0;
+    if (knob) return *knob > 0 ? std::size_t(*knob) << 20 : 0;
+    int dev = 0, l2 = 0;
     ASB_CUDA(cudaGetDevice(&dev));
-    const std::size_t bytes = std::size_t(mib) << 20;
-    std::lock_guard<std::mutex> lk(mu);
-    auto& b = bufs[dev];
-    if (b.second < bytes) {
-        if (b.first) ASB_CUDA(cudaFree(b.first));
-        b = {nullptr, 0};
-        ASB_CUDA(cudaMalloc(&b.first, bytes));
-        b.second = bytes;
-    }
-    ASB_CUDA(cudaMemsetAsync(b.first, int(b.second >> 20) & 0xff, bytes, s));
+    ASB_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
+    return std::size_t(std::max(l2, 1 << 20)) * 2;
 }
 
-TimeOnce event_timer(cudaStream_t s) {
-    return [s](const std::string&, const std::function<void()>& run) {
+TimeOnce event_timer(cudaStream_t s, std::shared_ptr<DevBuf<char>> flush) {
+    return [s, flush](const std::string&, const std::function<void()>& run) {
         cudaEvent_t e0, e1;
         ASB_CUDA(cudaEventCreate(&e0));
         ASB_CUDA(cudaEventCreate(&e1));
-        probe_flush_l2(s);
+        if (flush && flush->size())
+            ASB_CUDA(cudaMemsetAsync(flush->get(), 0x5a, flush->size(), s));
         ASB_CUDA(cudaEventRecord(e0, s));
         run();
         ASB_CUDA(cudaEventRecord(e1, s));
@@ -185,7 +177,12 @@ as_decision decide_common(const Context& ctx, const as_probe_config& cfg,
     const std::uint64_t sample_rows = hooks.prepare ? hooks.prepare() : 0;
     d.sample_ms = ms_since(t_phase);
 
-    TimeOnce timer = ctx.timer ? ctx.timer : event_timer(hooks.stream);
+    std::shared_ptr<DevBuf<char>> flush;
+    if (!ctx.timer) {
+        flush = std::make_shared<DevBuf<char>>();
+        if (const std::size_t fb = probe_flush_bytes()) flush->alloc(fb);
+    }
+    TimeOnce timer = ctx.timer ? ctx.timer : event_timer(hooks.stream, flush);
     std::lock_guard<std::mutex> probe_lock(g_probe_mutex);
     cudaStream_t ps = hooks.stream;
     set_warmup_sync(ps ? std::function<void()>([ps] { cudaStreamSynchronize(ps); })
@@ -279,10 +276,20 @@ void check_sddmm_dims(const Graph& p, std::uint64_t x_rows, std::uint64_t y_rows
 // XU pipe is a limiter.  A gathered operand larger than ~3/4 of L2 streams from
 // DRAM, where the widening is not on the critical path (Products-shape B,
 // 980 MB: the scan alone was 0.15 ms per call).
+// A probe sample scans its operand once (decide_*'s prepare hook) and
+// freezes the flag, so candidate timings do not include a scan the
+// baseline's do not.
 const unsigned* mix_flag(Graph& g, const float* p, std::uint64_t n, cudaStream_t s) {
     constexpr std::uint64_t kMaxBytes = std::uint64_t(96) << 20;
     if (n * 4 > kMaxBytes) return nullptr;
+    if (g.flag_frozen) return g.flag.get();
     return finite_flag(g, p, n, s);
+}
+
+void freeze_mix_flag(Graph& g, const float* p, std::uint64_t n, cudaStream_t s) {
+    g.flag_frozen = false;
+    mix_flag(g, p, n, s);
+    g.flag_frozen = true;
 }
 
 // rmax/rsum (softmax mode, fused attention): vals are raw scores and the
@@ -676,6 +683,7 @@ as_decision decide_spmm(const Context& ctx, const as_probe_config& cfg, Graph& a
         const auto rows = sample_row_indices(a, cfg.frac, probe_min_rows(a, cfg, dp));
         sample = slice_rows(a, rows, graph_values(a, vals));
         ensure_order(*sample);
+        freeze_mix_flag(*sample, b, a.n_cols * f, s);
         cbuf.alloc(std::max<std::uint64_t>(rows.size() * f, 1));
         return rows.size();
     };
@@ -711,6 +719,7 @@ as_decision decide_sddmm(const Context& ctx, const as_probe_config& cfg, Graph& 
         xs.alloc(std::max<std::uint64_t>(ns * f, 1));
         gather_dense_rows(x, f, rows, xs.get(), s);
         obuf.alloc(std::max<std::uint64_t>(sample->nnz, 1));
+        freeze_mix_flag(*sample, y, y_rows * f, s);
         return ns;
     };
     h.run_baseline = [&] { launch_sddmm_baseline(*sample, xs.get(), y, std::uint32_t(f), obuf.get(), s); };

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstring>
 #include <thread>
+#include <tuple>
 
 namespace asb {
 
@@ -95,6 +96,27 @@ __global__ void gather_rows_kernel(const float* __restrict__ src, std::uint64_t 
     }
 }
 
+// Structure check of a device-built CSR (src/csr.cpp:62-93: columns in range,
+// strictly increasing within each row): bit 0 = a column >= n_cols, bit 1 =
+// a row whose columns do not increase.  Warp per row, lanes over entries.
+__global__ void validate_cols_kernel(const std::uint64_t* __restrict__ rowptr, std::uint64_t n_rows,
+                                     const std::uint32_t* __restrict__ colind, std::uint64_t n_cols,
+                                     unsigned* __restrict__ bad) {
+    const unsigned lane = threadIdx.x & 31;
+    unsigned mine = 0;
+    for (std::uint64_t i = (blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x) >> 5; i < n_rows;
+         i += (std::uint64_t(gridDim.x) * blockDim.x) >> 5) {
+        const std::uint64_t e0 = rowptr[i], e1 = rowptr[i + 1];
+        for (std::uint64_t e = e0 + lane; e < e1; e += 32) {
+            const std::uint32_t c = colind[e];
+            if (c >= n_cols) mine |= 1u;
+            if (e > e0 && colind[e - 1] >= c) mine |= 2u;
+        }
+    }
+    mine = __reduce_or_sync(0xffffffffu, mine);
+    if (lane == 0 && mine) atomicOr(bad, mine);
+}
+
 unsigned grid_for(std::uint64_t n, unsigned block, unsigned cap = 148u * 16u) {
     std::uint64_t g = (n + block - 1) / block;
     if (g == 0) g = 1;
@@ -114,6 +136,7 @@ Graph::~Graph() {
     }
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
+    if (ev_last_op) cudaEventDestroy(ev_last_op);
     for (cudaStream_t q : {pipe.h2d, pipe.d2h}) {
         if (q) {
             cudaStreamSynchronize(q);
@@ -169,7 +192,9 @@ static std::unique_ptr<Graph> alloc_graph(std::uint64_t n_rows, std::uint64_t n_
     g->n_cols = n_cols;
     g->nnz = nnz;
     g->has_val = has_val;
+    g->sms = device_sms();
     ASB_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+    ASB_CUDA(cudaEventCreateWithFlags(&g->ev_last_op, cudaEventDisableTiming));
     g->rowptr.alloc(n_rows + 1);
     g->colind.alloc(nnz);
     if (has_val) g->val.alloc(nnz);
@@ -202,9 +227,18 @@ std::unique_ptr<Graph> graph_create_host(const std::uint64_t* rowptr, const std:
 
 std::unique_ptr<Graph> graph_create_device(const std::uint64_t* rowptr, const std::uint32_t* colind,
                                            const float* val, std::uint64_t n_rows,
-                                           std::uint64_t n_cols, std::uint64_t nnz, int device) {
+                                           std::uint64_t n_cols, std::uint64_t nnz, int device,
+                                           cudaStream_t caller) {
+    if (rowptr == nullptr) throw InvalidArgument("graph: rowptr required");
+    if (nnz > 0 && colind == nullptr) throw InvalidArgument("graph: colind required");
     auto g = alloc_graph(n_rows, n_cols, nnz, val != nullptr && nnz > 0, device);
     DeviceGuard dg(g->device);
+    // the caller's arrays may still be in flight on its stream: copy after them
+    cudaEvent_t ready = nullptr;
+    ASB_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    ASB_CUDA(cudaEventRecord(ready, caller));
+    ASB_CUDA(cudaStreamWaitEvent(g->stream, ready, 0));
+    cudaEventDestroy(ready);
     ASB_CUDA(cudaMemcpyAsync(g->rowptr.get(), rowptr, (n_rows + 1) * 8, cudaMemcpyDeviceToDevice,
                              g->stream));
     if (nnz) {
@@ -216,12 +250,69 @@ std::unique_ptr<Graph> graph_create_device(const std::uint64_t* rowptr, const st
     ASB_CUDA(cudaMemcpyAsync(g->h_rowptr.data(), rowptr, (n_rows + 1) * 8, cudaMemcpyDeviceToHost,
                              g->stream));
     ASB_CUDA(cudaStreamSynchronize(g->stream));
-    if (g->h_rowptr[0] != 0 || g->h_rowptr[n_rows] != nnz)
-        throw InvalidArgument("graph: rowptr/nnz mismatch");
+    if (g->h_rowptr[0] != 0) throw InvalidArgument("graph: rowptr[0] != 0 at index 0");
+    if (g->h_rowptr[n_rows] != nnz) throw InvalidArgument("graph: rowptr[n_rows] != nnz at index " +
+                                                          std::to_string(n_rows));
     for (std::uint64_t i = 1; i <= n_rows; ++i)
         if (g->h_rowptr[i] < g->h_rowptr[i - 1])
             throw InvalidArgument("graph: rowptr non-decreasing at index " + std::to_string(i));
+    if (nnz) {
+        DevBuf<unsigned> bad(1);
+        ASB_CUDA(cudaMemsetAsync(bad.get(), 0, 4, g->stream));
+        validate_cols_kernel<<<grid_for(n_rows * 32, 256, unsigned(g->sms) * 8u), 256, 0, g->stream>>>(
+            g->rowptr.get(), n_rows, g->colind.get(), n_cols, bad.get());
+        check_launch("validate_cols_kernel");
+        unsigned hb = 0;
+        ASB_CUDA(cudaMemcpyAsync(&hb, bad.get(), 4, cudaMemcpyDeviceToHost, g->stream));
+        ASB_CUDA(cudaStreamSynchronize(g->stream));
+        if (hb & 1u) throw InvalidArgument("graph: column index >= n_cols");
+        if (hb & 2u) throw InvalidArgument("graph: columns not strictly increasing within a row");
+    }
     return g;
+}
+
+// ---- operator serialisation and launch setup ---------------------------------------
+GraphUse::GraphUse(Graph& g, cudaStream_t s) : g_(g), s_(s), lk_(g.op_mu) {
+    if (g_.op_depth++ == 0 && g_.last_op_stream && g_.last_op_stream != s_)
+        ASB_CUDA(cudaStreamWaitEvent(s_, g_.ev_last_op, 0));
+}
+
+GraphUse::~GraphUse() {
+    if (--g_.op_depth == 0) {
+        if (cudaEventRecord(g_.ev_last_op, s_) == cudaSuccess) g_.last_op_stream = s_;
+        else g_.last_op_stream = nullptr;
+    }
+}
+
+int device_sms() {
+    static std::mutex mu;
+    static std::map<int, int> cache;
+    int dev = 0;
+    ASB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    int sms = 148;
+    ASB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    cache[dev] = sms;
+    return sms;
+}
+
+int kernel_setup(const void* kernel, std::size_t smem, int threads) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, int, std::size_t, int>, int> done;
+    int dev = 0;
+    ASB_CUDA(cudaGetDevice(&dev));
+    const auto key = std::make_tuple(kernel, dev, smem, threads);
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = done.find(key);
+    if (it != done.end()) return it->second;
+    if (smem > 48 * 1024)
+        ASB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int per_sm = 1;
+    ASB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+    done[key] = per_sm;
+    return per_sm;
 }
 
 // graph_sig (src/cache.cpp:66-74), memoized.  colind streams down in chunks
@@ -579,14 +670,13 @@ __global__ void finite_check_bf16_kernel(const unsigned short* __restrict__ p, s
 
 const unsigned* finite_flag_bf16(Graph& g, const unsigned short* p, std::uint64_t n, cudaStream_t s) {
     g.flag.ensure(1);
-    ASB_CUDA(cudaMemsetAsync(g.flag.get(), 0, 4, s));
-    if (n == 0 || p == nullptr) return g.flag.get();
-    ASB_CUDA(cudaMemsetAsync(g.flag.get(), 1, 1, s));
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // nothing to widen: 0, the safe path; else 0x01010101 (nonzero = finite)
+    // until the scan clears it -- one memset
+    const bool empty = n == 0 || p == nullptr;
+    ASB_CUDA(cudaMemsetAsync(g.flag.get(), empty ? 0 : 1, 4, s));
+    if (empty) return g.flag.get();
     const std::uint64_t want = (n / 8 + 255) / 256 + 1;
-    const unsigned blocks = unsigned(std::min<std::uint64_t>(want, std::uint64_t(sms) * 8));
+    const unsigned blocks = unsigned(std::min<std::uint64_t>(want, std::uint64_t(g.sms) * 8));
     finite_check_bf16_kernel<<<blocks, 256, 0, s>>>(p, n, g.flag.get());
     check_launch("finite_check_bf16_kernel");
     return g.flag.get();
@@ -594,14 +684,13 @@ const unsigned* finite_flag_bf16(Graph& g, const unsigned short* p, std::uint64_
 
 const unsigned* finite_flag(Graph& g, const float* p, std::uint64_t n, cudaStream_t s) {
     g.flag.ensure(1);
-    ASB_CUDA(cudaMemsetAsync(g.flag.get(), 0, 4, s));
-    if (n == 0 || p == nullptr) return g.flag.get();  // nothing to widen: take the safe path
-    ASB_CUDA(cudaMemsetAsync(g.flag.get(), 1, 1, s));  // little-endian 1u
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // nothing to widen: 0, the safe path; else 0x01010101 (nonzero = finite)
+    // until the scan clears it -- one memset
+    const bool empty = n == 0 || p == nullptr;
+    ASB_CUDA(cudaMemsetAsync(g.flag.get(), empty ? 0 : 1, 4, s));
+    if (empty) return g.flag.get();
     const std::uint64_t want = (n / 4 + 255) / 256 + 1;
-    const unsigned blocks = unsigned(std::min<std::uint64_t>(want, std::uint64_t(sms) * 8));
+    const unsigned blocks = unsigned(std::min<std::uint64_t>(want, std::uint64_t(g.sms) * 8));
     finite_check_kernel<<<blocks, 256, 0, s>>>(p, n, g.flag.get());
     check_launch("finite_check_kernel");
     return g.flag.get();

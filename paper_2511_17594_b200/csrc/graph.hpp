@@ -73,6 +73,7 @@ struct HubPlan {
 
 struct Graph {
     int device = 0;
+    int sms = 148;  // multiprocessors of `device` (queried once at creation)
     std::uint64_t n_rows = 0, n_cols = 0, nnz = 0;
     bool has_val = false;
     // kernel-path heuristics see this many entries (a probe sample stands in
@@ -103,6 +104,7 @@ struct Graph {
     DevBuf<float> stage_in, stage_out; // host-buffer row softmax
     std::map<std::uint64_t, std::uint64_t> ge_count;  // rows with degree >= key
     DevBuf<unsigned> flag;             // finiteness flag of the current dense operand
+    bool flag_frozen = false;          // probe sample: flag computed once per decide
     DevBuf<double> xwide;              // SDDMM: X widened to f64 (fixed-width path)
     bool is_transpose = false;         // built by transpose_graph (backward.cu) ...
     DevBuf<std::uint32_t> src_perm;    // ... entry k came from source entry src_perm[k]
@@ -111,6 +113,14 @@ struct Graph {
     const std::uint32_t* val_perm = nullptr;
     cudaStream_t aux = nullptr;        // fork/join stream for concurrent kernels
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+
+    // operator serialisation (GraphUse): the scratch above is per graph, so
+    // operators on one handle run one at a time -- host side under op_mu,
+    // device side ordered across streams by ev_last_op
+    std::recursive_mutex op_mu;
+    int op_depth = 0;
+    cudaStream_t last_op_stream = nullptr;
+    cudaEvent_t ev_last_op = nullptr;
 
     // host-buffer pipeline (as_*_host, as_*_host_async): copies in on h2d,
     // kernels on `stream`, copies out on d2h; per-op staging so an SpMM and
@@ -143,13 +153,50 @@ struct DeviceGuard {
     }
 };
 
+// One operator call on a graph handle.  The handle's scratch (X widening,
+// hub partials, finite flag, attention buffers, the transpose's value
+// permutation) is shared by every operator on it, so calls serialise: a
+// recursive host mutex (entry points nest: attention -> SDDMM -> SpMM), and
+// on the device the outermost call on stream s waits for the previous call's
+// work when that was enqueued on another stream (one event per graph).  A
+// graph can therefore be used from several threads and streams; its
+// operators never overlap one another.
+class GraphUse {
+public:
+    GraphUse(Graph& g, cudaStream_t s);
+    ~GraphUse();
+    GraphUse(const GraphUse&) = delete;
+    GraphUse& operator=(const GraphUse&) = delete;
+
+private:
+    Graph& g_;
+    cudaStream_t s_;
+    std::unique_lock<std::recursive_mutex> lk_;
+};
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) and the occupancy query
+// of a kernel, once per (kernel, device, smem, threads) -- off the per-launch
+// path.  Returns resident CTAs per SM.
+int kernel_setup(const void* kernel, std::size_t smem, int threads);
+template <class K>
+int kernel_setup(K* kernel, std::size_t smem, int threads) {
+    return kernel_setup(reinterpret_cast<const void*>(kernel), smem, threads);
+}
+// multiprocessors of the current device (cached per device)
+int device_sms();
+
 std::unique_ptr<Graph> graph_create_host(const std::uint64_t* rowptr, const std::uint32_t* colind,
                                          const float* val, std::uint64_t n_rows,
                                          std::uint64_t n_cols, std::uint64_t nnz, int device,
                                          bool validate);
+// Device arrays in: the copies run after the work already enqueued on
+// `caller` (the stream that produced them; nullptr = legacy default stream),
+// and the structure is validated on the device (columns in range and
+// strictly increasing per row, src/csr.cpp:62-93).
 std::unique_ptr<Graph> graph_create_device(const std::uint64_t* rowptr, const std::uint32_t* colind,
                                            const float* val, std::uint64_t n_rows,
-                                           std::uint64_t n_cols, std::uint64_t nnz, int device);
+                                           std::uint64_t n_cols, std::uint64_t nnz, int device,
+                                           cudaStream_t caller);
 cudaStream_t resolve_stream(Graph& g, void* stream);
 
 std::uint64_t graph_sig(Graph& g);

@@ -917,12 +917,7 @@ bool fixed_eligible(const float* x, const float* y, std::uint32_t f, std::uint32
 // all four components re-biased on the ALU pipe (dev knob; default: half)
 int mix_all() { return dev_knob("AUTOSAGE_DEV_SDDMM_MIXALL", 0); }
 
-int sm_count() {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return sms;
-}
+int sm_count() { return device_sms(); }
 
 // X widened to f64 (prepass of the fixed-width path, once per call)
 // rows [r0, r1) of X (the host pipeline widens each slice's rows as they land)
@@ -946,9 +941,7 @@ void launch_sddmm_fixed(Graph& g, const float* y, std::uint32_t f, float* out, s
     auto go = [&](auto kernel, std::uint64_t warp_bytes) {
         constexpr int kWarps = 8;
         const std::size_t smem = std::size_t(warp_bytes * kWarps);
-        ASB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        int per_sm = 1;
-        ASB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kWarps * 32, smem));
+        const int per_sm = kernel_setup(kernel, smem, int(kWarps * 32));
         const std::uint64_t want = (c_end - c_begin + kWarps - 1) / kWarps;
         const std::uint64_t cap = std::uint64_t(sms) * std::max(per_sm, 1);
         const unsigned blocks = unsigned(std::max<std::uint64_t>(1, std::min(want, cap)));
@@ -975,9 +968,7 @@ void launch_sddmm_fixed(Graph& g, const float* y, std::uint32_t f, float* out, s
             const int kWarps = 4;
             auto run = [&](auto kernel) {
                 const std::size_t smem = std::size_t(wb * kWarps);
-                ASB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-                int per_sm = 1;
-                ASB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kWarps * 32, smem));
+                const int per_sm = kernel_setup(kernel, smem, int(kWarps * 32));
                 const std::uint64_t pairs = (c_end - c_begin + 1) / 2;
                 const std::uint64_t want = (pairs + kWarps - 1) / kWarps;
                 const std::uint64_t cap = std::uint64_t(sms) * std::max(per_sm, 1);
@@ -1002,9 +993,7 @@ void launch_sddmm_fixed(Graph& g, const float* y, std::uint32_t f, float* out, s
                 const int kWarps = 4;
                 auto run = [&](auto kernel) {
                     const std::size_t smem = std::size_t(wb * kWarps);
-                    ASB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-                    int per_sm = 1;
-                    ASB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kWarps * 32, smem));
+                    const int per_sm = kernel_setup(kernel, smem, int(kWarps * 32));
                     const std::uint64_t pairs = (c_end - c_begin + 1) / 2;
                     const std::uint64_t want = (pairs + kWarps - 1) / kWarps;
                     const std::uint64_t cap = std::uint64_t(sms) * std::max(per_sm, 1);
@@ -1120,10 +1109,8 @@ void launch_sddmm_chunks(Graph& g, const float* x, const float* y, std::uint32_t
     }
     const std::size_t smem = std::size_t(per_warp * wpb);
     const int sms = sm_count();
-    int per_sm = 1;
     auto go = [&](auto kernel) {
-        ASB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        ASB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, int(wpb * 32), smem));
+        const int per_sm = kernel_setup(kernel, smem, int(wpb * 32));
         const std::uint64_t want = (c_end - c_begin + wpb - 1) / wpb;
         const std::uint64_t cap = std::uint64_t(sms) * std::max(per_sm, 1);
         const unsigned blocks = unsigned(std::max<std::uint64_t>(1, std::min(want, cap)));
@@ -1188,9 +1175,7 @@ void launch_sddmm_bf16(Graph& g, const std::uint16_t* x, const std::uint16_t* y,
         const int kWarps = 4;
         auto run = [&](auto kernel) {
             const std::size_t smem = std::size_t(wbytes * kWarps);
-            ASB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-            int per_sm = 1;
-            ASB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kWarps * 32, smem));
+            const int per_sm = kernel_setup(kernel, smem, int(kWarps * 32));
             const std::uint64_t pairs = (c_end + 1) / 2;
             const std::uint64_t want = (pairs + kWarps - 1) / kWarps;
             const std::uint64_t cap = std::uint64_t(sms) * std::max(per_sm, 1);

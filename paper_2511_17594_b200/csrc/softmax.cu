@@ -393,12 +393,10 @@ void launch_softmax(Graph& g, const float* vin, float* vout, float* rmax, double
         al.n = n_long;
         cudaStream_t aux = n_short ? graph_fork(g, s) : s;
         constexpr int smem = 2 * kCtaSmem * 4;
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int sms = g.sms;
         const unsigned grid = unsigned(std::min<std::uint64_t>(n_long, std::uint64_t(sms) * 3));
         auto go = [&](auto kern) {
-            ASB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            kernel_setup(kern, smem, 256);
             kern<<<grid, 256, smem, aux>>>(al);
         };
         g.sm_chain_row.ensure(n_long);
@@ -418,9 +416,7 @@ void launch_softmax(Graph& g, const float* vin, float* vout, float* rmax, double
         check_launch("softmax_chain_kernel");
     }
     if (n_short) {
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int sms = g.sms;
         a.order = g.order.get() + n_long;
         a.n = n_short;
         const std::uint64_t want = (n_short + kWarpsPerCta - 1) / kWarpsPerCta;

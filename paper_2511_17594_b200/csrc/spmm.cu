@@ -317,7 +317,7 @@ void launch_longrow(const SegArgs& a, std::uint64_t n, cudaStream_t s) {
     const int fpl = f % 128 == 0 ? 4 : (f % 64 == 0 ? 2 : (f % 32 == 0 ? 1 : 4));
     const unsigned threads = 32 + (f / fpl + 31) / 32 * 32;
     auto go = [&](auto kern) {
-        ASB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        kernel_setup(kern, smem, int(threads));
         kern<<<unsigned(n), threads, smem, s>>>(a, ch);
         check_launch("spmm_longrow_kernel");
     };
@@ -686,10 +686,7 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const void* b, std::uint32
         // kernel's deep per-piece prefetch wins (c1: 0.163 -> 0.106 ms); with
         // thousands of pieces the group kernel's throughput wins (Products
         // 8-way shard: 1.36 ms vs 1.72 ms)
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const bool few = plan.n_pieces <= std::uint64_t(4) * std::uint64_t(sms);
+        const bool few = plan.n_pieces <= std::uint64_t(4) * std::uint64_t(g.sms);
         if (few && !bf16 && !g.val_perm && longrow_ok(f, vec)) launch_longrow<true>(a, plan.n_pieces, s);
         else if (v8) launch_seg_vec<8>(a, val != nullptr, t.lanes, wpb, s);
         else if (vec) launch_seg_vec<4>(a, val != nullptr, t.lanes, wpb, s);

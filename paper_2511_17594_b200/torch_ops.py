@@ -37,55 +37,87 @@ from . import (Graph, ProbeConfig, ScheduleCache, ScheduleContext, _check, _lib,
                variant_from_string)
 from . import _capi as _c
 
-_GRAPHS: "OrderedDict[tuple, Graph]" = OrderedDict()
-_TRANSPOSES: "OrderedDict[tuple, Graph]" = OrderedDict()
+_GRAPHS: "OrderedDict[tuple, _Entry]" = OrderedDict()
+_TRANSPOSES: "OrderedDict[tuple, _Entry]" = OrderedDict()
 _MAX_GRAPHS = 8
 _CACHE = None
 
 
-def _key(crow, col, val, n_cols):
-    return (crow.data_ptr(), col.data_ptr(), val.data_ptr() if val.numel() else 0, crow.numel() - 1,
-            int(n_cols), col.numel(), crow._version, col._version, val._version, crow.device.index)
+class _Entry:
+    """A cached device graph and the CSR tensors it was built from.  Holding
+    the tensors keeps their storage alive, so while the entry is cached no
+    other tensor can be allocated at the same addresses and hit it."""
+
+    __slots__ = ("graph", "crow", "col")
+
+    def __init__(self, graph: Graph, crow: torch.Tensor, col: torch.Tensor):
+        self.graph, self.crow, self.col = graph, crow, col
 
 
-def _graph(crow: torch.Tensor, col: torch.Tensor, val: torch.Tensor, n_cols: int) -> Graph:
+def _key(crow, col, n_cols):
+    # structure only: edge weights are passed per call (as_spmm_values /
+    # as_spmm_auto_values), so updating them never rebuilds the graph
+    return (crow.data_ptr(), col.data_ptr(), crow.numel() - 1, int(n_cols), col.numel(), crow._version,
+            col._version, crow.device.index)
+
+
+def _check_csr(crow: torch.Tensor, col: torch.Tensor):
     if not (crow.is_cuda and col.is_cuda):
         raise ValueError("autosage ops take CUDA CSR tensors")
     if crow.dtype != torch.int64 or col.dtype != torch.int32:
         raise ValueError("crow must be int64 and col int32")
-    k = _key(crow, col, val, n_cols)
-    g = _GRAPHS.get(k)
-    if g is not None:
+    if crow.dim() != 1 or col.dim() != 1 or crow.numel() < 1:
+        raise ValueError("crow and col must be 1-D (crow has n_rows + 1 entries)")
+
+
+def _graph(crow: torch.Tensor, col: torch.Tensor, n_cols: int) -> Graph:
+    """The pattern graph of (crow, col) with n_cols columns, uploaded and
+    validated on the device once (columns in range and increasing per row),
+    then cached per CSR storage."""
+    _check_csr(crow, col)
+    k = _key(crow, col, n_cols)
+    e = _GRAPHS.get(k)
+    if e is not None:
         _GRAPHS.move_to_end(k)
-        return g
+        return e.graph
     crow_c, col_c = crow.contiguous(), col.contiguous()
-    has_val = val.numel() > 0
-    val_c = val.contiguous().float() if has_val else None
     h = C.c_void_p()
-    _check(_lib.as_graph_create_device(C.c_void_p(crow_c.data_ptr()), C.c_void_p(col_c.data_ptr()),
-                                       C.c_void_p(val_c.data_ptr()) if has_val else None,
+    # the copies are ordered after torch's current stream (which produced the arrays)
+    _check(_lib.as_graph_create_device(C.c_void_p(crow_c.data_ptr()), C.c_void_p(col_c.data_ptr()), None,
                                        crow_c.numel() - 1, int(n_cols), col_c.numel(),
-                                       crow.device.index or 0, C.byref(h)))
+                                       crow.device.index or 0, _stream(crow), C.byref(h)))
     g = Graph(h.value, crow.device.index or 0)
-    _GRAPHS[k] = g
+    _GRAPHS[k] = _Entry(g, crow, col)
     while len(_GRAPHS) > _MAX_GRAPHS:
-        _GRAPHS.popitem(last=False)[1].close()
+        _GRAPHS.popitem(last=False)[1].graph.close()
     return g
 
 
 def _transpose(crow: torch.Tensor, col: torch.Tensor, n_cols: int) -> Graph:
     """Pattern-only A^T (device), cached per CSR storage like _graph."""
-    empty = torch.empty(0, dtype=torch.float32, device=crow.device)
-    k = _key(crow, col, empty, n_cols)
-    g = _TRANSPOSES.get(k)
-    if g is not None:
+    k = _key(crow, col, n_cols)
+    e = _TRANSPOSES.get(k)
+    if e is not None:
         _TRANSPOSES.move_to_end(k)
-        return g
-    g = _graph(crow, col, empty, n_cols).transpose()
-    _TRANSPOSES[k] = g
+        return e.graph
+    g = _graph(crow, col, n_cols).transpose()
+    _TRANSPOSES[k] = _Entry(g, crow, col)
     while len(_TRANSPOSES) > _MAX_GRAPHS:
-        _TRANSPOSES.popitem(last=False)[1].close()
+        _TRANSPOSES.popitem(last=False)[1].graph.close()
     return g
+
+
+def _values(val: torch.Tensor, nnz: int):
+    """Edge weights as f32 (None: pattern-only, implicit 1.0)."""
+    if val.numel() == 0:
+        return None
+    if val.numel() != nnz:
+        raise ValueError(f"values must have nnz = {nnz} entries (got {val.numel()})")
+    return val.contiguous().float()
+
+
+def _vptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
 
 
 def _variant(s: str):
@@ -109,18 +141,23 @@ def spmm_csr(crow: torch.Tensor, col: torch.Tensor, val: torch.Tensor, b: torch.
     """C = A B (dispatch(variant, A, B), src/kernels.cpp:485-506; "" = baseline).
     A bfloat16 B is read as bf16 (as_spmm_bf16: half the gather bytes, the
     f32 result on float(B) bit for bit); C is float32 either way."""
+    if b.dim() != 2:
+        raise ValueError("spmm_csr: b must be 2-D")
+    g = _graph(crow, col, b.shape[0])
+    vals = _values(val, g.nnz)
+    c = torch.empty((g.n_rows, b.shape[1]), dtype=torch.float32, device=b.device)
     if b.dtype == torch.bfloat16:
         b = b.contiguous()
-        g = _graph(crow, col, val, b.shape[0])
-        c = torch.empty((g.n_rows, b.shape[1]), dtype=torch.float32, device=b.device)
-        _check(_lib.as_spmm_bf16(_variant(variant), g.handle, None, C.c_void_p(b.data_ptr()), b.shape[0],
+        _check(_lib.as_spmm_bf16(_variant(variant), g.handle, _vptr(vals), C.c_void_p(b.data_ptr()), b.shape[0],
                                  b.shape[1], C.c_void_p(c.data_ptr()), _stream(b), None))
         return c
     b = b.contiguous().float()
-    g = _graph(crow, col, val, b.shape[0])
-    c = torch.empty((g.n_rows, b.shape[1]), dtype=torch.float32, device=b.device)
-    _check(_lib.as_spmm(_variant(variant), g.handle, C.c_void_p(b.data_ptr()), b.shape[0], b.shape[1],
-                        C.c_void_p(c.data_ptr()), _stream(b), None))
+    if vals is None:
+        _check(_lib.as_spmm(_variant(variant), g.handle, C.c_void_p(b.data_ptr()), b.shape[0], b.shape[1],
+                            C.c_void_p(c.data_ptr()), _stream(b), None))
+    else:
+        _check(_lib.as_spmm_values(_variant(variant), g.handle, _vptr(vals), C.c_void_p(b.data_ptr()),
+                                   b.shape[0], b.shape[1], C.c_void_p(c.data_ptr()), _stream(b), None))
     return c
 
 
@@ -132,14 +169,22 @@ def _(crow, col, val, b, variant):
 @torch.library.custom_op("autosage::spmm_csr_auto", mutates_args=())
 def spmm_csr_auto(crow: torch.Tensor, col: torch.Tensor, val: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     """spmm_auto (src/scheduler.cpp:226-232) with a process-wide schedule cache."""
+    if b.dim() != 2:
+        raise ValueError("spmm_csr_auto: b must be 2-D")
     b = b.contiguous().float()
-    g = _graph(crow, col, val, b.shape[0])
+    g = _graph(crow, col, b.shape[0])
+    vals = _values(val, g.nnz)
     c = torch.empty((g.n_rows, b.shape[1]), dtype=torch.float32, device=b.device)
     cctx, keep = _ctx(b).to_c()
     ccfg = ProbeConfig.from_env().to_c()
     d = _c.as_decision()
-    _check(_lib.as_spmm_auto(C.byref(cctx), C.byref(ccfg), g.handle, C.c_void_p(b.data_ptr()), b.shape[0],
-                             b.shape[1], C.c_void_p(c.data_ptr()), C.byref(d)))
+    if vals is None:
+        _check(_lib.as_spmm_auto(C.byref(cctx), C.byref(ccfg), g.handle, C.c_void_p(b.data_ptr()), b.shape[0],
+                                 b.shape[1], C.c_void_p(c.data_ptr()), C.byref(d)))
+    else:
+        _check(_lib.as_spmm_auto_values(C.byref(cctx), C.byref(ccfg), g.handle, _vptr(vals),
+                                        C.c_void_p(b.data_ptr()), b.shape[0], b.shape[1],
+                                        C.c_void_p(c.data_ptr()), C.byref(d)))
     del keep
     return c
 
@@ -155,23 +200,30 @@ def sddmm_csr(crow: torch.Tensor, col: torch.Tensor, x: torch.Tensor, y: torch.T
     """out[e] = <x[i], y[col[e]]> on A's pattern (src/kernels.cpp:336-429).
     bfloat16 x and y are read as bf16 (as_sddmm_bf16; the f32 result on the
     widened operands, bit for bit); out is float32 either way."""
+    _check_dense_pair("sddmm_csr", crow, x, y)
+    g = _graph(crow, col, y.shape[0])
+    out = torch.empty(col.numel(), dtype=torch.float32, device=x.device)
     if x.dtype == torch.bfloat16 and y.dtype == torch.bfloat16:
         x, y = x.contiguous(), y.contiguous()
-        empty = torch.empty(0, dtype=torch.float32, device=x.device)
-        g = _graph(crow, col, empty, y.shape[0])
-        out = torch.empty(col.numel(), dtype=torch.float32, device=x.device)
         _check(_lib.as_sddmm_bf16(_variant(variant), g.handle, C.c_void_p(x.data_ptr()), x.shape[0],
                                   C.c_void_p(y.data_ptr()), y.shape[0], x.shape[1],
                                   C.c_void_p(out.data_ptr()) if out.numel() else None, _stream(x), None))
         return out
     x, y = x.contiguous().float(), y.contiguous().float()
-    empty = torch.empty(0, dtype=torch.float32, device=x.device)
-    g = _graph(crow, col, empty, y.shape[0])
-    out = torch.empty(col.numel(), dtype=torch.float32, device=x.device)
     _check(_lib.as_sddmm(_variant(variant), g.handle, C.c_void_p(x.data_ptr()), x.shape[0],
                          C.c_void_p(y.data_ptr()), y.shape[0], x.shape[1],
                          C.c_void_p(out.data_ptr()) if out.numel() else None, _stream(x), None))
     return out
+
+
+def _check_dense_pair(name, crow, x, y):
+    """x: n_rows x F (one row per CSR row), y: n_cols x F (same F)."""
+    if x.dim() != 2 or y.dim() != 2:
+        raise ValueError(f"{name}: dense operands must be 2-D")
+    if x.shape[0] != crow.numel() - 1:
+        raise ValueError(f"{name}: x has {x.shape[0]} rows, the CSR {crow.numel() - 1}")
+    if x.shape[1] != y.shape[1]:
+        raise ValueError(f"{name}: feature widths differ ({x.shape[1]} vs {y.shape[1]})")
 
 
 @sddmm_csr.register_fake
@@ -185,11 +237,11 @@ def csr_attention(crow: torch.Tensor, col: torch.Tensor, q: torch.Tensor, k: tor
     """csr_attention_forward (src/attention.cpp:9-40), decisions cached.
     bfloat16 q, k and v take the staged bf16 route (_attention_bf16; `fused`
     does not apply there)."""
+    _check_attention(crow, q, k, v)
     if _all_bf16(q, k, v):
         return _attention_bf16(crow, col, q, k, v)[0]
     q, k, v = q.contiguous().float(), k.contiguous().float(), v.contiguous().float()
-    empty = torch.empty(0, dtype=torch.float32, device=q.device)
-    g = _graph(crow, col, empty, k.shape[0])
+    g = _graph(crow, col, k.shape[0])
     out = torch.empty((g.n_rows, v.shape[1]), dtype=torch.float32, device=q.device)
     cctx, keep = _ctx(q).to_c()
     ccfg = ProbeConfig.from_env().to_c()
@@ -208,6 +260,12 @@ def _(crow, col, q, k, v, fused):
     return q.new_empty((crow.shape[0] - 1, v.shape[1]), dtype=torch.float32)
 
 
+def _check_attention(crow, q, k, v):
+    _check_dense_pair("csr_attention", crow, q, k)
+    if v.dim() != 2 or v.shape[0] != k.shape[0]:
+        raise ValueError("csr_attention: k and v need the same row count")
+
+
 def _all_bf16(*ts) -> bool:
     return all(t.dtype == torch.bfloat16 for t in ts)
 
@@ -221,12 +279,11 @@ def _attention_bf16(crow, col, q, k, v):
     v.float() with the same variants, bit for bit, while the Q/K/V gathers
     read half the bytes.  out and p are float32."""
     q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
-    if k.shape[0] != v.shape[0]:
-        raise ValueError("csr_attention: k and v need the same row count")
+    _check_attention(crow, q, k, v)
     n_cols = k.shape[0]
     s = sddmm_csr(crow, col, q, k, _BWD_SDDMM)
     p = row_softmax_csr(crow, col, s, n_cols)
-    pat = _graph(crow, col, torch.empty(0, dtype=torch.float32, device=q.device), n_cols)
+    pat = _graph(crow, col, n_cols)
     out = torch.empty((pat.n_rows, v.shape[1]), dtype=torch.float32, device=q.device)
     _check(_lib.as_spmm_bf16(_variant(_BWD_SPMM), pat.handle, C.c_void_p(p.data_ptr()) if p.numel() else None,
                              C.c_void_p(v.data_ptr()), v.shape[0], v.shape[1], C.c_void_p(out.data_ptr()),
@@ -277,8 +334,9 @@ def _spmm_t(crow, col, vals, n_cols: int, dc: torch.Tensor) -> torch.Tensor:
 def row_softmax_csr(crow: torch.Tensor, col: torch.Tensor, s: torch.Tensor, n_cols: int) -> torch.Tensor:
     """row_softmax over explicit values (src/kernels.cpp:431-461)."""
     s = s.contiguous().float()
-    empty = torch.empty(0, dtype=torch.float32, device=s.device)
-    g = _graph(crow, col, empty, n_cols)
+    g = _graph(crow, col, n_cols)
+    if s.numel() != g.nnz:
+        raise ValueError(f"row_softmax_csr: {s.numel()} values for {g.nnz} entries")
     out = torch.empty_like(s)
     if s.numel():
         _check(_lib.as_row_softmax(g.handle, C.c_void_p(s.data_ptr()), C.c_void_p(out.data_ptr()),
@@ -296,8 +354,9 @@ def row_softmax_csr_backward(crow: torch.Tensor, col: torch.Tensor, p: torch.Ten
                              grad: torch.Tensor, n_cols: int) -> torch.Tensor:
     """ds = p * (grad - sum_row p*grad) (as_row_softmax_backward)."""
     p, grad = p.contiguous().float(), grad.contiguous().float()
-    empty = torch.empty(0, dtype=torch.float32, device=p.device)
-    g = _graph(crow, col, empty, n_cols)
+    g = _graph(crow, col, n_cols)
+    if p.numel() != g.nnz or grad.numel() != g.nnz:
+        raise ValueError("row_softmax_csr_backward: p and grad need nnz entries")
     ds = torch.empty_like(p)  # every entry is written (empty rows have none)
     if p.numel():
         _check(_lib.as_row_softmax_backward(g.handle, C.c_void_p(p.data_ptr()), C.c_void_p(grad.data_ptr()),
@@ -362,7 +421,7 @@ def _sddmm_bwd(ctx, dout):
     crow, col, x, y = ctx.saved_tensors
     dx = dy = None
     if ctx.needs_input_grad[2]:
-        dx = _spmm_vals(_graph(crow, col, torch.empty(0, device=x.device), y.shape[0]), dout, y).to(x.dtype)
+        dx = _spmm_vals(_graph(crow, col, y.shape[0]), dout, y).to(x.dtype)
     if ctx.needs_input_grad[3]:
         dy = _spmm_t(crow, col, dout, y.shape[0], x).to(y.dtype)
     return None, None, dx, dy, None
@@ -385,7 +444,7 @@ def _attention_bwd(ctx, do):
     dv = _spmm_t(crow, col, p, k.shape[0], do) if ctx.needs_input_grad[4] else None
     dp = sddmm_csr(crow, col, do, v, _BWD_SDDMM)
     ds = row_softmax_csr_backward(crow, col, p, dp, k.shape[0])
-    pat = _graph(crow, col, torch.empty(0, device=q.device), k.shape[0])
+    pat = _graph(crow, col, k.shape[0])
     dq = _spmm_vals(pat, ds, k).to(q.dtype) if ctx.needs_input_grad[2] else None
     dk = _spmm_t(crow, col, ds, k.shape[0], q).to(k.dtype) if ctx.needs_input_grad[3] else None
     return None, None, dq, dk, None if dv is None else dv.to(v.dtype), None
@@ -404,11 +463,11 @@ def csr_attention_with_probs(crow: torch.Tensor, col: torch.Tensor, q: torch.Ten
     softmax of the scores (nnz floats).  out is bit-identical to csr_attention;
     its backward reuses p instead of recomputing SDDMM + softmax.  bfloat16
     q, k and v take the staged bf16 route (_attention_bf16)."""
+    _check_attention(crow, q, k, v)
     if _all_bf16(q, k, v):
         return _attention_bf16(crow, col, q, k, v)
     q, k, v = q.contiguous().float(), k.contiguous().float(), v.contiguous().float()
-    empty = torch.empty(0, dtype=torch.float32, device=q.device)
-    g = _graph(crow, col, empty, k.shape[0])
+    g = _graph(crow, col, k.shape[0])
     out = torch.empty((g.n_rows, v.shape[1]), dtype=torch.float32, device=q.device)
     p = torch.empty(col.numel(), dtype=torch.float32, device=q.device)
     cctx, keep = _ctx(q).to_c()
@@ -449,7 +508,7 @@ def _attention_p_bwd(ctx, do, gp):
         dp = dp + gp
     ds = row_softmax_csr_backward(crow, col, p, dp, n_cols)
     if ctx.needs_input_grad[2]:
-        dq = _spmm_vals(_graph(crow, col, torch.empty(0, device=q.device), n_cols), ds, k).to(q.dtype)
+        dq = _spmm_vals(_graph(crow, col, n_cols), ds, k).to(q.dtype)
     if ctx.needs_input_grad[3]:
         dk = _spmm_t(crow, col, ds, n_cols, q).to(k.dtype)
     return None, None, dq, dk, None if dv is None else dv.to(v.dtype)

@@ -60,3 +60,83 @@ def test_attention_op_matches_library_path():
     got = torch.ops.autosage.csr_attention(crow, col, q, k, v, False)
     want = asb.csr_attention_forward(a, q, k, v)
     assert bit_equal(got.cpu().numpy(), want.cpu().numpy() if hasattr(want, "cpu") else want)
+
+
+@pytest.mark.gpu
+def test_graph_cache_survives_address_reuse_and_weight_updates():
+    """a freed CSR's addresses reused by a different graph must not
+    hit the stale cached graph; updating the weights in place must take
+    effect without rebuilding the structure."""
+    rng = np.random.default_rng(63)
+    b = random_dense(rng, 400, 32)
+    bt = torch.from_numpy(b).cuda()
+    for trial in range(4):
+        a = hub_graph(rng, 400, [300 - trial], 5 + trial)
+        crow, col, val = _csr(a)
+        got = torch.ops.autosage.spmm_csr(crow, col, val, bt, "").cpu().numpy()
+        assert bit_equal(got, oracle.spmm_baseline(a, b)), trial
+        del crow, col, val  # the next trial's tensors may land on the same addresses
+    a = hub_graph(rng, 400, [350], 9)
+    crow, col, val = _csr(a)
+    torch.ops.autosage.spmm_csr(crow, col, val, bt, "")
+    val.mul_(0.5)  # in place: same storage, new weights
+    w = a.val * np.float32(0.5)
+    want = oracle.spmm_baseline(asb.CsrMatrix(a.n_rows, a.n_cols, a.rowptr, a.colind, w), b)
+    assert bit_equal(torch.ops.autosage.spmm_csr(crow, col, val, bt, "").cpu().numpy(), want)
+    assert bit_equal(torch.ops.autosage.spmm_csr_auto(crow, col, val, bt).cpu().numpy(), want) or \
+        bit_equal(torch.ops.autosage.spmm_csr_auto(crow, col, val, bt).cpu().numpy(),
+                  oracle.spmm_hubsplit(asb.CsrMatrix(a.n_rows, a.n_cols, a.rowptr, a.colind, w), b, 256))
+
+
+@pytest.mark.gpu
+def test_ops_reject_malformed_operands():
+    rng = np.random.default_rng(64)
+    a = hub_graph(rng, 200, [150], 4)
+    crow, col, val = _csr(a)
+    b = torch.from_numpy(random_dense(rng, 200, 16)).cuda()
+    with pytest.raises(asb.InvalidArgument):  # a column past the dense operand's rows
+        torch.ops.autosage.spmm_csr(crow, col, val, b[:100], "")
+    bad = col.clone()
+    bad[1], bad[2] = col[2], col[1]  # row 0 (degree 150) out of order
+    with pytest.raises(asb.InvalidArgument):
+        torch.ops.autosage.spmm_csr(crow, bad, val, b, "")
+    x = torch.from_numpy(random_dense(rng, 200, 16)).cuda()
+    with pytest.raises(ValueError):  # feature widths differ
+        torch.ops.autosage.sddmm_csr(crow, col, x, b[:, :8].contiguous(), "")
+    with pytest.raises(ValueError):  # k and v row counts differ
+        torch.ops.autosage.csr_attention(crow, col, x, b, b[:150].contiguous(), False)
+    with pytest.raises(ValueError):  # weights of the wrong length
+        torch.ops.autosage.spmm_csr(crow, col, val[:-1], b, "")
+
+
+@pytest.mark.gpu
+def test_one_graph_from_two_streams_and_threads():
+    """operators on one cached graph from different streams and
+    threads share its scratch; they must serialise (GraphUse), giving the
+    same bits as one stream."""
+    import threading
+    rng = np.random.default_rng(65)
+    a = hub_graph(rng, 3000, [2500, 2100, 900], 30)
+    crow, col, val = _csr(a)
+    xs = [torch.from_numpy(random_dense(rng, 3000, 64)).cuda() for _ in range(4)]
+    want_s = [oracle.sddmm(a, x.cpu().numpy(), x.cpu().numpy(), 64, False) for x in xs]
+    want_c = [oracle.spmm_hubsplit(a, x.cpu().numpy(), 64) for x in xs]
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    outs = [None] * 4
+    torch.ops.autosage.spmm_csr(crow, col, val, xs[0], "")  # build + cache the graph first
+    torch.cuda.synchronize()
+
+    def work(i):
+        with torch.cuda.stream(streams[i]):
+            for _ in range(3):
+                s = torch.ops.autosage.sddmm_csr(crow, col, xs[i], xs[i], "sddmm:rowparallel:ft=32:rpc=1:vec=0:hubt=256")
+                c = torch.ops.autosage.spmm_csr(crow, col, val, xs[i], "spmm:hubsplit:ft=64:rpc=1:vec=1:hubt=64")
+            streams[i].synchronize()
+            outs[i] = (s.cpu().numpy(), c.cpu().numpy())
+    th = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for i in range(4):
+        assert bit_equal(outs[i][0], want_s[i]) and bit_equal(outs[i][1], want_c[i]), i

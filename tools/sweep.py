@@ -199,29 +199,7 @@ def case_c3(res):
     res["c3"] = out
 
 
-def with_hubs(m, hub_degrees, seed):
-    """Replace the first rows by hubs of the given degrees (distinct sorted
-    columns), keeping the rest of the power-law graph."""
-    rng = np.random.default_rng(seed)
-    deg = np.diff(m.rowptr.astype(np.int64))
-    rows = []
-    for i in range(m.n_rows):
-        if i < len(hub_degrees):
-            cols = np.sort(rng.permutation(m.n_cols)[:hub_degrees[i]]).astype(np.uint32)
-        else:
-            break
-        rows.append(cols)
-    k = len(rows)
-    head = np.concatenate(rows)
-    tail = m.colind[int(m.rowptr[k]):]
-    deg2 = np.concatenate([np.array([r.size for r in rows], np.int64), deg[k:]])
-    rp = np.zeros(m.n_rows + 1, np.uint64)
-    rp[1:] = np.cumsum(deg2)
-    val = None
-    if m.val is not None:
-        val = np.concatenate([asb.fill_uniform(head.size, seed, (head.size,)) * 0.5 + 0.5,
-                              m.val[int(m.rowptr[k]):]]).astype(np.float32)
-    return asb.CsrMatrix(m.n_rows, m.n_cols, rp, np.concatenate([head, tail]), val)
+with_hubs = bench.with_hubs
 
 
 def case_c4(res):
