@@ -206,7 +206,9 @@ std::unique_ptr<Graph> transpose_graph(Graph& g) {
     t->n_cols = g.n_rows;
     t->nnz = g.nnz;
     t->has_val = g.has_val;
+    t->sms = g.sms;
     ASB_CUDA(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
+    ASB_CUDA(cudaEventCreateWithFlags(&t->ev_last_op, cudaEventDisableTiming));
     t->rowptr.alloc(t->n_rows + 1);
     t->colind.alloc(g.nnz);
     if (t->has_val) t->val.alloc(g.nnz);

@@ -273,14 +273,19 @@ std::unique_ptr<Graph> graph_create_device(const std::uint64_t* rowptr, const st
 
 // ---- operator serialisation and launch setup ---------------------------------------
 GraphUse::GraphUse(Graph& g, cudaStream_t s) : g_(g), s_(s), lk_(g.op_mu) {
+    if (!g_.ev_last_op) ASB_CUDA(cudaEventCreateWithFlags(&g_.ev_last_op, cudaEventDisableTiming));
     if (g_.op_depth++ == 0 && g_.last_op_stream && g_.last_op_stream != s_)
         ASB_CUDA(cudaStreamWaitEvent(s_, g_.ev_last_op, 0));
 }
 
 GraphUse::~GraphUse() {
     if (--g_.op_depth == 0) {
-        if (cudaEventRecord(g_.ev_last_op, s_) == cudaSuccess) g_.last_op_stream = s_;
-        else g_.last_op_stream = nullptr;
+        if (cudaEventRecord(g_.ev_last_op, s_) == cudaSuccess) {
+            g_.last_op_stream = s_;
+        } else {
+            g_.last_op_stream = nullptr;
+            (void)cudaGetLastError();  // a destructor cannot throw: do not leave it sticky
+        }
     }
 }
 
