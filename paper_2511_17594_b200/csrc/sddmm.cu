@@ -21,6 +21,7 @@
 // (widen.cuh) when Y is finite.  Row pitch: an odd number of 16-byte units,
 // so each lane's LDS.128 walk along its own row is conflict-free.
 #include "ops.hpp"
+#include "l2hint.cuh"
 #include "widen.cuh"
 
 #include <algorithm>
@@ -769,7 +770,7 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
                                                 const std::uint32_t* __restrict__ chunk_row, std::uint64_t n_rows,
                                                 const double* __restrict__ xd, const void* __restrict__ yv,
                                                 float* __restrict__ out, std::uint64_t nnz, std::uint64_t c_begin,
-                                                std::uint64_t c_end) {
+                                                std::uint64_t c_end, int keep) {
     using Sh = Pair1Shape<F, BF>;
     using YT = typename std::conditional<BF, unsigned short, float>::type;
     constexpr int kUnitElems = 16 / Sh::kYElem;  // Y elements per 16-byte unit
@@ -782,6 +783,9 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
     const std::uint64_t e_end = min(c_end * 32, nnz);
     const std::uint64_t n_pairs = (c_end - c_begin + 1) / 2;
     const std::uint64_t stride = std::uint64_t(gridDim.x) * (blockDim.x >> 5);
+    // colind and the outputs stream once (evict_first); Y rows and the
+    // widened X are re-read for every entry that hits them (evict_last)
+    const std::uint64_t pol_s = l2_evict_first(), pol_k = l2_reuse_policy(keep != 0);
 
     struct Meta {
         std::uint32_t ca, cb, r_first;
@@ -791,8 +795,8 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
         Meta m{0u, 0u, 0u, ~0ull};
         if (pc >= n_pairs) return m;
         const std::uint64_t e0 = (c_begin + 2 * pc) * 32;
-        m.ca = e0 + lane < e_end ? __ldg(colind + e0 + lane) : 0u;
-        m.cb = e0 + 32 + lane < e_end ? __ldg(colind + e0 + 32 + lane) : 0u;
+        m.ca = e0 + lane < e_end ? ld_stream(colind + e0 + lane, pol_s) : 0u;
+        m.cb = e0 + 32 + lane < e_end ? ld_stream(colind + e0 + 32 + lane, pol_s) : 0u;
         m.r_first = __ldg(chunk_row + c_begin + 2 * pc);
         const std::uint64_t bi = std::uint64_t(m.r_first) + 1 + lane;
         if (bi <= n_rows) m.bound = __ldg(rowptr + bi);
@@ -807,13 +811,14 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
             const int idx = it * 32 + lane;
             const int j = idx / Sh::NV, q = idx % Sh::NV;
             const std::uint32_t cj = __shfl_sync(FULL, j < 32 ? cur.ca : cur.cb, j & 31);
-            cp_async16(ys + j * F + kUnitElems * (q ^ swz<Sh::NV>(j)), y + std::uint64_t(cj) * F + kUnitElems * q);
+            cp_async16_pol(ys + j * F + kUnitElems * (q ^ swz<Sh::NV>(j)), y + std::uint64_t(cj) * F + kUnitElems * q,
+                           pol_k);
         }
 #pragma unroll
         for (int u = lane; u < Sh::kXUnits; u += 32) {
             const int k = u / (F / 2), uu = u % (F / 2);
             const std::uint64_t xr = std::uint64_t(cur.r_first) + k;
-            if (xr < n_rows) cp_async16(xs + 2 * u, xd + xr * F + 2 * uu);
+            if (xr < n_rows) cp_async16_pol(xs + 2 * u, xd + xr * F + 2 * uu, pol_k);
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
         const Meta nxt = meta(pc + stride);
@@ -850,8 +855,8 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
             pair1_pass<F, ORD, FT, false, MIX, false, BF>(xd + std::uint64_t(ra) * F, xd + std::uint64_t(rb) * F,
                                                          ya, yb, ka, kb, c);
         }
-        if (ea < e_end) out[ea] = float(c[0][0]);
-        if (eb < e_end) out[eb] = float(c[1][0]);
+        if (ea < e_end) st_stream(out + ea, float(c[0][0]), pol_s);
+        if (eb < e_end) st_stream(out + eb, float(c[1][0]), pol_s);
         __syncwarp();
         cur = nxt;
     }
@@ -867,11 +872,14 @@ __global__ void __launch_bounds__(128, MINB)
                       const std::uint32_t* __restrict__ chunk_row, std::uint64_t n_rows,
                       const double* __restrict__ xd, const void* __restrict__ y, float* __restrict__ out,
                       std::uint64_t nnz, std::uint32_t /*f*/, std::uint64_t c_begin, std::uint64_t c_end,
-                      const unsigned* __restrict__ finite, int /*mix_all*/) {
+                      const unsigned* __restrict__ finite, int keep) {
+    // keep: Y fits the L2 (kKeepMaxBytes) -- the Y and X staging reads evict_last
     if (finite && *finite)
-        sddmm_pair1_body<F, ORD, FT, 1, BF>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin, c_end);
+        sddmm_pair1_body<F, ORD, FT, 1, BF>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin, c_end,
+                                            keep);
     else
-        sddmm_pair1_body<F, ORD, FT, 0, BF>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin, c_end);
+        sddmm_pair1_body<F, ORD, FT, 0, BF>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin, c_end,
+                                            keep);
 }
 
 // Guardrail baseline / large-F fallback: lane per entry, both rows read
@@ -937,6 +945,9 @@ void widen_x(Graph& g, const float* x, std::uint32_t f, cudaStream_t s, const un
 
 void launch_sddmm_fixed(Graph& g, const float* y, std::uint32_t f, float* out, std::uint32_t ft, int ord,
                         cudaStream_t s, const unsigned* finite, std::uint64_t c_begin, std::uint64_t c_end) {
+    // Y (re-read by every entry of its column) fits the L2 beside the
+    // streams: the staging reads evict_last
+    const int keep_y = int(std::uint64_t(g.n_cols) * f * 4 <= kKeepMaxBytes);
     const int sms = sm_count();
     auto go = [&](auto kernel, std::uint64_t warp_bytes) {
         constexpr int kWarps = 8;
@@ -1000,7 +1011,7 @@ void launch_sddmm_fixed(Graph& g, const float* y, std::uint32_t f, float* out, s
                     const unsigned blocks = unsigned(std::max<std::uint64_t>(1, std::min(want, cap)));
                     kernel<<<blocks, kWarps * 32, smem, s>>>(g.rowptr.get(), g.colind.get(), g.chunk_row.get(),
                                                              g.n_rows, g.xwide.get(), y, out, g.nnz, f, c_begin,
-                                                             c_end, finite, mix_all());
+                                                             c_end, finite, keep_y);
                     check_launch("sddmm_pair_kernel");
                 };
                 // F=32 stages 8.7 KB per warp, so shared memory admits more than 3
@@ -1181,7 +1192,8 @@ void launch_sddmm_bf16(Graph& g, const std::uint16_t* x, const std::uint16_t* y,
             const std::uint64_t cap = std::uint64_t(sms) * std::max(per_sm, 1);
             const unsigned blocks = unsigned(std::max<std::uint64_t>(1, std::min(want, cap)));
             kernel<<<blocks, kWarps * 32, smem, s>>>(g.rowptr.get(), g.colind.get(), g.chunk_row.get(), g.n_rows,
-                                                     g.xwide.get(), y, out, g.nnz, f, 0, c_end, fin, mix_all());
+                                                     g.xwide.get(), y, out, g.nnz, f, 0, c_end, fin,
+                                                     int(std::uint64_t(g.n_cols) * f * 2 <= kKeepMaxBytes));
             check_launch("sddmm_pair_kernel");
         };
         // 4 resident CTAs (<= 128 registers): Reddit-shape F=32 1.32 -> 1.16 ms,

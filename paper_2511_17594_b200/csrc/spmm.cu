@@ -627,6 +627,7 @@ void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uin
         a.f = f;
         a.off32 = fast_gather_ok(g, f);
         a.bf16 = bf16;
+        a.keep_b = std::uint64_t(g.n_cols) * f * (bf16 ? 2 : 4) <= kKeepMaxBytes;
         a.tile_w = t.tile_w;
         wpb = warps_per_cta(wpb);
         if (v8) launch_seg_vec<8>(a, val != nullptr, t.lanes, wpb, s);
@@ -680,6 +681,7 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const void* b, std::uint32
         a.f = f;
         a.off32 = fast_gather_ok(g, f);
         a.bf16 = bf16;
+        a.keep_b = std::uint64_t(g.n_cols) * f * (bf16 ? 2 : 4) <= kKeepMaxBytes;
         a.tile_w = t.tile_w;
         // pieces are up to 2048-entry dependent chains: when there are too
         // few of them to fill the lane-group kernel (under a wave), the ring

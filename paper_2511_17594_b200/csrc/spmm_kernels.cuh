@@ -5,6 +5,7 @@
 #pragma once
 
 #include "ops.hpp"
+#include "l2hint.cuh"
 #include "softmax.cuh"
 #include "widen.cuh"
 
@@ -35,6 +36,7 @@ struct SegArgs {
     const double* rsum;               // p_e = softmax of the row (softmax.cuh)
     int off32;                        // n_cols * f < 2^32: 32-bit element offsets
     int bf16;                         // B holds bf16 (seg kernels' BF instantiation)
+    int keep_b;                       // B fits L2 (kKeepMaxBytes): gathers evict_last
     std::uint64_t n_items;
     std::uint32_t n_tiles;
     std::uint32_t f;
@@ -195,6 +197,8 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
     // (a separate instantiation: a runtime branch here cost the forward kernel ~3%)
     const std::uint32_t* vpp = VP ? a.vperm + e0 : nullptr;
     const BT* __restrict__ bmat = static_cast<const BT*>(a.b);
+    // CSR streams once (evict_first); B is re-gathered ~mean-degree times (evict_last)
+    const std::uint64_t pol_s = l2_evict_first(), pol_k = l2_reuse_policy(a.keep_b != 0);
 
     // Fast path: while every group of the warp still has W whole entries
     // left and every lane's features are in range, no predicates at all (a
@@ -233,11 +237,11 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
 #pragma unroll
                 for (int s = 0; s < S; ++s) {
                     const std::uint32_t k = base + std::uint32_t(s * LPR + gl);
-                    const std::uint32_t o = __ldg(colp + k) * f;
+                    const std::uint32_t o = ld_stream(colp + k, pol_s) * f;
                     float v;
-                    if constexpr (SMX) v = sm_prob_of(__ldg(valp + k), rmx, rsm, rrc);
-                    else if constexpr (VP) v = __ldg(a.val + __ldg(vpp + k));
-                    else if constexpr (HAS_VAL) v = __ldg(valp + k);
+                    if constexpr (SMX) v = sm_prob_of(ld_stream(valp + k, pol_s), rmx, rsm, rrc);
+                    else if constexpr (VP) v = __ldg(a.val + ld_stream(vpp + k, pol_s));
+                    else if constexpr (HAS_VAL) v = ld_stream(valp + k, pol_s);
                     else v = 1.f;
                     if constexpr (E64) ent[s * 32 + lane] = make_uint2(__float_as_uint(v), o);
                     else ent[s * 32 + lane] = make_double2(double(v), __hiloint2double(0, int(o)));
@@ -264,7 +268,7 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
                     for (int u = 0; u < U; ++u)
 #pragma unroll
                         for (int ch = 0; ch < NCH; ++ch)
-                            bv[u][ch] = __ldg(reinterpret_cast<const VT*>(bl[ch] + oj[u]));
+                            bv[u][ch] = ld_keep(reinterpret_cast<const VT*>(bl[ch] + oj[u]), pol_k);
 #pragma unroll
                     for (int u = 0; u < U; ++u)
                         seg_accumulate<VEC, NCH, MIX, VT, mix_from<VEC, BF>()>(acc, vj[u], bv[u]);
@@ -280,10 +284,10 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
         for (int s = 0; s < S; ++s) {
             const std::uint32_t k = base + std::uint32_t(s * LPR + gl);
             const bool ok = k < deg;
-            cs[s] = ok ? __ldg(colp + k) : 0u;
-            if constexpr (SMX) vs[s] = ok ? double(sm_prob_of(__ldg(valp + k), rmx, rsm, rrc)) : 0.0;
-            else if constexpr (VP) vs[s] = ok ? double(__ldg(a.val + __ldg(vpp + k))) : 0.0;
-            else if constexpr (HAS_VAL) vs[s] = ok ? double(__ldg(valp + k)) : 0.0;
+            cs[s] = ok ? ld_stream(colp + k, pol_s) : 0u;
+            if constexpr (SMX) vs[s] = ok ? double(sm_prob_of(ld_stream(valp + k, pol_s), rmx, rsm, rrc)) : 0.0;
+            else if constexpr (VP) vs[s] = ok ? double(__ldg(a.val + ld_stream(vpp + k, pol_s))) : 0.0;
+            else if constexpr (HAS_VAL) vs[s] = ok ? double(ld_stream(valp + k, pol_s)) : 0.0;
             else vs[s] = 1.0;
         }
 #pragma unroll
@@ -305,8 +309,8 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch) {
                     if (okj && fok[ch])
-                        bv[u][ch] = __ldg(reinterpret_cast<const VT*>(
-                            bmat + std::uint64_t(cj[u]) * a.f + fidx[ch]));
+                        bv[u][ch] = ld_keep(reinterpret_cast<const VT*>(
+                            bmat + std::uint64_t(cj[u]) * a.f + fidx[ch]), pol_k);
                 }
             }
 #pragma unroll
@@ -338,7 +342,7 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
         if (!PIECES || slot == 0xffffffffu) {
             float* cp = a.c + std::uint64_t(row) * a.f + fidx[ch];
 #pragma unroll
-            for (int q = 0; q < VEC; ++q) cp[q] = float(acc[ch][q]);
+            for (int q = 0; q < VEC; ++q) st_stream(cp + q, float(acc[ch][q]), pol_s);
         } else {
             double* sp = a.scratch + std::uint64_t(slot) * a.f + fidx[ch];
 #pragma unroll
