@@ -21,6 +21,7 @@
 // (widen.cuh) when Y is finite.  Row pitch: an odd number of 16-byte units,
 // so each lane's LDS.128 walk along its own row is conflict-free.
 #include "ops.hpp"
+#include "dcheck.cuh"
 #include "l2hint.cuh"
 #include "widen.cuh"
 
@@ -770,7 +771,8 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
                                                 const std::uint32_t* __restrict__ chunk_row, std::uint64_t n_rows,
                                                 const double* __restrict__ xd, const void* __restrict__ yv,
                                                 float* __restrict__ out, std::uint64_t nnz, std::uint64_t c_begin,
-                                                std::uint64_t c_end, int keep) {
+                                                std::uint64_t c_end, int keep, std::uint64_t n_cols) {
+    (void)n_cols;  // bounds of the checked build
     using Sh = Pair1Shape<F, BF>;
     using YT = typename std::conditional<BF, unsigned short, float>::type;
     constexpr int kUnitElems = 16 / Sh::kYElem;  // Y elements per 16-byte unit
@@ -811,6 +813,7 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
             const int idx = it * 32 + lane;
             const int j = idx / Sh::NV, q = idx % Sh::NV;
             const std::uint32_t cj = __shfl_sync(FULL, j < 32 ? cur.ca : cur.cb, j & 31);
+            ASB_DCHECK(cj < n_cols);
             cp_async16_pol(ys + j * F + kUnitElems * (q ^ swz<Sh::NV>(j)), y + std::uint64_t(cj) * F + kUnitElems * q,
                            pol_k);
         }
@@ -841,6 +844,9 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         __syncwarp();
         const std::uint32_t rela = ra - cur.r_first, relb = rb - cur.r_first;
+        ASB_DCHECK(ra < n_rows && rb < n_rows);
+        ASB_DCHECK(ea >= e_end || (rowptr[ra] <= ea && ea < rowptr[ra + 1]));
+        ASB_DCHECK(eb >= e_end || (rowptr[rb] <= eb && eb < rowptr[rb + 1]));
         double c[2][5] = {{0.0, 0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0, 0.0}};
         const YT* ya = ys + lane * F;
         const YT* yb = ys + (lane + 32) * F;
@@ -872,14 +878,14 @@ __global__ void __launch_bounds__(128, MINB)
                       const std::uint32_t* __restrict__ chunk_row, std::uint64_t n_rows,
                       const double* __restrict__ xd, const void* __restrict__ y, float* __restrict__ out,
                       std::uint64_t nnz, std::uint32_t /*f*/, std::uint64_t c_begin, std::uint64_t c_end,
-                      const unsigned* __restrict__ finite, int keep) {
+                      const unsigned* __restrict__ finite, int keep, std::uint64_t n_cols) {
     // keep: Y fits the L2 (kKeepMaxBytes) -- the Y and X staging reads evict_last
     if (finite && *finite)
         sddmm_pair1_body<F, ORD, FT, 1, BF>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin, c_end,
-                                            keep);
+                                            keep, n_cols);
     else
         sddmm_pair1_body<F, ORD, FT, 0, BF>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin, c_end,
-                                            keep);
+                                            keep, n_cols);
 }
 
 // Guardrail baseline / large-F fallback: lane per entry, both rows read
@@ -1011,7 +1017,7 @@ void launch_sddmm_fixed(Graph& g, const float* y, std::uint32_t f, float* out, s
                     const unsigned blocks = unsigned(std::max<std::uint64_t>(1, std::min(want, cap)));
                     kernel<<<blocks, kWarps * 32, smem, s>>>(g.rowptr.get(), g.colind.get(), g.chunk_row.get(),
                                                              g.n_rows, g.xwide.get(), y, out, g.nnz, f, c_begin,
-                                                             c_end, finite, keep_y);
+                                                             c_end, finite, keep_y, g.n_cols);
                     check_launch("sddmm_pair_kernel");
                 };
                 // F=32 stages 8.7 KB per warp, so shared memory admits more than 3
@@ -1193,7 +1199,7 @@ void launch_sddmm_bf16(Graph& g, const std::uint16_t* x, const std::uint16_t* y,
             const unsigned blocks = unsigned(std::max<std::uint64_t>(1, std::min(want, cap)));
             kernel<<<blocks, kWarps * 32, smem, s>>>(g.rowptr.get(), g.colind.get(), g.chunk_row.get(), g.n_rows,
                                                      g.xwide.get(), y, out, g.nnz, f, 0, c_end, fin,
-                                                     int(std::uint64_t(g.n_cols) * f * 2 <= kKeepMaxBytes));
+                                                     int(std::uint64_t(g.n_cols) * f * 2 <= kKeepMaxBytes), g.n_cols);
             check_launch("sddmm_pair_kernel");
         };
         // 4 resident CTAs (<= 128 registers): Reddit-shape F=32 1.32 -> 1.16 ms,

@@ -175,9 +175,11 @@ __device__ __forceinline__ void longrow_body(const SegArgs& A, std::uint32_t ch,
         slot = A.piece_slot[blockIdx.x];
     } else {
         row = A.rowlist[blockIdx.x];
+        ASB_DCHECK(row < A.n_rows);
         e0 = rowptr[row];
         deg = std::uint32_t(rowptr[row + 1] - e0);
     }
+    ASB_DCHECK(row < A.n_rows && e0 + deg <= A.nnz);
     const std::uint32_t nchunks = (deg + ch - 1) / ch;
     const int warp = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
     float rmx = 0.f;
@@ -237,6 +239,7 @@ __device__ __forceinline__ void longrow_body(const SegArgs& A, std::uint32_t ch,
             // incrementally (no division in the loop)
             std::uint32_t j = j0, qq = q0;
             for (std::uint32_t pidx = lane; pidx < n * per_row; pidx += 32) {
+                ASB_DCHECK(j < n && cs[j] < A.n_cols);
                 cp_async16(dst + j * f + 4 * qq, b + std::uint64_t(cs[j]) * f + 4 * qq);
                 j += dj;
                 qq += dq;
@@ -603,6 +606,9 @@ void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uin
         a.rmax = rmax;
         a.rsum = rsum;
         a.f = f;
+        a.n_rows = g.n_rows;
+        a.n_cols = g.n_cols;
+        a.nnz = g.nnz;
         a.off32 = fast_gather_ok(g, f);
         launch_longrow<false>(a, n_long, graph_fork(g, s));
         offset += n_long;
@@ -625,6 +631,9 @@ void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uin
         a.n_items = n_list * t.n_tiles;
         a.n_tiles = t.n_tiles;
         a.f = f;
+        a.n_rows = g.n_rows;
+        a.n_cols = g.n_cols;
+        a.nnz = g.nnz;
         a.off32 = fast_gather_ok(g, f);
         a.bf16 = bf16;
         a.keep_b = std::uint64_t(g.n_cols) * f * (bf16 ? 2 : 4) <= kKeepMaxBytes;
@@ -679,6 +688,9 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const void* b, std::uint32
         a.n_items = plan.n_pieces * t.n_tiles;
         a.n_tiles = t.n_tiles;
         a.f = f;
+        a.n_rows = g.n_rows;
+        a.n_cols = g.n_cols;
+        a.nnz = g.nnz;
         a.off32 = fast_gather_ok(g, f);
         a.bf16 = bf16;
         a.keep_b = std::uint64_t(g.n_cols) * f * (bf16 ? 2 : 4) <= kKeepMaxBytes;

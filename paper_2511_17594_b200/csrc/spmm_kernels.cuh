@@ -5,6 +5,7 @@
 #pragma once
 
 #include "ops.hpp"
+#include "dcheck.cuh"
 #include "l2hint.cuh"
 #include "softmax.cuh"
 #include "widen.cuh"
@@ -38,6 +39,7 @@ struct SegArgs {
     int bf16;                         // B holds bf16 (seg kernels' BF instantiation)
     int keep_b;                       // B fits L2 (kKeepMaxBytes): gathers evict_last
     std::uint64_t n_items;
+    std::uint64_t n_rows, n_cols, nnz;  // bounds of the checked build (dcheck.cuh)
     std::uint32_t n_tiles;
     std::uint32_t f;
     std::uint32_t tile_w;
@@ -159,9 +161,11 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
             slot = a.piece_slot[si];
         } else {
             row = a.rowlist ? a.rowlist[si] : std::uint32_t(si);
+            ASB_DCHECK(row < a.n_rows);
             e0 = a.rowptr[row];
             deg = std::uint32_t(a.rowptr[row + 1] - e0);
         }
+        ASB_DCHECK(row < a.n_rows && e0 + deg <= a.nnz);
     }
     std::uint32_t maxdeg = deg;
     if constexpr (GPW > 1) maxdeg = __reduce_max_sync(FULL, deg);
@@ -237,7 +241,9 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
 #pragma unroll
                 for (int s = 0; s < S; ++s) {
                     const std::uint32_t k = base + std::uint32_t(s * LPR + gl);
-                    const std::uint32_t o = ld_stream(colp + k, pol_s) * f;
+                    const std::uint32_t col = ld_stream(colp + k, pol_s);
+                    ASB_DCHECK(k < deg && col < a.n_cols);
+                    const std::uint32_t o = col * f;
                     float v;
                     if constexpr (SMX) v = sm_prob_of(ld_stream(valp + k, pol_s), rmx, rsm, rrc);
                     else if constexpr (VP) v = __ldg(a.val + ld_stream(vpp + k, pol_s));
@@ -285,6 +291,7 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
             const std::uint32_t k = base + std::uint32_t(s * LPR + gl);
             const bool ok = k < deg;
             cs[s] = ok ? ld_stream(colp + k, pol_s) : 0u;
+            ASB_DCHECK(cs[s] < a.n_cols);
             if constexpr (SMX) vs[s] = ok ? double(sm_prob_of(ld_stream(valp + k, pol_s), rmx, rsm, rrc)) : 0.0;
             else if constexpr (VP) vs[s] = ok ? double(__ldg(a.val + ld_stream(vpp + k, pol_s))) : 0.0;
             else if constexpr (HAS_VAL) vs[s] = ok ? double(ld_stream(valp + k, pol_s)) : 0.0;
