@@ -635,6 +635,11 @@ __device__ __forceinline__ void sddmm_pair_body(const std::uint64_t* __restrict_
                 rb = row_of(rowptr, rb, eb < e_end ? eb : e_end - 1);
             }
         }
+        // lanes past the last entry (tail chunk) counted the trailing empty
+        // rows' boundaries too and may sit at n_rows: park them on a real row
+        // (their results are not stored; found by the checked build)
+        if (ea >= e_end) ra = cur.r_first;
+        if (eb >= e_end) rb = cur.r_first;
         const std::uint32_t rela = ra - cur.r_first, relb = rb - cur.r_first;
         const bool staged = rela < Sh::KX && relb < Sh::KX;
         double c[2][5] = {{0.0, 0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0, 0.0}};
@@ -843,6 +848,11 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
         }
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         __syncwarp();
+        // lanes past the last entry (tail chunk) counted the trailing empty
+        // rows' boundaries too and may sit at n_rows: park them on a real row
+        // (their results are not stored; found by the checked build)
+        if (ea >= e_end) ra = cur.r_first;
+        if (eb >= e_end) rb = cur.r_first;
         const std::uint32_t rela = ra - cur.r_first, relb = rb - cur.r_first;
         ASB_DCHECK(ra < n_rows && rb < n_rows);
         ASB_DCHECK(ea >= e_end || (rowptr[ra] <= ea && ea < rowptr[ra + 1]));
