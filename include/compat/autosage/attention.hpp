@@ -1,0 +1,3 @@
+// autosage/attention.hpp -- forwards to the B200 compat layer (proj/include/autosage/attention.hpp API).
+#pragma once
+#include "../../autosage_b200_compat.hpp"

@@ -1,0 +1,3 @@
+// autosage/csr.hpp -- forwards to the B200 compat layer (proj/include/autosage/csr.hpp API).
+#pragma once
+#include "../../autosage_b200_compat.hpp"

@@ -1,0 +1,3 @@
+// autosage/env.hpp -- forwards to the B200 compat layer (proj/include/autosage/env.hpp API).
+#pragma once
+#include "../../autosage_b200_compat.hpp"

@@ -1,0 +1,3 @@
+// autosage/kernels.hpp -- forwards to the B200 compat layer (proj/include/autosage/kernels.hpp API).
+#pragma once
+#include "../../autosage_b200_compat.hpp"

@@ -1,0 +1,3 @@
+// autosage/scheduler.hpp -- forwards to the B200 compat layer (proj/include/autosage/scheduler.hpp API).
+#pragma once
+#include "../../autosage_b200_compat.hpp"

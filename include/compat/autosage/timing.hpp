@@ -1,0 +1,3 @@
+// autosage/timing.hpp -- forwards to the B200 compat layer (proj/include/autosage/timing.hpp API).
+#pragma once
+#include "../../autosage_b200_compat.hpp"
