@@ -306,14 +306,20 @@ int device_sms() {
 int kernel_setup(const void* kernel, std::size_t smem, int threads) {
     static std::mutex mu;
     static std::map<std::tuple<const void*, int, std::size_t, int>, int> done;
+    // the attribute is per function: only ever raise it, so a launch with a
+    // larger footprint is never left under a later, smaller setting
+    static std::map<std::pair<const void*, int>, std::size_t> smem_set;
     int dev = 0;
     ASB_CUDA(cudaGetDevice(&dev));
     const auto key = std::make_tuple(kernel, dev, smem, threads);
     std::lock_guard<std::mutex> lk(mu);
     auto it = done.find(key);
     if (it != done.end()) return it->second;
-    if (smem > 48 * 1024)
+    std::size_t& cur = smem_set[std::make_pair(kernel, dev)];
+    if (smem > 48 * 1024 && smem > cur) {
         ASB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        cur = smem;
+    }
     int per_sm = 1;
     ASB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
     done[key] = per_sm;

@@ -66,10 +66,25 @@ __global__ void hub_reduce_kernel(const std::uint32_t* __restrict__ red_row,
 //     out of shared memory, then release the stage on its "empty" mbarrier.
 // No __syncthreads in the steady state; a stage holds ch B rows.  Bit-equal
 // to the group kernel.
-constexpr int kLongStages = 8;
-constexpr std::uint32_t kLongStageBytes = 4096;
-constexpr int kIdxAhead = 4;
-constexpr int kIdxRing = 8;
+// Ring shape (-D overridable for sweeps): 4 stages of 16 KB (64 rows of F=64
+// per stage, 256 entries in flight per row).  Each stage costs a producer/
+// consumer mbarrier round trip and the producer's cp.async group wait, so
+// fewer, larger stages win on the
+// c1 long rows (hub-split SpMM 0.101 -> 0.074 ms; 8 x 4 KB, 8 x 8 KB, 12 x
+// 8 KB, 6 x 12 KB, 8 x 16 KB measured in profiles/r02g_c1_ring.md).
+#ifndef ASB_LONG_STAGES
+#define ASB_LONG_STAGES 4
+#endif
+#ifndef ASB_LONG_STAGE_BYTES
+#define ASB_LONG_STAGE_BYTES 16384
+#endif
+#ifndef ASB_LONG_IDX_AHEAD
+#define ASB_LONG_IDX_AHEAD 3
+#endif
+constexpr int kLongStages = ASB_LONG_STAGES;
+constexpr std::uint32_t kLongStageBytes = ASB_LONG_STAGE_BYTES;
+constexpr int kIdxAhead = ASB_LONG_IDX_AHEAD;
+constexpr int kIdxRing = 2 * ASB_LONG_IDX_AHEAD;
 static_assert(kIdxRing > kIdxAhead, "index ring too small");
 constexpr int kLongMaxConsumers = 256;  // consumer threads; features beyond loop
 
@@ -316,8 +331,19 @@ void launch_longrow(const SegArgs& a, std::uint64_t n, cudaStream_t s) {
     const std::uint32_t f = a.f;
     const std::uint32_t ch = std::max<std::uint32_t>(4, kLongStageBytes / (4 * f));
     const std::size_t smem = long_layout(f, ch).total;
-    // features per consumer lane: fill whole warps where f allows
-    const int fpl = f % 128 == 0 ? 4 : (f % 64 == 0 ? 2 : (f % 32 == 0 ? 1 : 4));
+    // features per consumer lane.  The ring kernel only runs when its items
+    // are few (small graphs' long rows, a handful of hub pieces), so it is
+    // latency-bound: each consumer warp advances its chains one entry per
+    // ~6 instructions, and more warps per row shorten the longest row.  One
+    // feature per lane while f fits kLongMaxConsumers (c1 F=64: 2 consumer
+    // warps instead of 1, 73 -> see profiles/r02g_c1_fpl.md); the old
+    // warp-filling choice (F=64 -> 2 per lane) via AUTOSAGE_DEV_LONG_FPL=2.
+    static const int fpl_knob = [] {
+        const char* e = std::getenv("AUTOSAGE_DEV_LONG_FPL");
+        return e ? std::atoi(e) : 0;
+    }();
+    int fpl = f <= std::uint32_t(kLongMaxConsumers) ? 1 : (f <= 2u * kLongMaxConsumers ? 2 : 4);
+    if (fpl_knob == 1 || fpl_knob == 2 || fpl_knob == 4) fpl = std::max(fpl, fpl_knob);
     const unsigned threads = 32 + (f / fpl + 31) / 32 * 32;
     auto go = [&](auto kern) {
         kernel_setup(kern, smem, int(threads));
