@@ -13,9 +13,10 @@ own cost formulas, proj/src/cost.cpp:21-27) over all ranks / max-rank time.
 
 --gpus N without a torchrun environment re-launches itself under
 torch.distributed.run with N ranks (one per GPU, NCCL).  Rows are
-nnz-balanced across ranks (as_partition_rows); each step all-gathers the
-dense B/Y row shards, Y in column blocks that the SDDMM consumes as they land
-(dist.py), and runs the local SpMM/SDDMM on the rank's row range.
+nnz-balanced across ranks (as_partition_rows); each step broadcasts the
+B row shards per owner and runs the rank's SpMM on them in column blocks as
+they land (dist.py blocked_spmm, as_spmm_blocked_*: bit-identical), while Y's
+all-gather runs under the SpMM for the SDDMM that follows.
 
 At N=1 the line also carries
   parity        our full-graph outputs vs the reference library
@@ -470,16 +471,36 @@ def run_ours(args):
         cache.store(args.cache)
 
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    blocked = None
+    groups = int(os.environ.get("AUTOSAGE_BENCH_BLOCKS", "2"))
+    if world > 1:
+        # B's shards are broadcast per owner and consumed in column blocks as
+        # they land (dist.py blocked_spmm; as_spmm_blocked_*, bit-identical to
+        # the decided variant); Y's all-gather follows on NCCL's stream under
+        # the SpMM
+        blocked = asb.BlockedSpmm(g, dec_spmm.choice, sh.column_cuts(groups))
 
     def step(i=None):
         flush.zero_()  # L2 flush between steps (untimed)
         e = ev[i] if i is not None else None
         if e:
             e[0].record(stream)
-        bm, hy = gather_b()
-        if e:
-            e[1].record(stream)
-        spmm(bm)
+        if world == 1:
+            bm, hy = gather_b()
+            if e:
+                e[1].record(stream)
+            spmm(bm)
+        else:
+            if e:
+                e[1].record(stream)
+            hy_box = []
+
+            def run_block(k):
+                if k == 0:  # Y queues behind B's broadcasts on NCCL's stream
+                    hy_box.append(sh.allgather_padded(y_loc, pad_y, async_op=True))
+                blocked.run(k, pad_b, c)
+            sh.blocked_spmm(b_loc, pad_b, run_block, groups=groups)
+            hy = hy_box[0]
         if e:
             e[2].record(stream)
         sddmm(y_operand(hy))  # Y's all-gather overlapped the SpMM
@@ -548,8 +569,10 @@ def run_ours(args):
                        "F": f, "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU",
                        "l2": "flushed between steps (256 MiB write, untimed)",
                        "exchange": ("none (1 GPU)" if world == 1 else
-                                    "NCCL all-gather of B row shards before the SpMM; Y's all-gather on "
-                                    "NCCL's stream under the SpMM; kernels read the padded buffers in place"),
+                                    f"B row shards broadcast per owner over NCCL and consumed by the SpMM in "
+                                    f"{blocked.n_blocks} column blocks as they land (as_spmm_blocked_*); Y's "
+                                    "all-gather on NCCL's stream under the SpMM; kernels read the padded "
+                                    "buffers in place"),
                        "spmm_choice": dec_spmm.choice_string(),
                        "sddmm_choice": dec_sddmm.choice_string(),
                        "decision_source": {"spmm": dec_spmm.source_name,
@@ -578,6 +601,8 @@ def run_ours(args):
             line["parity"] = parity
         print(json.dumps(line), flush=True)
     del keep
+    if blocked is not None:
+        blocked.close()
     if dist:
         dist.destroy_process_group()
 

@@ -424,6 +424,23 @@ as_status as_partition_rows(const uint64_t* rowptr_host, uint64_t n_rows, uint32
  * column indices. */
 as_status as_graph_row_range(as_graph g, uint64_t r0, uint64_t r1, as_graph* out);
 
+/* Column-blocked SpMM (new): C = A * B consumed one column
+ * block of B at a time, so a rank can start on each B row shard as the
+ * all-gather lands it.  col_cuts[0..n_blocks] split [0, n_cols); run blocks
+ * 0, 1, ..., n_blocks-1 in order on one stream (block 0 resets the f64 row
+ * state, the last writes C).  Every row / HubSplit piece keeps an f64
+ * accumulator across blocks, so C is bit-identical to as_spmm with the same
+ * variant (v == NULL: baseline; RowParallel = row chains; HubSplit = the
+ * 2048-nnz pieces of rows >= hub_threshold, src/kernels.cpp:260-334).  A
+ * plan references its graph (which must outlive it) and is single-stream. */
+typedef struct as_blocked_s* as_blocked;
+as_status as_spmm_blocked_create(as_graph a, const as_variant* v, const uint64_t* col_cuts, uint32_t n_blocks,
+                                 as_blocked* out);
+/* vals_dev == NULL: the graph's own values (implicit 1.0 when pattern-only). */
+as_status as_spmm_blocked_run(as_blocked p, uint32_t block, const float* vals_dev, const float* b_dev,
+                              uint64_t b_rows, uint64_t f, float* c_dev, void* stream);
+as_status as_spmm_blocked_destroy(as_blocked p);
+
 /* ------------------------------------------------------------------ */
 /* Backward pass (new, PAPER.md:334 -- the reference has  */
 /* no gradients).  C = A B gives dB = A^T dC (as_spmm_values on the      */

@@ -71,6 +71,7 @@ def port():
         for name, args in {
             "orc_spmm_baseline": [vp, vp, vp, u64, vp, u64, vp],
             "orc_spmm_hubsplit": [vp, vp, vp, u64, vp, u64, u64, vp],
+            "orc_spmm_blocked": [vp, vp, vp, u64, vp, u64, u64, vp, C.c_uint32, vp],
             "orc_sddmm": [vp, vp, u64, vp, vp, u64, u64, C.c_int, vp],
             "orc_row_softmax": [vp, u64, vp, vp],
             "orc_attention": [vp, vp, u64, vp, vp, u64, vp, u64, u64, C.c_int, u64, vp],
@@ -167,6 +168,17 @@ def spmm_hubsplit(m, b: np.ndarray, hub_t: int) -> np.ndarray:
     c = np.empty((m.n_rows, f), dtype=np.float32)
     port().orc_spmm_hubsplit(_ptr(m.rowptr), _ptr(m.colind), _ptr(m.val if m.has_values() else None),
                              m.n_rows, _ptr(b), f, hub_t, _ptr(c))
+    return c
+
+
+def spmm_blocked(m, b: np.ndarray, cuts, hub_t: int = 0) -> np.ndarray:
+    """Column-blocked SpMM restatement (segment accumulators carried across
+    ascending column blocks); equals spmm_baseline / spmm_hubsplit bit for bit."""
+    b = np.ascontiguousarray(b, dtype=np.float32)
+    cuts = np.ascontiguousarray(cuts, dtype=np.uint64)
+    c = np.empty((m.n_rows, b.shape[1]), dtype=np.float32)
+    port().orc_spmm_blocked(_ptr(m.rowptr), _ptr(m.colind), _ptr(m.val if m.has_values() else None), m.n_rows,
+                            _ptr(b), b.shape[1], hub_t, _ptr(cuts), cuts.size - 1, _ptr(c))
     return c
 
 

@@ -470,3 +470,39 @@ void orc_row_softmax_backward(const uint64_t* rowptr, uint64_t n_rows, const flo
         for (uint64_t e = e0; e < e1; ++e) ds[e] = (float)((double)p[e] * ((double)g[e] - dot));
     }
 }
+
+/* Column-blocked SpMM (the B200 library's as_spmm_blocked_*): each segment
+ * -- a row, or under HubSplit (hub_t > 0) a 2048-nnz piece of a row with
+ * degree >= hub_t (src/kernels.cpp:129-142) -- keeps one f64 accumulator per
+ * feature across the column blocks [cuts[b], cuts[b+1]), visited in ascending
+ * order; C[i] = f32(0.0 + s_0 + s_1 + ...) over the row's segments
+ * (src/kernels.cpp:320-331).  Equal to orc_spmm_baseline / orc_spmm_hubsplit
+ * bit for bit for every cut vector (columns are sorted within a row). */
+void orc_spmm_blocked(const uint64_t* rowptr, const uint32_t* colind, const float* val, uint64_t n_rows,
+                      const float* b, uint64_t f, uint64_t hub_t, const uint64_t* cuts, uint32_t n_blocks,
+                      float* c) {
+    double* acc = (double*)calloc(f ? f : 1, sizeof(double));
+    double* sum = (double*)calloc(f ? f : 1, sizeof(double));
+    for (uint64_t i = 0; i < n_rows; ++i) {
+        const uint64_t e0 = rowptr[i], e1 = rowptr[i + 1];
+        const uint64_t step = (hub_t && e1 - e0 >= hub_t) ? ORC_HUB_NNZ_CHUNK : (e1 > e0 ? e1 - e0 : 1);
+        for (uint64_t t = 0; t < f; ++t) sum[t] = 0.0;
+        for (uint64_t s0 = e0; s0 < e1; s0 += step) {
+            const uint64_t s1 = s0 + step < e1 ? s0 + step : e1;
+            for (uint64_t t = 0; t < f; ++t) acc[t] = 0.0;
+            uint64_t e = s0;
+            for (uint32_t blk = 0; blk < n_blocks; ++blk) {
+                /* this block's run of the segment: columns below cuts[blk + 1] */
+                for (; e < s1 && colind[e] < cuts[blk + 1]; ++e) {
+                    const float* brow = b + (uint64_t)colind[e] * f;
+                    const double v = val ? (double)val[e] : 1.0;
+                    for (uint64_t t = 0; t < f; ++t) acc[t] += v * (double)brow[t];
+                }
+            }
+            for (uint64_t t = 0; t < f; ++t) sum[t] += acc[t];
+        }
+        for (uint64_t t = 0; t < f; ++t) c[i * f + t] = (float)sum[t];
+    }
+    free(acc);
+    free(sum);
+}

@@ -128,6 +128,13 @@ void orc_transpose(const uint64_t* rowptr, const uint32_t* colind, uint64_t n_ro
 void orc_row_softmax_backward(const uint64_t* rowptr, uint64_t n_rows, const float* p,
                               const float* g, float* ds);
 
+/* Column-blocked SpMM restated (see oracle.c): segment accumulators carried
+ * across ascending column blocks [cuts[b], cuts[b+1]); hub_t == 0 for row
+ * chains (baseline / RowParallel), else HubSplit pieces. */
+void orc_spmm_blocked(const uint64_t* rowptr, const uint32_t* colind, const float* val, uint64_t n_rows,
+                      const float* b, uint64_t f, uint64_t hub_t, const uint64_t* cuts, uint32_t n_blocks,
+                      float* c);
+
 /* ---- input generators (gen.c; no reference counterpart -- see gen.c) ---- */
 /* Heavy-tailed degrees: deg_i = min(cap, floor(d_min * u^(-1/(alpha-1)))),
  * u from row i's own stream, rescaled to nnz_target (0 = keep) and settled

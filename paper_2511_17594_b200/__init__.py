@@ -1072,6 +1072,41 @@ def csr_attention_forward(pattern, q, k, v, cfg: Optional[ProbeConfig] = None,
 
 
 # ---- multi-GPU partition, synthetic inputs, I/O -------------------------------------------
+class BlockedSpmm:
+    """Column-blocked SpMM plan (as_spmm_blocked_*): C = A B consumed one
+    column block of B per run(), in ascending block order on one stream, so a
+    rank can start on each B row shard as it lands (dist.py).  Bit-identical
+    to as_spmm with the same variant (None: baseline)."""
+
+    def __init__(self, g: "Graph", variant: Optional[KernelVariant], cuts):
+        self.g = g
+        self.cuts = np.ascontiguousarray(cuts, dtype=np.uint64)
+        self.n_blocks = int(self.cuts.size - 1)
+        h = C.c_void_p()
+        cv = variant.to_c() if variant is not None else None
+        _check(_lib.as_spmm_blocked_create(g.handle, C.byref(cv) if cv is not None else None, _ptr(self.cuts),
+                                           self.n_blocks, C.byref(h)))
+        self._h = h.value
+
+    def run(self, block: int, b, c, vals=None, stream=None) -> None:
+        """Block `block` of C = A B (b, c, vals: CUDA tensors; the last block
+        writes c)."""
+        s = stream if stream is not None else torch_stream_handle(b.device)
+        _check(_lib.as_spmm_blocked_run(self._h, block, _vptr(vals) if vals is not None else None, _vptr(b),
+                                        int(b.shape[0]), int(b.shape[1]), _vptr(c), C.c_void_p(s)))
+
+    def close(self) -> None:
+        if self._h:
+            _lib.as_spmm_blocked_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def partition_rows(rowptr, g: int) -> np.ndarray:
     """nnz-balanced row cuts (g+1 entries), SURVEY 8(e)."""
     rowptr = np.ascontiguousarray(rowptr, dtype=np.uint64)

@@ -191,6 +191,9 @@ _proto("as_csr_attention_forward_p", st, P(as_context), P(as_probe_config), vp, 
        vp, u64, u64, u64, vp, vp, P(as_decision), P(as_decision))
 _proto("as_partition_rows", st, vp, u64, u32, vp)
 _proto("as_graph_row_range", st, vp, u64, u64, P(vp))
+_proto("as_spmm_blocked_create", st, vp, P(as_variant), vp, u32, P(vp))
+_proto("as_spmm_blocked_run", st, vp, u32, vp, vp, u64, u64, vp, vp)
+_proto("as_spmm_blocked_destroy", st, vp)
 _proto("as_graph_transpose", st, vp, P(vp))
 _proto("as_graph_transpose_perm", st, vp, P(vp))
 _proto("as_permute_values", st, vp, vp, vp, vp)
@@ -230,5 +233,6 @@ EXPORTED = [
     "as_fill_uniform", "as_free", "as_save_csr", "as_load_csr", "as_host_alloc",
     "as_host_free", "as_kernel_launch_count", "as_graph_transpose", "as_graph_transpose_perm",
     "as_permute_values", "as_spmm_values", "as_row_softmax_backward", "as_spmm_bf16",
-    "as_sddmm_bf16", "as_spmm_transpose_values", "as_csr_attention_forward_p",
+    "as_sddmm_bf16", "as_spmm_transpose_values", "as_csr_attention_forward_p", "as_spmm_auto_values",
+    "as_spmm_blocked_create", "as_spmm_blocked_run", "as_spmm_blocked_destroy",
 ]

@@ -15,6 +15,13 @@
 #include <new>
 
 namespace asb {
+struct BlockedPlan;
+BlockedPlan* blocked_plan_create(Graph& g, const as_variant* v, const std::uint64_t* cuts,
+                                 std::uint32_t n_blocks);
+void blocked_plan_run(BlockedPlan& p, std::uint32_t block, const float* vals, const float* b, std::uint64_t b_rows,
+                      std::uint64_t f, float* c, cudaStream_t s);
+void blocked_plan_destroy(BlockedPlan* p);
+Graph& blocked_plan_graph(BlockedPlan& p);
 void gen_powerlaw(std::uint64_t, std::uint64_t, std::uint64_t, double, std::uint64_t,
                   std::uint64_t, std::uint64_t, bool, std::vector<std::uint64_t>&,
                   std::vector<std::uint32_t>&, std::vector<float>&);
@@ -698,6 +705,30 @@ as_status as_partition_rows(const uint64_t* rowptr_host, uint64_t n_rows, uint32
 
 as_status as_graph_row_range(as_graph g, uint64_t r0, uint64_t r1, as_graph* out) {
     return guard([&] { *out = reinterpret_cast<as_graph>(row_range(G(g), r0, r1).release()); });
+}
+
+as_status as_spmm_blocked_create(as_graph a, const as_variant* v, const uint64_t* col_cuts, uint32_t n_blocks,
+                                 as_blocked* out) {
+    return guard([&] {
+        if (!out || !col_cuts) throw InvalidArgument("spmm_blocked: null argument");
+        *out = reinterpret_cast<as_blocked>(blocked_plan_create(G(a), v, col_cuts, n_blocks));
+    });
+}
+
+as_status as_spmm_blocked_run(as_blocked p, uint32_t block, const float* vals_dev, const float* b_dev,
+                              uint64_t b_rows, uint64_t f, float* c_dev, void* stream) {
+    return guard([&] {
+        if (!p) throw InvalidArgument("spmm_blocked: null plan");
+        auto& plan = *reinterpret_cast<BlockedPlan*>(p);
+        Graph& g = blocked_plan_graph(plan);
+        const cudaStream_t s = resolve_stream(g, stream);
+        GraphUse use(g, s);
+        blocked_plan_run(plan, block, graph_values(g, vals_dev), b_dev, b_rows, f, c_dev, s);
+    });
+}
+
+as_status as_spmm_blocked_destroy(as_blocked p) {
+    return guard([&] { blocked_plan_destroy(reinterpret_cast<BlockedPlan*>(p)); });
 }
 
 // ---- backward (backward.cu) -----------------------------------------------------------

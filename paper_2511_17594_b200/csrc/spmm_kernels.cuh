@@ -132,7 +132,12 @@ __device__ __forceinline__ void seg_accumulate(double (&acc)[NCH][VEC], double v
 // re-biased on the ALU pipe.  SMX: the entry values are softmax
 // probabilities computed from raw scores and the row's (max, sum) by the lane
 // that loads them (fused attention), instead of stored values.
-template <int VEC, int LPR, int NCH, bool HAS_VAL, bool PIECES, int U, int MIX, bool SMX, bool BF, bool VP>
+// CARRY (column-blocked SpMM, spmm_blocked.cu): every item is a segment
+// with an f64 state slot; the accumulators start from scratch[slot] instead
+// of 0.0 and are written back there, so a row's entries can be consumed in
+// ascending column blocks across launches with the reference's order.
+template <int VEC, int LPR, int NCH, bool HAS_VAL, bool PIECES, int U, int MIX, bool SMX, bool BF, bool VP,
+          bool CARRY = false>
 __device__ __forceinline__ void seg_body(const SegArgs& a) {
     using VT = typename VecT<VEC, BF>::T;
     using BT = typename std::conditional<BF, unsigned short, float>::type;
@@ -193,6 +198,19 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
     for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll
         for (int q = 0; q < VEC; ++q) acc[ch][q] = 0.0;
+    if constexpr (CARRY) {
+        static_assert(PIECES, "carry mode runs on segment lists");
+        if (active) {
+            ASB_DCHECK(slot != 0xffffffffu);
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch)
+                if (fok[ch]) {
+                    const double* sp = a.scratch + std::uint64_t(slot) * a.f + fidx[ch];
+#pragma unroll
+                    for (int q = 0; q < VEC; ++q) acc[ch][q] = sp[q];
+                }
+        }
+    }
 
     const unsigned gbase = unsigned(grp * LPR);
     const std::uint32_t* colp = a.colind + e0;
@@ -359,10 +377,10 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
 }
 
 template <int VEC, int LPR, int NCH, bool HAS_VAL, bool PIECES, int U = unroll_for(VEC, NCH),
-          int MAXR = maxreg_for(VEC, NCH), bool SMX = false, bool BF = false, bool VP = false>
+          int MAXR = maxreg_for(VEC, NCH), bool SMX = false, bool BF = false, bool VP = false, bool CARRY = false>
 __global__ void __launch_bounds__(512) __maxnreg__(MAXR) spmm_seg_kernel(SegArgs a) {
-    if (a.finite && *a.finite) seg_body<VEC, LPR, NCH, HAS_VAL, PIECES, U, 1, SMX, BF, VP>(a);
-    else seg_body<VEC, LPR, NCH, HAS_VAL, PIECES, U, 0, SMX, BF, VP>(a);
+    if (a.finite && *a.finite) seg_body<VEC, LPR, NCH, HAS_VAL, PIECES, U, 1, SMX, BF, VP, CARRY>(a);
+    else seg_body<VEC, LPR, NCH, HAS_VAL, PIECES, U, 0, SMX, BF, VP, CARRY>(a);
 }
 
 // dynamic shared memory of the lane-group kernels: the fast loop's
