@@ -472,8 +472,15 @@ def run_ours(args):
 
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     blocked = None
-    groups = int(os.environ.get("AUTOSAGE_BENCH_BLOCKS", "2"))
-    if world > 1:
+    # column-blocked exchange when B's transfer is worth hiding: a B larger
+    # than twice the L2 is gathered from DRAM by a ~1 ms SpMM per shard
+    # (Products-shape), a smaller one costs more in carried state than the
+    # exchange takes (profiles/r02i_blocked.md); AUTOSAGE_BENCH_BLOCKS forces
+    # the block count (1 = plain all-gather)
+    groups = int(os.environ.get("AUTOSAGE_BENCH_BLOCKS", "0"))
+    if groups <= 0:
+        groups = 2 if m.n_cols * f * 4 > 2 * torch.cuda.get_device_properties(dev).L2_cache_size else 1
+    if world > 1 and groups > 1:
         # B's shards are broadcast per owner and consumed in column blocks as
         # they land (dist.py blocked_spmm; as_spmm_blocked_*, bit-identical to
         # the decided variant); Y's all-gather follows on NCCL's stream under
@@ -485,7 +492,7 @@ def run_ours(args):
         e = ev[i] if i is not None else None
         if e:
             e[0].record(stream)
-        if world == 1:
+        if blocked is None:
             bm, hy = gather_b()
             if e:
                 e[1].record(stream)
@@ -569,9 +576,10 @@ def run_ours(args):
                        "F": f, "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU",
                        "l2": "flushed between steps (256 MiB write, untimed)",
                        "exchange": ("none (1 GPU)" if world == 1 else
-                                    f"B row shards broadcast per owner over NCCL and consumed by the SpMM in "
-                                    f"{blocked.n_blocks} column blocks as they land (as_spmm_blocked_*); Y's "
-                                    "all-gather on NCCL's stream under the SpMM; kernels read the padded "
+                                    (f"B row shards broadcast per owner over NCCL and consumed by the SpMM in "
+                                     f"{blocked.n_blocks} column blocks as they land (as_spmm_blocked_*); "
+                                     if blocked is not None else "NCCL all-gather of B row shards before the SpMM; ")
+                                    + "Y's all-gather on NCCL's stream under the SpMM; kernels read the padded "
                                     "buffers in place"),
                        "spmm_choice": dec_spmm.choice_string(),
                        "sddmm_choice": dec_sddmm.choice_string(),
