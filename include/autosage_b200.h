@@ -475,6 +475,27 @@ as_status as_spmm_bf16(const as_variant* v, as_graph a, const float* vals_dev, c
 as_status as_sddmm_bf16(const as_variant* v, as_graph pattern, const uint16_t* x_dev, uint64_t x_rows,
                         const uint16_t* y_dev, uint64_t y_rows, uint64_t f, float* out_dev, void* stream,
                         as_kernel_result* res);
+/* CSR attention on 16-bit q, k, v words (wt 1 = bf16, 2 = f16; new, SURVEY
+ * 8(f) N4) with given variants (NULL = baseline): scores = SDDMM(q, k), p =
+ * row_softmax(scores), out = SpMM(p, v) (f32 out, n_rows x fv).  fused != 0
+ * and p_out == NULL: SDDMM -> per-row (max, sum) -> an SpMM that turns each
+ * score into its probability as it loads it (needs a mapped SpMM variant and
+ * fv % 4 == 0 with an 8-byte aligned v; else staged).  p_out (nnz floats)
+ * receives p (staged).  The bits equal the f32 staged pipeline on the widened
+ * operands with the same variants. */
+as_status as_csr_attention_half(as_graph pattern, const as_variant* sddmm_v, const as_variant* spmm_v,
+                                const uint16_t* q_dev, uint64_t q_rows, const uint16_t* k_dev, uint64_t k_rows,
+                                const uint16_t* v_dev, uint64_t v_rows, uint64_t f, uint64_t fv, float* out_dev,
+                                float* p_dev, int wt, int fused, void* stream);
+/* The same two operators on IEEE binary16 words (new): f16
+ * -> f32 is exact too, so the results equal as_spmm / as_sddmm on the f32
+ * copies bit for bit (Inf/NaN included; a device scan gates the re-bias
+ * widening as for f32). */
+as_status as_spmm_f16(const as_variant* v, as_graph a, const float* vals_dev, const uint16_t* b_dev,
+                      uint64_t b_rows, uint64_t f, float* c_dev, void* stream, as_kernel_result* res);
+as_status as_sddmm_f16(const as_variant* v, as_graph pattern, const uint16_t* x_dev, uint64_t x_rows,
+                       const uint16_t* y_dev, uint64_t y_rows, uint64_t f, float* out_dev, void* stream,
+                       as_kernel_result* res);
 /* A^T[vals] * B on a transpose gt, with vals in the SOURCE graph's entry
  * order (nnz floats, device): the kernels read val[perm[k]] at the value
  * load, so no permuted copy is written (as_permute_values + as_spmm_values

@@ -202,6 +202,10 @@ _proto("as_row_softmax_backward", st, vp, vp, vp, vp, vp)
 _proto("as_spmm_bf16", st, P(as_variant), vp, vp, vp, u64, u64, vp, vp, P(as_kernel_result))
 _proto("as_spmm_transpose_values", st, P(as_variant), vp, vp, vp, u64, u64, vp, vp, P(as_kernel_result))
 _proto("as_sddmm_bf16", st, P(as_variant), vp, vp, u64, vp, u64, u64, vp, vp, P(as_kernel_result))
+_proto("as_csr_attention_half", st, vp, P(as_variant), P(as_variant), vp, u64, vp, u64, vp, u64, u64, u64, vp, vp,
+       C.c_int, C.c_int, vp)
+_proto("as_spmm_f16", st, P(as_variant), vp, vp, vp, u64, u64, vp, vp, P(as_kernel_result))
+_proto("as_sddmm_f16", st, P(as_variant), vp, vp, u64, vp, u64, u64, vp, vp, P(as_kernel_result))
 _proto("as_gen_powerlaw", st, u64, u64, u64, dbl, u64, u64, u64, C.c_int, P(vp), P(vp), P(vp),
        P(u64))
 _proto("as_fill_uniform", st, vp, u64, u64)
@@ -234,5 +238,6 @@ EXPORTED = [
     "as_host_free", "as_kernel_launch_count", "as_graph_transpose", "as_graph_transpose_perm",
     "as_permute_values", "as_spmm_values", "as_row_softmax_backward", "as_spmm_bf16",
     "as_sddmm_bf16", "as_spmm_transpose_values", "as_csr_attention_forward_p", "as_spmm_auto_values",
-    "as_spmm_blocked_create", "as_spmm_blocked_run", "as_spmm_blocked_destroy",
+    "as_spmm_blocked_create", "as_spmm_blocked_run", "as_spmm_blocked_destroy", "as_spmm_f16", "as_sddmm_f16",
+    "as_csr_attention_half",
 ]

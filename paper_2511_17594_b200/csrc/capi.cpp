@@ -785,14 +785,38 @@ as_status as_permute_values(as_graph gt, const float* src_dev, float* dst_dev, v
     });
 }
 
-as_status as_spmm_bf16(const as_variant* v, as_graph a, const float* vals_dev, const uint16_t* b_dev,
-                       uint64_t b_rows, uint64_t f, float* c_dev, void* stream, as_kernel_result* res) {
+static as_status spmm_half_entry(const as_variant* v, as_graph a, const float* vals_dev, const uint16_t* b_dev,
+                                 uint64_t b_rows, uint64_t f, float* c_dev, void* stream, as_kernel_result* res,
+                                 int wt, const char* name) {
     return guard([&] {
         Graph& g = G(a);
-        if (g.n_rows && f && (!b_dev || !c_dev)) throw InvalidArgument("spmm_bf16: null operand");
+        if (g.n_rows && f && (!b_dev || !c_dev)) throw InvalidArgument(std::string(name) + ": null operand");
         GraphUse use(g, resolve_stream(g, stream));
-        const KernelResult r = dispatch_spmm_bf16(v, g, vals_dev, b_dev, b_rows, f, c_dev,
-                                                  resolve_stream(g, stream), res != nullptr);
+        const KernelResult r = dispatch_spmm_half(v, g, vals_dev, b_dev, b_rows, f, c_dev,
+                                                  resolve_stream(g, stream), res != nullptr, wt);
+        fill_result(res, r);
+    });
+}
+
+as_status as_spmm_bf16(const as_variant* v, as_graph a, const float* vals_dev, const uint16_t* b_dev,
+                       uint64_t b_rows, uint64_t f, float* c_dev, void* stream, as_kernel_result* res) {
+    return spmm_half_entry(v, a, vals_dev, b_dev, b_rows, f, c_dev, stream, res, 1, "spmm_bf16");
+}
+
+as_status as_spmm_f16(const as_variant* v, as_graph a, const float* vals_dev, const uint16_t* b_dev,
+                      uint64_t b_rows, uint64_t f, float* c_dev, void* stream, as_kernel_result* res) {
+    return spmm_half_entry(v, a, vals_dev, b_dev, b_rows, f, c_dev, stream, res, 2, "spmm_f16");
+}
+
+static as_status sddmm_half_entry(const as_variant* v, as_graph pattern, const uint16_t* x_dev, uint64_t x_rows,
+                                  const uint16_t* y_dev, uint64_t y_rows, uint64_t f, float* out_dev, void* stream,
+                                  as_kernel_result* res, int wt, const char* name) {
+    return guard([&] {
+        Graph& g = G(pattern);
+        if (g.nnz && f && (!x_dev || !y_dev || !out_dev)) throw InvalidArgument(std::string(name) + ": null operand");
+        GraphUse use(g, resolve_stream(g, stream));
+        const KernelResult r = dispatch_sddmm_half(v, g, x_dev, x_rows, y_dev, y_rows, f, out_dev,
+                                                   resolve_stream(g, stream), res != nullptr, wt);
         fill_result(res, r);
     });
 }
@@ -800,13 +824,29 @@ as_status as_spmm_bf16(const as_variant* v, as_graph a, const float* vals_dev, c
 as_status as_sddmm_bf16(const as_variant* v, as_graph pattern, const uint16_t* x_dev, uint64_t x_rows,
                         const uint16_t* y_dev, uint64_t y_rows, uint64_t f, float* out_dev, void* stream,
                         as_kernel_result* res) {
+    return sddmm_half_entry(v, pattern, x_dev, x_rows, y_dev, y_rows, f, out_dev, stream, res, 1, "sddmm_bf16");
+}
+
+as_status as_sddmm_f16(const as_variant* v, as_graph pattern, const uint16_t* x_dev, uint64_t x_rows,
+                       const uint16_t* y_dev, uint64_t y_rows, uint64_t f, float* out_dev, void* stream,
+                       as_kernel_result* res) {
+    return sddmm_half_entry(v, pattern, x_dev, x_rows, y_dev, y_rows, f, out_dev, stream, res, 2, "sddmm_f16");
+}
+
+as_status as_csr_attention_half(as_graph pattern, const as_variant* sddmm_v, const as_variant* spmm_v,
+                                const uint16_t* q_dev, uint64_t q_rows, const uint16_t* k_dev, uint64_t k_rows,
+                                const uint16_t* v_dev, uint64_t v_rows, uint64_t f, uint64_t fv, float* out_dev,
+                                float* p_dev, int wt, int fused, void* stream) {
     return guard([&] {
         Graph& g = G(pattern);
-        if (g.nnz && f && (!x_dev || !y_dev || !out_dev)) throw InvalidArgument("sddmm_bf16: null operand");
-        GraphUse use(g, resolve_stream(g, stream));
-        const KernelResult r = dispatch_sddmm_bf16(v, g, x_dev, x_rows, y_dev, y_rows, f, out_dev,
-                                                   resolve_stream(g, stream), res != nullptr);
-        fill_result(res, r);
+        if (wt != 1 && wt != 2) throw InvalidArgument("attention_half: wt must be 1 (bf16) or 2 (f16)");
+        if (g.n_rows && fv && !out_dev) throw InvalidArgument("attention_half: null output");
+        if (g.nnz && f && (!q_dev || !k_dev)) throw InvalidArgument("attention_half: null operand");
+        if (g.nnz && fv && !v_dev) throw InvalidArgument("attention_half: null operand");
+        const cudaStream_t s = resolve_stream(g, stream);
+        GraphUse use(g, s);
+        attention_half(g, sddmm_v, spmm_v, q_dev, q_rows, k_dev, k_rows, v_dev, v_rows, f, fv, out_dev, p_dev,
+                       fused != 0, wt, s);
     });
 }
 

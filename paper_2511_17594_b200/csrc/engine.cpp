@@ -367,13 +367,15 @@ KernelResult dispatch_spmm(const as_variant& v, Graph& a, const float* vals, con
     return r;
 }
 
-// SpMM with a bf16 B: the same kernels reading
-// half the gather bytes.  bf16 -> f32 is exact, so the result equals the f32
+// SpMM with a 16-bit B (bf16 or f16 words, wt):
+// the same kernels reading half the gather bytes.  Either -> f32 is exact, so
+// the result equals the f32
 // SpMM on float(B) bit for bit.  v == nullptr: baseline.  The 4-wide path
 // (8-byte loads) needs f % 4 == 0 and an 8-byte aligned base; the ring
 // kernel and the softmax mode stay f32-only.
-KernelResult dispatch_spmm_bf16(const as_variant* v, Graph& a, const float* vals, const std::uint16_t* b,
-                                std::uint64_t b_rows, std::uint64_t f, float* c, cudaStream_t s, bool timed) {
+KernelResult dispatch_spmm_half(const as_variant* v, Graph& a, const float* vals, const std::uint16_t* b,
+                                std::uint64_t b_rows, std::uint64_t f, float* c, cudaStream_t s, bool timed,
+                                int wt) {
     check_spmm_dims(a, b_rows);
     KernelResult r;
     if (v) {
@@ -392,20 +394,20 @@ KernelResult dispatch_spmm_bf16(const as_variant* v, Graph& a, const float* vals
     if (r.variant.mapping != AS_MAP_BASELINE) {
         if (r.variant.mapping == AS_MAP_ROWPARALLEL) ensure_order(a);
         else ensure_hub_plan(a, r.variant.hub_threshold);
-        if (a.n_cols * f * 2 <= (std::uint64_t(96) << 20)) fin = finite_flag_bf16(a, b, a.n_cols * f, s);
+        if (a.n_cols * f * 2 <= (std::uint64_t(96) << 20)) fin = finite_flag_half(a, b, a.n_cols * f, s, wt);
     }
     TimedRegion tr(s, timed);
     switch (r.variant.mapping) {
         case AS_MAP_BASELINE:
-            launch_spmm_baseline(a, va, b, std::uint32_t(f), c, s, true);
+            launch_spmm_baseline(a, va, b, std::uint32_t(f), c, s, wt);
             break;
         case AS_MAP_ROWPARALLEL:
             launch_spmm_rows(a, va, 0, a.n_rows, b, std::uint32_t(f), c, r.variant.f_tile, vec_ok, wpb, s, fin,
-                             nullptr, nullptr, true);
+                             nullptr, nullptr, wt);
             break;
         case AS_MAP_HUBSPLIT:
             launch_spmm_hubsplit(a, va, b, std::uint32_t(f), c, r.variant.f_tile, vec_ok, wpb,
-                                 r.variant.hub_threshold, s, fin, nullptr, nullptr, true);
+                                 r.variant.hub_threshold, s, fin, nullptr, nullptr, wt);
             break;
     }
     r.elapsed_ms = tr.stop();
@@ -417,9 +419,9 @@ KernelResult dispatch_spmm_bf16(const as_variant* v, Graph& a, const float* vals
 // four-way block order (src/kernels.cpp:103-127) whenever f % 4 == 0 -- the
 // gate the f32 copies of X and Y would pass -- so the result is as_sddmm on
 // float(X), float(Y) with the same variant, bit for bit.
-KernelResult dispatch_sddmm_bf16(const as_variant* v, Graph& p, const std::uint16_t* x, std::uint64_t x_rows,
+KernelResult dispatch_sddmm_half(const as_variant* v, Graph& p, const std::uint16_t* x, std::uint64_t x_rows,
                                  const std::uint16_t* y, std::uint64_t y_rows, std::uint64_t f, float* out,
-                                 cudaStream_t s, bool timed) {
+                                 cudaStream_t s, bool timed, int wt) {
     check_sddmm_dims(p, x_rows, y_rows);
     KernelResult r;
     if (v) {
@@ -436,7 +438,7 @@ KernelResult dispatch_sddmm_bf16(const as_variant* v, Graph& p, const std::uint1
     const std::uint32_t ft = std::uint32_t(baseline ? std::max<std::uint64_t>(f, 1) : effective_tile(r.variant.f_tile, f));
     DeviceGuard dg(p.device);
     TimedRegion tr(s, timed);
-    launch_sddmm_bf16(p, x, y, std::uint32_t(f), out, ft, ord, baseline, s);
+    launch_sddmm_half(p, x, y, std::uint32_t(f), out, ft, ord, baseline, s, wt);
     r.elapsed_ms = tr.stop();
     r.vectorized_path = ord == 1;
     return r;
@@ -844,6 +846,49 @@ void attention_forward(const Context& ctx, const as_probe_config& cfg, Graph& pa
     }
     if (sd_out) *sd_out = sd;
     if (pd_out) *pd_out = pd;
+}
+
+// CSR attention on 16-bit q, k, v words (wt: 1 bf16, 2 f16)
+// with given variants (the torch training path fixes them): scores =
+// SDDMM(q, k) -> row softmax -> SpMM over v.  fused: SDDMM -> per-row (max,
+// sum) -> the SpMM turning each score into its probability as it loads it
+// (softmax.cuh, as the f32 fused path); p_out, when given, receives p (the
+// staged form).  Either way the bits are those of the f32 staged pipeline on
+// float(q), float(k), float(v) with the same variants.
+void attention_half(Graph& pattern, const as_variant* sv, const as_variant* pv, const std::uint16_t* q,
+                    std::uint64_t q_rows, const std::uint16_t* k, std::uint64_t k_rows, const std::uint16_t* v,
+                    std::uint64_t v_rows, std::uint64_t f, std::uint64_t fv, float* out, float* p_out, bool fused,
+                    int wt, cudaStream_t s) {
+    if (q_rows != pattern.n_rows || k_rows != pattern.n_cols || v_rows != pattern.n_cols)
+        throw InvalidArgument("attention: operand row counts incompatible with pattern");
+    if (sv && sv->op != AS_OP_SDDMM) throw InvalidArgument("attention: sddmm variant expected");
+    if (pv && pv->op != AS_OP_SPMM) throw InvalidArgument("attention: spmm variant expected");
+    DeviceGuard dg(pattern.device);
+    pattern.att_buf.ensure(std::max<std::uint64_t>(2 * pattern.nnz, 2));
+    float* scores = pattern.att_buf.get();
+    dispatch_sddmm_half(sv, pattern, q, q_rows, k, k_rows, f, scores, s, false, wt);
+    as_variant pvar = pv ? apply_env_overrides(*pv) : default_variant();
+    if (!pv) pvar.mapping = AS_MAP_BASELINE;
+    check_variant(pvar);
+    const bool vec_ok = fv % 4 == 0 && (reinterpret_cast<std::uintptr_t>(v) & 7) == 0;
+    if (fused && !p_out && pvar.mapping != AS_MAP_BASELINE && vec_ok && pattern.nnz) {
+        pattern.att_max.ensure(std::max<std::uint64_t>(pattern.n_rows, 1));
+        pattern.att_sum.ensure(std::max<std::uint64_t>(pattern.n_rows, 1));
+        launch_row_softmax_stats(pattern, scores, pattern.att_max.get(), pattern.att_sum.get(), s);
+        const std::uint32_t wpb = std::uint32_t(std::min<std::uint64_t>(pvar.rows_per_chunk, 16));
+        if (pvar.mapping == AS_MAP_ROWPARALLEL) {
+            ensure_order(pattern);
+            launch_spmm_rows(pattern, scores, 0, pattern.n_rows, v, std::uint32_t(fv), out, pvar.f_tile, true, wpb, s,
+                             nullptr, pattern.att_max.get(), pattern.att_sum.get(), wt);
+        } else {
+            launch_spmm_hubsplit(pattern, scores, v, std::uint32_t(fv), out, pvar.f_tile, true, wpb,
+                                 pvar.hub_threshold, s, nullptr, pattern.att_max.get(), pattern.att_sum.get(), wt);
+        }
+        return;
+    }
+    float* p = p_out ? p_out : scores + pattern.nnz;
+    if (pattern.nnz) row_softmax(pattern, scores, p, s);
+    dispatch_spmm_half(pv, pattern, p, v, v_rows, fv, out, s, false, wt);
 }
 
 } // namespace asb

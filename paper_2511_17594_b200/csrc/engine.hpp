@@ -33,13 +33,22 @@ void spmm_mapped(const as_variant& v, int expect_mapping, Graph& a, const float*
 KernelResult dispatch_spmm(const as_variant& v, Graph& a, const float* vals, const float* b,
                            std::uint64_t b_rows, std::uint64_t f, float* c, cudaStream_t s,
                            bool timed);
-// SpMM with bf16 B words (v == nullptr: baseline); the f32 result on float(B).
-KernelResult dispatch_spmm_bf16(const as_variant* v, Graph& a, const float* vals, const std::uint16_t* b,
-                                std::uint64_t b_rows, std::uint64_t f, float* c, cudaStream_t s, bool timed);
-// SDDMM on bf16 X, Y words (v == nullptr: baseline); the f32 result on float(X), float(Y).
-KernelResult dispatch_sddmm_bf16(const as_variant* v, Graph& p, const std::uint16_t* x, std::uint64_t x_rows,
+// SpMM with 16-bit B words (wt: 1 bf16, 2 f16; v == nullptr: baseline); the
+// f32 result on float(B).
+KernelResult dispatch_spmm_half(const as_variant* v, Graph& a, const float* vals, const std::uint16_t* b,
+                                std::uint64_t b_rows, std::uint64_t f, float* c, cudaStream_t s, bool timed,
+                                int wt);
+// CSR attention on 16-bit q, k, v words with given variants (staged or
+// fused), the f32 staged pipeline's bits on the widened operands.
+void attention_half(Graph& pattern, const as_variant* sv, const as_variant* pv, const std::uint16_t* q,
+                    std::uint64_t q_rows, const std::uint16_t* k, std::uint64_t k_rows, const std::uint16_t* v,
+                    std::uint64_t v_rows, std::uint64_t f, std::uint64_t fv, float* out, float* p_out, bool fused,
+                    int wt, cudaStream_t s);
+// SDDMM on 16-bit X, Y words (v == nullptr: baseline); the f32 result on
+// float(X), float(Y).
+KernelResult dispatch_sddmm_half(const as_variant* v, Graph& p, const std::uint16_t* x, std::uint64_t x_rows,
                                  const std::uint16_t* y, std::uint64_t y_rows, std::uint64_t f, float* out,
-                                 cudaStream_t s, bool timed);
+                                 cudaStream_t s, bool timed, int wt);
 void sddmm_baseline(Graph& p, const float* x, std::uint64_t x_rows, const float* y,
                     std::uint64_t y_rows, std::uint64_t f, float* out, cudaStream_t s);
 // sddmm_rowparallel (src/kernels.cpp:357-429): variant as given, no env.

@@ -2,6 +2,7 @@
 // stable degree ordering (CUB radix sort), GraphFeatures, probe sampling,
 // row slicing, hub plans and the SDDMM nnz-chunk row map.
 #include "graph.hpp"
+#include "half.cuh"
 #include "policy.hpp"
 
 #include <cub/device/device_radix_sort.cuh>
@@ -657,8 +658,10 @@ __global__ void finite_check_kernel(const float* __restrict__ p, std::uint64_t n
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *flag = 0u;
 }
 
-// bf16 words: exponent field 0x7F80 all ones = Inf/NaN
-__global__ void finite_check_bf16_kernel(const unsigned short* __restrict__ p, std::uint64_t n,
+// 16-bit words (half.cuh): exponent field all ones (bf16 0x7F80, f16 0x7C00)
+// = Inf/NaN
+template <unsigned M>
+__global__ void finite_check_half_kernel(const unsigned short* __restrict__ p, std::uint64_t n,
                                          unsigned* __restrict__ flag) {
     bool bad = false;
     const std::uint64_t stride = std::uint64_t(gridDim.x) * blockDim.x;
@@ -669,17 +672,17 @@ __global__ void finite_check_bf16_kernel(const unsigned short* __restrict__ p, s
         for (std::uint64_t k = i; k < n8; k += stride) {
             const uint4 v = __ldg(p8 + k);
             for (unsigned w : {v.x, v.y, v.z, v.w})
-                bad |= ((w & 0x7F80u) == 0x7F80u) | ((w & 0x7F800000u) == 0x7F800000u);
+                bad |= ((w & M) == M) | ((w & (M << 16)) == (M << 16));
         }
-        for (std::uint64_t k = n8 * 8 + i; k < n; k += stride) bad |= (p[k] & 0x7F80u) == 0x7F80u;
+        for (std::uint64_t k = n8 * 8 + i; k < n; k += stride) bad |= (p[k] & M) == M;
     } else {
-        for (std::uint64_t k = i; k < n; k += stride) bad |= (p[k] & 0x7F80u) == 0x7F80u;
+        for (std::uint64_t k = i; k < n; k += stride) bad |= (p[k] & M) == M;
     }
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *flag = 0u;
 }
 }  // namespace
 
-const unsigned* finite_flag_bf16(Graph& g, const unsigned short* p, std::uint64_t n, cudaStream_t s) {
+const unsigned* finite_flag_half(Graph& g, const std::uint16_t* p, std::uint64_t n, cudaStream_t s, int wt) {
     g.flag.ensure(1);
     // nothing to widen: 0, the safe path; else 0x01010101 (nonzero = finite)
     // until the scan clears it -- one memset
@@ -688,8 +691,9 @@ const unsigned* finite_flag_bf16(Graph& g, const unsigned short* p, std::uint64_
     if (empty) return g.flag.get();
     const std::uint64_t want = (n / 8 + 255) / 256 + 1;
     const unsigned blocks = unsigned(std::min<std::uint64_t>(want, std::uint64_t(g.sms) * 8));
-    finite_check_bf16_kernel<<<blocks, 256, 0, s>>>(p, n, g.flag.get());
-    check_launch("finite_check_bf16_kernel");
+    if (wt == kWtF16) finite_check_half_kernel<half_inf_mask<kWtF16>()><<<blocks, 256, 0, s>>>(p, n, g.flag.get());
+    else finite_check_half_kernel<half_inf_mask<kWtBF16>()><<<blocks, 256, 0, s>>>(p, n, g.flag.get());
+    check_launch("finite_check_half_kernel");
     return g.flag.get();
 }
 

@@ -8,10 +8,11 @@ namespace asb {
 
 // ---- SpMM (src/kernels.cpp:210-334) ------------------------------------
 // K1: warp per row, lane per feature, scalar loads, natural row order.
-// b: f32, or bf16 words when bf16 (every kernel reads B through an exact
-// bf16 -> f32 step, so a bf16 B gives the f32 result on float(B) bit for bit)
+// b: f32, or 16-bit words when wt != 0 (half.cuh: 1 bf16, 2 f16; every
+// kernel reads B through an exact -> f32 step, so the result is the f32
+// result on float(B) bit for bit)
 void launch_spmm_baseline(Graph& g, const float* val, const void* b, std::uint32_t f, float* c, cudaStream_t s,
-                          bool bf16 = false);
+                          int wt = 0);
 // K2: row groups over rows in degree-descending order; f_tile splits the
 // feature dimension into independent work items; wpb warps per CTA.
 // Rows order[offset, offset+n_list) of the degree-descending order; rows of
@@ -20,14 +21,14 @@ void launch_spmm_baseline(Graph& g, const float* val, const void* b, std::uint32
 void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uint64_t n_list,
                       const void* b, std::uint32_t f, float* c, std::uint64_t f_tile, bool vec,
                       std::uint32_t wpb, cudaStream_t s, const unsigned* finite = nullptr,
-                      const float* rmax = nullptr, const double* rsum = nullptr, bool bf16 = false);
+                      const float* rmax = nullptr, const double* rsum = nullptr, int wt = 0);
 // K3: hub split -- light rows via K2 plus 2048-nnz pieces with ordered
 // fp64 partial reduction.
 void launch_spmm_hubsplit(Graph& g, const float* val, const void* b, std::uint32_t f, float* c,
                           std::uint64_t f_tile, bool vec, std::uint32_t wpb,
                           std::uint64_t hub_threshold, cudaStream_t s,
                           const unsigned* finite = nullptr, const float* rmax = nullptr,
-                          const double* rsum = nullptr, bool bf16 = false);
+                          const double* rsum = nullptr, int wt = 0);
 // Softmax mode of K2/K3 (rmax != nullptr): `val` holds raw scores and each
 // entry's value is p_e = softmax of its row from (rmax[row], rsum[row])
 // (softmax.cuh), computed by the loading lane -- the SpMM half of the fused
@@ -53,17 +54,18 @@ void sddmm_chunks_prepare(Graph& g, const float* x, const float* y, std::uint32_
                           std::uint64_t f_tile, bool vec, cudaStream_t s, const unsigned* finite,
                           std::uint64_t r0 = 0, std::uint64_t r1 = ~0ull);
 
-// SDDMM on bf16 X, Y (raw words): ord 0 sequential, 1 the four-way vec blocks
-// of width ft; baseline = the direct kernel (guardrail mapping)
-void launch_sddmm_bf16(Graph& g, const std::uint16_t* x, const std::uint16_t* y, std::uint32_t f, float* out,
-                       std::uint32_t ft, int ord, bool baseline, cudaStream_t s);
+// SDDMM on 16-bit X, Y words (wt: 1 bf16, 2 f16; half.cuh): ord 0
+// sequential, 1 the four-way vec blocks of width ft; baseline = the direct
+// kernel (guardrail mapping)
+void launch_sddmm_half(Graph& g, const std::uint16_t* x, const std::uint16_t* y, std::uint32_t f, float* out,
+                       std::uint32_t ft, int ord, bool baseline, cudaStream_t s, int wt);
 
 // Device flag: 1 iff p[0..n) has no Inf/NaN (gates the re-bias widening,
 // widen.cuh).  Written into g.flag (one flag per graph; a graph handle runs
 // one operator at a time).
 const unsigned* finite_flag(Graph& g, const float* p, std::uint64_t n, cudaStream_t s);
-// the same over n bf16 words
-const unsigned* finite_flag_bf16(Graph& g, const unsigned short* p, std::uint64_t n, cudaStream_t s);
+// the same over n 16-bit words of type wt (1 bf16, 2 f16)
+const unsigned* finite_flag_half(Graph& g, const std::uint16_t* p, std::uint64_t n, cudaStream_t s, int wt);
 
 // ---- row softmax (src/kernels.cpp:431-461) ----------------------------
 void launch_row_softmax(Graph& g, const float* vin, float* vout, cudaStream_t s);

@@ -22,6 +22,7 @@
 // so each lane's LDS.128 walk along its own row is conflict-free.
 #include "ops.hpp"
 #include "dcheck.cuh"
+#include "half.cuh"
 #include "l2hint.cuh"
 #include "widen.cuh"
 
@@ -60,10 +61,17 @@ __device__ __forceinline__ double x_at(const float* p, std::uint32_t t) { return
 __device__ __forceinline__ double x_at(const double* p, std::uint32_t t) { return p[t]; }
 // bf16 operands (raw 16-bit words): bf16 -> f32 is exact, so every product
 // is the f32 path's on float(X), float(Y)
-__device__ __forceinline__ float bf16f(unsigned short h) { return __uint_as_float(unsigned(h) << 16); }
+__device__ __forceinline__ float bf16f(unsigned short h) { return half_to_f32<kWtBF16>(h); }
 __device__ __forceinline__ double x_at(const unsigned short* p, std::uint32_t t) { return double(bf16f(p[t])); }
 __device__ __forceinline__ float y_at(const float* p, std::uint32_t t) { return p[t]; }
 __device__ __forceinline__ float y_at(const unsigned short* p, std::uint32_t t) { return bf16f(p[t]); }
+// IEEE half words as their own element type, so the generic dot loops pick
+// the f16 conversion by overload
+struct f16w {
+    unsigned short v;
+};
+__device__ __forceinline__ double x_at(const f16w* p, std::uint32_t t) { return double(half_to_f32<kWtF16>(p[t].v)); }
+__device__ __forceinline__ float y_at(const f16w* p, std::uint32_t t) { return half_to_f32<kWtF16>(p[t].v); }
 
 // Sequential dot over [0, f): VLDS uses 16-byte reads (f % 4 == 0, both
 // pointers 16-byte aligned).
@@ -297,16 +305,17 @@ __global__ void widen_kernel(const float4* __restrict__ x, double2* __restrict__
     }
 }
 
-// bf16 X (4 words per uint2) -> f64, the same layout and scaling
-__global__ void widen_bf16_kernel(const uint2* __restrict__ x, double2* __restrict__ xd, std::uint64_t n4,
+// 16-bit X (4 words per uint2, half.cuh) -> f64, the same layout and scaling
+template <int WT>
+__global__ void widen_half_kernel(const uint2* __restrict__ x, double2* __restrict__ xd, std::uint64_t n4,
                                   const unsigned* __restrict__ finite, int mix_all) {
     const double up = (finite && *finite) ? kWidenUp : 1.0;
     const double up01 = mix_all ? up : 1.0;
     for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
          i += std::uint64_t(gridDim.x) * blockDim.x) {
         const uint2 v = __ldg(x + i);
-        const float a = __uint_as_float(v.x << 16), b = __uint_as_float(v.x & 0xffff0000u);
-        const float c = __uint_as_float(v.y << 16), d = __uint_as_float(v.y & 0xffff0000u);
+        const float a = half_lo<WT>(v.x), b = half_hi<WT>(v.x);
+        const float c = half_lo<WT>(v.y), d = half_hi<WT>(v.y);
         xd[2 * i] = make_double2(double(a) * up01, double(b) * up01);
         xd[2 * i + 1] = make_double2(double(c) * up, double(d) * up);
     }
@@ -711,31 +720,29 @@ struct Pair1Shape {
 };
 
 // Y features [t, t+4) of the lane's two rows as f32 (u for entry a, w for b)
-template <int F, bool BF>
+template <int F, int WT>
 __device__ __forceinline__ void pair1_y4(const void* ya, const void* yb, int ka, int kb, int t, float4& u,
                                          float4& w) {
-    if constexpr (BF) {
+    if constexpr (WT != kWtF32) {
         const unsigned short* pa = static_cast<const unsigned short*>(ya);
         const unsigned short* pb = static_cast<const unsigned short*>(yb);
         const uint2 ua = *reinterpret_cast<const uint2*>(pa + 8 * ((t >> 3) ^ ka) + (t & 4));
         const uint2 wb = *reinterpret_cast<const uint2*>(pb + 8 * ((t >> 3) ^ kb) + (t & 4));
-        u = make_float4(__uint_as_float(ua.x << 16), __uint_as_float(ua.x & 0xffff0000u),
-                        __uint_as_float(ua.y << 16), __uint_as_float(ua.y & 0xffff0000u));
-        w = make_float4(__uint_as_float(wb.x << 16), __uint_as_float(wb.x & 0xffff0000u),
-                        __uint_as_float(wb.y << 16), __uint_as_float(wb.y & 0xffff0000u));
+        u = make_float4(half_lo<WT>(ua.x), half_hi<WT>(ua.x), half_lo<WT>(ua.y), half_hi<WT>(ua.y));
+        w = make_float4(half_lo<WT>(wb.x), half_hi<WT>(wb.x), half_lo<WT>(wb.y), half_hi<WT>(wb.y));
     } else {
         u = *reinterpret_cast<const float4*>(static_cast<const float*>(ya) + 4 * ((t >> 2) ^ ka));
         w = *reinterpret_cast<const float4*>(static_cast<const float*>(yb) + 4 * ((t >> 2) ^ kb));
     }
 }
 
-template <int F, int ORD, int FT, bool XS, int MIX, bool SAME, bool BF = false>
+template <int F, int ORD, int FT, bool XS, int MIX, bool SAME, int WT = kWtF32>
 __device__ __forceinline__ void pair1_pass(const double* __restrict__ xa, const double* __restrict__ xb,
                                           const void* ya, const void* yb, int ka, int kb, double (&c)[2][5]) {
 #pragma unroll 4
     for (int t = 0; t < F; t += 4) {
         float4 u, w;
-        pair1_y4<F, BF>(ya, yb, ka, kb, t, u, w);
+        pair1_y4<F, WT>(ya, yb, ka, kb, t, u, w);
         const double2 x01 = ld_x2<XS>(xa + t);
         const double2 x23 = ld_x2<XS>(xa + t + 2);
         double2 z01 = x01, z23 = x23;
@@ -770,7 +777,7 @@ __device__ __forceinline__ void pair1_pass(const double* __restrict__ xa, const 
     }
 }
 
-template <int F, int ORD, int FT, int MIX, bool BF = false>
+template <int F, int ORD, int FT, int MIX, int WT = kWtF32>
 __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict__ rowptr,
                                                 const std::uint32_t* __restrict__ colind,
                                                 const std::uint32_t* __restrict__ chunk_row, std::uint64_t n_rows,
@@ -778,8 +785,8 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
                                                 float* __restrict__ out, std::uint64_t nnz, std::uint64_t c_begin,
                                                 std::uint64_t c_end, int keep, std::uint64_t n_cols) {
     (void)n_cols;  // bounds of the checked build
-    using Sh = Pair1Shape<F, BF>;
-    using YT = typename std::conditional<BF, unsigned short, float>::type;
+    using Sh = Pair1Shape<F, WT != kWtF32>;
+    using YT = typename std::conditional<WT != kWtF32, unsigned short, float>::type;
     constexpr int kUnitElems = 16 / Sh::kYElem;  // Y elements per 16-byte unit
     const YT* __restrict__ y = static_cast<const YT*>(yv);
     extern __shared__ __align__(16) char smem[];
@@ -864,11 +871,11 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
         const bool all_same = __all_sync(FULL, rela == relb);  // warp-uniform, before the split
         if (rela < Sh::KX && relb < Sh::KX) {
             if (all_same)
-                pair1_pass<F, ORD, FT, true, MIX, true, BF>(xs + rela * F, xs + relb * F, ya, yb, ka, kb, c);
+                pair1_pass<F, ORD, FT, true, MIX, true, WT>(xs + rela * F, xs + relb * F, ya, yb, ka, kb, c);
             else
-                pair1_pass<F, ORD, FT, true, MIX, false, BF>(xs + rela * F, xs + relb * F, ya, yb, ka, kb, c);
+                pair1_pass<F, ORD, FT, true, MIX, false, WT>(xs + rela * F, xs + relb * F, ya, yb, ka, kb, c);
         } else {
-            pair1_pass<F, ORD, FT, false, MIX, false, BF>(xd + std::uint64_t(ra) * F, xd + std::uint64_t(rb) * F,
+            pair1_pass<F, ORD, FT, false, MIX, false, WT>(xd + std::uint64_t(ra) * F, xd + std::uint64_t(rb) * F,
                                                          ya, yb, ka, kb, c);
         }
         if (ea < e_end) st_stream(out + ea, float(c[0][0]), pol_s);
@@ -882,7 +889,7 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
 // (17.4 KB per warp at F=64) caps residency at 3 CTAs through shared memory
 // anyway; bf16 staging halves that, so its kernels can trade registers for
 // occupancy.
-template <int F, int ORD, int FT, bool BF = false, int MINB = 3>
+template <int F, int ORD, int FT, int WT = kWtF32, int MINB = 3>
 __global__ void __launch_bounds__(128, MINB)
     sddmm_pair1_kernel(const std::uint64_t* __restrict__ rowptr, const std::uint32_t* __restrict__ colind,
                       const std::uint32_t* __restrict__ chunk_row, std::uint64_t n_rows,
@@ -891,10 +898,10 @@ __global__ void __launch_bounds__(128, MINB)
                       const unsigned* __restrict__ finite, int keep, std::uint64_t n_cols) {
     // keep: Y fits the L2 (kKeepMaxBytes) -- the Y and X staging reads evict_last
     if (finite && *finite)
-        sddmm_pair1_body<F, ORD, FT, 1, BF>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin, c_end,
+        sddmm_pair1_body<F, ORD, FT, 1, WT>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin, c_end,
                                             keep, n_cols);
     else
-        sddmm_pair1_body<F, ORD, FT, 0, BF>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin, c_end,
+        sddmm_pair1_body<F, ORD, FT, 0, WT>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin, c_end,
                                             keep, n_cols);
 }
 
@@ -1155,12 +1162,14 @@ void launch_sddmm_chunks(Graph& g, const float* x, const float* y, std::uint32_t
     }
 }
 
-// SDDMM on bf16 X and Y: the pair kernel with bf16 Y staging
-// for F in {32, 64} (16-byte aligned operands, blocks that line up), the
-// direct kernel otherwise.  ord/ft as in launch_sddmm_chunks; the result is
-// the f32 SDDMM on float(X), float(Y) bit for bit.
-void launch_sddmm_bf16(Graph& g, const std::uint16_t* x, const std::uint16_t* y, std::uint32_t f, float* out,
-                       std::uint32_t ft, int ord, bool baseline, cudaStream_t s) {
+// SDDMM on 16-bit X and Y (half.cuh: bf16 or f16): the pair
+// kernel with 16-bit Y staging for F in {32, 64} (16-byte aligned operands,
+// blocks that line up), the direct kernel otherwise.  ord/ft as in
+// launch_sddmm_chunks; the result is the f32 SDDMM on float(X), float(Y) bit
+// for bit.
+template <int WT>
+void launch_sddmm_half_t(Graph& g, const std::uint16_t* x, const std::uint16_t* y, std::uint32_t f, float* out,
+                         std::uint32_t ft, int ord, bool baseline, cudaStream_t s) {
     if (g.nnz == 0) return;
     ensure_chunk_rows(g);
     const std::uint64_t c_end = (g.nnz + 31) / 32;
@@ -1168,8 +1177,10 @@ void launch_sddmm_bf16(Graph& g, const std::uint16_t* x, const std::uint16_t* y,
         ASB_CUDA(cudaMemsetAsync(out, 0, g.nnz * 4, s));
         return;
     }
-    const auto* xs = reinterpret_cast<const unsigned short*>(x);
-    const auto* ys = reinterpret_cast<const unsigned short*>(y);
+    // element type of the direct kernel's generic loops: ushort = bf16, f16w = half
+    using ET = typename std::conditional<WT == kWtF16, f16w, unsigned short>::type;
+    const auto* xs = reinterpret_cast<const ET*>(x);
+    const auto* ys = reinterpret_cast<const ET*>(y);
     const bool pair_ok = !baseline && (f == 32 || f == 64) && aligned16(x) && aligned16(y) &&
                          (ord == 0 || ft >= f || ft == 32) && dev_knob("AUTOSAGE_DEV_SDDMM_PAIR", 1);
     if (!pair_ok) {
@@ -1185,20 +1196,20 @@ void launch_sddmm_bf16(Graph& g, const std::uint16_t* x, const std::uint16_t* y,
     }
     const unsigned* fin = nullptr;
     if (dev_knob("AUTOSAGE_DEV_SDDMM_MIX", 1) && g.n_cols * f * 2 <= (std::uint64_t(96) << 20))
-        fin = finite_flag_bf16(g, ys, g.n_cols * f, s);
+        fin = finite_flag_half(g, y, g.n_cols * f, s, WT);
     g.xwide.ensure(std::max<std::uint64_t>(g.n_rows * f, 1));
     const std::uint64_t n4 = g.n_rows * f / 4;
     if (n4) {
         const unsigned wb = unsigned(std::min<std::uint64_t>((n4 + 255) / 256, std::uint64_t(sm_count()) * 8));
-        widen_bf16_kernel<<<std::max(wb, 1u), 256, 0, s>>>(reinterpret_cast<const uint2*>(x),
+        widen_half_kernel<WT><<<std::max(wb, 1u), 256, 0, s>>>(reinterpret_cast<const uint2*>(x),
                                                            reinterpret_cast<double2*>(g.xwide.get()), n4, fin,
                                                            mix_all());
-        check_launch("widen_bf16_kernel");
+        check_launch("widen_half_kernel");
     }
     const int sms = sm_count();
     auto pair1 = [&](auto fc) {
         constexpr int F = decltype(fc)::value;
-        const std::uint64_t wbytes = Pair1Shape<F, true>::kWarpBytes;
+        const std::uint64_t wbytes = Pair1Shape<F, WT != kWtF32>::kWarpBytes;
         const int kWarps = 4;
         auto run = [&](auto kernel) {
             const std::size_t smem = std::size_t(wbytes * kWarps);
@@ -1216,14 +1227,20 @@ void launch_sddmm_bf16(Graph& g, const std::uint16_t* x, const std::uint16_t* y,
         // F=64 2.03 -> 1.95 ms against 3; 5 (96 registers) is slower at F=64
         const int minb = dev_knob("AUTOSAGE_DEV_SDDMM_BF16_MINB", 4);
         if (ord == 0) {
-            if (minb == 3) run(sddmm_pair1_kernel<F, 0, 0, true, 3>);
-            else if (minb == 5) run(sddmm_pair1_kernel<F, 0, 0, true, 5>);
-            else run(sddmm_pair1_kernel<F, 0, 0, true, 4>);
-        } else if (ft >= f) run(sddmm_pair1_kernel<F, 1, 0, true, 4>);
-        else run(sddmm_pair1_kernel<F, 1, 32, true, 4>);
+            if (minb == 3) run(sddmm_pair1_kernel<F, 0, 0, WT, 3>);
+            else if (minb == 5) run(sddmm_pair1_kernel<F, 0, 0, WT, 5>);
+            else run(sddmm_pair1_kernel<F, 0, 0, WT, 4>);
+        } else if (ft >= f) run(sddmm_pair1_kernel<F, 1, 0, WT, 4>);
+        else run(sddmm_pair1_kernel<F, 1, 32, WT, 4>);
     };
     if (f == 32) pair1(std::integral_constant<int, 32>{});
     else pair1(std::integral_constant<int, 64>{});
+}
+
+void launch_sddmm_half(Graph& g, const std::uint16_t* x, const std::uint16_t* y, std::uint32_t f, float* out,
+                       std::uint32_t ft, int ord, bool baseline, cudaStream_t s, int wt) {
+    if (wt == kWtF16) launch_sddmm_half_t<kWtF16>(g, x, y, f, out, ft, ord, baseline, s);
+    else launch_sddmm_half_t<kWtBF16>(g, x, y, f, out, ft, ord, baseline, s);
 }
 
 } // namespace asb

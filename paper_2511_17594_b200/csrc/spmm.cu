@@ -371,7 +371,7 @@ bool longrow_ok(std::uint32_t f, bool vec) {
 // ---------------------------------------------------------------------------
 // K1: the guardrail baseline.  Warp per row in natural order, lane per
 // feature (NF features per lane per pass), scalar loads, no prefetch.
-template <int NF, class BT = float>
+template <int NF, class BT = float, int WT = kWtF32>
 __global__ void spmm_baseline_kernel(const std::uint64_t* __restrict__ rowptr,
                                      const std::uint32_t* __restrict__ colind,
                                      const float* __restrict__ val, const BT* __restrict__ b,
@@ -391,7 +391,7 @@ __global__ void spmm_baseline_kernel(const std::uint64_t* __restrict__ rowptr,
 #pragma unroll
             for (int q = 0; q < NF; ++q) {
                 const std::uint32_t t = std::uint32_t(lane + 32 * q);
-                if (f0 + t < f) acc[q] = __fma_rn(v, double(comp(brow[t], 0)), acc[q]);
+                if (f0 + t < f) acc[q] = __fma_rn(v, double(comp<WT>(brow[t], 0)), acc[q]);
             }
         }
 #pragma unroll
@@ -477,14 +477,14 @@ void launch_seg(const SegArgs& a, bool has_val, std::uint32_t wpb, cudaStream_t 
     // the permuted-value (spmm_vp.cu) and bf16 (spmm_bf16.cu) instantiations
     // live in their own translation units so the three compile in parallel
     if (a.vperm) {  // values read through a transpose permutation (f32 B, values present)
-        if (VEC == 8 || a.bf16 || a.rmax || !has_val)
+        if (VEC == 8 || a.wt || a.rmax || !has_val)
             throw LogicError("spmm: permuted values take f32 B and values");
         launch_seg_vp(VEC, LPR, NCH, a, pieces, nb, nt, s);
         return;
     }
-    if (VEC == 8 || a.bf16) {  // bf16 B: default tuning, no softmax mode
-        if (a.rmax) throw LogicError("spmm softmax mode takes f32 operands");
-        launch_seg_bf16(VEC, LPR, NCH, a, has_val, pieces, nb, nt, s);
+    if (VEC == 8 || a.wt) {  // 16-bit B (bf16 / f16): default tuning (softmax mode included)
+        if (a.wt == kWtF16) launch_seg_f16(VEC, LPR, NCH, a, has_val, pieces, nb, nt, s);
+        else launch_seg_bf16(VEC, LPR, NCH, a, has_val, pieces, nb, nt, s);
         return;
     }
     if constexpr (VEC == 8) {
@@ -532,8 +532,8 @@ struct TileShape {
 // lane).  Below f = 64 the 4-wide tiles keep more lanes per row in flight
 // (Reddit-shape F=32: 0.90 ms 4-wide vs 1.10 ms 8-wide; F=64: 1.72 vs 1.56;
 // F=128: 3.80 vs 3.29).
-bool vec8_ok(const void* b, std::uint32_t f, bool vec, bool bf16) {
-    return bf16 && vec && f >= 64 && f % 8 == 0 && (reinterpret_cast<std::uintptr_t>(b) & 15) == 0;
+bool vec8_ok(const void* b, std::uint32_t f, bool vec, int wt) {
+    return wt != kWtF32 && vec && f >= 64 && f % 8 == 0 && (reinterpret_cast<std::uintptr_t>(b) & 15) == 0;
 }
 
 TileShape tile_shape(std::uint32_t f, std::uint64_t f_tile, bool vec, bool vec8 = false) {
@@ -577,18 +577,23 @@ std::uint64_t long_row_min(const Graph& g) {
 } // namespace
 
 void launch_spmm_baseline(Graph& g, const float* val, const void* bv, std::uint32_t f, float* c,
-                          cudaStream_t s, bool bf16) {
+                          cudaStream_t s, int wt) {
     if (g.n_rows == 0 || f == 0) return;
     const std::uint64_t threads = g.n_rows * 32;
     const unsigned blocks = unsigned((threads + 255) / 256);
-    if (bf16) {
+    if (wt != kWtF32) {
         const auto* b = static_cast<const unsigned short*>(bv);
-        if (f <= 32)
-            spmm_baseline_kernel<1><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f, g.val_perm);
-        else if (f <= 64)
-            spmm_baseline_kernel<2><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f, g.val_perm);
-        else
-            spmm_baseline_kernel<4><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f, g.val_perm);
+        auto go = [&](auto wc) {
+            constexpr int W = decltype(wc)::value;
+            if (f <= 32)
+                spmm_baseline_kernel<1, unsigned short, W><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f, g.val_perm);
+            else if (f <= 64)
+                spmm_baseline_kernel<2, unsigned short, W><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f, g.val_perm);
+            else
+                spmm_baseline_kernel<4, unsigned short, W><<<blocks, 256, 0, s>>>(g.rowptr.get(), g.colind.get(), val, b, c, g.n_rows, f, g.val_perm);
+        };
+        if (wt == kWtF16) go(std::integral_constant<int, kWtF16>{});
+        else go(std::integral_constant<int, kWtBF16>{});
         check_launch("spmm_baseline_kernel");
         return;
     }
@@ -607,7 +612,7 @@ void launch_spmm_baseline(Graph& g, const float* val, const void* bv, std::uint3
 void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uint64_t n_list,
                       const void* b, std::uint32_t f, float* c, std::uint64_t f_tile, bool vec,
                       std::uint32_t wpb, cudaStream_t s, const unsigned* finite, const float* rmax,
-                      const double* rsum, bool bf16) {
+                      const double* rsum, int wt) {
     if (rmax) vec = true;  // softmax mode runs float4 tiles (same numerics, engine gates f % 4)
     if (n_list == 0 || f == 0) return;
     ensure_order(g);
@@ -615,7 +620,7 @@ void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uin
     // kernel on a forked stream, concurrent with the group kernel
     const std::uint64_t lmin = long_row_min(g);
     std::uint64_t n_long = 0;
-    if (lmin > 0 && !bf16 && !g.val_perm && longrow_ok(f, vec)) {
+    if (lmin > 0 && !wt && !g.val_perm && longrow_ok(f, vec)) {
         const std::uint64_t ge = rows_with_degree_at_least(g, lmin);
         n_long = ge > offset ? std::min(ge - offset, n_list) : 0;
     }
@@ -641,7 +646,7 @@ void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uin
         n_list -= n_long;
     }
     if (n_list) {
-        const bool v8 = vec8_ok(b, f, vec, bf16);
+        const bool v8 = vec8_ok(b, f, vec, wt);
         const TileShape t = tile_shape(f, f_tile, vec, v8);
         SegArgs a{};
         a.rowptr = g.rowptr.get();
@@ -661,8 +666,8 @@ void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uin
         a.n_cols = g.n_cols;
         a.nnz = g.nnz;
         a.off32 = fast_gather_ok(g, f);
-        a.bf16 = bf16;
-        a.keep_b = std::uint64_t(g.n_cols) * f * (bf16 ? 2 : 4) <= kKeepMaxBytes;
+        a.wt = wt;
+        a.keep_b = std::uint64_t(g.n_cols) * f * (wt ? 2 : 4) <= kKeepMaxBytes;
         a.tile_w = t.tile_w;
         wpb = warps_per_cta(wpb);
         if (v8) launch_seg_vec<8>(a, val != nullptr, t.lanes, wpb, s);
@@ -675,12 +680,12 @@ void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uin
 void launch_spmm_hubsplit(Graph& g, const float* val, const void* b, std::uint32_t f, float* c,
                           std::uint64_t f_tile, bool vec, std::uint32_t wpb,
                           std::uint64_t hub_threshold, cudaStream_t s, const unsigned* finite,
-                          const float* rmax, const double* rsum, bool bf16) {
+                          const float* rmax, const double* rsum, int wt) {
     if (g.n_rows == 0 || f == 0) return;
     if (rmax) vec = true;
     const HubPlan& plan = ensure_hub_plan(g, hub_threshold);
     wpb = warps_per_cta(wpb);
-    const bool v8 = vec8_ok(b, f, vec, bf16);
+    const bool v8 = vec8_ok(b, f, vec, wt);
     const TileShape t = tile_shape(f, f_tile, vec, v8);
     if (plan.n_slots) g.scratch.ensure(plan.n_slots * f);
     // light rows on the forked stream, concurrent with the pieces: their
@@ -693,7 +698,7 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const void* b, std::uint32
     if (fork_light) {
         cudaStream_t aux = graph_fork(g, s);
         launch_spmm_rows(g, val, plan.n_heavy, plan.n_light, b, f, c, f_tile, vec, wpb, aux, finite, rmax, rsum,
-                         bf16);
+                         wt);
     }
     if (plan.n_pieces) {
         SegArgs a{};
@@ -718,8 +723,8 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const void* b, std::uint32
         a.n_cols = g.n_cols;
         a.nnz = g.nnz;
         a.off32 = fast_gather_ok(g, f);
-        a.bf16 = bf16;
-        a.keep_b = std::uint64_t(g.n_cols) * f * (bf16 ? 2 : 4) <= kKeepMaxBytes;
+        a.wt = wt;
+        a.keep_b = std::uint64_t(g.n_cols) * f * (wt ? 2 : 4) <= kKeepMaxBytes;
         a.tile_w = t.tile_w;
         // pieces are up to 2048-entry dependent chains: when there are too
         // few of them to fill the lane-group kernel (under a wave), the ring
@@ -727,7 +732,7 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const void* b, std::uint32
         // thousands of pieces the group kernel's throughput wins (Products
         // 8-way shard: 1.36 ms vs 1.72 ms)
         const bool few = plan.n_pieces <= std::uint64_t(4) * std::uint64_t(g.sms);
-        if (few && !bf16 && !g.val_perm && longrow_ok(f, vec)) launch_longrow<true>(a, plan.n_pieces, s);
+        if (few && !wt && !g.val_perm && longrow_ok(f, vec)) launch_longrow<true>(a, plan.n_pieces, s);
         else if (v8) launch_seg_vec<8>(a, val != nullptr, t.lanes, wpb, s);
         else if (vec) launch_seg_vec<4>(a, val != nullptr, t.lanes, wpb, s);
         else launch_seg_vec<1>(a, val != nullptr, t.lanes, wpb, s);
@@ -735,7 +740,7 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const void* b, std::uint32
     if (fork_light) graph_join(g, s);
     else if (plan.n_light)
         launch_spmm_rows(g, val, plan.n_heavy, plan.n_light, b, f, c, f_tile, vec, wpb, s, finite, rmax, rsum,
-                         bf16);
+                         wt);
     if (plan.n_red) {
         const std::uint64_t total = plan.n_red * f;
         const unsigned blocks = unsigned(std::min<std::uint64_t>((total + 255) / 256, 148 * 32));

@@ -1,59 +1,11 @@
-// spmm_bf16.cu -- lane-group SpMM instantiations for a bf16 B (raw 16-bit
-// words; exact bf16 -> f32, so the f32 path's bits on float(B)): 1-, 4- and
-// 8-wide tiles, with and without values, rows or hub pieces.
-#include "spmm_kernels.cuh"
+// spmm_bf16.cu -- the lane-group SpMM on a bf16 B (spmm_half.cuh, WT = bf16).
+#include "spmm_half.cuh"
 
 namespace asb {
 
-namespace {
-
-// (LPR, NCH) pairs the lane-group launcher uses: groups of 1..32 lanes with one
-// chunk, and whole warps with 2, 4 or 8 chunks per lane
-template <class F>
-void by_shape(int lpr, int nch, F&& f) {
-    switch (lpr) {
-    case 1: f(std::integral_constant<int, 1>{}, std::integral_constant<int, 1>{}); return;
-    case 2: f(std::integral_constant<int, 2>{}, std::integral_constant<int, 1>{}); return;
-    case 4: f(std::integral_constant<int, 4>{}, std::integral_constant<int, 1>{}); return;
-    case 8: f(std::integral_constant<int, 8>{}, std::integral_constant<int, 1>{}); return;
-    case 16: f(std::integral_constant<int, 16>{}, std::integral_constant<int, 1>{}); return;
-    default: break;
-    }
-    switch (nch) {
-    case 1: f(std::integral_constant<int, 32>{}, std::integral_constant<int, 1>{}); return;
-    case 2: f(std::integral_constant<int, 32>{}, std::integral_constant<int, 2>{}); return;
-    case 4: f(std::integral_constant<int, 32>{}, std::integral_constant<int, 4>{}); return;
-    default: f(std::integral_constant<int, 32>{}, std::integral_constant<int, 8>{}); return;
-    }
-}
-
-}  // namespace
-
 void launch_seg_bf16(int vec, int lpr, int nch, const SegArgs& a, bool has_val, bool pieces, unsigned nb,
                      unsigned nt, cudaStream_t s) {
-    auto go = [&](auto vc) {
-        constexpr int VEC = decltype(vc)::value;
-        by_shape(lpr, nch, [&](auto lc, auto cc) {
-            constexpr int LPR = decltype(lc)::value, NCH = decltype(cc)::value;
-            if constexpr (VEC == 8 && NCH == 8) {
-                throw LogicError("8-wide tiles take at most 4 chunks per lane");
-            } else {
-                constexpr int U = unroll_for(VEC, NCH), R = maxreg_for(VEC, NCH);
-                const std::size_t sm = seg_smem(nt);
-                if (has_val) {
-                    if (pieces) spmm_seg_kernel<VEC, LPR, NCH, true, true, U, R, false, true><<<nb, nt, sm, s>>>(a);
-                    else spmm_seg_kernel<VEC, LPR, NCH, true, false, U, R, false, true><<<nb, nt, sm, s>>>(a);
-                } else {
-                    if (pieces) spmm_seg_kernel<VEC, LPR, NCH, false, true, U, R, false, true><<<nb, nt, sm, s>>>(a);
-                    else spmm_seg_kernel<VEC, LPR, NCH, false, false, U, R, false, true><<<nb, nt, sm, s>>>(a);
-                }
-            }
-        });
-    };
-    if (vec == 8) go(std::integral_constant<int, 8>{});
-    else if (vec == 4) go(std::integral_constant<int, 4>{});
-    else go(std::integral_constant<int, 1>{});
-    check_launch("spmm_seg_kernel");
+    launch_seg_half_t<kWtBF16>(vec, lpr, nch, a, has_val, pieces, nb, nt, s);
 }
 
 }  // namespace asb

@@ -6,6 +6,7 @@
 
 #include "ops.hpp"
 #include "dcheck.cuh"
+#include "half.cuh"
 #include "l2hint.cuh"
 #include "softmax.cuh"
 #include "widen.cuh"
@@ -23,7 +24,7 @@ struct SegArgs {
     const std::uint64_t* rowptr;
     const std::uint32_t* colind;
     const float* val;
-    const void* b;                    // f32, or bf16 words when BF
+    const void* b;                    // f32, or 16-bit words (half.cuh) when wt != 0
     float* c;
     double* scratch;
     const std::uint32_t* rowlist;     // row mode: row ids (nullptr: identity)
@@ -36,7 +37,7 @@ struct SegArgs {
     const float* rmax;                // softmax mode: val holds raw scores, and
     const double* rsum;               // p_e = softmax of the row (softmax.cuh)
     int off32;                        // n_cols * f < 2^32: 32-bit element offsets
-    int bf16;                         // B holds bf16 (seg kernels' BF instantiation)
+    int wt;                           // B word type (half.cuh): 0 f32, 1 bf16, 2 f16
     int keep_b;                       // B fits L2 (kKeepMaxBytes): gathers evict_last
     std::uint64_t n_items;
     std::uint64_t n_rows, n_cols, nnz;  // bounds of the checked build (dcheck.cuh)
@@ -50,45 +51,51 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int kSegMaxS = 8;  // max entries per lane per fast-loop block (seg_smem)
 
-// Load type of VEC consecutive B elements: f32 (float / float4) or, with BF,
-// bf16 (as raw 16-bit words: ushort / uint2 -- 8-byte loads for 4 features).
-template <int VEC, bool BF = false>
+// Load type of VEC consecutive B elements: f32 (float / float4) or, for the
+// 16-bit word types (WT, half.cuh), raw words: ushort / uint2 (8-byte loads
+// for 4 features) / uint4 (8 features).
+template <int VEC, int WT = kWtF32>
 struct VecT;
 template <>
-struct VecT<1, false> {
+struct VecT<1, kWtF32> {
     using T = float;
 };
 template <>
-struct VecT<4, false> {
+struct VecT<4, kWtF32> {
     using T = float4;
 };
-template <>
-struct VecT<1, true> {
+template <int WT>
+struct VecT<1, WT> {
     using T = unsigned short;
 };
-template <>
-struct VecT<4, true> {
+template <int WT>
+struct VecT<4, WT> {
     using T = uint2;
 };
-template <>
-struct VecT<8, true> {
+template <int WT>
+struct VecT<8, WT> {
     using T = uint4;
 };
 
+template <int WT>
 __device__ __forceinline__ float comp(const float& v, int) { return v; }
+template <int WT>
 __device__ __forceinline__ float comp(const float4& v, int q) {
     return q == 0 ? v.x : (q == 1 ? v.y : (q == 2 ? v.z : v.w));
 }
-// bf16 -> f32 is exact (the f32 with the same top 16 bits), so every later
-// widening and product is the f32 path's on float(B)
-__device__ __forceinline__ float comp(const unsigned short& h, int) { return __uint_as_float(unsigned(h) << 16); }
+// 16-bit words -> f32 is exact (half.cuh), so every later widening and
+// product is the f32 path's on float(B)
+template <int WT>
+__device__ __forceinline__ float comp(const unsigned short& h, int) { return half_to_f32<WT>(h); }
+template <int WT>
 __device__ __forceinline__ float comp(const uint2& w, int q) {
     const unsigned x = q < 2 ? w.x : w.y;
-    return __uint_as_float((q & 1) ? (x & 0xffff0000u) : (x << 16));
+    return (q & 1) ? half_hi<WT>(x) : half_lo<WT>(x);
 }
+template <int WT>
 __device__ __forceinline__ float comp(const uint4& w, int q) {
     const unsigned x = q < 2 ? w.x : (q < 4 ? w.y : (q < 6 ? w.z : w.w));
-    return __uint_as_float((q & 1) ? (x & 0xffff0000u) : (x << 16));
+    return (q & 1) ? half_hi<WT>(x) : half_lo<WT>(x);
 }
 
 [[maybe_unused]] __host__ __device__ constexpr int unroll_for(int vec, int nch) {
@@ -108,11 +115,12 @@ __device__ __forceinline__ float comp(const uint4& w, int q) {
 // acc[ch][q] += v * B component, one DFMA each, with MIX's widening split
 // first component of a VEC-wide load re-biased on the ALU (MIX): f32 float4
 // splits half/half with the XU's F2F; a bf16 component's re-bias is two ALU
-// ops (its low mantissa word is zero), so bf16 loads put 3/4 on the ALU
-template <int VEC, bool BF>
-__host__ __device__ constexpr int mix_from() { return VEC == 1 ? 0 : (BF ? VEC / 4 : 2); }
+// ops (its low mantissa word is zero), so bf16 loads put 3/4 on the ALU (an
+// f16 word is first converted to f32, then split like f32)
+template <int VEC, int WT>
+__host__ __device__ constexpr int mix_from() { return VEC == 1 ? 0 : (WT == kWtBF16 ? VEC / 4 : 2); }
 
-template <int VEC, int NCH, int MIX, class VT, int MQ = mix_from<VEC, false>()>
+template <int VEC, int NCH, int MIX, class VT, int MQ = mix_from<VEC, kWtF32>(), int WT = kWtF32>
 __device__ __forceinline__ void seg_accumulate(double (&acc)[NCH][VEC], double v, const VT (&bv)[NCH]) {
     const double vu = MIX ? v * kWidenUp : v;
 #pragma unroll
@@ -120,9 +128,9 @@ __device__ __forceinline__ void seg_accumulate(double (&acc)[NCH][VEC], double v
 #pragma unroll
         for (int q = 0; q < VEC; ++q) {
             if (MIX && q >= MQ)
-                acc[ch][q] = __fma_rn(vu, widen_scaled(comp(bv[ch], q)), acc[ch][q]);
+                acc[ch][q] = __fma_rn(vu, widen_scaled(comp<WT>(bv[ch], q)), acc[ch][q]);
             else
-                acc[ch][q] = __fma_rn(v, double(comp(bv[ch], q)), acc[ch][q]);
+                acc[ch][q] = __fma_rn(v, double(comp<WT>(bv[ch], q)), acc[ch][q]);
         }
 }
 
@@ -136,11 +144,11 @@ __device__ __forceinline__ void seg_accumulate(double (&acc)[NCH][VEC], double v
 // with an f64 state slot; the accumulators start from scratch[slot] instead
 // of 0.0 and are written back there, so a row's entries can be consumed in
 // ascending column blocks across launches with the reference's order.
-template <int VEC, int LPR, int NCH, bool HAS_VAL, bool PIECES, int U, int MIX, bool SMX, bool BF, bool VP,
+template <int VEC, int LPR, int NCH, bool HAS_VAL, bool PIECES, int U, int MIX, bool SMX, int WT, bool VP,
           bool CARRY = false>
 __device__ __forceinline__ void seg_body(const SegArgs& a) {
-    using VT = typename VecT<VEC, BF>::T;
-    using BT = typename std::conditional<BF, unsigned short, float>::type;
+    using VT = typename VecT<VEC, WT>::T;
+    using BT = typename std::conditional<WT != kWtF32, unsigned short, float>::type;
     constexpr int GPW = 32 / LPR;
     constexpr int W = LPR > U ? LPR : U;
     constexpr int S = W / LPR;
@@ -295,7 +303,7 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
                             bv[u][ch] = ld_keep(reinterpret_cast<const VT*>(bl[ch] + oj[u]), pol_k);
 #pragma unroll
                     for (int u = 0; u < U; ++u)
-                        seg_accumulate<VEC, NCH, MIX, VT, mix_from<VEC, BF>()>(acc, vj[u], bv[u]);
+                        seg_accumulate<VEC, NCH, MIX, VT, mix_from<VEC, WT>(), WT>(acc, vj[u], bv[u]);
                 }
             }
         }
@@ -348,11 +356,11 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
                     if (okj && fok[ch]) {
 #pragma unroll
                         for (int q = 0; q < VEC; ++q) {
-                            const bool rebias = MIX && q >= mix_from<VEC, BF>();
+                            const bool rebias = MIX && q >= mix_from<VEC, WT>();
                             if (rebias)
-                                acc[ch][q] = __fma_rn(vu, widen_scaled(comp(bv[u][ch], q)), acc[ch][q]);
+                                acc[ch][q] = __fma_rn(vu, widen_scaled(comp<WT>(bv[u][ch], q)), acc[ch][q]);
                             else
-                                acc[ch][q] = __fma_rn(v, double(comp(bv[u][ch], q)), acc[ch][q]);
+                                acc[ch][q] = __fma_rn(v, double(comp<WT>(bv[u][ch], q)), acc[ch][q]);
                         }
                     }
                 }
@@ -377,10 +385,10 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
 }
 
 template <int VEC, int LPR, int NCH, bool HAS_VAL, bool PIECES, int U = unroll_for(VEC, NCH),
-          int MAXR = maxreg_for(VEC, NCH), bool SMX = false, bool BF = false, bool VP = false, bool CARRY = false>
+          int MAXR = maxreg_for(VEC, NCH), bool SMX = false, int WT = kWtF32, bool VP = false, bool CARRY = false>
 __global__ void __launch_bounds__(512) __maxnreg__(MAXR) spmm_seg_kernel(SegArgs a) {
-    if (a.finite && *a.finite) seg_body<VEC, LPR, NCH, HAS_VAL, PIECES, U, 1, SMX, BF, VP, CARRY>(a);
-    else seg_body<VEC, LPR, NCH, HAS_VAL, PIECES, U, 0, SMX, BF, VP, CARRY>(a);
+    if (a.finite && *a.finite) seg_body<VEC, LPR, NCH, HAS_VAL, PIECES, U, 1, SMX, WT, VP, CARRY>(a);
+    else seg_body<VEC, LPR, NCH, HAS_VAL, PIECES, U, 0, SMX, WT, VP, CARRY>(a);
 }
 
 // dynamic shared memory of the lane-group kernels: the fast loop's
@@ -394,6 +402,8 @@ inline std::size_t seg_smem(unsigned threads) { return std::size_t(threads / 32)
 // chunks) select the instantiation at run time.
 void launch_seg_bf16(int vec, int lpr, int nch, const SegArgs& a, bool has_val, bool pieces, unsigned nb,
                      unsigned nt, cudaStream_t s);
+void launch_seg_f16(int vec, int lpr, int nch, const SegArgs& a, bool has_val, bool pieces, unsigned nb,
+                    unsigned nt, cudaStream_t s);
 void launch_seg_vp(int vec, int lpr, int nch, const SegArgs& a, bool pieces, unsigned nb, unsigned nt,
                    cudaStream_t s);
 

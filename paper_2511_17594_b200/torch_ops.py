@@ -120,6 +120,13 @@ def _vptr(t):
     return None if t is None else C.c_void_p(t.data_ptr())
 
 
+# 16-bit operand words (csrc/half.cuh): dtype -> (SpMM, SDDMM, word type)
+_HALF = {
+    torch.bfloat16: (_lib.as_spmm_bf16, _lib.as_sddmm_bf16, 1),
+    torch.float16: (_lib.as_spmm_f16, _lib.as_sddmm_f16, 2),
+}
+
+
 def _variant(s: str):
     return None if not s or s == "baseline" else C.byref(variant_from_string(s).to_c())
 
@@ -139,16 +146,16 @@ def _ctx(t: torch.Tensor):
 def spmm_csr(crow: torch.Tensor, col: torch.Tensor, val: torch.Tensor, b: torch.Tensor,
              variant: str) -> torch.Tensor:
     """C = A B (dispatch(variant, A, B), src/kernels.cpp:485-506; "" = baseline).
-    A bfloat16 B is read as bf16 (as_spmm_bf16: half the gather bytes, the
+    A bfloat16 / float16 B is read as 16-bit words (as_spmm_bf16 / as_spmm_f16: half the gather bytes, the
     f32 result on float(B) bit for bit); C is float32 either way."""
     if b.dim() != 2:
         raise ValueError("spmm_csr: b must be 2-D")
     g = _graph(crow, col, b.shape[0])
     vals = _values(val, g.nnz)
     c = torch.empty((g.n_rows, b.shape[1]), dtype=torch.float32, device=b.device)
-    if b.dtype == torch.bfloat16:
+    if b.dtype in _HALF:
         b = b.contiguous()
-        _check(_lib.as_spmm_bf16(_variant(variant), g.handle, _vptr(vals), C.c_void_p(b.data_ptr()), b.shape[0],
+        _check(_HALF[b.dtype][0](_variant(variant), g.handle, _vptr(vals), C.c_void_p(b.data_ptr()), b.shape[0],
                                  b.shape[1], C.c_void_p(c.data_ptr()), _stream(b), None))
         return c
     b = b.contiguous().float()
@@ -198,14 +205,14 @@ def _(crow, col, val, b):
 def sddmm_csr(crow: torch.Tensor, col: torch.Tensor, x: torch.Tensor, y: torch.Tensor,
               variant: str) -> torch.Tensor:
     """out[e] = <x[i], y[col[e]]> on A's pattern (src/kernels.cpp:336-429).
-    bfloat16 x and y are read as bf16 (as_sddmm_bf16; the f32 result on the
+    bfloat16 / float16 x and y are read as 16-bit words (as_sddmm_bf16 / _f16; the f32 result on the
     widened operands, bit for bit); out is float32 either way."""
     _check_dense_pair("sddmm_csr", crow, x, y)
     g = _graph(crow, col, y.shape[0])
     out = torch.empty(col.numel(), dtype=torch.float32, device=x.device)
-    if x.dtype == torch.bfloat16 and y.dtype == torch.bfloat16:
+    if x.dtype in _HALF and y.dtype == x.dtype:
         x, y = x.contiguous(), y.contiguous()
-        _check(_lib.as_sddmm_bf16(_variant(variant), g.handle, C.c_void_p(x.data_ptr()), x.shape[0],
+        _check(_HALF[x.dtype][1](_variant(variant), g.handle, C.c_void_p(x.data_ptr()), x.shape[0],
                                   C.c_void_p(y.data_ptr()), y.shape[0], x.shape[1],
                                   C.c_void_p(out.data_ptr()) if out.numel() else None, _stream(x), None))
         return out
@@ -235,11 +242,11 @@ def _(crow, col, x, y, variant):
 def csr_attention(crow: torch.Tensor, col: torch.Tensor, q: torch.Tensor, k: torch.Tensor,
                   v: torch.Tensor, fused: bool) -> torch.Tensor:
     """csr_attention_forward (src/attention.cpp:9-40), decisions cached.
-    bfloat16 q, k and v take the staged bf16 route (_attention_bf16; `fused`
-    does not apply there)."""
+    bfloat16 / float16 q, k and v take the 16-bit route (_attention_half,
+    fused or staged)."""
     _check_attention(crow, q, k, v)
-    if _all_bf16(q, k, v):
-        return _attention_bf16(crow, col, q, k, v)[0]
+    if _all_half(q, k, v):
+        return _attention_half(crow, col, q, k, v, fused=fused)[0]
     q, k, v = q.contiguous().float(), k.contiguous().float(), v.contiguous().float()
     g = _graph(crow, col, k.shape[0])
     out = torch.empty((g.n_rows, v.shape[1]), dtype=torch.float32, device=q.device)
@@ -266,28 +273,30 @@ def _check_attention(crow, q, k, v):
         raise ValueError("csr_attention: k and v need the same row count")
 
 
-def _all_bf16(*ts) -> bool:
-    return all(t.dtype == torch.bfloat16 for t in ts)
+def _all_half(*ts) -> bool:
+    return ts[0].dtype in _HALF and all(t.dtype == ts[0].dtype for t in ts)
 
 
-def _attention_bf16(crow, col, q, k, v):
-    """Staged attention on bf16 q, k, v: scores =
-    as_sddmm_bf16(q, k), p = as_row_softmax(scores), out = as_spmm_bf16 with
-    values p over bf16 v.  Fixed variants (_BWD_SDDMM: the sequential dot
-    order, src/kernels.cpp:336-355; _BWD_SPMM), so (out, p) equal the f32
+def _attention_half(crow, col, q, k, v, fused=False, keep_p=False):
+    """CSR attention on 16-bit q, k, v (bf16 or f16) through
+    as_csr_attention_half with fixed variants (_BWD_SDDMM: the sequential dot
+    order, src/kernels.cpp:336-355; _BWD_SPMM): (out, p) equal the f32
     pipeline sddmm_csr -> row_softmax_csr -> spmm_csr on q.float(), k.float(),
     v.float() with the same variants, bit for bit, while the Q/K/V gathers
-    read half the bytes.  out and p are float32."""
+    read half the bytes.  fused (and not keep_p): the probabilities are
+    applied inside the SpMM and never stored (p returned empty).  out and p
+    are float32."""
     q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
     _check_attention(crow, q, k, v)
-    n_cols = k.shape[0]
-    s = sddmm_csr(crow, col, q, k, _BWD_SDDMM)
-    p = row_softmax_csr(crow, col, s, n_cols)
-    pat = _graph(crow, col, n_cols)
+    pat = _graph(crow, col, k.shape[0])
     out = torch.empty((pat.n_rows, v.shape[1]), dtype=torch.float32, device=q.device)
-    _check(_lib.as_spmm_bf16(_variant(_BWD_SPMM), pat.handle, C.c_void_p(p.data_ptr()) if p.numel() else None,
-                             C.c_void_p(v.data_ptr()), v.shape[0], v.shape[1], C.c_void_p(out.data_ptr()),
-                             _stream(q), None))
+    p = torch.empty(col.numel() if keep_p or not fused else 0, dtype=torch.float32, device=q.device)
+    sv, pv = variant_from_string(_BWD_SDDMM).to_c(), variant_from_string(_BWD_SPMM).to_c()
+    _check(_lib.as_csr_attention_half(pat.handle, C.byref(sv), C.byref(pv), C.c_void_p(q.data_ptr()), q.shape[0],
+                                      C.c_void_p(k.data_ptr()), k.shape[0], C.c_void_p(v.data_ptr()), v.shape[0],
+                                      q.shape[1], v.shape[1], C.c_void_p(out.data_ptr()),
+                                      C.c_void_p(p.data_ptr()) if p.numel() else None, _HALF[q.dtype][2],
+                                      0 if p.numel() else 1, _stream(q)))
     return out, p
 
 
@@ -461,11 +470,11 @@ def csr_attention_with_probs(crow: torch.Tensor, col: torch.Tensor, q: torch.Ten
                              v: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
     """(out, p): the staged pipeline (as_csr_attention_forward_p), p = the row
     softmax of the scores (nnz floats).  out is bit-identical to csr_attention;
-    its backward reuses p instead of recomputing SDDMM + softmax.  bfloat16
-    q, k and v take the staged bf16 route (_attention_bf16)."""
+    its backward reuses p instead of recomputing SDDMM + softmax.  bfloat16 /
+    float16 q, k and v take the 16-bit route (_attention_half, p kept)."""
     _check_attention(crow, q, k, v)
-    if _all_bf16(q, k, v):
-        return _attention_bf16(crow, col, q, k, v)
+    if _all_half(q, k, v):
+        return _attention_half(crow, col, q, k, v, keep_p=True)
     q, k, v = q.contiguous().float(), k.contiguous().float(), v.contiguous().float()
     g = _graph(crow, col, k.shape[0])
     out = torch.empty((g.n_rows, v.shape[1]), dtype=torch.float32, device=q.device)
