@@ -549,6 +549,15 @@ TileShape tile_shape(std::uint32_t f, std::uint64_t f_tile, bool vec, bool vec8 
     return t;
 }
 
+// AUTOSAGE_DEV_TILE_MAJOR=0: items row-major (the round-1 numbering; A/B knob)
+int tile_major() {
+    static const int v = [] {
+        const char* e = std::getenv("AUTOSAGE_DEV_TILE_MAJOR");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
 // 32-bit gather offsets (col * f) fit; AUTOSAGE_DEV_SPMM_NOFAST=1 disables
 // the predicate-free fast loop (developer A/B knob)
 int fast_gather_ok(const Graph& g, std::uint32_t f) {
@@ -668,6 +677,7 @@ void launch_spmm_rows(Graph& g, const float* val, std::uint64_t offset, std::uin
         a.off32 = fast_gather_ok(g, f);
         a.wt = wt;
         a.keep_b = std::uint64_t(g.n_cols) * f * (wt ? 2 : 4) <= kKeepMaxBytes;
+        a.tile_major = tile_major();
         a.tile_w = t.tile_w;
         wpb = warps_per_cta(wpb);
         if (v8) launch_seg_vec<8>(a, val != nullptr, t.lanes, wpb, s);
@@ -725,6 +735,7 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const void* b, std::uint32
         a.off32 = fast_gather_ok(g, f);
         a.wt = wt;
         a.keep_b = std::uint64_t(g.n_cols) * f * (wt ? 2 : 4) <= kKeepMaxBytes;
+        a.tile_major = tile_major();
         a.tile_w = t.tile_w;
         // pieces are up to 2048-entry dependent chains: when there are too
         // few of them to fill the lane-group kernel (under a wave), the ring

@@ -39,6 +39,7 @@ struct SegArgs {
     int off32;                        // n_cols * f < 2^32: 32-bit element offsets
     int wt;                           // B word type (half.cuh): 0 f32, 1 bf16, 2 f16
     int keep_b;                       // B fits L2 (kKeepMaxBytes): gathers evict_last
+    int tile_major;                   // items numbered tile-major (n_tiles > 1)
     std::uint64_t n_items;
     std::uint64_t n_rows, n_cols, nnz;  // bounds of the checked build (dcheck.cuh)
     std::uint32_t n_tiles;
@@ -164,8 +165,17 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
     if (active) {
         std::uint64_t si = item;
         if (a.n_tiles != 1) {
-            si = item / a.n_tiles;
-            tile = std::uint32_t(item - si * a.n_tiles);
+            if (a.tile_major) {
+                // feature tile outermost: the grid sweeps every row's tile 0
+                // before tile 1, so the B columns in flight (one tile of
+                // every gathered row) stay L2-resident at large F
+                const std::uint64_t n_seg = a.n_items / a.n_tiles;
+                tile = std::uint32_t(item / n_seg);
+                si = item - std::uint64_t(tile) * n_seg;
+            } else {
+                si = item / a.n_tiles;
+                tile = std::uint32_t(item - si * a.n_tiles);
+            }
         }
         if constexpr (PIECES) {
             row = a.piece_row[si];
