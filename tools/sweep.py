@@ -129,7 +129,8 @@ def run_graph(m, f, ops=("spmm", "sddmm"), reps=5, seed=1, with_baseline=True, c
 def case_c1(res):
     m, f = bench.make_graph("c1", 1)
     r, _ = run_graph(m, f, reps=20)
-    cpu = bench.cpu_reference_run(m, f, 1, 3, 1, 1)
+    cpu, _ = bench.cpu_reference_run(m, f, 1, 12, 2, "c1")
+    cpu = {k: v for k, v in cpu.items() if k != "choices"}
     res["c1"] = {"graph": {"n": m.n_rows, "nnz": m.nnz, "F": f}, "gpu": r, "cpu_reference": cpu}
 
 
