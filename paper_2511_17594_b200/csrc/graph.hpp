@@ -95,6 +95,7 @@ struct Graph {
     std::map<std::uint64_t, std::unique_ptr<HubPlan>> hub_plans;
     std::map<std::uint64_t, as_features> features;
     DevBuf<double> scratch;            // hub partials
+    DevBuf<double> sddmm_state;        // pass-major SDDMM: per-entry f64 chains
     DevBuf<float> att_buf;             // attention: scores | probabilities (staged)
     DevBuf<float> att_max;             // fused attention: per-row score max ...
     DevBuf<double> att_sum;            // ... and softmax denominator

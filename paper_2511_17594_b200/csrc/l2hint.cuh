@@ -116,6 +116,28 @@ __device__ __forceinline__ void st_stream(float* p, float v, std::uint64_t pol) 
 #endif
 }
 
+// f64 carried state of a multi-launch reduction (written by the previous
+// launch, so the coherent path)
+__device__ __forceinline__ double ld_state(const double* p, std::uint64_t pol) {
+#if ASB_L2_HINTS
+    double v;
+    asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+#else
+    (void)pol;
+    return *p;
+#endif
+}
+
+__device__ __forceinline__ void st_state(double* p, double v, std::uint64_t pol) {
+#if ASB_L2_HINTS
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+#else
+    (void)pol;
+    *p = v;
+#endif
+}
+
 // 16-byte cp.async of a reused row with an L2 policy
 __device__ __forceinline__ void cp_async16_pol(void* smem, const void* gmem, std::uint64_t pol) {
     const unsigned s = unsigned(__cvta_generic_to_shared(smem));

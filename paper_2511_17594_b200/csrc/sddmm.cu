@@ -777,14 +777,31 @@ __device__ __forceinline__ void pair1_pass(const double* __restrict__ xa, const 
     }
 }
 
-template <int F, int ORD, int FT, int MIX, int WT = kWtF32>
+// Pass-major form (PM; F = 64 features of a wider row): features
+// [f0, f0 + 64) of rows of width ld, each entry's f64 chain continued from
+// state[e] (f0 > 0) and left in state[e] (not last) or rounded to out[e]
+// (last).  One launch per 64-feature pass keeps the pass's 64-column Y slice
+// L2-resident where the whole Y (n_cols x ld) is not; the chains and the
+// ORD 1 blocks (ft 32 / 64: every block ends inside a pass) fold exactly as
+// in the single-launch kernels, so the result is unchanged bit for bit.
+struct PassArgs {
+    std::uint32_t ld = 0, f0 = 0;
+    double* state = nullptr;
+    int last = 1;
+};
+
+template <int F, int ORD, int FT, int MIX, int WT = kWtF32, bool PM = false>
 __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict__ rowptr,
                                                 const std::uint32_t* __restrict__ colind,
                                                 const std::uint32_t* __restrict__ chunk_row, std::uint64_t n_rows,
                                                 const double* __restrict__ xd, const void* __restrict__ yv,
                                                 float* __restrict__ out, std::uint64_t nnz, std::uint64_t c_begin,
-                                                std::uint64_t c_end, int keep, std::uint64_t n_cols) {
+                                                std::uint64_t c_end, int keep, std::uint64_t n_cols,
+                                                PassArgs pa = PassArgs{}) {
     (void)n_cols;  // bounds of the checked build
+    // row stride of X and Y, and the pass's first feature
+    const std::uint64_t LD = PM ? pa.ld : F;
+    const std::uint32_t F0 = PM ? pa.f0 : 0u;
     using Sh = Pair1Shape<F, WT != kWtF32>;
     using YT = typename std::conditional<WT != kWtF32, unsigned short, float>::type;
     constexpr int kUnitElems = 16 / Sh::kYElem;  // Y elements per 16-byte unit
@@ -799,7 +816,12 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
     const std::uint64_t stride = std::uint64_t(gridDim.x) * (blockDim.x >> 5);
     // colind and the outputs stream once (evict_first); Y rows and the
     // widened X are re-read for every entry that hits them (evict_last)
-    const std::uint64_t pol_s = l2_evict_first(), pol_k = l2_reuse_policy(keep != 0);
+    // keep bit 0: Y fits the L2 budget; bits 2:1 the widened X's policy
+    // (0 as Y, 1 evict_normal, 2 evict_first: X rows are read by the
+    // neighbouring chunk pairs only, so they need not outlive them)
+    const std::uint64_t pol_s = l2_evict_first(), pol_k = l2_reuse_policy((keep & 1) != 0);
+    const int xp = (keep >> 1) & 3;
+    const std::uint64_t pol_x = xp == 0 ? pol_k : xp == 1 ? l2_evict_normal() : pol_s;
 
     struct Meta {
         std::uint32_t ca, cb, r_first;
@@ -826,14 +848,14 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
             const int j = idx / Sh::NV, q = idx % Sh::NV;
             const std::uint32_t cj = __shfl_sync(FULL, j < 32 ? cur.ca : cur.cb, j & 31);
             ASB_DCHECK(cj < n_cols);
-            cp_async16_pol(ys + j * F + kUnitElems * (q ^ swz<Sh::NV>(j)), y + std::uint64_t(cj) * F + kUnitElems * q,
+            cp_async16_pol(ys + j * F + kUnitElems * (q ^ swz<Sh::NV>(j)), y + std::uint64_t(cj) * LD + F0 + kUnitElems * q,
                            pol_k);
         }
 #pragma unroll
         for (int u = lane; u < Sh::kXUnits; u += 32) {
             const int k = u / (F / 2), uu = u % (F / 2);
             const std::uint64_t xr = std::uint64_t(cur.r_first) + k;
-            if (xr < n_rows) cp_async16_pol(xs + 2 * u, xd + xr * F + 2 * uu, pol_k);
+            if (xr < n_rows) cp_async16_pol(xs + 2 * u, xd + xr * LD + F0 + 2 * uu, pol_x);
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
         const Meta nxt = meta(pc + stride);
@@ -865,6 +887,12 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
         ASB_DCHECK(ea >= e_end || (rowptr[ra] <= ea && ea < rowptr[ra + 1]));
         ASB_DCHECK(eb >= e_end || (rowptr[rb] <= eb && eb < rowptr[rb + 1]));
         double c[2][5] = {{0.0, 0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0, 0.0}};
+        if constexpr (PM) {
+            if (F0 > 0) {
+                if (ea < e_end) c[0][0] = ld_state(pa.state + ea, pol_s);
+                if (eb < e_end) c[1][0] = ld_state(pa.state + eb, pol_s);
+            }
+        }
         const YT* ya = ys + lane * F;
         const YT* yb = ys + (lane + 32) * F;
         const int ka = swz<Sh::NV>(lane), kb = swz<Sh::NV>(lane + 32);
@@ -875,11 +903,16 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
             else
                 pair1_pass<F, ORD, FT, true, MIX, false, WT>(xs + rela * F, xs + relb * F, ya, yb, ka, kb, c);
         } else {
-            pair1_pass<F, ORD, FT, false, MIX, false, WT>(xd + std::uint64_t(ra) * F, xd + std::uint64_t(rb) * F,
-                                                         ya, yb, ka, kb, c);
+            pair1_pass<F, ORD, FT, false, MIX, false, WT>(xd + std::uint64_t(ra) * LD + F0,
+                                                         xd + std::uint64_t(rb) * LD + F0, ya, yb, ka, kb, c);
         }
-        if (ea < e_end) st_stream(out + ea, float(c[0][0]), pol_s);
-        if (eb < e_end) st_stream(out + eb, float(c[1][0]), pol_s);
+        if (PM && !pa.last) {
+            if (ea < e_end) st_state(pa.state + ea, c[0][0], pol_s);
+            if (eb < e_end) st_state(pa.state + eb, c[1][0], pol_s);
+        } else {
+            if (ea < e_end) st_stream(out + ea, float(c[0][0]), pol_s);
+            if (eb < e_end) st_stream(out + eb, float(c[1][0]), pol_s);
+        }
         __syncwarp();
         cur = nxt;
     }
@@ -903,6 +936,22 @@ __global__ void __launch_bounds__(128, MINB)
     else
         sddmm_pair1_body<F, ORD, FT, 0, WT>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin, c_end,
                                             keep, n_cols);
+}
+
+// One 64-feature pass of an F >= 128 SDDMM (PassArgs above)
+template <int ORD, int FT>
+__global__ void __launch_bounds__(128, 3)
+    sddmm_pair1_pm_kernel(const std::uint64_t* __restrict__ rowptr, const std::uint32_t* __restrict__ colind,
+                          const std::uint32_t* __restrict__ chunk_row, std::uint64_t n_rows,
+                          const double* __restrict__ xd, const void* __restrict__ y, float* __restrict__ out,
+                          std::uint64_t nnz, std::uint64_t c_begin, std::uint64_t c_end,
+                          const unsigned* __restrict__ finite, int keep, std::uint64_t n_cols, PassArgs pa) {
+    if (finite && *finite)
+        sddmm_pair1_body<64, ORD, FT, 1, kWtF32, true>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin,
+                                                       c_end, keep, n_cols, pa);
+    else
+        sddmm_pair1_body<64, ORD, FT, 0, kWtF32, true>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin,
+                                                       c_end, keep, n_cols, pa);
 }
 
 // Guardrail baseline / large-F fallback: lane per entry, both rows read
@@ -945,6 +994,29 @@ bool fixed_eligible(const float* x, const float* y, std::uint32_t f, std::uint32
     return int(ft) % fw == 0 || fw % int(ft) == 0;
 }
 
+// L2 policy of the pair kernels' widened-X staging (keep bits 2:1; see
+// sddmm_pair1_body).  AUTOSAGE_DEV_SDDMM_XPOL: 0 as Y (default), 1 normal,
+// 2 first.  A/B on Reddit-shape F = 64 / 128 / 256: within 0.5% for 0 and 1,
+// 2 is 1-2% slower (profiles/r02m_pass_major.md).
+int x_policy_bits() { return (dev_knob("AUTOSAGE_DEV_SDDMM_XPOL", 0) & 3) << 1; }
+
+// Pass-major SDDMM (sddmm_pair1_pm_kernel) for F = 128, 192, ...: every
+// f_tile block must end inside a 64-feature pass (ord 0, or ft 32 / 64).
+// Auto: when Y is more than twice the L2 budget the streams leave it
+// (kKeepMaxBytes) but one pass's 64-column slice fits; the carried chains
+// cost 16 B of DRAM traffic per entry per pass boundary, plus one more read
+// of colind per pass.  Reddit-shape, sequential order (profiles/
+// r02m_pass_major.md): F=256 13.4 -> 11.6 ms; F=128 5.24 -> 5.70 ms and
+// F=192 8.77 -> 9.32 ms (slower: the single launch is kept there).
+// AUTOSAGE_DEV_SDDMM_PM: -1 auto (default), 0 never, 1 whenever eligible.
+bool pass_major(const Graph& g, std::uint32_t f, std::uint32_t ft, int ord) {
+    if (f < 128 || f % 64 != 0) return false;
+    if (!(ord == 0 || ft == 32 || ft == 64)) return false;
+    const int knob = dev_knob("AUTOSAGE_DEV_SDDMM_PM", -1);
+    if (knob >= 0) return knob != 0;
+    return std::uint64_t(g.n_cols) * f * 4 > 2 * kKeepMaxBytes && std::uint64_t(g.n_cols) * 64 * 4 <= kKeepMaxBytes;
+}
+
 // all four components re-biased on the ALU pipe (dev knob; default: half)
 int mix_all() { return dev_knob("AUTOSAGE_DEV_SDDMM_MIXALL", 0); }
 
@@ -970,7 +1042,7 @@ void launch_sddmm_fixed(Graph& g, const float* y, std::uint32_t f, float* out, s
                         cudaStream_t s, const unsigned* finite, std::uint64_t c_begin, std::uint64_t c_end) {
     // Y (re-read by every entry of its column) fits the L2 beside the
     // streams: the staging reads evict_last
-    const int keep_y = int(std::uint64_t(g.n_cols) * f * 4 <= kKeepMaxBytes);
+    const int keep_y = int(std::uint64_t(g.n_cols) * f * 4 <= kKeepMaxBytes) | x_policy_bits();
     const int sms = sm_count();
     auto go = [&](auto kernel, std::uint64_t warp_bytes) {
         constexpr int kWarps = 8;
@@ -1054,6 +1126,35 @@ void launch_sddmm_fixed(Graph& g, const float* y, std::uint32_t f, float* out, s
             };
             if (f == 32) pair1(std::integral_constant<int, 32>{});
             else pair1(std::integral_constant<int, 64>{});
+        } else if (pass_major(g, f, ft, ord)) {
+            // one launch per 64-feature pass (PassArgs): the slice of Y a
+            // pass gathers fits the L2 where the whole Y does not
+            const int npass = int(f / 64);
+            g.sddmm_state.ensure(std::max<std::uint64_t>(g.nnz, 1));
+            const int keep_slice = int(std::uint64_t(g.n_cols) * 64 * 4 <= kKeepMaxBytes) | x_policy_bits();
+            const int kWarps = 4;
+            const std::size_t smem = std::size_t(Pair1Shape<64>::kWarpBytes * kWarps);
+            auto run = [&](auto kernel) {
+                const int per_sm = kernel_setup(kernel, smem, int(kWarps * 32));
+                const std::uint64_t pairs = (c_end - c_begin + 1) / 2;
+                const std::uint64_t want = (pairs + kWarps - 1) / kWarps;
+                const std::uint64_t cap = std::uint64_t(sms) * std::max(per_sm, 1);
+                const unsigned blocks = unsigned(std::max<std::uint64_t>(1, std::min(want, cap)));
+                for (int p = 0; p < npass; ++p) {
+                    PassArgs pa;
+                    pa.ld = f;
+                    pa.f0 = std::uint32_t(p * 64);
+                    pa.state = g.sddmm_state.get();
+                    pa.last = p == npass - 1;
+                    kernel<<<blocks, kWarps * 32, smem, s>>>(g.rowptr.get(), g.colind.get(), g.chunk_row.get(),
+                                                             g.n_rows, g.xwide.get(), y, out, g.nnz, c_begin, c_end,
+                                                             finite, keep_slice, g.n_cols, pa);
+                    check_launch("sddmm_pair1_pm_kernel");
+                }
+            };
+            if (ord == 0) run(sddmm_pair1_pm_kernel<0, 0>);
+            else if (ft == 32) run(sddmm_pair1_pm_kernel<1, 32>);
+            else run(sddmm_pair1_pm_kernel<1, 0>);  // ft 64: one block per pass
         } else {
             pair(std::integral_constant<int, 64>{}, std::integral_constant<int, 0>{});
         }
@@ -1220,7 +1321,9 @@ void launch_sddmm_half_t(Graph& g, const std::uint16_t* x, const std::uint16_t* 
             const unsigned blocks = unsigned(std::max<std::uint64_t>(1, std::min(want, cap)));
             kernel<<<blocks, kWarps * 32, smem, s>>>(g.rowptr.get(), g.colind.get(), g.chunk_row.get(), g.n_rows,
                                                      g.xwide.get(), y, out, g.nnz, f, 0, c_end, fin,
-                                                     int(std::uint64_t(g.n_cols) * f * 2 <= kKeepMaxBytes), g.n_cols);
+                                                     int(std::uint64_t(g.n_cols) * f * 2 <= kKeepMaxBytes) |
+                                                         x_policy_bits(),
+                                                     g.n_cols);
             check_launch("sddmm_pair_kernel");
         };
         // 4 resident CTAs (<= 128 registers): Reddit-shape F=32 1.32 -> 1.16 ms,

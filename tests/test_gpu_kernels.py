@@ -216,6 +216,37 @@ def test_sddmm_special_values_bit_exact(f):
             assert bit_equal(np.nan_to_num(got), np.nan_to_num(want)), (vec, ft)
 
 
+@pytest.mark.parametrize("force", ["1", "0"])
+def test_sddmm_pass_major_bit_exact(monkeypatch, force):
+    """F >= 128 in one launch per 64-feature pass, each entry's f64 chain
+    carried between launches (sddmm_pair1_pm_kernel; forced on small graphs,
+    auto only when Y overflows the L2): sequential order and the ft 32 / 64
+    four-way blocks, special values, chunks spanning many rows -- bit-equal
+    to the oracle and to the single-launch kernel."""
+    monkeypatch.setenv("AUTOSAGE_DEV_SDDMM_PM", force)
+    rng = np.random.default_rng(47)
+    n = 1500
+    deg = rng.choice([0, 1, 2, 9], size=n).astype(np.int64)
+    deg[:3] = [1400, 700, 65]
+    rp = np.zeros(n + 1, np.uint64)
+    rp[1:] = np.cumsum(deg)
+    cols = np.concatenate([np.sort(rng.choice(n, size=d, replace=False)) for d in deg]).astype(np.uint32)
+    p = asb.CsrMatrix(n, n, rp, cols, None)
+    g = asb.Graph.from_csr(p)
+    for f in (128, 192, 256):
+        x, y = random_dense(rng, n, f), random_dense(rng, n, f)
+        y[1::5, 2::4] = np.float32(1e-41)
+        x[::11, 2::4] = np.float32(2.5e38)
+        y2 = y.copy()
+        y2[5, 70] = np.nan
+        for yy in (y, y2):
+            for vec, ft in ((False, 64), (True, 32), (True, 64)):
+                got = asb.dispatch(V(SD, RP, ft, 4, vec), g, cuda(x), cuda(yy)).values.cpu().numpy()
+                want = oracle.sddmm(p, x, yy, ft, vec)
+                assert np.array_equal(np.isnan(got), np.isnan(want))
+                assert bit_equal(np.nan_to_num(got), np.nan_to_num(want)), (f, vec, ft)
+
+
 def test_sddmm_chunks_spanning_many_rows():
     """Degree-0/1/2 rows: one 32-entry chunk meets more than 32 rows."""
     rng = np.random.default_rng(44)
@@ -494,11 +525,12 @@ def test_sddmm_host_slices_bit_exact(monkeypatch, slices):
     """The SDDMM values leave in slices of 32-entry chunks; every slicing
     returns the same bytes (odd nnz, fixed-width and generic widths)."""
     monkeypatch.setenv("AUTOSAGE_HOST_SLICES", slices)
+    monkeypatch.setenv("AUTOSAGE_DEV_SDDMM_PM", "1")  # F=128: pass-major per slice
     rng = np.random.default_rng(51)
     p = hub_graph(rng, 900, [850, 333, 70], 7, with_values=False)
     assert p.nnz % 32 != 0
     g = asb.Graph.from_csr(p)
-    for f in (64, 24):
+    for f in (64, 24, 128):
         x, y = random_dense(rng, 900, f), random_dense(rng, 900, f)
         for v in (None, V(SD, RP, 64, 4, True), V(SD, HS, 32, 1, False)):
             got = asb.sddmm_baseline(g, x, y) if v is None else asb.dispatch(v, g, x, y).values
