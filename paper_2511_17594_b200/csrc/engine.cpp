@@ -279,16 +279,26 @@ void check_sddmm_dims(const Graph& p, std::uint64_t x_rows, std::uint64_t y_rows
 // A probe sample scans its operand once (decide_*'s prepare hook) and
 // freezes the flag, so candidate timings do not include a scan the
 // baseline's do not.
-const unsigned* mix_flag(Graph& g, const float* p, std::uint64_t n, cudaStream_t s) {
-    constexpr std::uint64_t kMaxBytes = std::uint64_t(96) << 20;
-    if (n * 4 > kMaxBytes) return nullptr;
+// Finite scan of the dense operand (gates the ALU re-bias widening).
+// Operands above the cap skip it and widen every component on the XU pipe.
+// SpMM: 96 MiB -- past the L2 the gathers bound the kernel and the scan is
+// pure cost (Reddit F=256 8.38 -> 8.72 ms, Products F=100 8.98 -> 9.54 ms
+// with it).  SDDMM: no cap -- its dot is XU-bound at any size (F=128 5.77 ->
+// 5.25 ms, F=256 11.72 -> 10.58 ms, Products 11.98 -> 11.85 ms with it,
+// scan included; profiles/r02o_mix_scan.md).  AUTOSAGE_DEV_MIX_SCAN_MB
+// (MiB) overrides both caps (A/B knob).
+const unsigned* mix_flag(Graph& g, const float* p, std::uint64_t n, cudaStream_t s, bool sddmm = false) {
+    const auto knob = env::get_int("AUTOSAGE_DEV_MIX_SCAN_MB");
+    const std::uint64_t dflt = sddmm ? ~0ull : std::uint64_t(96) << 20;
+    const std::uint64_t max_bytes = knob && *knob >= 0 ? std::uint64_t(*knob) << 20 : dflt;
+    if (n * 4 > max_bytes) return nullptr;
     if (g.flag_frozen) return g.flag.get();
     return finite_flag(g, p, n, s);
 }
 
-void freeze_mix_flag(Graph& g, const float* p, std::uint64_t n, cudaStream_t s) {
+void freeze_mix_flag(Graph& g, const float* p, std::uint64_t n, cudaStream_t s, bool sddmm = false) {
     g.flag_frozen = false;
-    mix_flag(g, p, n, s);
+    mix_flag(g, p, n, s, sddmm);
     g.flag_frozen = true;
 }
 
@@ -461,7 +471,7 @@ void sddmm_mapped(const as_variant& v, Graph& p, const float* x, std::uint64_t x
     const void* bases[2] = {x, y};
     const bool vec = v.vectorized && vec4_eligible(f, bases, 2);
     DeviceGuard dg(p.device);
-    const unsigned* fin = mix_flag(p, y, y_rows * f, s);
+    const unsigned* fin = mix_flag(p, y, y_rows * f, s, true);
     launch_sddmm_chunks(p, x, y, std::uint32_t(f), out, v.f_tile, vec,
                         std::uint32_t(std::min<std::uint64_t>(v.rows_per_chunk, 16)), s, fin);
 }
@@ -483,7 +493,7 @@ KernelResult dispatch_sddmm(const as_variant& v, Graph& p, const float* x, std::
     if (r.variant.mapping == AS_MAP_BASELINE) {
         launch_sddmm_baseline(p, x, y, std::uint32_t(f), out, s);
     } else {
-        const unsigned* fin = mix_flag(p, y, y_rows * f, s);
+        const unsigned* fin = mix_flag(p, y, y_rows * f, s, true);
         launch_sddmm_chunks(p, x, y, std::uint32_t(f), out, r.variant.f_tile, vec,
                             std::uint32_t(std::min<std::uint64_t>(r.variant.rows_per_chunk, 16)), s,
                             fin);
@@ -601,7 +611,7 @@ KernelResult sddmm_host(const as_variant* v, Graph& g, const float* x_host, std:
     ensure_slices(g, std::size_t(k));
     const unsigned* fin = nullptr;
     const std::uint32_t wpb = std::uint32_t(std::min<std::uint64_t>(r.variant.rows_per_chunk, 16));
-    if (r.variant.mapping != AS_MAP_BASELINE) fin = mix_flag(g, y, y_rows * f, g.stream);
+    if (r.variant.mapping != AS_MAP_BASELINE) fin = mix_flag(g, y, y_rows * f, g.stream, true);
     std::uint64_t x_done = 0;  // X rows [0, x_done) queued
     for (std::uint64_t i = 0; i < k && n_chunks; ++i) {
         const std::uint64_t c0 = i * per, c1 = std::min(n_chunks, c0 + per);
@@ -721,7 +731,7 @@ as_decision decide_sddmm(const Context& ctx, const as_probe_config& cfg, Graph& 
         xs.alloc(std::max<std::uint64_t>(ns * f, 1));
         gather_dense_rows(x, f, rows, xs.get(), s);
         obuf.alloc(std::max<std::uint64_t>(sample->nnz, 1));
-        freeze_mix_flag(*sample, y, y_rows * f, s);
+        freeze_mix_flag(*sample, y, y_rows * f, s, true);
         return ns;
     };
     h.run_baseline = [&] { launch_sddmm_baseline(*sample, xs.get(), y, std::uint32_t(f), obuf.get(), s); };

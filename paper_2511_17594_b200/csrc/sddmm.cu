@@ -340,9 +340,13 @@ struct FixedShape {
 // 8 distinct 16-B bank groups (NV >= 8: j & 7 permutes the chunk index
 // within 128 B; NV == 4: rows are 64 B, so alternate lanes already sit in
 // opposite halves of a 128-B segment and (j >> 1) & 3 separates the rest).
+// An odd unit count per row (F = 100: 25 units) needs no swizzle: row j then
+// starts at 16-byte bank group 25j mod 8, distinct for any 8 consecutive rows.
 template <int NV>
 __device__ __forceinline__ int swz(int j) {
-    if constexpr (NV >= 8) return j & 7;
+    static_assert(NV % 2 == 1 || NV % 8 == 0 || NV == 4, "XOR swizzle must stay inside the row");
+    if constexpr (NV % 2 == 1) return 0;
+    else if constexpr (NV >= 8) return j & 7;
     else return (j >> 1) & 3;
 }
 
@@ -984,8 +988,15 @@ int fixed_fw(std::uint32_t f) {
     return 0;
 }
 
+// F = 100 (the Products-shape width): the pair kernel with an odd 25-unit
+// row pitch; its f_tile blocks (32, 64 or all of F) end inside the row
+constexpr std::uint32_t kPairOddF = 100;
+
 bool fixed_eligible(const float* x, const float* y, std::uint32_t f, std::uint32_t ft, int ord) {
     if (!dev_knob("AUTOSAGE_DEV_SDDMM_FIXED", 1)) return false;
+    if (f == kPairOddF)
+        return dev_knob("AUTOSAGE_DEV_SDDMM_PAIR", 1) && aligned16(x) && aligned16(y) &&
+               (ord == 0 || ft >= f || ft == 32 || ft == 64);
     const int fw = fixed_fw(f);
     if (!fw || f > 4096) return false;
     if (!aligned16(x) || !aligned16(y)) return false;
@@ -1066,7 +1077,8 @@ void launch_sddmm_fixed(Graph& g, const float* y, std::uint32_t f, float* out, s
         else if (ft == 64) go(sddmm_fixed_kernel<FW, 1, 64, NP>, wb);
         else go(sddmm_fixed_kernel<FW, 1, 128, NP>, wb);
     };
-    const bool pair_ok = (f == 32 || f % 64 == 0) && (ord == 0 || ft >= f || ft == 32 || ft % 64 == 0);
+    const bool pair_ok = (f == 32 || f % 64 == 0 || f == kPairOddF) &&
+                         (ord == 0 || ft >= f || ft == 32 || ft % 64 == 0);
     if (pair_ok && dev_knob("AUTOSAGE_DEV_SDDMM_PAIR", 1)) {
         auto pair = [&](auto fc, auto npc) {
             constexpr int FW = decltype(fc)::value, NP = decltype(npc)::value;
@@ -1126,6 +1138,27 @@ void launch_sddmm_fixed(Graph& g, const float* y, std::uint32_t f, float* out, s
             };
             if (f == 32) pair1(std::integral_constant<int, 32>{});
             else pair1(std::integral_constant<int, 64>{});
+        } else if (f == kPairOddF) {
+            // 27.2 KB per warp: 2 CTAs of 4 warps per SM
+            constexpr int F = int(kPairOddF);
+            const std::uint64_t wb = Pair1Shape<F>::kWarpBytes;
+            const int kWarps = 4;
+            auto run = [&](auto kernel) {
+                const std::size_t smem = std::size_t(wb * kWarps);
+                const int per_sm = kernel_setup(kernel, smem, int(kWarps * 32));
+                const std::uint64_t pairs = (c_end - c_begin + 1) / 2;
+                const std::uint64_t want = (pairs + kWarps - 1) / kWarps;
+                const std::uint64_t cap = std::uint64_t(sms) * std::max(per_sm, 1);
+                const unsigned blocks = unsigned(std::max<std::uint64_t>(1, std::min(want, cap)));
+                kernel<<<blocks, kWarps * 32, smem, s>>>(g.rowptr.get(), g.colind.get(), g.chunk_row.get(),
+                                                         g.n_rows, g.xwide.get(), y, out, g.nnz, f, c_begin, c_end,
+                                                         finite, keep_y, g.n_cols);
+                check_launch("sddmm_pair_kernel");
+            };
+            if (ord == 0) run(sddmm_pair1_kernel<F, 0, 0, kWtF32, 2>);
+            else if (ft >= f) run(sddmm_pair1_kernel<F, 1, 0, kWtF32, 2>);
+            else if (ft == 32) run(sddmm_pair1_kernel<F, 1, 32, kWtF32, 2>);
+            else run(sddmm_pair1_kernel<F, 1, 64, kWtF32, 2>);
         } else if (pass_major(g, f, ft, ord)) {
             // one launch per 64-feature pass (PassArgs): the slice of Y a
             // pass gathers fits the L2 where the whole Y does not
