@@ -1016,9 +1016,9 @@ int x_policy_bits() { return (dev_knob("AUTOSAGE_DEV_SDDMM_XPOL", 0) & 3) << 1; 
 // Auto: when Y is more than twice the L2 budget the streams leave it
 // (kKeepMaxBytes) but one pass's 64-column slice fits; the carried chains
 // cost 16 B of DRAM traffic per entry per pass boundary, plus one more read
-// of colind per pass.  Reddit-shape, sequential order (profiles/
-// r02m_pass_major.md): F=256 13.4 -> 11.6 ms; F=128 5.24 -> 5.70 ms and
-// F=192 8.77 -> 9.32 ms (slower: the single launch is kept there).
+// of colind per pass.  Reddit-shape, sequential order, with the finite
+// scan (profiles/r02m_pass_major.md, r02p): F=256 11.62 -> 11.25 ms; F=128
+// 4.76 -> 5.41 ms and F=192 7.85 -> 8.86 ms (slower: single launch there).
 // AUTOSAGE_DEV_SDDMM_PM: -1 auto (default), 0 never, 1 whenever eligible.
 bool pass_major(const Graph& g, std::uint32_t f, std::uint32_t ft, int ord) {
     if (f < 128 || f % 64 != 0) return false;
