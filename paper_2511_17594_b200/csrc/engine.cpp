@@ -281,15 +281,15 @@ void check_sddmm_dims(const Graph& p, std::uint64_t x_rows, std::uint64_t y_rows
 // baseline's do not.
 // Finite scan of the dense operand (gates the ALU re-bias widening).
 // Operands above the cap skip it and widen every component on the XU pipe.
-// SpMM: 96 MiB -- past the L2 the gathers bound the kernel and the scan is
-// pure cost (Reddit F=256 8.38 -> 8.72 ms, Products F=100 8.98 -> 9.54 ms
-// with it).  SDDMM: no cap -- its dot is XU-bound at any size (F=128 5.77 ->
+// SpMM: 128 MiB -- Reddit F=128 (B 119 MB) 4.16 -> 4.04 ms with it, but
+// further past the L2 the gathers bound the kernel and the scan is pure
+// cost (Reddit F=256 8.38 -> 8.72 ms, Products F=100 8.98 -> 9.54 ms).  SDDMM: no cap -- its dot is XU-bound at any size (F=128 5.77 ->
 // 5.25 ms, F=256 11.72 -> 10.58 ms, Products 11.98 -> 11.85 ms with it,
 // scan included; profiles/r02o_mix_scan.md).  AUTOSAGE_DEV_MIX_SCAN_MB
 // (MiB) overrides both caps (A/B knob).
 const unsigned* mix_flag(Graph& g, const float* p, std::uint64_t n, cudaStream_t s, bool sddmm = false) {
     const auto knob = env::get_int("AUTOSAGE_DEV_MIX_SCAN_MB");
-    const std::uint64_t dflt = sddmm ? ~0ull : std::uint64_t(96) << 20;
+    const std::uint64_t dflt = sddmm ? ~0ull : std::uint64_t(128) << 20;
     const std::uint64_t max_bytes = knob && *knob >= 0 ? std::uint64_t(*knob) << 20 : dflt;
     if (n * 4 > max_bytes) return nullptr;
     if (g.flag_frozen) return g.flag.get();

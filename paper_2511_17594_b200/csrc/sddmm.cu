@@ -1329,8 +1329,8 @@ void launch_sddmm_half_t(Graph& g, const std::uint16_t* x, const std::uint16_t* 
         return;
     }
     const unsigned* fin = nullptr;
-    if (dev_knob("AUTOSAGE_DEV_SDDMM_MIX", 1) && g.n_cols * f * 2 <= (std::uint64_t(96) << 20))
-        fin = finite_flag_half(g, y, g.n_cols * f, s, WT);
+    // scanned at any size, as the f32 SDDMM's Y (engine.cpp mix_flag)
+    if (dev_knob("AUTOSAGE_DEV_SDDMM_MIX", 1)) fin = finite_flag_half(g, y, g.n_cols * f, s, WT);
     g.xwide.ensure(std::max<std::uint64_t>(g.n_rows * f, 1));
     const std::uint64_t n4 = g.n_rows * f / 4;
     if (n4) {
