@@ -50,6 +50,9 @@ struct SegArgs {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
+#ifndef ASB_SEG_E64_MAXLPR
+#define ASB_SEG_E64_MAXLPR 16  // widest lane group that takes the 8-byte entry (A/B build knob)
+#endif
 constexpr int kSegMaxS = 8;  // max entries per lane per fast-loop block (seg_smem)
 
 // Load type of VEC consecutive B elements: f32 (float / float4) or, for the
@@ -267,7 +270,7 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
             // and every lane widens the value itself: F=64 rowparallel 2.59 ->
             // 2.29 ms, F=32 1.07 -> 0.97; one group per warp (F >= 128) keeps
             // the 16-byte pre-widened entry (F=128: 4.19 vs 4.37 ms).
-            constexpr bool E64 = LPR <= 16;
+            constexpr bool E64 = LPR <= ASB_SEG_E64_MAXLPR;
             using Ent = typename std::conditional<E64, uint2, double2>::type;
             extern __shared__ __align__(16) double2 seg_ent[];
             static_assert(S <= kSegMaxS, "seg_smem too small");
