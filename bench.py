@@ -377,9 +377,18 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    # AUTOSAGE_BENCH_DIST1=1: the multi-rank code path (NCCL, sharded layout,
+    # shared decisions, exchange) at world size 1 -- the check this 1-GPU
+    # environment can run of what the N-GPU launch executes
+    use_dist = world > 1 or os.environ.get("AUTOSAGE_BENCH_DIST1") == "1"
     dist = None
-    if world > 1:
+    if use_dist:
         import torch.distributed as dist
+        # NCCL's communicator lines on stderr show the rank count (also when
+        # the driver launches torchrun itself)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # stdout carries only the JSON line
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
@@ -395,13 +404,13 @@ def run_ours(args):
     r0, r1 = sh.r0, sh.r1
     # N>1: this rank's rows, columns remapped into the padded all-gather layout
     # (dist.py), so the kernels gather straight from the NCCL buffer
-    g = asb.Graph.from_csr(m if world == 1 else sh.shard_graph_host(m), device=local)
+    g = asb.Graph.from_csr(sh.shard_graph_host(m) if use_dist else m, device=local)
     b_host, x_host, y_host = dense_inputs(asb.fill_uniform, m, f, args.seed)
     # square graph: rank r owns the B/Y rows of its own node range
     b_full = torch.from_numpy(b_host).to(dev)
     y_full = torch.from_numpy(y_host).to(dev)
     x_loc = torch.from_numpy(x_host[r0:r1]).to(dev)
-    if world > 1:
+    if use_dist:
         # own rows as the all-gather input in place (padded to the largest shard)
         b_loc = torch.zeros((sh.shard, f), dtype=torch.float32, device=dev)
         y_loc = torch.zeros((sh.shard, f), dtype=torch.float32, device=dev)
@@ -439,13 +448,13 @@ def run_ours(args):
     def gather_b():
         """B for the SpMM; starts Y's all-gather on NCCL's stream so it runs
         under the SpMM (returned handle: wait before the SDDMM)."""
-        if world == 1:
+        if not use_dist:
             return b_full, None
         sh.allgather_padded(b_loc, pad_b)
         return pad_b, sh.allgather_padded(y_loc, pad_y, async_op=True)
 
     def y_operand(hy):
-        if world == 1:
+        if not use_dist:
             return y_full
         hy.wait()
         return pad_y
@@ -469,6 +478,29 @@ def run_ours(args):
     dec_sddmm = asb.ScheduleDecision.from_c(d_sddmm)
     if args.cache and rank == 0 and not args.replay_only:
         cache.store(args.cache)
+    if dist:
+        # one variant per op for the whole job: rank 0's
+        # decision on its shard, dispatched by every rank, so the row-sharded
+        # outputs concatenate to one reference dispatch's result
+        shared = [dec_spmm.choice_string(), dec_sddmm.choice_string(), decision_report(dec_spmm),
+                  decision_report(dec_sddmm), dec_spmm.source_name, dec_sddmm.source_name]
+        dist.broadcast_object_list(shared, src=0)
+        v_sp = None if shared[0] == "baseline" else asb.variant_from_string(shared[0]).to_c()
+        v_sd = None if shared[1] == "baseline" else asb.variant_from_string(shared[1]).to_c()
+        s_h = C.c_void_p(asb.torch_stream_handle(dev))
+
+        def spmm(bm):  # noqa: F811 -- the shared variant through the dispatch entry point
+            asb._check(lib.as_spmm(C.byref(v_sp) if v_sp is not None else None, g.handle, P(bm), bm.shape[0], f,
+                                   P(c), s_h, None))
+
+        def sddmm(ym):  # noqa: F811
+            asb._check(lib.as_sddmm(C.byref(v_sd) if v_sd is not None else None, g.handle, P(x_loc), r1 - r0,
+                                    P(ym), ym.shape[0], f, P(sv), s_h, None))
+        if rank != 0:
+            dec_spmm.choice = None if v_sp is None else asb.variant_from_string(shared[0])
+            dec_sddmm.choice = None if v_sd is None else asb.variant_from_string(shared[1])
+    else:
+        shared = None
 
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     blocked = None
@@ -480,7 +512,7 @@ def run_ours(args):
     groups = int(os.environ.get("AUTOSAGE_BENCH_BLOCKS", "0"))
     if groups <= 0:
         groups = 2 if m.n_cols * f * 4 > 2 * torch.cuda.get_device_properties(dev).L2_cache_size else 1
-    if world > 1 and groups > 1:
+    if use_dist and groups > 1:
         # B's shards are broadcast per owner and consumed in column blocks as
         # they land (dist.py blocked_spmm; as_spmm_blocked_*, bit-identical to
         # the decided variant); Y's all-gather follows on NCCL's stream under
@@ -558,7 +590,9 @@ def run_ours(args):
     if world == 1 and rank == 0 and not args.no_cpu:
         # the device outputs of the last timed step, checked against the
         # reference library on the full graph; then the reference timed
-        del b_full, y_full, flush
+        if not use_dist:
+            del b_full, y_full
+        del flush
         cpu, w = cpu_reference_run(m, f, args.seed, CPU_ITERS, CPU_WARMUP, args.config)
         parity = parity_check(w, c, sv, dec_spmm.choice_string(), dec_sddmm.choice_string())
         del w
@@ -573,9 +607,9 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": workload_name(args.config, f), "n_rows": n_rows, "nnz": nnz,
-                       "F": f, "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU",
+                       "F": f, "parallelism": f"row-sharded x{world}" if use_dist else "1 GPU",
                        "l2": "flushed between steps (256 MiB write, untimed)",
-                       "exchange": ("none (1 GPU)" if world == 1 else
+                       "exchange": ("none (1 GPU)" if not use_dist else
                                     (f"B row shards broadcast per owner over NCCL and consumed by the SpMM in "
                                      f"{blocked.n_blocks} column blocks as they land (as_spmm_blocked_*); "
                                      if blocked is not None else "NCCL all-gather of B row shards before the SpMM; ")
@@ -583,6 +617,7 @@ def run_ours(args):
                                     "buffers in place"),
                        "spmm_choice": dec_spmm.choice_string(),
                        "sddmm_choice": dec_sddmm.choice_string(),
+                       "decided_on": "rank 0's shard, dispatched by every rank" if use_dist else "the graph",
                        "decision_source": {"spmm": dec_spmm.source_name,
                                            "sddmm": dec_sddmm.source_name},
                        "probe": dataclasses_asdict(cfg), "input_gen_s": gen_s},
@@ -598,7 +633,7 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "clocks": clk,
         }
-        if world > 1:
+        if dist:
             line["nccl"] = {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
                             "nccl_version": ".".join(map(str, torch.cuda.nccl.version()))}
         if e2e:
