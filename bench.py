@@ -512,7 +512,7 @@ def run_ours(args):
     groups = int(os.environ.get("AUTOSAGE_BENCH_BLOCKS", "0"))
     if groups <= 0:
         groups = 2 if m.n_cols * f * 4 > 2 * torch.cuda.get_device_properties(dev).L2_cache_size else 1
-    if use_dist and groups > 1:
+    if use_dist and groups > 1 and world > 1:  # one rank: a single block, nothing to overlap
         # B's shards are broadcast per owner and consumed in column blocks as
         # they land (dist.py blocked_spmm; as_spmm_blocked_*, bit-identical to
         # the decided variant); Y's all-gather follows on NCCL's stream under
