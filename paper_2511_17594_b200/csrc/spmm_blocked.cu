@@ -15,9 +15,12 @@
 // ascending order therefore yields the unblocked result bit for bit, for
 // any cut positions.
 //
-// Cost: the state (segments x F doubles) is read and written once per block
-// a segment has entries in -- worth it when B's exchange is long against the
-// SpMM (Products-shape shards), not for an L2-resident B.
+// Cost: the state (segments x F doubles) is written by every block a segment
+// has entries in but its last, and read by every such block but its first
+// (slot flags, spmm_kernels.cuh); single-segment rows are rounded into C by
+// their last block, so only hub rows and empty rows go through the fold --
+// worth it when B's exchange is long against the SpMM (Products-shape
+// shards), not for an L2-resident B.
 #include "engine.hpp"
 #include "spmm_kernels.cuh"
 
@@ -127,27 +130,36 @@ BlockedPlan* blocked_plan_create(Graph& g, const as_variant* v, const std::uint6
         const std::uint64_t e0 = g.h_rowptr[i], e1 = g.h_rowptr[i + 1];
         const std::uint64_t step = hub && e1 - e0 >= var.hub_threshold ? kHubNnzChunk : std::max<std::uint64_t>(e1 - e0, 1);
         const std::uint64_t nseg = e1 > e0 ? (e1 - e0 + step - 1) / step : 0;
-        rrow.push_back(std::uint32_t(i));
-        rfirst.push_back(std::uint32_t(slots));
-        rcount.push_back(std::uint32_t(nseg));
+        // the fold sums multi-segment rows and zero-fills empty ones; a
+        // single-segment row is rounded into C by its last block
+        if (nseg != 1) {
+            rrow.push_back(std::uint32_t(i));
+            rfirst.push_back(std::uint32_t(slots));
+            rcount.push_back(std::uint32_t(nseg));
+        }
         for (std::uint64_t sg = 0; sg < nseg; ++sg, ++slots) {
             const std::uint64_t s0 = e0 + sg * step, s1 = std::min(e1, s0 + step);
             const std::uint32_t* c0 = colind.data() + s0;
             const std::uint32_t* c1 = colind.data() + s1;
             const std::uint32_t* lo = c0;
+            std::uint32_t first = kCarryFirst;
+            std::int64_t last_b = -1;
             for (std::uint32_t b = 0; b < n_blocks; ++b) {
                 const std::uint32_t* hi = std::lower_bound(lo, c1, cuts[b + 1]);
                 if (hi > lo) {
                     brow[b].push_back(std::uint32_t(i));
                     be0[b].push_back(std::uint64_t(lo - colind.data()));
                     blen[b].push_back(std::uint32_t(hi - lo));
-                    bslot[b].push_back(std::uint32_t(slots));
+                    bslot[b].push_back(std::uint32_t(slots) | first);
+                    first = 0;
+                    last_b = b;
                 }
                 lo = hi;
             }
+            if (nseg == 1 && last_b >= 0) bslot[std::size_t(last_b)].back() |= kCarryFinal;
         }
     }
-    if (slots >= (1ull << 32)) throw InvalidArgument("spmm_blocked: too many segments");
+    if (slots > kCarrySlotMask) throw InvalidArgument("spmm_blocked: too many segments");
     p->n_slots = slots;
     auto up = [&](auto& d, const auto& h) {
         using T = typename std::decay_t<decltype(h)>::value_type;
@@ -197,7 +209,7 @@ void blocked_plan_run(BlockedPlan& p, std::uint32_t block, const float* vals, co
             p.state.alloc(std::max<std::uint64_t>(p.n_slots * f, 1));
             p.state_f = f;
         }
-        if (p.n_slots) ASB_CUDA(cudaMemsetAsync(p.state.get(), 0, p.n_slots * f * 8, s));
+        // no clearing: every slot's first block starts its chain from 0.0
     } else if (p.state_f != f) {
         throw InvalidArgument("spmm_blocked: blocks of one product need the same F, starting at block 0");
     }

@@ -50,6 +50,9 @@ struct SegArgs {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
+// carried-state slot flags of the column-blocked SpMM (CARRY mode)
+constexpr std::uint32_t kCarryFirst = 1u << 30, kCarryFinal = 1u << 31, kCarrySlotMask = (1u << 30) - 1;
+
 #ifndef ASB_SEG_E64_MAXLPR
 #define ASB_SEG_E64_MAXLPR 16  // widest lane group that takes the 8-byte entry (A/B build knob)
 #endif
@@ -147,7 +150,11 @@ __device__ __forceinline__ void seg_accumulate(double (&acc)[NCH][VEC], double v
 // CARRY (column-blocked SpMM, spmm_blocked.cu): every item is a segment
 // with an f64 state slot; the accumulators start from scratch[slot] instead
 // of 0.0 and are written back there, so a row's entries can be consumed in
-// ascending column blocks across launches with the reference's order.
+// ascending column blocks across launches with the reference's order.  Slot
+// flags (kCarryFirst: the segment's first block -- start from 0.0, nothing
+// to load; kCarryFinal: the last block of a single-segment row -- round into
+// C instead of storing the state) keep the carried traffic to one store and
+// one load per block boundary.
 template <int VEC, int LPR, int NCH, bool HAS_VAL, bool PIECES, int U, int MIX, bool SMX, int WT, bool VP,
           bool CARRY = false>
 __device__ __forceinline__ void seg_body(const SegArgs& a) {
@@ -219,10 +226,13 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
     for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll
         for (int q = 0; q < VEC; ++q) acc[ch][q] = 0.0;
+    bool carry_final = false;
     if constexpr (CARRY) {
         static_assert(PIECES, "carry mode runs on segment lists");
-        if (active) {
-            ASB_DCHECK(slot != 0xffffffffu);
+        const bool carry_first = (slot & kCarryFirst) != 0;
+        carry_final = (slot & kCarryFinal) != 0;
+        slot &= kCarrySlotMask;
+        if (active && !carry_first) {
 #pragma unroll
             for (int ch = 0; ch < NCH; ++ch)
                 if (fok[ch]) {
@@ -385,7 +395,7 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) {
         if (!fok[ch]) continue;
-        if (!PIECES || slot == 0xffffffffu) {
+        if (!PIECES || (!CARRY && slot == 0xffffffffu) || carry_final) {
             float* cp = a.c + std::uint64_t(row) * a.f + fidx[ch];
 #pragma unroll
             for (int q = 0; q < VEC; ++q) st_stream(cp + q, float(acc[ch][q]), pol_s);
