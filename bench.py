@@ -679,12 +679,23 @@ def roofline(args, g, f, rows, n_cols, spmm_ms, sddmm_ms, peak, peak_src):
     oc = profile_json("onchip_roofs.json")
     if oc and dom in oc.get("ops", {}):
         # the row gathers themselves: one 4F-byte B (SpMM) / Y (SDDMM) row per
-        # nonzero, the traffic the measured gather roof moves
+        # nonzero, the traffic the measured gather roof moves -- from L2 while
+        # the gathered operand fits it, from HBM past that (Products-shape)
         rows_b = 4.0 * f * g.nnz
-        roof = float(oc["ops"][dom]["gbs"])
-        r["onchip"] = {"row_gather_bytes": rows_b, "achieved_gbs": to_gbs(rows_b), "roof_gbs": roof,
-                       "frac": to_gbs(rows_b) / roof, "what": oc["ops"][dom]["what"],
-                       "source": oc.get("source")}
+        import torch
+        l2 = torch.cuda.get_device_properties(torch.cuda.current_device()).L2_cache_size
+        if 4.0 * f * n_cols <= l2 or "gather_hbm_gbs" not in oc:
+            roof = float(oc["ops"][dom]["gbs"])
+            r["onchip"] = {"row_gather_bytes": rows_b, "achieved_gbs": to_gbs(rows_b), "roof_gbs": roof,
+                           "frac": to_gbs(rows_b) / roof, "what": oc["ops"][dom]["what"],
+                           "source": oc.get("source")}
+        else:
+            roof = float(oc["gather_hbm_gbs"])
+            r["hbm_gather"] = {"row_gather_bytes": rows_b, "achieved_gbs": to_gbs(rows_b), "roof_gbs": roof,
+                               "frac": to_gbs(rows_b) / roof,
+                               "what": "random 256-B row gather from an HBM-resident 1 GB operand "
+                                       "(the gathered operand is larger than the L2 here)",
+                               "source": oc.get("source")}
     return r
 
 
