@@ -419,8 +419,6 @@ int dev_tune() {
         if (v == "2x48") return 7;
         if (v == "4x56") return 8;
         if (v == "4x64") return 9;
-        if (v == "6x64") return 10;
-        if (v == "6x80") return 11;
         if (v == "8x80") return 12;
         if (v == "8x96") return 13;
         if (v == "4x72") return 14;
@@ -442,8 +440,6 @@ void launch_tuned(const SegArgs& a, unsigned blocks, unsigned threads, cudaStrea
             case 7: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 2, 48><<<blocks, threads, seg_smem(threads), s>>>(a); return;
             case 8: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 4, 56><<<blocks, threads, seg_smem(threads), s>>>(a); return;
             case 9: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 4, 64><<<blocks, threads, seg_smem(threads), s>>>(a); return;
-            case 10: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 6, 64><<<blocks, threads, seg_smem(threads), s>>>(a); return;
-            case 11: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 6, 80><<<blocks, threads, seg_smem(threads), s>>>(a); return;
             case 12: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 8, 80><<<blocks, threads, seg_smem(threads), s>>>(a); return;
             case 13: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 8, 96><<<blocks, threads, seg_smem(threads), s>>>(a); return;
             case 14: spmm_seg_kernel<VEC, LPR, NCH, HV, PC, 4, 72><<<blocks, threads, seg_smem(threads), s>>>(a); return;

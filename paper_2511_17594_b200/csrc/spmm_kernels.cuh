@@ -163,6 +163,9 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
     constexpr int GPW = 32 / LPR;
     constexpr int W = LPR > U ? LPR : U;
     constexpr int S = W / LPR;
+    // the fast loop walks W-entry blocks U entries at a time (a U that does
+    // not divide W read past the block: the removed 6-wide dev tunings)
+    static_assert(W % U == 0, "entries in flight must divide the block");
     const int lane = threadIdx.x & 31;
     const int grp = lane / LPR;
     const int gl = lane % LPR;
