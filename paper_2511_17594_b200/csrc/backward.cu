@@ -31,7 +31,9 @@ namespace asb {
 
 namespace {
 
-unsigned grid_for(std::uint64_t n, unsigned block, unsigned cap = 148u * 16u) {
+// grid-stride launches: at most `cap` CTAs (default 16 per SM of the device)
+unsigned grid_for(std::uint64_t n, unsigned block, unsigned cap = 0) {
+    if (cap == 0) cap = unsigned(device_sms()) * 16u;
     std::uint64_t g = (n + block - 1) / block;
     if (g == 0) g = 1;
     return unsigned(std::min<std::uint64_t>(g, cap));
@@ -273,13 +275,13 @@ void launch_row_softmax_backward(Graph& g, const float* p, const float* grad, fl
     ensure_order(g);
     const std::uint64_t n_long = rows_with_degree_at_least(g, kSbwLongRow);
     if (n_long) {
-        softmax_backward_cta_kernel<<<unsigned(std::min<std::uint64_t>(n_long, 148u * 8u)), 256, 0, s>>>(
+        softmax_backward_cta_kernel<<<unsigned(std::min<std::uint64_t>(n_long, unsigned(device_sms()) * 8u)), 256, 0, s>>>(
             g.rowptr.get(), g.order.get(), n_long, p, grad, ds);
         check_launch("softmax_backward_cta_kernel");
     }
     const std::uint64_t n_rest = g.n_rows - n_long;
     if (n_rest) {
-        softmax_backward_kernel<<<grid_for(n_rest * 32, 256, 148u * 8u), 256, 0, s>>>(
+        softmax_backward_kernel<<<grid_for(n_rest * 32, 256, unsigned(device_sms()) * 8u), 256, 0, s>>>(
             g.rowptr.get(), g.order.get() + n_long, n_rest, p, grad, ds);
         check_launch("softmax_backward_kernel");
     }

@@ -118,7 +118,9 @@ __global__ void validate_cols_kernel(const std::uint64_t* __restrict__ rowptr, s
     if (lane == 0 && mine) atomicOr(bad, mine);
 }
 
-unsigned grid_for(std::uint64_t n, unsigned block, unsigned cap = 148u * 16u) {
+// grid-stride launches: at most `cap` CTAs (default 16 per SM of the device)
+unsigned grid_for(std::uint64_t n, unsigned block, unsigned cap = 0) {
+    if (cap == 0) cap = unsigned(device_sms()) * 16u;
     std::uint64_t g = (n + block - 1) / block;
     if (g == 0) g = 1;
     return unsigned(std::min<std::uint64_t>(g, cap));

@@ -750,7 +750,7 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const void* b, std::uint32
                          wt);
     if (plan.n_red) {
         const std::uint64_t total = plan.n_red * f;
-        const unsigned blocks = unsigned(std::min<std::uint64_t>((total + 255) / 256, 148 * 32));
+        const unsigned blocks = unsigned(std::min<std::uint64_t>((total + 255) / 256, std::uint64_t(g.sms) * 32));
         hub_reduce_kernel<<<blocks, 256, 0, s>>>(plan.red_row.get(), plan.red_first.get(),
                                                  plan.red_count.get(), plan.n_red, g.scratch.get(),
                                                  c, f);
