@@ -8,8 +8,10 @@ against the oracle (so a race that corrupts data also fails here):
   SpMM   lane-group kernel row mode (fast loop + ragged tail), hub pieces +
          reduce, the cp.async ring kernel (rows >= 256 on a small graph),
          baseline; f32, bf16 B, transpose values (backward)
-  SDDMM  pair1 kernel (F=32, 64), pair kernel (F=128), chunk kernel (F=100),
-         direct (baseline), bf16
+  SDDMM  pair1 kernel (F=32, 64, 100), pair kernel (F=128), pass-major
+         pair kernel (F=128, forced), chunk kernel (F=24), direct
+         (baseline), bf16
+  blocked SpMM (carried state, 3 column blocks, hub pieces)
   softmax warp / CTA / chain kernels, fused and staged attention
 
   python tools/sanitize_cases.py        # prints SANITIZE_CASES_OK
@@ -59,6 +61,27 @@ def main():
             bb = bd.to(torch.bfloat16)
             got = torch.ops.autosage.spmm_csr(*_csr(a), bb, "spmm:hubsplit:ft=64:rpc=1:vec=1:hubt=256")
             assert bit_equal(got.cpu().numpy(), oracle.spmm_hubsplit(a, bb.float().cpu().numpy(), 256))
+    # pass-major SDDMM (forced on this small graph) and the general chunk kernel
+    for f, pm in ((128, "1"), (24, "0")):
+        os.environ["AUTOSAGE_DEV_SDDMM_PM"] = pm
+        x, y = random_dense(rng, 2000, f), random_dense(rng, 6000, f)
+        xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+        for ft, vec in ((32, False), (32, True), (64, True)):
+            got = asb.dispatch(V(asb.SDDMM, asb.ROWPARALLEL, ft, 1, vec), g, xd, yd).values.cpu().numpy()
+            assert bit_equal(got, oracle.sddmm(a, x, y, ft, vec and f % 4 == 0)), ("sddmm pm", f, ft, vec)
+    os.environ.pop("AUTOSAGE_DEV_SDDMM_PM", None)
+    # column-blocked SpMM: carried f64 state across 3 blocks, hub pieces
+    b = random_dense(rng, 6000, 64)
+    bd = torch.from_numpy(b).cuda()
+    cd = torch.empty((2000, 64), device="cuda")
+    for var in (V(asb.SPMM, asb.HUBSPLIT, 64, 1, True, 256), None):
+        bp = asb.BlockedSpmm(g, var, [0, 1500, 1501, 6000])
+        for k in range(bp.n_blocks):
+            bp.run(k, bd, cd)
+        torch.cuda.synchronize()
+        want = oracle.spmm_hubsplit(a, b, 256) if var is not None else oracle.spmm_baseline(a, b)
+        assert bit_equal(cd.cpu().numpy(), want), ("blocked", var)
+        bp.close()
     # softmax over wide scores (forces the chain path on long rows)
     vals = (rng.standard_normal(a.nnz) * 30).astype(np.float32)
     got = asb.row_softmax(a.with_values(vals)).val
