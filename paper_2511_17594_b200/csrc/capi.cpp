@@ -790,7 +790,10 @@ static as_status spmm_half_entry(const as_variant* v, as_graph a, const float* v
                                  int wt, const char* name) {
     return guard([&] {
         Graph& g = G(a);
-        if (g.n_rows && f && (!b_dev || !c_dev)) throw InvalidArgument(std::string(name) + ": null operand");
+        // B is read only through entries: a graph without entries may pass
+        // an empty (null) B, as the f32 entry points allow
+        if ((g.n_rows && f && !c_dev) || (g.nnz && f && !b_dev))
+            throw InvalidArgument(std::string(name) + ": null operand");
         GraphUse use(g, resolve_stream(g, stream));
         const KernelResult r = dispatch_spmm_half(v, g, vals_dev, b_dev, b_rows, f, c_dev,
                                                   resolve_stream(g, stream), res != nullptr, wt);
