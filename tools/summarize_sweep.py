@@ -19,8 +19,10 @@ def main():
     r = json.load(open(src))
     peak = r.get("peak_gbs", 6550.1)
     L = [f"# Config sweep ({tag}) — {r.get('gpu', 'B200')}", "",
-         "`python tools/sweep.py` (one GPU). Times are CUDA-event medians per launch after the decision is",
-         "cached; GB/s is the reference gather model (proj/src/cost.cpp:21-27) over that time, so it can exceed",
+         "`python tools/sweep.py` (one GPU). Times are CUDA-event medians per call after the decision is",
+         "cached (device time: calls queued back to back, a 256 MB L2-flush write between them; sweeps up to",
+         "r02l synchronized after every call instead); GB/s is the reference gather model",
+         "(proj/src/cost.cpp:21-27) over that time, so it can exceed",
          f"HBM when the dense operand is L2-resident. `frac` = GB/s / {peak:.0f} (MEASURED_PEAKS.json).", ""]
     m = r.get("meta")
     if m:

@@ -48,20 +48,32 @@ def P(t):
     return C.c_void_p(t.data_ptr())
 
 
+_FLUSH = None
+
+
 def ev_time(fn, reps=5, warm=2):
-    """Median per-launch ms of fn() (CUDA events per call)."""
+    """Median per-call GPU ms of fn(): CUDA events around each call, calls
+    queued back to back with a 256 MB L2-flush write between them (outside
+    the events; it also gives the host time to enqueue the next call), one
+    synchronize at the end -- the device time of a call, as bench.py times
+    its steps (round-1/2 sweeps up to r02l synchronized after every call, so
+    their small-graph times include the host enqueue)."""
+    global _FLUSH
+    if _FLUSH is None:
+        _FLUSH = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
-    ts = []
+    evs = []
     for _ in range(reps):
+        _FLUSH.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         fn()
         e1.record()
-        e1.synchronize()
-        ts.append(e0.elapsed_time(e1))
-    return statistics.median(ts)
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    return statistics.median(e0.elapsed_time(e1) for e0, e1 in evs)
 
 
 class Ops:
