@@ -546,6 +546,22 @@ std::unique_ptr<Graph> row_range(Graph& g, std::uint64_t r0, std::uint64_t r1) {
 // (src/kernels.cpp:129-142).  A heavy row with a single piece reduces to
 // 0.0 + partial == partial (the partial is never -0.0), so it writes C
 // directly; multi-piece rows get partial slots and an ordered reduce.
+// the light rows of a hub plan as direct-write items (HubPlan::all_*)
+__global__ void light_items_kernel(const std::uint32_t* __restrict__ rows, std::uint64_t n,
+                                   const std::uint64_t* __restrict__ rowptr, std::uint32_t* __restrict__ row,
+                                   std::uint64_t* __restrict__ e0, std::uint32_t* __restrict__ len,
+                                   std::uint32_t* __restrict__ slot) {
+    for (std::uint64_t i = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += std::uint64_t(gridDim.x) * blockDim.x) {
+        const std::uint32_t r = rows[i];
+        const std::uint64_t a = rowptr[r];
+        row[i] = r;
+        e0[i] = a;
+        len[i] = std::uint32_t(rowptr[r + 1] - a);
+        slot[i] = 0xffffffffu;
+    }
+}
+
 const HubPlan& ensure_hub_plan(Graph& g, std::uint64_t threshold) {
     {
         std::lock_guard<std::mutex> lk(g.mu);
@@ -615,6 +631,31 @@ const HubPlan& ensure_hub_plan(Graph& g, std::uint64_t threshold) {
     if (!pe0.empty())
         ASB_CUDA(cudaMemcpyAsync(plan->piece_e0.get(), pe0.data(), pe0.size() * 8,
                                  cudaMemcpyHostToDevice, g.stream));
+    {
+        const std::uint64_t n_all = plan->n_pieces + plan->n_light;
+        plan->all_row.alloc(std::max<std::uint64_t>(n_all, 1));
+        plan->all_len.alloc(std::max<std::uint64_t>(n_all, 1));
+        plan->all_slot.alloc(std::max<std::uint64_t>(n_all, 1));
+        plan->all_e0.alloc(std::max<std::uint64_t>(n_all, 1));
+        if (plan->n_pieces) {
+            const std::uint64_t np = plan->n_pieces;
+            ASB_CUDA(cudaMemcpyAsync(plan->all_row.get(), plan->piece_row.get(), np * 4, cudaMemcpyDeviceToDevice,
+                                     g.stream));
+            ASB_CUDA(cudaMemcpyAsync(plan->all_len.get(), plan->piece_len.get(), np * 4, cudaMemcpyDeviceToDevice,
+                                     g.stream));
+            ASB_CUDA(cudaMemcpyAsync(plan->all_slot.get(), plan->piece_slot.get(), np * 4, cudaMemcpyDeviceToDevice,
+                                     g.stream));
+            ASB_CUDA(cudaMemcpyAsync(plan->all_e0.get(), plan->piece_e0.get(), np * 8, cudaMemcpyDeviceToDevice,
+                                     g.stream));
+        }
+        if (plan->n_light) {
+            light_items_kernel<<<grid_for(plan->n_light, 256), 256, 0, g.stream>>>(
+                g.order.get() + plan->n_heavy, plan->n_light, g.rowptr.get(), plan->all_row.get() + plan->n_pieces,
+                plan->all_e0.get() + plan->n_pieces, plan->all_len.get() + plan->n_pieces,
+                plan->all_slot.get() + plan->n_pieces);
+            check_launch("light_items_kernel");
+        }
+    }
     ASB_CUDA(cudaStreamSynchronize(g.stream));
     std::lock_guard<std::mutex> lk(g.mu);
     auto& slot = g.hub_plans[threshold];

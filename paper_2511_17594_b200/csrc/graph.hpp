@@ -69,6 +69,10 @@ struct HubPlan {
     DevBuf<std::uint32_t> red_first;   // first slot
     DevBuf<std::uint32_t> red_count;   // pieces
     std::uint64_t n_heavy = 0;
+    // one item list for a single launch: the pieces (longest first) followed
+    // by the light rows as direct-write items (degree-descending)
+    DevBuf<std::uint32_t> all_row, all_len, all_slot;
+    DevBuf<std::uint64_t> all_e0;
 };
 
 struct Graph {

@@ -700,6 +700,56 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const void* b, std::uint32
         const char* e = std::getenv("AUTOSAGE_DEV_SPMM_CONCURRENT");
         return e ? std::atoi(e) != 0 : true;
     }();
+    // one launch over pieces + light rows (HubPlan::all_*: pieces longest
+    // first, then the light rows degree-descending) instead of two kernels on
+    // forked streams: one tail instead of two and no fork/join.  Same items,
+    // same bits; Products F=100 9.03 -> 8.71 ms, its 8-way shard 1.22 -> 1.19,
+    // c4 1.13 -> 1.10, Reddit unchanged (profiles/r02z_merged.md).
+    // AUTOSAGE_DEV_SPMM_MERGED=0 restores the two-kernel form.
+    static const bool merged_knob = [] {
+        const char* e = std::getenv("AUTOSAGE_DEV_SPMM_MERGED");
+        return e ? std::atoi(e) != 0 : true;
+    }();
+    const bool few_pieces = plan.n_pieces <= std::uint64_t(4) * std::uint64_t(g.sms);
+    if (merged_knob && plan.n_pieces && plan.n_light && !few_pieces) {
+        SegArgs a{};
+        a.rowptr = g.rowptr.get();
+        a.colind = g.colind.get();
+        a.val = val;
+        a.vperm = g.val_perm;
+        a.b = b;
+        a.c = c;
+        a.scratch = g.scratch.get();
+        a.piece_row = plan.all_row.get();
+        a.piece_e0 = plan.all_e0.get();
+        a.piece_len = plan.all_len.get();
+        a.piece_slot = plan.all_slot.get();
+        a.finite = finite;
+        a.rmax = rmax;
+        a.rsum = rsum;
+        a.n_items = (plan.n_pieces + plan.n_light) * t.n_tiles;
+        a.n_tiles = t.n_tiles;
+        a.f = f;
+        a.n_rows = g.n_rows;
+        a.n_cols = g.n_cols;
+        a.nnz = g.nnz;
+        a.off32 = fast_gather_ok(g, f);
+        a.wt = wt;
+        a.keep_b = std::uint64_t(g.n_cols) * f * (wt ? 2 : 4) <= kKeepMaxBytes;
+        a.tile_major = tile_major();
+        a.tile_w = t.tile_w;
+        if (v8) launch_seg_vec<8>(a, val != nullptr, t.lanes, wpb, s);
+        else if (vec) launch_seg_vec<4>(a, val != nullptr, t.lanes, wpb, s);
+        else launch_seg_vec<1>(a, val != nullptr, t.lanes, wpb, s);
+        if (plan.n_red) {
+            const std::uint64_t total = plan.n_red * f;
+            const unsigned blocks = unsigned(std::min<std::uint64_t>((total + 255) / 256, std::uint64_t(g.sms) * 32));
+            hub_reduce_kernel<<<blocks, 256, 0, s>>>(plan.red_row.get(), plan.red_first.get(),
+                                                     plan.red_count.get(), plan.n_red, g.scratch.get(), c, f);
+            check_launch("hub_reduce_kernel");
+        }
+        return;
+    }
     const bool fork_light = concurrent && plan.n_light && plan.n_pieces;
     if (fork_light) {
         cudaStream_t aux = graph_fork(g, s);
