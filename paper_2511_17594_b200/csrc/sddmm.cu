@@ -391,7 +391,7 @@ __device__ __forceinline__ void fixed_pass(const double* __restrict__ xr, const 
         }
     }
     if constexpr (ORD == 1 && (FT == 0 || FT > FW)) {
-        const bool end = p == npass - 1 || (FT != 0 && ((p + 1) * FW) % FT == 0);
+        const bool end = p == npass - 1 || (FT != 0 && ((p + 1) * FW) % (FT != 0 ? FT : 1) == 0);
         if (end) fold4(acc, a0, a1, a2, a3);
     }
 }
@@ -568,7 +568,7 @@ __device__ __forceinline__ void pair_pass(const double* __restrict__ xa, const d
         }
     }
     if constexpr (ORD == 1 && (FT == 0 || FT > FW)) {
-        const bool end = p == npass - 1 || (FT != 0 && ((p + 1) * FW) % FT == 0);
+        const bool end = p == npass - 1 || (FT != 0 && ((p + 1) * FW) % (FT != 0 ? FT : 1) == 0);
         if (end) {
             fold4(c[0][0], c[0][1], c[0][2], c[0][3], c[0][4]);
             fold4(c[1][0], c[1][1], c[1][2], c[1][3], c[1][4]);
@@ -712,12 +712,17 @@ __global__ void __launch_bounds__(128, 3)
 // specialisation measured 6% faster than the pass loop at F = 64).
 // BF: Y rows staged as bf16 (half the cp.async and LDS wavefronts; one
 // 16-byte unit holds 8 features)
+#ifndef ASB_PAIR_KX
+#define ASB_PAIR_KX 2  // X rows a pair-kernel warp stages for F <= 64 (A/B build knob)
+#endif
 template <int F, bool BF = false>
 struct Pair1Shape {
     static constexpr int kYElem = BF ? 2 : 4;
     static constexpr int NV = F * kYElem / 16;  // 16-byte units per Y row
     static constexpr int kCopies = 2 * NV;      // cp.async per lane per chunk (64 rows)
-    static constexpr int KX = 2;                // X rows staged
+    // X rows staged: the first KX rows of the 64-entry window are read from
+    // shared memory, lanes in later rows read the widened X from L1/L2
+    static constexpr int KX = F <= 64 ? ASB_PAIR_KX : 2;
     static constexpr int kXUnits = KX * F / 2;
     static constexpr std::uint64_t kYBytes = 64ull * F * kYElem;
     static constexpr std::uint64_t kWarpBytes = kYBytes + std::uint64_t(KX) * F * 8;
