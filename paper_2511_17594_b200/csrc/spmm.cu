@@ -705,13 +705,14 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const void* b, std::uint32
     // forked streams: one tail instead of two and no fork/join.  Same items,
     // same bits; Products F=100 9.03 -> 8.71 ms, its 8-way shard 1.22 -> 1.19,
     // c4 1.13 -> 1.10, Reddit unchanged (profiles/r02z_merged.md).
-    // AUTOSAGE_DEV_SPMM_MERGED=0 restores the two-kernel form.
-    static const bool merged_knob = [] {
+    // AUTOSAGE_DEV_SPMM_MERGED=0 restores the two-kernel form, =2 forces the
+    // one launch also where the pieces would take the ring kernel (tests).
+    const int merged_knob = [] {
         const char* e = std::getenv("AUTOSAGE_DEV_SPMM_MERGED");
-        return e ? std::atoi(e) != 0 : true;
+        return e ? std::atoi(e) : 1;
     }();
     const bool few_pieces = plan.n_pieces <= std::uint64_t(4) * std::uint64_t(g.sms);
-    if (merged_knob && plan.n_pieces && plan.n_light && !few_pieces) {
+    if (merged_knob && plan.n_pieces && plan.n_light && (!few_pieces || merged_knob == 2)) {
         SegArgs a{};
         a.rowptr = g.rowptr.get();
         a.colind = g.colind.get();

@@ -96,6 +96,39 @@ def test_spmm_hubsplit_bit_exact_vs_oracle(hub_t, f):
             assert bit_equal(got, want), (vec, ft, n_bit_diff(got, want))
 
 
+@pytest.mark.parametrize("mode", ["2", "0"])
+def test_spmm_hubsplit_one_launch_bit_exact(monkeypatch, mode):
+    """Hub pieces and light rows as one item list in one launch (forced with
+    AUTOSAGE_DEV_SPMM_MERGED=2 on graphs small enough for the ring kernel;
+    0 = the two-kernel form): empty rows, one-entry rows, multi-piece hubs,
+    f32 / bf16 B, vec and scalar tiles -- bit-equal to the oracle."""
+    import torch
+    import paper_2511_17594_b200.torch_ops  # noqa: F401  (torch.ops.autosage)
+    monkeypatch.setenv("AUTOSAGE_DEV_SPMM_MERGED", mode)
+    rng = np.random.default_rng(57)
+    n = 3000
+    deg = rng.choice([0, 0, 1, 3, 17, 40], size=n).astype(np.int64)
+    deg[:5] = [2900, 2049, 2048, 700, 256]
+    from tests.util import csr_from_degrees
+    a = csr_from_degrees(rng, n, n, deg, True)
+    g = asb.Graph.from_csr(a)
+    for f in (4, 64, 100):
+        b = random_dense(rng, n, f)
+        bd = cuda(b)
+        for hub_t in (1, 256):
+            want = oracle.spmm_hubsplit(a, b, hub_t)
+            for vec in (False, True):
+                got = asb.dispatch(V(SP, HS, 64, 1, vec, hub_t), g, bd).output.cpu().numpy()
+                assert bit_equal(got, want), (mode, f, hub_t, vec, n_bit_diff(got, want))
+        if f == 64:  # bf16 B words through the same item list
+            b16 = bd.to(torch.bfloat16)
+            crow = torch.from_numpy(a.rowptr.astype(np.int64)).cuda()
+            col = torch.from_numpy(a.colind.astype(np.int32)).cuda()
+            got = torch.ops.autosage.spmm_csr(crow, col, cuda(a.val), b16, "spmm:hubsplit:ft=64:rpc=1:vec=1:hubt=256")
+            assert bit_equal(got.cpu().numpy(), oracle.spmm_hubsplit(a, b16.float().cpu().numpy(), 256)), mode
+    g.close()
+
+
 def test_spmm_hubsplit_unreachable_threshold_equals_rowparallel():
     rng = np.random.default_rng(6)
     a = random_csr(rng, 128, 128, 10)
