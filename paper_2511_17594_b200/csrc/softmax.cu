@@ -46,6 +46,9 @@ struct SoftmaxArgs {
     float* rmax;    // !OUT
     double* rsum;   // !OUT
     int force_seq;  // developer/test knob: always run the sequential chain
+    // CTA kernel: defer a row straight to the chain kernel when its value
+    // range already proves the exactness certificate fails (see below)
+    int predefer;
     // CTA kernel: rows whose certificate failed are handed to the chain
     // kernel (row, max) instead of serialising the CTA on one sum chain
     std::uint32_t* chain_row;
@@ -160,6 +163,7 @@ __global__ void __launch_bounds__(256, 3) softmax_warp_kernel(SoftmaxArgs a) {
 // block-wide reductions over the 8 warps (every thread gets the result)
 struct CtaRed {
     float f[kWarpsPerCta];
+    float g[kWarpsPerCta];
     double d[kWarpsPerCta];
     unsigned u[kWarpsPerCta];
     double seq;
@@ -174,6 +178,27 @@ __device__ __forceinline__ float cta_max(CtaRed& r, float v) {
 #pragma unroll
     for (int i = 1; i < kWarpsPerCta; ++i) v = fmaxf(v, r.f[i]);
     return v;
+}
+// max and min in one pass (one barrier)
+__device__ __forceinline__ void cta_max_min(CtaRed& r, float& mx, float& mn) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
+        mn = fminf(mn, __shfl_xor_sync(FULL, mn, o));
+    }
+    if (lane == 0) {
+        r.f[warp] = mx;
+        r.g[warp] = mn;
+    }
+    __syncthreads();
+    mx = r.f[0];
+    mn = r.g[0];
+#pragma unroll
+    for (int i = 1; i < kWarpsPerCta; ++i) {
+        mx = fmaxf(mx, r.f[i]);
+        mn = fminf(mn, r.g[i]);
+    }
 }
 // sum (exact under the certificate, so any order) and certificate minimum
 __device__ __forceinline__ void cta_sum(CtaRed& r, double& sum, unsigned& mn) {
@@ -245,16 +270,52 @@ __global__ void __launch_bounds__(256, 3) softmax_cta_kernel(SoftmaxArgs a) {
         float* cexs = cbuf + slot * kCtaSmem;
         const float* vin = a.vin + cur.e0;
 
-        float mx = -INFINITY;
+        float mx = -INFINITY, mnv = INFINITY;
         if (staged) {
 #pragma unroll 8
-            for (std::uint32_t k = tid; k < deg; k += 256) mx = fmaxf(mx, cexs[k]);
+            for (std::uint32_t k = tid; k < deg; k += 256) {
+                mx = fmaxf(mx, cexs[k]);
+                mnv = fminf(mnv, cexs[k]);
+            }
         } else {
 #pragma unroll 8
-            for (std::uint32_t k = tid; k < deg; k += 256) mx = fmaxf(mx, __ldg(vin + k));
+            for (std::uint32_t k = tid; k < deg; k += 256) {
+                const float v = __ldg(vin + k);
+                mx = fmaxf(mx, v);
+                mnv = fminf(mnv, v);
+            }
         }
-        mx = cta_max(red, mx);
+        if (a.predefer && !a.force_seq) cta_max_min(red, mx, mnv);
+        else mx = cta_max(red, mx);
         const double dmx = double(mx);
+        // The row's maximum contributes ex = 1, so the total is >= 1.  If the
+        // smallest value gives a normal, non-zero ex below 2^-31 (mnv - mx in
+        // (-87, -22)), its ulp is below 2^-54 and the certificate
+        // (total < 2^(q+53), softmax.cuh) cannot hold: skip the parallel
+        // exp + sum and hand the row to the chain kernel at once.  Deferring
+        // is always exact -- the chain is the reference's own order -- so
+        // this only saves work.
+        if (a.predefer && !a.force_seq) {
+            const double span = double(mnv) - dmx;
+            // predefer 2 adds an estimate: values spread over [mnv, mx] put the
+            // total near deg / |span|, so the certificate likely fails once
+            // log2(deg / |span|) >= span / ln 2 + 30 (a wrong guess only
+            // moves the row to the other exact path)
+            const bool certain = span < -22.0 && span > -87.0;
+            const bool likely = a.predefer == 2 && span < -1.0 && span > -87.0 &&
+                                log2(double(deg) / -span) >= span * 1.4426950408889634 + 30.0;
+            if (certain || likely) {  // block-uniform
+                if (tid == 0) {
+                    const unsigned i = atomicAdd(a.chain_n, 1u);
+                    a.chain_row[i] = cur.row;
+                    a.chain_mx[i] = mx;
+                }
+                __syncthreads();
+                cur = nxt;
+                nxt = nn;
+                continue;
+            }
+        }
 
         double sum = 0.0;
         unsigned mn = 0xffffffffu;
@@ -384,6 +445,13 @@ void launch_softmax(Graph& g, const float* vin, float* vout, float* rmax, double
     a.rmax = rmax;
     a.rsum = rsum;
     a.force_seq = env_flag("AUTOSAGE_DEV_SOFTMAX_SEQ") ? 1 : 0;
+    {
+        // 0 off, 1 certain failures only, 2 (default) also likely ones:
+        // Reddit-shape fused attention 5.233 -> 5.197 ms, row softmax over
+        // N(0, 8^2) values 2.045 -> 1.837 ms (profiles/r02ad_predefer.log)
+        const char* e = std::getenv("AUTOSAGE_DEV_SOFTMAX_PREDEFER");
+        a.predefer = e ? std::atoi(e) : 2;
+    }
     const bool lib = env_flag("AUTOSAGE_DEV_SOFTMAX_LIBEXP");
     const std::uint64_t n_long = rows_with_degree_at_least(g, kRowSmem + 1);
     const std::uint64_t n_short = g.n_rows - n_long;
