@@ -394,6 +394,27 @@ def test_row_softmax_parallel_sum_equals_sequential_chain(monkeypatch):
     assert bit_equal(fast, seq)
 
 
+def test_row_softmax_predeferral_keeps_bits(monkeypatch):
+    """CTA-kernel rows whose value span makes the certificate fail go to the
+    chain kernel before the parallel attempt (AUTOSAGE_DEV_SOFTMAX_PREDEFER
+    0 / 1 / 2): spans around the -22 bound and the estimate, NaN/Inf rows --
+    the same bits every way, and the oracle's values."""
+    rng = np.random.default_rng(63)
+    m, vals, _ = _softmax_stress_graph(rng)
+    rp = m.rowptr.astype(np.int64)
+    for r, lo in ((0, -21.9), (4, -22.1), (6, -16.0), (7, -90.0), (8, -30.0)):
+        vals[rp[r]:rp[r + 1]] = rng.uniform(lo, 0, size=rp[r + 1] - rp[r]).astype(np.float32)
+    outs = []
+    for knob in ("0", "1", "2"):
+        monkeypatch.setenv("AUTOSAGE_DEV_SOFTMAX_PREDEFER", knob)
+        outs.append(asb.row_softmax(m.with_values(vals)).val)
+    assert bit_equal(outs[0], outs[1]) and bit_equal(outs[0], outs[2])
+    want = oracle.row_softmax(m, vals)
+    nan = np.isnan(want)
+    assert np.array_equal(np.isnan(outs[2]), nan)
+    assert ulp_diff(outs[2][~nan], want[~nan]) <= 1
+
+
 def test_row_softmax_written_out_exp_equals_cuda_exp(monkeypatch):
     """sm_exp (softmax.cuh) is CUDA's f64 exp instruction sequence written
     out; AUTOSAGE_DEV_SOFTMAX_LIBEXP=1 runs exp() itself.  Same bits over
