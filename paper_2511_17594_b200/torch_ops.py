@@ -4,6 +4,8 @@ integration surface).
     import paper_2511_17594_b200.torch_ops  # registers torch.ops.autosage.*
     c = torch.ops.autosage.spmm_csr(crow, col, val, b, "spmm:hubsplit:ft=64:rpc=4:vec=1:hubt=256")
     c = torch.ops.autosage.spmm_csr_auto(crow, col, val, b)       # decide (cached) + run
+    c = torch.ops.autosage.spmm_csr_split(crow, col, val, b, 256, 64, True)  # hub split at hubT 256
+    s = torch.ops.autosage.sddmm_csr_auto(crow, col, x, y)         # decide (cached) + run
     s = torch.ops.autosage.sddmm_csr(crow, col, x, y, "")          # "" = baseline
     o = torch.ops.autosage.csr_attention(crow, col, q, k, v, False)
     p = torch.ops.autosage.row_softmax_csr(crow, col, s, n_cols)
@@ -148,6 +150,10 @@ def spmm_csr(crow: torch.Tensor, col: torch.Tensor, val: torch.Tensor, b: torch.
     """C = A B (dispatch(variant, A, B), src/kernels.cpp:485-506; "" = baseline).
     A bfloat16 / float16 B is read as 16-bit words (as_spmm_bf16 / as_spmm_f16: half the gather bytes, the
     f32 result on float(B) bit for bit); C is float32 either way."""
+    return _spmm_impl(crow, col, val, b, variant)
+
+
+def _spmm_impl(crow, col, val, b, variant: str) -> torch.Tensor:
     if b.dim() != 2:
         raise ValueError("spmm_csr: b must be 2-D")
     g = _graph(crow, col, b.shape[0])
@@ -170,6 +176,24 @@ def spmm_csr(crow: torch.Tensor, col: torch.Tensor, val: torch.Tensor, b: torch.
 
 @spmm_csr.register_fake
 def _(crow, col, val, b, variant):
+    return b.new_empty((crow.shape[0] - 1, b.shape[1]), dtype=torch.float32)
+
+
+@torch.library.custom_op("autosage::spmm_csr_split", mutates_args=())
+def spmm_csr_split(crow: torch.Tensor, col: torch.Tensor, val: torch.Tensor, b: torch.Tensor,
+                   hub_threshold: int, f_tile: int, vec: bool) -> torch.Tensor:
+    """The paper's split SpMM (light rows + hubs): the hub-split
+    mapping (src/kernels.cpp:260-334) with rows of degree >= hub_threshold cut
+    into 2048-entry pieces whose f64 partials are summed in piece order;
+    f_tile 0 = 64.  AUTOSAGE_HUB_T / AUTOSAGE_FTILE override as in dispatch."""
+    if hub_threshold <= 0:
+        raise ValueError("spmm_csr_split: hub_threshold must be > 0")
+    variant = f"spmm:hubsplit:ft={f_tile if f_tile > 0 else 64}:rpc=1:vec={int(bool(vec))}:hubt={hub_threshold}"
+    return _spmm_impl(crow, col, val, b, variant)
+
+
+@spmm_csr_split.register_fake
+def _(crow, col, val, b, hub_threshold, f_tile, vec):
     return b.new_empty((crow.shape[0] - 1, b.shape[1]), dtype=torch.float32)
 
 
@@ -221,6 +245,29 @@ def sddmm_csr(crow: torch.Tensor, col: torch.Tensor, x: torch.Tensor, y: torch.T
                          C.c_void_p(y.data_ptr()), y.shape[0], x.shape[1],
                          C.c_void_p(out.data_ptr()) if out.numel() else None, _stream(x), None))
     return out
+
+
+@torch.library.custom_op("autosage::sddmm_csr_auto", mutates_args=())
+def sddmm_csr_auto(crow: torch.Tensor, col: torch.Tensor, x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
+    """sddmm_auto (src/scheduler.cpp:234-239; the paper's sddmm_csr_auto,
+    PAPER.md:286) with the process-wide schedule cache."""
+    _check_dense_pair("sddmm_csr_auto", crow, x, y)
+    x, y = x.contiguous().float(), y.contiguous().float()
+    g = _graph(crow, col, y.shape[0])
+    out = torch.empty(col.numel(), dtype=torch.float32, device=x.device)
+    cctx, keep = _ctx(x).to_c()
+    ccfg = ProbeConfig.from_env().to_c()
+    d = _c.as_decision()
+    _check(_lib.as_sddmm_auto(C.byref(cctx), C.byref(ccfg), g.handle, C.c_void_p(x.data_ptr()), x.shape[0],
+                              C.c_void_p(y.data_ptr()), y.shape[0], x.shape[1],
+                              C.c_void_p(out.data_ptr()) if out.numel() else None, C.byref(d)))
+    del keep
+    return out
+
+
+@sddmm_csr_auto.register_fake
+def _(crow, col, x, y):
+    return x.new_empty((col.shape[0],), dtype=torch.float32)
 
 
 def _check_dense_pair(name, crow, x, y):
@@ -417,13 +464,20 @@ def _spmm_setup_auto(ctx, inputs, output):
     ctx.n_extra = 0
 
 
+def _spmm_setup_split(ctx, inputs, output):
+    _spmm_setup(ctx, inputs, output)
+    ctx.n_extra = 3
+
+
 spmm_csr.register_autograd(_spmm_bwd, setup_context=_spmm_setup_v)
+spmm_csr_split.register_autograd(_spmm_bwd, setup_context=_spmm_setup_split)
 spmm_csr_auto.register_autograd(_spmm_bwd, setup_context=_spmm_setup_auto)
 
 
 def _sddmm_setup(ctx, inputs, output):
-    crow, col, x, y, _ = inputs
+    crow, col, x, y = inputs[:4]
     ctx.save_for_backward(crow, col, x, y)
+    ctx.n_extra = len(inputs) - 4
 
 
 def _sddmm_bwd(ctx, dout):
@@ -433,10 +487,11 @@ def _sddmm_bwd(ctx, dout):
         dx = _spmm_vals(_graph(crow, col, y.shape[0]), dout, y).to(x.dtype)
     if ctx.needs_input_grad[3]:
         dy = _spmm_t(crow, col, dout, y.shape[0], x).to(y.dtype)
-    return None, None, dx, dy, None
+    return (None, None, dx, dy) + (None,) * ctx.n_extra
 
 
 sddmm_csr.register_autograd(_sddmm_bwd, setup_context=_sddmm_setup)
+sddmm_csr_auto.register_autograd(_sddmm_bwd, setup_context=_sddmm_setup)
 
 
 def _attention_setup(ctx, inputs, output):

@@ -12,7 +12,7 @@ from tests.util import bit_equal, hub_graph, random_dense
 
 def test_ops_are_registered_with_fake_shapes():
     from torch._subclasses.fake_tensor import FakeTensorMode
-    for name in ("spmm_csr", "spmm_csr_auto", "sddmm_csr", "csr_attention"):
+    for name in ("spmm_csr", "spmm_csr_split", "spmm_csr_auto", "sddmm_csr", "sddmm_csr_auto", "csr_attention"):
         assert hasattr(torch.ops.autosage, name)
     with FakeTensorMode():
         crow = torch.empty(11, dtype=torch.int64)
@@ -21,6 +21,8 @@ def test_ops_are_registered_with_fake_shapes():
         b = torch.empty(7, 16)
         assert torch.ops.autosage.spmm_csr(crow, col, val, b, "").shape == (10, 16)
         assert torch.ops.autosage.sddmm_csr(crow, col, torch.empty(10, 16), b, "").shape == (30,)
+        assert torch.ops.autosage.spmm_csr_split(crow, col, val, b, 256, 64, True).shape == (10, 16)
+        assert torch.ops.autosage.sddmm_csr_auto(crow, col, torch.empty(10, 16), b).shape == (30,)
         assert torch.ops.autosage.csr_attention(crow, col, torch.empty(10, 16), b, torch.empty(7, 8),
                                                 False).shape == (10, 8)
 
@@ -49,6 +51,40 @@ def test_spmm_and_sddmm_ops_bit_exact():
     got = torch.ops.autosage.sddmm_csr(crow, col, torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(),
                                        "sddmm:rowparallel:ft=32:rpc=4:vec=1:hubt=256")
     assert bit_equal(got.cpu().numpy(), oracle.sddmm(a, x, y, 32, True))
+
+
+@pytest.mark.gpu
+def test_split_and_sddmm_auto_ops_bit_exact_with_grads():
+    """spmm_csr_split (the paper's split SpMM) and sddmm_csr_auto
+    (PAPER.md:286): forward bit-exact against the oracle at several hub
+    thresholds, and gradients through the same backward as spmm_csr /
+    sddmm_csr."""
+    rng = np.random.default_rng(64)
+    a = hub_graph(rng, 900, [850, 400, 300], 9)
+    crow, col, val = _csr(a)
+    b = random_dense(rng, 900, 48)
+    for hub_t, ft, vec in ((1, 64, True), (64, 32, False), (256, 0, True), (5000, 64, True)):
+        bt = torch.from_numpy(b).cuda().requires_grad_(True)
+        c = torch.ops.autosage.spmm_csr_split(crow, col, val, bt, hub_t, ft, vec)
+        assert bit_equal(c.detach().cpu().numpy(), oracle.spmm_hubsplit(a, b, hub_t)), (hub_t, ft, vec)
+        c.sum().backward()
+        ref = torch.from_numpy(b).cuda().requires_grad_(True)
+        torch.ops.autosage.spmm_csr(crow, col, val, ref, "").sum().backward()
+        assert bit_equal(bt.grad.cpu().numpy(), ref.grad.cpu().numpy()), hub_t
+    with pytest.raises(ValueError):
+        torch.ops.autosage.spmm_csr_split(crow, col, val, torch.from_numpy(b).cuda(), 0, 64, True)
+    x = torch.from_numpy(random_dense(rng, 900, 32)).cuda().requires_grad_(True)
+    y = torch.from_numpy(random_dense(rng, 900, 32)).cuda().requires_grad_(True)
+    s = torch.ops.autosage.sddmm_csr_auto(crow, col, x, y)
+    xs, ys = x.detach().cpu().numpy(), y.detach().cpu().numpy()
+    got = s.detach().cpu().numpy()
+    assert bit_equal(got, oracle.sddmm(a, xs, ys)) or any(
+        bit_equal(got, oracle.sddmm(a, xs, ys, ft, True)) for ft in (32, 64, 128))
+    s.sum().backward()
+    x2, y2 = (t.detach().clone().requires_grad_(True) for t in (x, y))
+    torch.ops.autosage.sddmm_csr(crow, col, x2, y2, "").sum().backward()
+    assert bit_equal(x.grad.cpu().numpy(), x2.grad.cpu().numpy())
+    assert bit_equal(y.grad.cpu().numpy(), y2.grad.cpu().numpy())
 
 
 @pytest.mark.gpu
