@@ -31,12 +31,13 @@ scores and probabilities (staged) rather than keeping them from the forward.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from collections import OrderedDict
 
 import torch
 
-from . import (Graph, ProbeConfig, ScheduleCache, ScheduleContext, _check, _lib, torch_stream_handle,
-               variant_from_string)
+from . import (Graph, ProbeConfig, ReplayPolicy, ScheduleCache, ScheduleContext, _check, _lib,
+               torch_stream_handle, variant_from_string)
 from . import _capi as _c
 
 _GRAPHS: "OrderedDict[tuple, _Entry]" = OrderedDict()
@@ -138,10 +139,30 @@ def _stream(t: torch.Tensor):
 
 
 def _ctx(t: torch.Tensor):
+    """The process-wide schedule context of the *_auto ops.  The paper's
+    toggles apply: AUTOSAGE_CACHE names a cache file loaded on
+    first use and rewritten whenever a decision is added (persistent replay
+    across processes; the same TSV as the reference's), and
+    AUTOSAGE_REPLAY_ONLY / AUTOSAGE_REPLAY_STRICT set the replay policy
+    (ReplayPolicy::from_env)."""
     global _CACHE
     if _CACHE is None:
         _CACHE = ScheduleCache()
-    return ScheduleContext(cache=_CACHE, stream=torch_stream_handle(t.device))
+        path = os.environ.get("AUTOSAGE_CACHE", "")
+        if path and os.path.exists(path):
+            _CACHE.load(path)
+    return ScheduleContext(cache=_CACHE, stream=torch_stream_handle(t.device), replay=ReplayPolicy.from_env())
+
+
+def _persist(n_before: int) -> None:
+    """Write the cache back to AUTOSAGE_CACHE when a decision was added."""
+    path = os.environ.get("AUTOSAGE_CACHE", "")
+    if path and _CACHE is not None and _CACHE.size() != n_before:
+        _CACHE.store(path)
+
+
+def _cache_size() -> int:
+    return _CACHE.size() if _CACHE is not None else 0
 
 
 @torch.library.custom_op("autosage::spmm_csr", mutates_args=())
@@ -207,6 +228,7 @@ def spmm_csr_auto(crow: torch.Tensor, col: torch.Tensor, val: torch.Tensor, b: t
     vals = _values(val, g.nnz)
     c = torch.empty((g.n_rows, b.shape[1]), dtype=torch.float32, device=b.device)
     cctx, keep = _ctx(b).to_c()
+    n0 = _cache_size()
     ccfg = ProbeConfig.from_env().to_c()
     d = _c.as_decision()
     if vals is None:
@@ -217,6 +239,7 @@ def spmm_csr_auto(crow: torch.Tensor, col: torch.Tensor, val: torch.Tensor, b: t
                                         C.c_void_p(b.data_ptr()), b.shape[0], b.shape[1],
                                         C.c_void_p(c.data_ptr()), C.byref(d)))
     del keep
+    _persist(n0)
     return c
 
 
@@ -256,12 +279,14 @@ def sddmm_csr_auto(crow: torch.Tensor, col: torch.Tensor, x: torch.Tensor, y: to
     g = _graph(crow, col, y.shape[0])
     out = torch.empty(col.numel(), dtype=torch.float32, device=x.device)
     cctx, keep = _ctx(x).to_c()
+    n0 = _cache_size()
     ccfg = ProbeConfig.from_env().to_c()
     d = _c.as_decision()
     _check(_lib.as_sddmm_auto(C.byref(cctx), C.byref(ccfg), g.handle, C.c_void_p(x.data_ptr()), x.shape[0],
                               C.c_void_p(y.data_ptr()), y.shape[0], x.shape[1],
                               C.c_void_p(out.data_ptr()) if out.numel() else None, C.byref(d)))
     del keep
+    _persist(n0)
     return out
 
 
@@ -298,6 +323,7 @@ def csr_attention(crow: torch.Tensor, col: torch.Tensor, q: torch.Tensor, k: tor
     g = _graph(crow, col, k.shape[0])
     out = torch.empty((g.n_rows, v.shape[1]), dtype=torch.float32, device=q.device)
     cctx, keep = _ctx(q).to_c()
+    n0 = _cache_size()
     ccfg = ProbeConfig.from_env().to_c()
     sd, pd = _c.as_decision(), _c.as_decision()
     _check(_lib.as_csr_attention_forward(C.byref(cctx), C.byref(ccfg), g.handle, C.c_void_p(q.data_ptr()),
@@ -306,6 +332,7 @@ def csr_attention(crow: torch.Tensor, col: torch.Tensor, q: torch.Tensor, k: tor
                                          C.c_void_p(out.data_ptr()), 1 if fused else 0, C.byref(sd),
                                          C.byref(pd)))
     del keep
+    _persist(n0)
     return out
 
 
@@ -535,6 +562,7 @@ def csr_attention_with_probs(crow: torch.Tensor, col: torch.Tensor, q: torch.Ten
     out = torch.empty((g.n_rows, v.shape[1]), dtype=torch.float32, device=q.device)
     p = torch.empty(col.numel(), dtype=torch.float32, device=q.device)
     cctx, keep = _ctx(q).to_c()
+    n0 = _cache_size()
     ccfg = ProbeConfig.from_env().to_c()
     sd, pd = _c.as_decision(), _c.as_decision()
     _check(_lib.as_csr_attention_forward_p(C.byref(cctx), C.byref(ccfg), g.handle, C.c_void_p(q.data_ptr()),
@@ -543,6 +571,7 @@ def csr_attention_with_probs(crow: torch.Tensor, col: torch.Tensor, q: torch.Ten
                                            C.c_void_p(out.data_ptr()), C.c_void_p(p.data_ptr()) if p.numel() else None,
                                            C.byref(sd), C.byref(pd)))
     del keep
+    _persist(n0)
     return out, p
 
 

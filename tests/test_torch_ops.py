@@ -176,3 +176,33 @@ def test_one_graph_from_two_streams_and_threads():
         t.join()
     for i in range(4):
         assert bit_equal(outs[i][0], want_s[i]) and bit_equal(outs[i][1], want_c[i]), i
+
+
+@pytest.mark.gpu
+def test_auto_ops_persist_and_replay_the_cache_file(monkeypatch, tmp_path):
+    """AUTOSAGE_CACHE: the *_auto ops load the cache file on
+    first use and rewrite it when they add a decision; a fresh process-wide
+    cache under AUTOSAGE_REPLAY_ONLY + STRICT then replays it without a probe,
+    with the same bits."""
+    import paper_2511_17594_b200.torch_ops as tops
+    rng = np.random.default_rng(65)
+    a = hub_graph(rng, 700, [650, 300], 8)
+    crow, col, val = _csr(a)
+    b = torch.from_numpy(random_dense(rng, 700, 32)).cuda()
+    path = tmp_path / "autosage.cache"
+    monkeypatch.setenv("AUTOSAGE_CACHE", str(path))
+    monkeypatch.setattr(tops, "_CACHE", None)
+    first = torch.ops.autosage.spmm_csr_auto(crow, col, val, b).cpu().numpy()
+    lines = path.read_text().strip().splitlines()
+    assert len(lines) == 1 and "spmm" in lines[0]
+    monkeypatch.setattr(tops, "_CACHE", None)
+    monkeypatch.setenv("AUTOSAGE_REPLAY_ONLY", "1")
+    monkeypatch.setenv("AUTOSAGE_REPLAY_STRICT", "1")
+    asb.reset_probe_launch_count()
+    again = torch.ops.autosage.spmm_csr_auto(crow, col, val, b).cpu().numpy()
+    assert asb.probe_launch_count() == 0
+    assert bit_equal(first, again)
+    x = torch.from_numpy(random_dense(rng, 700, 16)).cuda()
+    with pytest.raises(asb.ReplayMiss):  # no SDDMM decision in the file, strict replay
+        torch.ops.autosage.sddmm_csr_auto(crow, col, x, b[:, :16].contiguous())
+    monkeypatch.setattr(tops, "_CACHE", None)
