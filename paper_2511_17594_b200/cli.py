@@ -72,6 +72,25 @@ def env_snapshot() -> dict:
     return {k: v for k, v in sorted(os.environ.items()) if k.startswith("AUTOSAGE_")}
 
 
+def versions() -> dict:
+    """The paper's sidecar extras: Torch / CUDA versions and the
+    GPU's SM architecture, beside the reference's fields."""
+    import platform
+    out = {"python": platform.python_version()}
+    try:
+        import torch
+        out["torch"] = torch.__version__
+        out["cuda_runtime"] = torch.version.cuda
+        if torch.cuda.is_available():
+            p = torch.cuda.get_device_properties(torch.cuda.current_device())
+            out["gpu"] = p.name
+            out["sm"] = f"sm_{p.major}{p.minor}"
+            out["sms"] = p.multi_processor_count
+    except Exception:  # noqa: BLE001 -- the sidecar is best-effort metadata
+        pass
+    return out
+
+
 def write_sidecar(csv_path: str, command: str, dp: asb.DeviceProfile, config: dict) -> None:
     """autosage_bench.cpp:144-164."""
     meta = {"artifact_version": dp.device_sig.rsplit("|", 1)[-1],
@@ -79,7 +98,7 @@ def write_sidecar(csv_path: str, command: str, dp: asb.DeviceProfile, config: di
             "timestamp_unix": int(time.time()),
             "device": {"device_sig": dp.device_sig, "bw_eff_bytes_per_s": dp.bw_eff,
                        "flops_eff_per_s": dp.flops_eff, "cores": dp.cores},
-            "config": config, "env": env_snapshot()}
+            "config": config, "env": env_snapshot(), "versions": versions()}
     path = csv_path + ".meta.json"
     try:
         with open(path, "w") as fh:

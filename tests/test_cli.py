@@ -58,6 +58,7 @@ def test_bench_sweep_ablate_attention_replay(tmp_path, monkeypatch):
     meta = json.load(open(out + ".meta.json"))
     assert meta["command"] == "bench" and meta["config"]["f_list"] == [32, 64]
     assert meta["device"]["device_sig"].startswith("NVIDIA") and "probe" in meta["config"]
+    assert meta["versions"]["sm"].startswith("sm_") and meta["versions"]["torch"]
 
     out = str(tmp_path / "sddmm.csv")
     assert cli.main(["bench", "--graph", g, "--op", "sddmm", "--f", "64", "--iters", "3",
