@@ -287,11 +287,23 @@ void check_sddmm_dims(const Graph& p, std::uint64_t x_rows, std::uint64_t y_rows
 // 5.25 ms, F=256 11.72 -> 10.58 ms, Products 11.98 -> 11.85 ms with it,
 // scan included; profiles/r02o_mix_scan.md).  AUTOSAGE_DEV_MIX_SCAN_MB
 // (MiB) overrides both caps (A/B knob).
+// Small products skip it too: the scan is a separate ~10 us launch in front
+// of a latency-bound op whose XU is not the limit -- c1 (1.6M nnz x 64)
+// SpMM 0.080 -> 0.066 ms, SDDMM 0.105 -> 0.095 ms without it
+// (profiles/r02aj_small_scan.md).  Rule: scan only when the op multiplies at
+// least 2^28 entry-features (nnz x F); AUTOSAGE_DEV_MIX_MIN_WORK overrides.
 const unsigned* mix_flag(Graph& g, const float* p, std::uint64_t n, cudaStream_t s, bool sddmm = false) {
     const auto knob = env::get_int("AUTOSAGE_DEV_MIX_SCAN_MB");
     const std::uint64_t dflt = sddmm ? ~0ull : std::uint64_t(128) << 20;
     const std::uint64_t max_bytes = knob && *knob >= 0 ? std::uint64_t(*knob) << 20 : dflt;
     if (n * 4 > max_bytes) return nullptr;
+    {
+        const auto w = env::get_int("AUTOSAGE_DEV_MIX_MIN_WORK");
+        const std::uint64_t min_work = w && *w >= 0 ? std::uint64_t(*w) : (std::uint64_t(1) << 28);
+        const std::uint64_t nnz = g.plan_nnz ? g.plan_nnz : g.nnz;
+        const std::uint64_t f = n / std::max<std::uint64_t>(g.n_cols, 1);
+        if (nnz * f < min_work) return nullptr;
+    }
     if (g.flag_frozen) return g.flag.get();
     return finite_flag(g, p, n, s);
 }

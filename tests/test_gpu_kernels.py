@@ -280,6 +280,30 @@ def test_sddmm_pass_major_bit_exact(monkeypatch, force):
                 assert bit_equal(np.nan_to_num(got), np.nan_to_num(want)), (f, vec, ft)
 
 
+def test_small_work_scan_rule_keeps_bits(monkeypatch):
+    """The default skips the finite scan (and the ALU re-bias widening) for
+    ops under 2^28 entry-features; forcing the scan gives the same bits for
+    SpMM (every mapping) and SDDMM (both orders)."""
+    rng = np.random.default_rng(51)
+    a = hub_graph(rng, 3000, [2900, 1200, 300], 12)
+    g = asb.Graph.from_csr(a)
+    b, x = random_dense(rng, 3000, 64), random_dense(rng, 3000, 64)
+    outs = []
+    for knob in ("0", None):
+        if knob is None:
+            monkeypatch.delenv("AUTOSAGE_DEV_MIX_MIN_WORK")
+        else:
+            monkeypatch.setenv("AUTOSAGE_DEV_MIX_MIN_WORK", knob)
+        r = [asb.dispatch(V(SP, m, ft, 4, True, 256), g, cuda(b)).output.cpu().numpy()
+             for m, ft in ((RP, 64), (HS, 64), (HS, 32))]
+        r += [asb.dispatch(V(SD, RP, 32, 1, vec), g, cuda(x), cuda(b)).values.cpu().numpy() for vec in (False, True)]
+        outs.append(r)
+    for u, v in zip(*outs):
+        assert bit_equal(u, v)
+    assert bit_equal(outs[1][0], oracle.spmm_baseline(a, b))
+    g.close()
+
+
 def test_sddmm_chunks_spanning_many_rows():
     """Degree-0/1/2 rows: one 32-entry chunk meets more than 32 rows."""
     rng = np.random.default_rng(44)
