@@ -129,6 +129,7 @@ unsigned grid_for(std::uint64_t n, unsigned block, unsigned cap = 0) {
 } // namespace
 
 Graph::~Graph() {
+    if (sig_future.valid()) sig_future.wait();  // the background hash reads colind
     if (stream) {
         cudaStreamSynchronize(stream);
         cudaStreamDestroy(stream);
@@ -225,6 +226,7 @@ std::unique_ptr<Graph> graph_create_host(const std::uint64_t* rowptr, const std:
             ASB_CUDA(cudaMemcpyAsync(g->val.get(), val, nnz * 4, cudaMemcpyHostToDevice, g->stream));
     }
     ASB_CUDA(cudaStreamSynchronize(g->stream));
+    start_sig(*g);
     return g;
 }
 
@@ -271,6 +273,7 @@ std::unique_ptr<Graph> graph_create_device(const std::uint64_t* rowptr, const st
         if (hb & 1u) throw InvalidArgument("graph: column index >= n_cols");
         if (hb & 2u) throw InvalidArgument("graph: columns not strictly increasing within a row");
     }
+    start_sig(*g);
     return g;
 }
 
@@ -329,12 +332,10 @@ int kernel_setup(const void* kernel, std::size_t smem, int threads) {
     return per_sm;
 }
 
-// graph_sig (src/cache.cpp:66-74), memoized.  colind streams down in chunks
-// while the previous chunk is hashed (FNV-1a is inherently serial).
-std::uint64_t graph_sig(Graph& g) {
-    std::lock_guard<std::mutex> lk(g.mu);
-    if (g.sig) return *g.sig;
-    DeviceGuard dg(g.device);
+// graph_sig (src/cache.cpp:66-74).  colind streams down in chunks on `s`
+// while the previous chunk is hashed (FNV-1a is inherently serial).  Reads
+// only what never changes after creation (sizes, h_rowptr, colind).
+static std::uint64_t compute_sig(const Graph& g, cudaStream_t s) {
     std::uint64_t h = kFnvOffset;
     h = fnv1a(h, &g.n_rows, 8);
     h = fnv1a(h, &g.n_cols, 8);
@@ -352,8 +353,8 @@ std::uint64_t graph_sig(Graph& g) {
         auto issue = [&](std::uint64_t k) {
             const std::uint64_t off = k * chunk, len = std::min(chunk, g.nnz - off);
             ASB_CUDA(cudaMemcpyAsync(pinned[k & 1], g.colind.get() + off, len * 4,
-                                     cudaMemcpyDeviceToHost, g.stream));
-            ASB_CUDA(cudaEventRecord(ev[k & 1], g.stream));
+                                     cudaMemcpyDeviceToHost, s));
+            ASB_CUDA(cudaEventRecord(ev[k & 1], s));
         };
         issue(0);
         for (std::uint64_t k = 0; k < n_chunks; ++k) {
@@ -367,8 +368,39 @@ std::uint64_t graph_sig(Graph& g) {
         cudaFreeHost(pinned[0]);
         cudaFreeHost(pinned[1]);
     }
-    g.sig = h;
     return h;
+}
+
+// memoized; waits for the background computation when one was started
+std::uint64_t graph_sig(Graph& g) {
+    std::lock_guard<std::mutex> lk(g.mu);
+    if (g.sig) return *g.sig;
+    DeviceGuard dg(g.device);
+    if (g.sig_future.valid()) {
+        g.sig = g.sig_future.get();  // rethrows a failure of the background pass
+        return *g.sig;
+    }
+    g.sig = compute_sig(g, g.stream);
+    return *g.sig;
+}
+
+// Start graph_sig in the background at creation (graphs of >= 1M entries;
+// AUTOSAGE_EAGER_SIG=0 turns it off): the first decide then finds the key
+// ready instead of spending ~0.5 s per 460 MB of colind on it.
+void start_sig(Graph& g) {
+    const auto knob = env::get_int("AUTOSAGE_EAGER_SIG");
+    if ((knob && *knob == 0) || g.nnz < (1u << 20)) return;
+    Graph* gp = &g;
+    g.sig_future = std::async(std::launch::async, [gp] {
+        ASB_CUDA(cudaSetDevice(gp->device));
+        cudaStream_t s = nullptr;
+        ASB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        struct StreamGuard {
+            cudaStream_t s;
+            ~StreamGuard() { cudaStreamDestroy(s); }
+        } sg{s};
+        return compute_sig(*gp, s);
+    });
 }
 
 // Stable sort of rows by degree, descending (std::stable_sort with

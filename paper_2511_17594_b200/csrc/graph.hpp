@@ -13,6 +13,7 @@
 
 #include "internal.hpp"
 
+#include <future>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -91,6 +92,9 @@ struct Graph {
 
     std::mutex mu;
     std::optional<std::uint64_t> sig;
+    // graph_sig computed in the background from creation on (FNV-1a is a
+    // serial ~1 GB/s pass over rowptr + colind); graph_sig() waits for it
+    std::future<std::uint64_t> sig_future;
     bool order_ready = false;
     DevBuf<std::uint32_t> order;       // degree-descending stable row order
     DevBuf<std::uint32_t> sorted_deg;  // degrees in that order
@@ -205,6 +209,7 @@ std::unique_ptr<Graph> graph_create_device(const std::uint64_t* rowptr, const st
 cudaStream_t resolve_stream(Graph& g, void* stream);
 
 std::uint64_t graph_sig(Graph& g);
+void start_sig(Graph& g);  // background graph_sig at creation (graph.cu)
 // number of rows with degree >= d (host count from the rowptr mirror, cached)
 std::uint64_t rows_with_degree_at_least(Graph& g, std::uint64_t d);
 // fork: returns the graph's aux stream ordered after `s`; join: `s` waits

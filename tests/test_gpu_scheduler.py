@@ -381,3 +381,24 @@ def test_gpu_model_probe_sample_fills_the_device(monkeypatch):
     ref = asb.DeviceProfile(gpu.device_sig, gpu.bw_eff, gpu.flops_eff, gpu.cores, 0)
     d0 = asb.decide_spmm(a, b, cfg, asb.ScheduleContext(device=ref))
     assert d0.sample_rows == max(64, math.ceil(0.02 * a.n_rows))
+
+
+@pytest.mark.parametrize("eager", ["1", "0"])
+def test_background_graph_sig_matches_oracle(monkeypatch, eager):
+    """graph_sig starts in the background at creation for graphs of >= 1M
+    entries (AUTOSAGE_EAGER_SIG=0: computed on first use); either way the key
+    is the reference's FNV-1a, for host- and device-created graphs, and a
+    graph closed before its hash finished is torn down cleanly."""
+    import torch
+    monkeypatch.setenv("AUTOSAGE_EAGER_SIG", eager)
+    m = asb.gen_powerlaw(60_000, 60_000, 1_500_000, 2.2, 4, 5_000, 9)
+    want = oracle.graph_sig(m)
+    g = asb.Graph.from_csr(m)
+    assert g.sig() == want
+    g.close()
+    asb.Graph.from_csr(m).close()  # destroyed while the background pass may still run
+    import paper_2511_17594_b200.torch_ops as tops
+    crow = torch.from_numpy(m.rowptr.astype(np.int64)).cuda()
+    col = torch.from_numpy(m.colind.astype(np.int32)).cuda()
+    gd = tops._graph(crow, col, m.n_cols)
+    assert gd.sig() == want
