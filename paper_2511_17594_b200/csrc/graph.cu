@@ -335,6 +335,42 @@ int kernel_setup(const void* kernel, std::size_t smem, int threads) {
 // graph_sig (src/cache.cpp:66-74).  colind streams down in chunks on `s`
 // while the previous chunk is hashed (FNV-1a is inherently serial).  Reads
 // only what never changes after creation (sizes, h_rowptr, colind).
+// Pinned staging buffers of compute_sig, kept for the process: cudaMallocHost
+// and cudaFreeHost synchronise with the device, which a hash running in the
+// background must not do to the caller's streams on every graph.
+namespace {
+constexpr std::uint64_t kSigChunk = 8u << 20;  // elements per staging buffer
+// never destroyed: a background hash may still return its buffers while the
+// process tears down its statics
+struct SigPool {
+    std::mutex mu;
+    std::vector<std::uint32_t*> free;
+};
+SigPool& sig_pool() {
+    static SigPool* pool = new SigPool;
+    return *pool;
+}
+
+std::uint32_t* sig_buf_acquire() {
+    {
+        std::lock_guard<std::mutex> lk(sig_pool().mu);
+        if (!sig_pool().free.empty()) {
+            std::uint32_t* p = sig_pool().free.back();
+            sig_pool().free.pop_back();
+            return p;
+        }
+    }
+    std::uint32_t* p = nullptr;
+    ASB_CUDA(cudaMallocHost(&p, kSigChunk * 4));
+    return p;
+}
+
+void sig_buf_release(std::uint32_t* p) {
+    std::lock_guard<std::mutex> lk(sig_pool().mu);
+    sig_pool().free.push_back(p);
+}
+}  // namespace
+
 static std::uint64_t compute_sig(const Graph& g, cudaStream_t s) {
     std::uint64_t h = kFnvOffset;
     h = fnv1a(h, &g.n_rows, 8);
@@ -342,10 +378,17 @@ static std::uint64_t compute_sig(const Graph& g, cudaStream_t s) {
     h = fnv1a(h, &g.nnz, 8);
     h = fnv1a(h, g.h_rowptr.data(), (g.n_rows + 1) * 8);
     if (g.nnz) {
-        const std::uint64_t chunk = 8u << 20;  // elements
-        std::uint32_t* pinned[2] = {nullptr, nullptr};
-        ASB_CUDA(cudaMallocHost(&pinned[0], chunk * 4));
-        ASB_CUDA(cudaMallocHost(&pinned[1], chunk * 4));
+        const std::uint64_t chunk = kSigChunk;
+        struct Bufs {
+            std::uint32_t* p[2] = {nullptr, nullptr};
+            ~Bufs() {
+                for (auto* q : p)
+                    if (q) sig_buf_release(q);
+            }
+        } bufs;
+        bufs.p[0] = sig_buf_acquire();
+        bufs.p[1] = sig_buf_acquire();
+        std::uint32_t* const* pinned = bufs.p;
         cudaEvent_t ev[2];
         ASB_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
         ASB_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
@@ -365,8 +408,6 @@ static std::uint64_t compute_sig(const Graph& g, cudaStream_t s) {
         }
         cudaEventDestroy(ev[0]);
         cudaEventDestroy(ev[1]);
-        cudaFreeHost(pinned[0]);
-        cudaFreeHost(pinned[1]);
     }
     return h;
 }
