@@ -403,6 +403,21 @@ as_status as_csr_attention_forward(const as_context* ctx, const as_probe_config*
                                    int fused, as_decision* sddmm_decision,
                                    as_decision* spmm_decision);
 
+/* Batched heads (the optional batched-heads variant of
+ * csr_attention_forward): n_heads independent heads on one pattern, head h
+ * reading q_devs[h], k_devs[h], v_devs[h] and writing out_devs[h] (same
+ * shapes as above for every head), in head order on one stream.  Every head
+ * decides under the same keys as the single-head call (src/attention.cpp:
+ * 21-38: head 1 probes, the rest hit the cache); without a cache in ctx a
+ * cache local to the call plays that role.  Decisions: those of the last
+ * head.  Each head's out equals the single-head call's bit for bit. */
+as_status as_csr_attention_forward_heads(const as_context* ctx, const as_probe_config* cfg,
+                                         as_graph pattern, uint32_t n_heads, const float* const* q_devs,
+                                         uint64_t q_rows, const float* const* k_devs, uint64_t k_rows,
+                                         const float* const* v_devs, uint64_t v_rows, uint64_t f,
+                                         uint64_t fv, float* const* out_devs, int fused,
+                                         as_decision* sddmm_decision, as_decision* spmm_decision);
+
 /* The staged pipeline with the probabilities p = row_softmax(SDDMM(q, k))
  * also written to p_dev (nnz floats, device): the training forward keeps p
  * for the backward instead of recomputing it (new).  out is

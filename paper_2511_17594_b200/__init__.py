@@ -1071,6 +1071,37 @@ def csr_attention_forward(pattern, q, k, v, cfg: Optional[ProbeConfig] = None,
     return attention_probe_breakdown(pattern, q, k, v, cfg, ctx, fused).output
 
 
+def csr_attention_forward_heads(pattern: "Graph", qs, ks, vs, cfg: Optional[ProbeConfig] = None,
+                                ctx: Optional[ScheduleContext] = None, fused: bool = True):
+    """Several heads on one device pattern graph in one call
+    (as_csr_attention_forward_heads): head 1 decides, the rest reuse its
+    decisions (a call-local cache when ctx has none).  qs / ks / vs: lists of
+    CUDA float32 tensors (n_rows x F, n_cols x F, n_cols x Fv); returns the
+    list of n_rows x Fv outputs, each equal to the single-head call."""
+    import torch
+    h = len(qs)
+    if not (len(ks) == h and len(vs) == h):
+        raise InvalidArgument("attention_heads: q, k, v head counts differ")
+    cfg = cfg or ProbeConfig()
+    ctx = ctx or ScheduleContext()
+    qs, ks, vs = ([t.contiguous().float() for t in seq] for seq in (qs, ks, vs))
+    f = int(qs[0].shape[1]) if h else 0
+    fv = int(vs[0].shape[1]) if h else 0
+    outs = [torch.empty((pattern.n_rows, fv), dtype=torch.float32, device=qs[0].device) for _ in range(h)]
+    arr = lambda ts: (C.c_void_p * max(h, 1))(*[t.data_ptr() for t in ts])  # noqa: E731
+    if ctx.stream is None and h:
+        ctx = dataclasses.replace(ctx, stream=torch_stream_handle(qs[0].device))
+    cctx, keep = ctx.to_c()
+    ccfg = cfg.to_c()
+    sd, pd = _c.as_decision(), _c.as_decision()
+    _check(_lib.as_csr_attention_forward_heads(
+        C.byref(cctx), C.byref(ccfg), pattern.handle, h, arr(qs), int(qs[0].shape[0]) if h else 0, arr(ks),
+        int(ks[0].shape[0]) if h else 0, arr(vs), int(vs[0].shape[0]) if h else 0, f, fv, arr(outs), int(fused),
+        C.byref(sd), C.byref(pd)))
+    del keep
+    return outs
+
+
 # ---- multi-GPU partition, synthetic inputs, I/O -------------------------------------------
 class BlockedSpmm:
     """Column-blocked SpMM plan (as_spmm_blocked_*): C = A B consumed one

@@ -187,6 +187,8 @@ _proto("as_decide_host", st, P(as_context), P(as_probe_config), u64, P(as_featur
        C.c_int, u64, P(as_decision))
 _proto("as_csr_attention_forward", st, P(as_context), P(as_probe_config), vp, vp, u64, vp, u64,
        vp, u64, u64, u64, vp, C.c_int, P(as_decision), P(as_decision))
+_proto("as_csr_attention_forward_heads", st, P(as_context), P(as_probe_config), vp, u32, vp, u64, vp, u64,
+       vp, u64, u64, u64, vp, C.c_int, P(as_decision), P(as_decision))
 _proto("as_csr_attention_forward_p", st, P(as_context), P(as_probe_config), vp, vp, u64, vp, u64,
        vp, u64, u64, u64, vp, vp, P(as_decision), P(as_decision))
 _proto("as_partition_rows", st, vp, u64, u32, vp)
@@ -239,5 +241,5 @@ EXPORTED = [
     "as_permute_values", "as_spmm_values", "as_row_softmax_backward", "as_spmm_bf16",
     "as_sddmm_bf16", "as_spmm_transpose_values", "as_csr_attention_forward_p", "as_spmm_auto_values",
     "as_spmm_blocked_create", "as_spmm_blocked_run", "as_spmm_blocked_destroy", "as_spmm_f16", "as_sddmm_f16",
-    "as_csr_attention_half",
+    "as_csr_attention_half", "as_csr_attention_forward_heads",
 ]

@@ -683,6 +683,26 @@ as_status as_csr_attention_forward(const as_context* ctx, const as_probe_config*
     });
 }
 
+as_status as_csr_attention_forward_heads(const as_context* ctx, const as_probe_config* cfg, as_graph pattern,
+                                         uint32_t n_heads, const float* const* q_devs, uint64_t q_rows,
+                                         const float* const* k_devs, uint64_t k_rows, const float* const* v_devs,
+                                         uint64_t v_rows, uint64_t f, uint64_t fv, float* const* out_devs, int fused,
+                                         as_decision* sd, as_decision* pd) {
+    return guard([&] {
+        if (n_heads && (!q_devs || !k_devs || !v_devs || !out_devs))
+            throw InvalidArgument("attention_heads: null head array");
+        Context c = make_ctx(ctx);
+        ScheduleCache local;  // heads 2..n replay head 1's decisions
+        if (!c.cache) c.cache = &local;
+        Graph& g = G(pattern);
+        GraphUse use(g, c.stream ? c.stream : g.stream);
+        const as_probe_config pc = cfg_or_default(cfg);
+        for (std::uint32_t h = 0; h < n_heads; ++h)
+            attention_forward(c, pc, g, q_devs[h], q_rows, k_devs[h], k_rows, v_devs[h], v_rows, f, fv,
+                              out_devs[h], fused != 0, sd, pd);
+    });
+}
+
 as_status as_csr_attention_forward_p(const as_context* ctx, const as_probe_config* cfg, as_graph pattern,
                                      const float* q_dev, uint64_t q_rows, const float* k_dev, uint64_t k_rows,
                                      const float* v_dev, uint64_t v_rows, uint64_t f, uint64_t fv, float* out_dev,

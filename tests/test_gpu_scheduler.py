@@ -402,3 +402,29 @@ def test_background_graph_sig_matches_oracle(monkeypatch, eager):
     col = torch.from_numpy(m.colind.astype(np.int32)).cuda()
     gd = tops._graph(crow, col, m.n_cols)
     assert gd.sig() == want
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_attention_heads_batched_equals_single_calls(fused):
+    """as_csr_attention_forward_heads: each head bit-identical to the
+    single-head call; decisions made once (head 1) from a call-local cache."""
+    import torch
+    rng = np.random.default_rng(77)
+    m = hub_graph(rng, 1200, [1100, 500], 9, with_values=False)
+    g = asb.Graph.from_csr(m)
+    heads = 4
+    qs = [torch.from_numpy(rng.uniform(-1, 1, (1200, 32)).astype(np.float32)).cuda() for _ in range(heads)]
+    ks = [torch.from_numpy(rng.uniform(-1, 1, (1200, 32)).astype(np.float32)).cuda() for _ in range(heads)]
+    vs = [torch.from_numpy(rng.uniform(-1, 1, (1200, 16)).astype(np.float32)).cuda() for _ in range(heads)]
+    asb.reset_probe_launch_count()
+    outs = asb.csr_attention_forward_heads(g, qs, ks, vs, fused=fused)
+    torch.cuda.synchronize()
+    batched_probes = asb.probe_launch_count()
+    ctx = asb.ScheduleContext(cache=asb.ScheduleCache())
+    asb.reset_probe_launch_count()
+    for h in range(heads):
+        one = asb.csr_attention_forward(g, qs[h], ks[h], vs[h], ctx=ctx, fused=fused)
+        one = one.cpu().numpy() if hasattr(one, "cpu") else one
+        assert bit_equal(outs[h].cpu().numpy(), one), h
+    assert batched_probes == asb.probe_launch_count() > 0  # one decide per op, as the cached single calls
+    g.close()
