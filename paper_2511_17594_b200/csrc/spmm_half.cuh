@@ -43,12 +43,20 @@ void launch_seg_half_t(int vec, int lpr, int nch, const SegArgs& a, bool has_val
             if constexpr (VEC == 8 && NCH == 8) {
                 throw LogicError("8-wide tiles take at most 4 chunks per lane");
             } else {
-                constexpr int U = unroll_for(VEC, NCH), R = maxreg_for(VEC, NCH);
+                // register caps: the 16-bit -> f32 step needs more live registers
+                // than the f32 kernels' caps leave in the scalar tiles (they
+                // spilled 24-160 B at 64).  Softmax mode keeps the f32 caps: 16
+                // more registers there cost the fused 16-bit attention 4%
+                // (occupancy), more than its small spills do.
+                constexpr int U = unroll_for(VEC, NCH);
+                constexpr int R0 = maxreg_for(VEC, NCH);
+                constexpr int R = VEC == 1 && R0 < 96 ? 96 : R0;
+                constexpr int RS = R;
                 const std::size_t sm = seg_smem(nt);
                 if (a.rmax) {  // softmax mode (fused attention over 16-bit V): values are raw scores
                     if (!has_val) throw LogicError("spmm softmax mode needs the score values");
-                    if (pieces) spmm_seg_kernel<VEC, LPR, NCH, true, true, U, R, true, WT><<<nb, nt, sm, s>>>(a);
-                    else spmm_seg_kernel<VEC, LPR, NCH, true, false, U, R, true, WT><<<nb, nt, sm, s>>>(a);
+                    if (pieces) spmm_seg_kernel<VEC, LPR, NCH, true, true, U, RS, true, WT><<<nb, nt, sm, s>>>(a);
+                    else spmm_seg_kernel<VEC, LPR, NCH, true, false, U, RS, true, WT><<<nb, nt, sm, s>>>(a);
                 } else if (has_val) {
                     if (pieces) spmm_seg_kernel<VEC, LPR, NCH, true, true, U, R, false, WT><<<nb, nt, sm, s>>>(a);
                     else spmm_seg_kernel<VEC, LPR, NCH, true, false, U, R, false, WT><<<nb, nt, sm, s>>>(a);
