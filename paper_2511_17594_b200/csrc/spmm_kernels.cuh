@@ -125,7 +125,12 @@ __device__ __forceinline__ float comp(const uint4& w, int q) {
 // ops (its low mantissa word is zero), so bf16 loads put 3/4 on the ALU (an
 // f16 word is first converted to f32, then split like f32)
 template <int VEC, int WT>
-__host__ __device__ constexpr int mix_from() { return VEC == 1 ? 0 : (WT == kWtBF16 ? VEC / 4 : 2); }
+#ifndef ASB_SEG_MIX_FROM
+#define ASB_SEG_MIX_FROM 2  // f32 float4 tiles: components [MIX_FROM, 4) re-biased on the ALU (A/B build knob)
+#endif
+__host__ __device__ constexpr int mix_from() {
+    return VEC == 1 ? 0 : (WT == kWtBF16 ? VEC / 4 : (WT == kWtF32 ? ASB_SEG_MIX_FROM : 2));
+}
 
 template <int VEC, int NCH, int MIX, class VT, int MQ = mix_from<VEC, kWtF32>(), int WT = kWtF32>
 __device__ __forceinline__ void seg_accumulate(double (&acc)[NCH][VEC], double v, const VT (&bv)[NCH]) {
