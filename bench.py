@@ -253,6 +253,39 @@ class RefWorkload:
             return o.ref_sddmm_baseline(self.rg, self.rx, self.ry)
         return o.ref_sddmm_dispatch(choice, self.rg, self.rx, self.ry, 0)
 
+    def serial_baseline(self, every: int = 64):
+        """the reference's serial guardrail kernels
+        (spmm_baseline / sddmm_baseline, src/kernels.cpp:210-228, :336-355;
+        what its bench reports as baseline_ms) on rows i % every == 0 of the
+        same graph (columns, B and Y untouched), one warm-up + one timed run,
+        scaled to the full graph by nnz.  None for the port."""
+        if self.kind != "reference":
+            return None
+        o, m = self.oracle, self.m
+        rows = np.arange(0, m.n_rows, every, dtype=np.int64)
+        rp = m.rowptr.astype(np.int64)
+        deg = rp[rows + 1] - rp[rows]
+        sub_rp = np.zeros(rows.size + 1, np.uint64)
+        sub_rp[1:] = np.cumsum(deg)
+        idx = np.concatenate([np.arange(rp[r], rp[r + 1]) for r in rows]) if deg.sum() else np.zeros(0, np.int64)
+        sub = o.HostCsr(rows.size, m.n_cols, sub_rp, m.colind[idx], None if m.val is None else m.val[idx])
+        if sub.nnz == 0:
+            return None
+        _, x, _ = dense_inputs(o.fill_uniform, m, self.f, 1)
+        rg, rx = o.RefGraph(sub), o.RefDense(np.ascontiguousarray(x[rows]))
+        o.ref_spmm_baseline(rg, self.rb)
+        o.ref_sddmm_baseline(rg, rx, self.ry)
+        t0 = time.perf_counter()
+        o.ref_spmm_baseline(rg, self.rb)
+        t1 = time.perf_counter()
+        o.ref_sddmm_baseline(rg, rx, self.ry)
+        t2 = time.perf_counter()
+        scale = m.nnz / sub.nnz
+        return {"spmm_ms": (t1 - t0) * 1e3 * scale, "sddmm_ms": (t2 - t1) * 1e3 * scale,
+                "ms_per_step": (t2 - t0) * 1e3 * scale, "cores": 1,
+                "sample": f"rows i % {every} == 0 ({rows.size} rows, {sub.nnz} nnz), one warm-up + one timed "
+                          f"run of spmm_baseline + sddmm_baseline, scaled by nnz x{scale:.1f}"}
+
     def time_steps(self, spmm_choice, sddmm_choice, steps, warmup):
         for _ in range(warmup):
             self.spmm(spmm_choice)
@@ -282,6 +315,10 @@ def cpu_reference_run(m, f, seed, steps, warmup, cfg_name):
            "sample": sample, "ms_per_step": mean_s * 1e3,
            "ms_per_step_median": statistics.median(times) * 1e3,
            "choices": {"spmm": spmm_choice, "sddmm": sddmm_choice}, "decide_ms": decide_ms}
+    ser = w.serial_baseline()
+    if ser:
+        ser["gbs"] = step_bytes / (ser["ms_per_step"] * 1e-3) / 1e9
+        res["serial_baseline"] = ser
     return res, w
 
 
@@ -324,6 +361,8 @@ def run_reference_arm(args):
         "choices": cpu["choices"], "decide_ms": cpu["decide_ms"],
         "ms_per_step_median": cpu["ms_per_step_median"],
     }
+    if "serial_baseline" in cpu:  # the reference's own guardrail baseline
+        line["serial_baseline"] = cpu["serial_baseline"]
     print(json.dumps(line), flush=True)
 
 
