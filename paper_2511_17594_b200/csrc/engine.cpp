@@ -171,7 +171,10 @@ as_decision decide_common(const Context& ctx, const as_probe_config& cfg,
     const as_features gf = hooks.features();
     d.features_ms = ms_since(t_phase);
     auto candidates = shortlist(gf, f, op, dp);
-    if (dp.model == AS_MODEL_B200) candidates = distinct_gpu_configs(candidates, f);
+    if (dp.model == AS_MODEL_B200) {
+        l2_tile_rule(candidates, f, gf.n_cols);
+        candidates = distinct_gpu_configs(candidates, f);
+    }
     if (candidates.size() > std::size_t(cfg.top_k)) candidates.resize(std::size_t(cfg.top_k));
     t_phase = clk::now();
     const std::uint64_t sample_rows = hooks.prepare ? hooks.prepare() : 0;

@@ -332,6 +332,21 @@ std::vector<as_variant> distinct_gpu_configs(const std::vector<as_variant>& rank
     return out;
 }
 
+// B200, SpMM at F > 64: the lane-group kernels walk feature tiles
+// tile-major, so with 64-wide tiles only a 64-column slice of B is live at a
+// time and it stays in the L2 where the whole B does not.  A probe sample
+// never fills the L2, so it cannot see this and ranks wider tiles first (one
+// colind pass fewer).  Where B is over the L2 budget and a 64-column slice is
+// within it, every SpMM candidate therefore takes f_tile 64 (all f_tiles give
+// the same bits).  Reddit-shape: F=128 3.49 ms at ft 64 vs 3.93 at ft 128,
+// F=192 6.44 vs 8.21, F=256 8.60 vs 8.65 (profiles/r02at_ftile.md).
+void l2_tile_rule(std::vector<as_variant>& cands, std::uint64_t f, std::uint64_t n_cols) {
+    constexpr std::uint64_t kL2Budget = std::uint64_t(96) << 20;  // l2hint.cuh kKeepMaxBytes
+    if (f <= 64 || n_cols * f * 4 <= kL2Budget || n_cols * 64 * 4 > kL2Budget) return;
+    for (auto& v : cands)
+        if (v.op == AS_OP_SPMM && v.mapping != AS_MAP_BASELINE) v.f_tile = 64;
+}
+
 // ---- time_kernel, src/timing.cpp:22-61 -----------------------------------
 namespace {
 thread_local std::function<void()> t_warmup_sync;

@@ -28,6 +28,9 @@ std::vector<as_variant> shortlist(const as_features& gf, std::uint64_t f, int op
                                   const as_device_profile& dp);
 // B200 model: drop variants that launch the same kernel as a better-ranked one.
 std::vector<as_variant> distinct_gpu_configs(const std::vector<as_variant>& ranked, std::uint64_t f);
+// SpMM candidates take f_tile 64 where B overflows the L2 but a 64-column
+// slice fits (tile-major walk; policy.cpp)
+void l2_tile_rule(std::vector<as_variant>& cands, std::uint64_t f, std::uint64_t n_cols);
 
 // ProbeTimer::time_once_ms (include/autosage/timing.hpp:10-15)
 using TimeOnce = std::function<double(const std::string&, const std::function<void()>&)>;
