@@ -4,6 +4,8 @@ Mirrors proj/tests/test_scheduler.cpp, test_attention.cpp, test_csr.cpp and
 test_generate.cpp; features / sample / slice / graph_sig are bit-exact
 against the oracle (and the reference library itself when built).
 """
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -427,4 +429,23 @@ def test_attention_heads_batched_equals_single_calls(fused):
         one = one.cpu().numpy() if hasattr(one, "cpu") else one
         assert bit_equal(outs[h].cpu().numpy(), one), h
     assert batched_probes == asb.probe_launch_count() > 0  # one decide per op, as the cached single calls
+    g.close()
+
+
+def test_l2_tile_rule_decides_64_wide_spmm_tiles():
+    """B200 scheduler: where B overflows the 96 MB L2 budget but a 64-column
+    slice fits, SpMM candidates take f_tile 64 (policy.cpp l2_tile_rule); a
+    small B keeps the probe's own pick.  The output is the same bits."""
+    import torch
+    rng = np.random.default_rng(81)
+    n = 300_000
+    m = asb.gen_powerlaw(n, n, 3_000_000, 2.2, 4, 3_000, 5)
+    g = asb.Graph.from_csr(m)
+    b = torch.from_numpy(rng.uniform(-1, 1, (n, 128)).astype(np.float32)).cuda()  # 154 MB
+    ctx = asb.ScheduleContext(cache=asb.ScheduleCache())
+    d = asb.decide_spmm(g, b, None, ctx)
+    assert d.choice is not None and d.choice.f_tile == 64, asb.variant_to_string(d.choice)
+    c = asb.spmm_auto(g, b, ctx=ctx).cpu().numpy()
+    wide = asb.dispatch(dataclasses.replace(d.choice, f_tile=128), g, b).output.cpu().numpy()
+    assert bit_equal(c, wide)  # the rule changes the speed, never the bits
     g.close()
