@@ -400,9 +400,14 @@ def test_sddmm_op_bf16_forward_and_grad():
 
 
 @pytest.mark.gpu
-def test_spmm_transpose_values_equals_permute_then_spmm():
+@pytest.mark.parametrize("merged", ["1", "2"])
+def test_spmm_transpose_values_equals_permute_then_spmm(monkeypatch, merged):
+    """A^T products with the values loaded through the entry permutation; with
+    AUTOSAGE_DEV_SPMM_MERGED=2 the hub-split runs as one launch over pieces +
+    light rows even on these small graphs."""
     import ctypes as C
     from paper_2511_17594_b200 import _lib
+    monkeypatch.setenv("AUTOSAGE_DEV_SPMM_MERGED", merged)
     rng = np.random.default_rng(35)
     for m in (hub_graph(rng, 1500, [1400, 500], 11), random_csr(rng, 300, 300, 30)):
         g = asb.Graph.from_csr(m.with_values(None))

@@ -577,7 +577,8 @@ def test_fused_attention_equals_unfused_bitwise():
 
 
 @pytest.mark.parametrize("force", [("AUTOSAGE_WPB", "4"), ("AUTOSAGE_HUB_T", "256"),
-                                   ("AUTOSAGE_HUB_T", "1"), ("AUTOSAGE_FTILE", "32")])
+                                   ("AUTOSAGE_HUB_T", "1"), ("AUTOSAGE_FTILE", "32"),
+                                   ("AUTOSAGE_DEV_SPMM_MERGED", "2")])
 @pytest.mark.parametrize("scale", [1.0, 40.0])
 def test_fused_attention_softmax_on_the_fly_bitwise(monkeypatch, force, scale):
     """Fused path = SDDMM -> per-row (max, sum) -> SpMM computing each
