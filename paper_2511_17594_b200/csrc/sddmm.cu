@@ -745,19 +745,40 @@ __device__ __forceinline__ void pair1_y4(const void* ya, const void* yb, int ka,
     }
 }
 
-template <int F, int ORD, int FT, bool XS, int MIX, bool SAME, int WT = kWtF32>
+// X features [t, t+4) of a row read as f32 from global memory and widened
+// here (the F=100 path has no f64 prepass): components 2, 3 pre-scaled by
+// 2^896 under MIX, as the prepass would have stored them
+template <int MIX>
+__device__ __forceinline__ void ld_xf4(const double* p, double2& x01, double2& x23) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+    const double up = MIX ? kWidenUp : 1.0;
+    x01 = make_double2(double(v.x), double(v.y));
+    x23 = make_double2(double(v.z) * up, double(v.w) * up);
+}
+
+// XF: the X pointers are f32 rows (reinterpreted; see ld_xf4) when !XS
+template <int F, int ORD, int FT, bool XS, int MIX, bool SAME, int WT = kWtF32, bool XF = false>
 __device__ __forceinline__ void pair1_pass(const double* __restrict__ xa, const double* __restrict__ xb,
                                           const void* ya, const void* yb, int ka, int kb, double (&c)[2][5]) {
 #pragma unroll 4
     for (int t = 0; t < F; t += 4) {
         float4 u, w;
         pair1_y4<F, WT>(ya, yb, ka, kb, t, u, w);
-        const double2 x01 = ld_x2<XS>(xa + t);
-        const double2 x23 = ld_x2<XS>(xa + t + 2);
+        double2 x01, x23;
+        if constexpr (XF && !XS) {
+            ld_xf4<MIX>(reinterpret_cast<const double*>(reinterpret_cast<const float*>(xa) + t), x01, x23);
+        } else {
+            x01 = ld_x2<XS>(xa + t);
+            x23 = ld_x2<XS>(xa + t + 2);
+        }
         double2 z01 = x01, z23 = x23;
         if constexpr (!SAME) {
-            z01 = ld_x2<XS>(xb + t);
-            z23 = ld_x2<XS>(xb + t + 2);
+            if constexpr (XF && !XS) {
+                ld_xf4<MIX>(reinterpret_cast<const double*>(reinterpret_cast<const float*>(xb) + t), z01, z23);
+            } else {
+                z01 = ld_x2<XS>(xb + t);
+                z23 = ld_x2<XS>(xb + t + 2);
+            }
         }
         if constexpr (ORD == 0) {
             c[0][0] = __fma_rn(x01.x, widen<0>(u.x), c[0][0]);
@@ -799,7 +820,7 @@ struct PassArgs {
     int last = 1;
 };
 
-template <int F, int ORD, int FT, int MIX, int WT = kWtF32, bool PM = false>
+template <int F, int ORD, int FT, int MIX, int WT = kWtF32, bool PM = false, bool XF = false>
 __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict__ rowptr,
                                                 const std::uint32_t* __restrict__ colind,
                                                 const std::uint32_t* __restrict__ chunk_row, std::uint64_t n_rows,
@@ -860,11 +881,27 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
             cp_async16_pol(ys + j * F + kUnitElems * (q ^ swz<Sh::NV>(j)), y + std::uint64_t(cj) * LD + F0 + kUnitElems * q,
                            pol_k);
         }
+        // XF: the f32 X rows are loaded here and widened into shared memory
+        // after the row search below, so the loads' latency overlaps it
+        constexpr int kXf = XF ? (Sh::KX * F / 4 + 31) / 32 : 1;  // float4 per lane
+        float4 xv[kXf];
+        if constexpr (XF) {
+            const float* xf = reinterpret_cast<const float*>(xd);
 #pragma unroll
-        for (int u = lane; u < Sh::kXUnits; u += 32) {
-            const int k = u / (F / 2), uu = u % (F / 2);
-            const std::uint64_t xr = std::uint64_t(cur.r_first) + k;
-            if (xr < n_rows) cp_async16_pol(xs + 2 * u, xd + xr * LD + F0 + 2 * uu, pol_x);
+            for (int i = 0; i < kXf; ++i) {
+                const int u = lane + 32 * i;
+                const int k = u / (F / 4), uu = u % (F / 4);
+                const std::uint64_t xr = std::uint64_t(cur.r_first) + k;
+                if (u < Sh::KX * F / 4 && xr < n_rows)
+                    xv[i] = __ldg(reinterpret_cast<const float4*>(xf + xr * LD + 4 * uu));
+            }
+        } else {
+#pragma unroll
+            for (int u = lane; u < Sh::kXUnits; u += 32) {
+                const int k = u / (F / 2), uu = u % (F / 2);
+                const std::uint64_t xr = std::uint64_t(cur.r_first) + k;
+                if (xr < n_rows) cp_async16_pol(xs + 2 * u, xd + xr * LD + F0 + 2 * uu, pol_x);
+            }
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
         const Meta nxt = meta(pc + stride);
@@ -882,6 +919,20 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
             if (k == 32) {  // more than 32 rows meet in these 64 entries
                 ra = row_of(rowptr, ra, ea < e_end ? ea : e_end - 1);
                 rb = row_of(rowptr, rb, eb < e_end ? eb : e_end - 1);
+            }
+        }
+        if constexpr (XF) {
+            const double up = MIX ? kWidenUp : 1.0;
+#pragma unroll
+            for (int i = 0; i < kXf; ++i) {
+                const int u = lane + 32 * i;
+                const int k = u / (F / 4), uu = u % (F / 4);
+                const std::uint64_t xr = std::uint64_t(cur.r_first) + k;
+                if (u < Sh::KX * F / 4 && xr < n_rows) {
+                    double2* dst = reinterpret_cast<double2*>(xs + k * F + 4 * uu);
+                    dst[0] = make_double2(double(xv[i].x), double(xv[i].y));
+                    dst[1] = make_double2(double(xv[i].z) * up, double(xv[i].w) * up);
+                }
             }
         }
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
@@ -911,6 +962,11 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
                 pair1_pass<F, ORD, FT, true, MIX, true, WT>(xs + rela * F, xs + relb * F, ya, yb, ka, kb, c);
             else
                 pair1_pass<F, ORD, FT, true, MIX, false, WT>(xs + rela * F, xs + relb * F, ya, yb, ka, kb, c);
+        } else if constexpr (XF) {
+            const float* xf = reinterpret_cast<const float*>(xd);
+            pair1_pass<F, ORD, FT, false, MIX, false, WT, true>(
+                reinterpret_cast<const double*>(xf + std::uint64_t(ra) * LD),
+                reinterpret_cast<const double*>(xf + std::uint64_t(rb) * LD), ya, yb, ka, kb, c);
         } else {
             pair1_pass<F, ORD, FT, false, MIX, false, WT>(xd + std::uint64_t(ra) * LD + F0,
                                                          xd + std::uint64_t(rb) * LD + F0, ya, yb, ka, kb, c);
@@ -931,7 +987,8 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
 // (17.4 KB per warp at F=64) caps residency at 3 CTAs through shared memory
 // anyway; bf16 staging halves that, so its kernels can trade registers for
 // occupancy.
-template <int F, int ORD, int FT, int WT = kWtF32, int MINB = 3>
+// XF: xd is the f32 X itself (widened in the kernel, no prepass)
+template <int F, int ORD, int FT, int WT = kWtF32, int MINB = 3, bool XF = false>
 __global__ void __launch_bounds__(128, MINB)
     sddmm_pair1_kernel(const std::uint64_t* __restrict__ rowptr, const std::uint32_t* __restrict__ colind,
                       const std::uint32_t* __restrict__ chunk_row, std::uint64_t n_rows,
@@ -940,11 +997,11 @@ __global__ void __launch_bounds__(128, MINB)
                       const unsigned* __restrict__ finite, int keep, std::uint64_t n_cols) {
     // keep: Y fits the L2 (kKeepMaxBytes) -- the Y and X staging reads evict_last
     if (finite && *finite)
-        sddmm_pair1_body<F, ORD, FT, 1, WT>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin, c_end,
-                                            keep, n_cols);
+        sddmm_pair1_body<F, ORD, FT, 1, WT, false, XF>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin,
+                                                       c_end, keep, n_cols);
     else
-        sddmm_pair1_body<F, ORD, FT, 0, WT>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin, c_end,
-                                            keep, n_cols);
+        sddmm_pair1_body<F, ORD, FT, 0, WT, false, XF>(rowptr, colind, chunk_row, n_rows, xd, y, out, nnz, c_begin,
+                                                       c_end, keep, n_cols);
 }
 
 // One 64-feature pass of an F >= 128 SDDMM (PassArgs above)
@@ -1054,8 +1111,13 @@ void widen_x(Graph& g, const float* x, std::uint32_t f, cudaStream_t s, const un
     check_launch("widen_kernel");
 }
 
-void launch_sddmm_fixed(Graph& g, const float* y, std::uint32_t f, float* out, std::uint32_t ft, int ord,
-                        cudaStream_t s, const unsigned* finite, std::uint64_t c_begin, std::uint64_t c_end) {
+// F=100: the pair kernel widens f32 X itself (no f64 prepass, half the X
+// bytes); AUTOSAGE_DEV_SDDMM_XF32=0 restores the prepass (A/B)
+bool x_widened_in_kernel(std::uint32_t f) { return f == kPairOddF && dev_knob("AUTOSAGE_DEV_SDDMM_XF32", 1) != 0; }
+
+void launch_sddmm_fixed(Graph& g, const float* x, const float* y, std::uint32_t f, float* out, std::uint32_t ft,
+                        int ord, cudaStream_t s, const unsigned* finite, std::uint64_t c_begin,
+                        std::uint64_t c_end) {
     // Y (re-read by every entry of its column) fits the L2 beside the
     // streams: the staging reads evict_last
     const int keep_y = int(std::uint64_t(g.n_cols) * f * 4 <= kKeepMaxBytes) | x_policy_bits();
@@ -1155,15 +1217,23 @@ void launch_sddmm_fixed(Graph& g, const float* y, std::uint32_t f, float* out, s
                 const std::uint64_t want = (pairs + kWarps - 1) / kWarps;
                 const std::uint64_t cap = std::uint64_t(sms) * std::max(per_sm, 1);
                 const unsigned blocks = unsigned(std::max<std::uint64_t>(1, std::min(want, cap)));
+                const double* xop = x_widened_in_kernel(f) ? reinterpret_cast<const double*>(x) : g.xwide.get();
                 kernel<<<blocks, kWarps * 32, smem, s>>>(g.rowptr.get(), g.colind.get(), g.chunk_row.get(),
-                                                         g.n_rows, g.xwide.get(), y, out, g.nnz, f, c_begin, c_end,
+                                                         g.n_rows, xop, y, out, g.nnz, f, c_begin, c_end,
                                                          finite, keep_y, g.n_cols);
                 check_launch("sddmm_pair_kernel");
             };
-            if (ord == 0) run(sddmm_pair1_kernel<F, 0, 0, kWtF32, 2>);
-            else if (ft >= f) run(sddmm_pair1_kernel<F, 1, 0, kWtF32, 2>);
-            else if (ft == 32) run(sddmm_pair1_kernel<F, 1, 32, kWtF32, 2>);
-            else run(sddmm_pair1_kernel<F, 1, 64, kWtF32, 2>);
+            if (x_widened_in_kernel(f)) {
+                if (ord == 0) run(sddmm_pair1_kernel<F, 0, 0, kWtF32, 2, true>);
+                else if (ft >= f) run(sddmm_pair1_kernel<F, 1, 0, kWtF32, 2, true>);
+                else if (ft == 32) run(sddmm_pair1_kernel<F, 1, 32, kWtF32, 2, true>);
+                else run(sddmm_pair1_kernel<F, 1, 64, kWtF32, 2, true>);
+            } else {
+                if (ord == 0) run(sddmm_pair1_kernel<F, 0, 0, kWtF32, 2>);
+                else if (ft >= f) run(sddmm_pair1_kernel<F, 1, 0, kWtF32, 2>);
+                else if (ft == 32) run(sddmm_pair1_kernel<F, 1, 32, kWtF32, 2>);
+                else run(sddmm_pair1_kernel<F, 1, 64, kWtF32, 2>);
+            }
         } else if (pass_major(g, f, ft, ord)) {
             // one launch per 64-feature pass (PassArgs): the slice of Y a
             // pass gathers fits the L2 where the whole Y does not
@@ -1242,7 +1312,7 @@ void sddmm_chunks_prepare(Graph& g, const float* x, const float* y, std::uint32_
     if (g.nnz == 0 || f == 0) return;
     ensure_chunk_rows(g);
     const std::uint32_t ft = std::uint32_t(effective_tile(f_tile, f));
-    if (fixed_eligible(x, y, f, ft, vec ? 1 : 0))
+    if (fixed_eligible(x, y, f, ft, vec ? 1 : 0) && !x_widened_in_kernel(f))
         widen_x(g, x, f, s, dev_knob("AUTOSAGE_DEV_SDDMM_MIX", 1) ? finite : nullptr, r0, r1);
 }
 
@@ -1264,8 +1334,8 @@ void launch_sddmm_chunks(Graph& g, const float* x, const float* y, std::uint32_t
     }
     if (fixed_eligible(x, y, f, ft, ord)) {
         const unsigned* fin = dev_knob("AUTOSAGE_DEV_SDDMM_MIX", 1) ? finite : nullptr;
-        if (prepare) widen_x(g, x, f, s, fin);
-        launch_sddmm_fixed(g, y, f, out, ft, ord, s, fin, c_begin, c_end);
+        if (prepare && !x_widened_in_kernel(f)) widen_x(g, x, f, s, fin);
+        launch_sddmm_fixed(g, x, y, f, out, ft, ord, s, fin, c_begin, c_end);
         return;
     }
     const bool vload = vec;  // vec4 gate already applied by dispatch
