@@ -712,6 +712,9 @@ __global__ void __launch_bounds__(128, 3)
 // specialisation measured 6% faster than the pass loop at F = 64).
 // BF: Y rows staged as bf16 (half the cp.async and LDS wavefronts; one
 // 16-byte unit holds 8 features)
+#ifndef ASB_PAIR_RF_PREFETCH
+#define ASB_PAIR_RF_PREFETCH 1  // chunk_row loaded an iteration ahead (A/B build knob)
+#endif
 #ifndef ASB_PAIR_KX
 #define ASB_PAIR_KX 2  // X rows a pair-kernel warp stages for F <= 64 (A/B build knob)
 #endif
@@ -857,20 +860,29 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
         std::uint32_t ca, cb, r_first;
         std::uint64_t bound;
     };
-    auto meta = [&](std::uint64_t pc) {
-        Meta m{0u, 0u, 0u, ~0ull};
+    // the chunk's first row is loaded one iteration before the rest of its
+    // metadata: the rowptr bounds load depends on it, and issuing both back
+    // to back stalled every iteration on the chunk_row load (the hottest
+    // stall line of the r02ak capture)
+    auto first_row = [&](std::uint64_t pc) {
+        return pc < n_pairs ? __ldg(chunk_row + c_begin + 2 * pc) : 0u;
+    };
+    auto meta = [&](std::uint64_t pc, std::uint32_t r_first) {
+        Meta m{0u, 0u, r_first, ~0ull};
         if (pc >= n_pairs) return m;
         const std::uint64_t e0 = (c_begin + 2 * pc) * 32;
         m.ca = e0 + lane < e_end ? ld_stream(colind + e0 + lane, pol_s) : 0u;
         m.cb = e0 + 32 + lane < e_end ? ld_stream(colind + e0 + 32 + lane, pol_s) : 0u;
-        m.r_first = __ldg(chunk_row + c_begin + 2 * pc);
-        const std::uint64_t bi = std::uint64_t(m.r_first) + 1 + lane;
+        const std::uint64_t bi = std::uint64_t(r_first) + 1 + lane;
         if (bi <= n_rows) m.bound = __ldg(rowptr + bi);
         return m;
     };
 
     std::uint64_t pc = std::uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    Meta cur = meta(pc);
+    Meta cur = meta(pc, first_row(pc));
+#if ASB_PAIR_RF_PREFETCH
+    std::uint32_t rf_next = first_row(pc + stride);
+#endif
     for (; pc < n_pairs; pc += stride) {
 #pragma unroll
         for (int it = 0; it < Sh::kCopies; ++it) {
@@ -904,7 +916,12 @@ __device__ __forceinline__ void sddmm_pair1_body(const std::uint64_t* __restrict
             }
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
-        const Meta nxt = meta(pc + stride);
+#if ASB_PAIR_RF_PREFETCH
+        const Meta nxt = meta(pc + stride, rf_next);
+        rf_next = first_row(pc + 2 * stride);
+#else
+        const Meta nxt = meta(pc + stride, first_row(pc + stride));
+#endif
         const std::uint64_t e0 = (c_begin + 2 * pc) * 32, ea = e0 + lane, eb = ea + 32;
         std::uint32_t ra = cur.r_first, rb = cur.r_first;
         const unsigned inside = __ballot_sync(FULL, cur.bound <= e0 + 63);
