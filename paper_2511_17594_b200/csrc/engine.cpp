@@ -551,6 +551,12 @@ std::uint64_t host_slices() {
     return k && *k > 0 ? std::uint64_t(*k) : 16;
 }
 
+// first host slice = 1/head of an even slice (AUTOSAGE_HOST_HEAD; 1 = even)
+std::uint64_t host_head() {
+    const auto h = env::get_int("AUTOSAGE_HOST_HEAD");
+    return h && *h > 0 ? std::uint64_t(*h) : 8;
+}
+
 }  // namespace
 
 KernelResult spmm_host(const as_variant* v, Graph& g, const float* b_host, std::uint64_t b_rows,
@@ -623,13 +629,21 @@ KernelResult sddmm_host(const as_variant* v, Graph& g, const float* x_host, std:
     const std::uint64_t n_chunks = (g.nnz + 31) / 32;
     const std::uint64_t k = std::max<std::uint64_t>(1, std::min(host_slices(), n_chunks));
     const std::uint64_t per = (n_chunks + k - 1) / std::max<std::uint64_t>(k, 1);
+    // the first slice is cut short (1/head of the others) so the D2H link,
+    // the step's bottleneck, starts as soon as Y has landed; the rest stay even
+    const std::uint64_t head = std::max<std::uint64_t>(1, per / host_head());
+    const std::uint64_t rest = k > 1 ? (n_chunks - std::min(n_chunks, head) + k - 2) / (k - 1) : per;
+    auto slice_begin = [&](std::uint64_t i) {
+        if (k == 1 || i == 0) return i == 0 ? std::uint64_t(0) : n_chunks;
+        return std::min(n_chunks, head + (i - 1) * rest);
+    };
     ensure_slices(g, std::size_t(k));
     const unsigned* fin = nullptr;
     const std::uint32_t wpb = std::uint32_t(std::min<std::uint64_t>(r.variant.rows_per_chunk, 16));
     if (r.variant.mapping != AS_MAP_BASELINE) fin = mix_flag(g, y, y_rows * f, g.stream, true);
     std::uint64_t x_done = 0;  // X rows [0, x_done) queued
     for (std::uint64_t i = 0; i < k && n_chunks; ++i) {
-        const std::uint64_t c0 = i * per, c1 = std::min(n_chunks, c0 + per);
+        const std::uint64_t c0 = slice_begin(i), c1 = i + 1 == k ? n_chunks : slice_begin(i + 1);
         if (c0 >= c1) break;
         // X rows of this slice's entries
         const std::uint64_t ra = host_row_of(g, c0 * 32);

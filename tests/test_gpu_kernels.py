@@ -599,11 +599,14 @@ def test_fused_attention_softmax_on_the_fly_bitwise(monkeypatch, force, scale):
 
 
 # ---- host-buffer pipeline (as_*_host, as_*_host_async) ------------------------------
-@pytest.mark.parametrize("slices", ["1", "3", "8", "1000000"])
-def test_sddmm_host_slices_bit_exact(monkeypatch, slices):
-    """The SDDMM values leave in slices of 32-entry chunks; every slicing
-    returns the same bytes (odd nnz, fixed-width and generic widths)."""
+@pytest.mark.parametrize("slices,head", [("1", "8"), ("3", "1"), ("3", "8"), ("8", "8"), ("8", "1000"),
+                                         ("1000000", "8")])
+def test_sddmm_host_slices_bit_exact(monkeypatch, slices, head):
+    """The SDDMM values leave in slices of 32-entry chunks (the first one
+    1/head of the rest); every slicing returns the same bytes (odd nnz,
+    fixed-width and generic widths)."""
     monkeypatch.setenv("AUTOSAGE_HOST_SLICES", slices)
+    monkeypatch.setenv("AUTOSAGE_HOST_HEAD", head)
     monkeypatch.setenv("AUTOSAGE_DEV_SDDMM_PM", "1")  # F=128: pass-major per slice
     rng = np.random.default_rng(51)
     p = hub_graph(rng, 900, [850, 333, 70], 7, with_values=False)
