@@ -317,8 +317,8 @@ void freeze_mix_flag(Graph& g, const float* p, std::uint64_t n, cudaStream_t s, 
     g.flag_frozen = true;
 }
 
-// rmax/rsum (softmax mode, fused attention): vals are raw scores and the
-// kernels apply the row softmax on the fly (ops.hpp)
+// rmax/rsum (softmax mode, fused attention): vals are the stats pass's ex and
+// the kernels turn them into probabilities on the fly (ops.hpp)
 void run_spmm_variant(const as_variant& v, Graph& a, const float* vals, const float* b,
                       std::uint64_t f, float* c, cudaStream_t s, bool vec,
                       const float* rmax = nullptr, const double* rsum = nullptr) {
@@ -861,9 +861,9 @@ void attention_forward(const Context& ctx, const as_probe_config& cfg, Graph& pa
 
     bool done = false;
     if (fused && !p_ready && pd.has_choice) {
-        // SDDMM -> per-row (max, sum) -> SpMM that turns each score into its
-        // probability as it loads it: p never touches memory, and the bits are
-        // those of the staged pipeline (same softmax.cuh arithmetic)
+        // SDDMM -> per-row (max, sum) and per-entry ex -> SpMM that turns each
+        // ex into its probability as it loads it: p never touches memory, and
+        // the bits are those of the staged pipeline (same softmax.cuh arithmetic)
         const as_variant pv = apply_env_overrides(pd.choice);
         check_variant(pv);
         const void* vv[1] = {v};
@@ -872,9 +872,9 @@ void attention_forward(const Context& ctx, const as_probe_config& cfg, Graph& pa
             else sddmm_baseline(pattern, q, q_rows, k, k_rows, f, scores, s);
             pattern.att_max.ensure(std::max<std::uint64_t>(pattern.n_rows, 1));
             pattern.att_sum.ensure(std::max<std::uint64_t>(pattern.n_rows, 1));
-            launch_row_softmax_stats(pattern, scores, pattern.att_max.get(), pattern.att_sum.get(), s);
-            run_spmm_variant(pv, pattern, scores, v, fv, out, s, true, pattern.att_max.get(),
-                             pattern.att_sum.get());
+            float* ex = scores + pattern.nnz;  // p's slot, unused on this path
+            launch_row_softmax_stats(pattern, scores, ex, pattern.att_max.get(), pattern.att_sum.get(), s);
+            run_spmm_variant(pv, pattern, ex, v, fv, out, s, true, pattern.att_max.get(), pattern.att_sum.get());
             done = true;
         }
     }
@@ -913,14 +913,15 @@ void attention_half(Graph& pattern, const as_variant* sv, const as_variant* pv, 
     if (fused && !p_out && pvar.mapping != AS_MAP_BASELINE && vec_ok && pattern.nnz) {
         pattern.att_max.ensure(std::max<std::uint64_t>(pattern.n_rows, 1));
         pattern.att_sum.ensure(std::max<std::uint64_t>(pattern.n_rows, 1));
-        launch_row_softmax_stats(pattern, scores, pattern.att_max.get(), pattern.att_sum.get(), s);
+        float* ex = scores + pattern.nnz;  // p's slot, unused on this path
+        launch_row_softmax_stats(pattern, scores, ex, pattern.att_max.get(), pattern.att_sum.get(), s);
         const std::uint32_t wpb = std::uint32_t(std::min<std::uint64_t>(pvar.rows_per_chunk, 16));
         if (pvar.mapping == AS_MAP_ROWPARALLEL) {
             ensure_order(pattern);
-            launch_spmm_rows(pattern, scores, 0, pattern.n_rows, v, std::uint32_t(fv), out, pvar.f_tile, true, wpb, s,
+            launch_spmm_rows(pattern, ex, 0, pattern.n_rows, v, std::uint32_t(fv), out, pvar.f_tile, true, wpb, s,
                              nullptr, pattern.att_max.get(), pattern.att_sum.get(), wt);
         } else {
-            launch_spmm_hubsplit(pattern, scores, v, std::uint32_t(fv), out, pvar.f_tile, true, wpb,
+            launch_spmm_hubsplit(pattern, ex, v, std::uint32_t(fv), out, pvar.f_tile, true, wpb,
                                  pvar.hub_threshold, s, nullptr, pattern.att_max.get(), pattern.att_sum.get(), wt);
         }
         return;

@@ -29,10 +29,11 @@ void launch_spmm_hubsplit(Graph& g, const float* val, const void* b, std::uint32
                           std::uint64_t hub_threshold, cudaStream_t s,
                           const unsigned* finite = nullptr, const float* rmax = nullptr,
                           const double* rsum = nullptr, int wt = 0);
-// Softmax mode of K2/K3 (rmax != nullptr): `val` holds raw scores and each
-// entry's value is p_e = softmax of its row from (rmax[row], rsum[row])
-// (softmax.cuh), computed by the loading lane -- the SpMM half of the fused
-// attention, bit-equal to SpMM over row_softmax's output.
+// Softmax mode of K2/K3 (rmax != nullptr): `val` holds each entry's ex =
+// f32(exp(score - max)) from launch_row_softmax_stats and each entry's value
+// is p_e = sm_prob(ex, rsum[row]) (softmax.cuh), computed by the loading lane
+// -- the SpMM half of the fused attention, bit-equal to SpMM over
+// row_softmax's output.
 
 // ---- SDDMM (src/kernels.cpp:336-429) -----------------------------------
 // order: 0 = sequential (scalar variants and the baseline), 1 = per-f_tile
@@ -69,8 +70,9 @@ const unsigned* finite_flag_half(Graph& g, const std::uint16_t* p, std::uint64_t
 
 // ---- row softmax (src/kernels.cpp:431-461) ----------------------------
 void launch_row_softmax(Graph& g, const float* vin, float* vout, cudaStream_t s);
-// per-row (max, sum) only (fused attention); rows of degree 0 are not written
-void launch_row_softmax_stats(Graph& g, const float* vin, float* rmax, double* rsum, cudaStream_t s);
+// per-row (max, sum) and per-entry ex (fused attention; ex must not alias
+// vin); rows of degree 0 are not written
+void launch_row_softmax_stats(Graph& g, const float* vin, float* ex, float* rmax, double* rsum, cudaStream_t s);
 
 // ---- backward (backward.cu) ----------------------------
 // dst[k] = src[perm[k]]

@@ -20,8 +20,11 @@
 // Either way one global read and one write per entry.  The CTA kernel runs
 // on a forked stream, concurrently with the warp kernel.
 //
-// Stats mode (OUT = false) writes only (mx, sum) per row: the fused
-// attention SpMM recomputes p_e from the raw scores with the same code.
+// Stats mode (OUT = false) writes (mx, sum) per row and, into vout, each
+// entry's ex = f32(exp(v - mx)): the fused attention SpMM turns ex into p_e
+// with the same sm_prob as the output pass, so it never recomputes the f64
+// exp.  Every path that computes a row's ex writes it (vout must not alias
+// vin: a row deferred to the chain kernel is read again there).
 #include "ops.hpp"
 #include "softmax.cuh"
 
@@ -42,7 +45,7 @@ struct SoftmaxArgs {
     const std::uint32_t* order;  // rows of this launch: order[0, n)
     std::uint64_t n;
     const float* vin;
-    float* vout;    // OUT
+    float* vout;    // OUT: probabilities; !OUT: ex (see above)
     float* rmax;    // !OUT
     double* rsum;   // !OUT
     int force_seq;  // developer/test knob: always run the sequential chain
@@ -148,9 +151,14 @@ __global__ void __launch_bounds__(256, 3) softmax_warp_kernel(SoftmaxArgs a) {
                 float* vout = a.vout + cur.e0;
 #pragma unroll 4
                 for (std::uint32_t k = lane; k < deg; k += 32) vout[k] = sm_prob(exs[k], sum, rcp);
-            } else if (lane == 0) {
-                a.rmax[cur.row] = mx;
-                a.rsum[cur.row] = sum;
+            } else {
+                float* vex = a.vout + cur.e0;
+#pragma unroll 4
+                for (std::uint32_t k = lane; k < deg; k += 32) vex[k] = exs[k];
+                if (lane == 0) {
+                    a.rmax[cur.row] = mx;
+                    a.rsum[cur.row] = sum;
+                }
             }
         }
         __syncwarp();  // buffer `slot` is refilled by the next iteration's issue
@@ -362,9 +370,19 @@ __global__ void __launch_bounds__(256, 3) softmax_cta_kernel(SoftmaxArgs a) {
                 for (std::uint32_t k = tid; k < deg; k += 256)
                     vout[k] = sm_prob(ex_of<LIB>(vin[k], dmx), sum, rcp);
             }
-        } else if (tid == 0) {
-            a.rmax[cur.row] = mx;
-            a.rsum[cur.row] = sum;
+        } else {
+            float* vex = a.vout + cur.e0;
+            if (staged) {
+#pragma unroll 4
+                for (std::uint32_t k = tid; k < deg; k += 256) vex[k] = cexs[k];
+            } else {
+#pragma unroll 4
+                for (std::uint32_t k = tid; k < deg; k += 256) vex[k] = ex_of<LIB>(__ldg(vin + k), dmx);
+            }
+            if (tid == 0) {
+                a.rmax[cur.row] = mx;
+                a.rsum[cur.row] = sum;
+            }
         }
         __syncthreads();  // buffer `slot` and `red` are reused next iteration
         cur = nxt;
@@ -401,7 +419,11 @@ __global__ void __launch_bounds__(256, 4) softmax_chain_kernel(SoftmaxArgs a) {
             const float v = vnext;
             const std::uint32_t kn = base + 32 + lane;
             vnext = kn < deg ? __ldg(vin + kn) : 0.f;
-            st[lane] = base + lane < deg ? double(ex_of<LIB>(v, dmx)) : 0.0;
+            const float ex = ex_of<LIB>(v, dmx);
+            st[lane] = base + lane < deg ? double(ex) : 0.0;
+            if constexpr (!OUT) {
+                if (base + lane < deg) a.vout[e0 + base + lane] = ex;
+            }
             __syncwarp();
             if (lane == 0) {
                 const std::uint32_t m = deg - base < 32 ? deg - base : 32;
@@ -502,8 +524,9 @@ void launch_row_softmax(Graph& g, const float* vin, float* vout, cudaStream_t s)
     launch_softmax<true>(g, vin, vout, nullptr, nullptr, s);
 }
 
-void launch_row_softmax_stats(Graph& g, const float* vin, float* rmax, double* rsum, cudaStream_t s) {
-    launch_softmax<false>(g, vin, nullptr, rmax, rsum, s);
+void launch_row_softmax_stats(Graph& g, const float* vin, float* ex, float* rmax, double* rsum, cudaStream_t s) {
+    if (ex == vin) throw LogicError("softmax stats: ex must not alias the scores");
+    launch_softmax<false>(g, vin, ex, rmax, rsum, s);
 }
 
 } // namespace asb

@@ -197,10 +197,8 @@ __device__ __forceinline__ void longrow_body(const SegArgs& A, std::uint32_t ch,
     ASB_DCHECK(row < A.n_rows && e0 + deg <= A.nnz);
     const std::uint32_t nchunks = (deg + ch - 1) / ch;
     const int warp = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
-    float rmx = 0.f;
     double rsm = 1.0, rrc = 1.0;
     if constexpr (SMX) {
-        rmx = A.rmax[row];
         rsm = A.rsum[row];
         rrc = sm_rcp(rsm);
     }
@@ -243,7 +241,7 @@ __device__ __forceinline__ void longrow_body(const SegArgs& A, std::uint32_t ch,
             const float* vs = vidx + (k % kIdxRing) * ch;
             double* vdst = vd + std::uint64_t(s) * ch;
             for (std::uint32_t j = lane; j < n; j += 32)
-                vdst[j] = SMX ? double(sm_prob_of(vs[j], rmx, rsm, rrc)) : (HAS_VAL ? double(vs[j]) : 1.0);
+                vdst[j] = SMX ? double(sm_prob(vs[j], rsm, rrc)) : (HAS_VAL ? double(vs[j]) : 1.0);
             __syncwarp();
             mbar_arrive(&full[s]);  // release: this lane's value stores
             // the stage's B rows as 16-byte cp.async pieces spread over the

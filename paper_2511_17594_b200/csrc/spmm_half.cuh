@@ -53,7 +53,7 @@ void launch_seg_half_t(int vec, int lpr, int nch, const SegArgs& a, bool has_val
                 constexpr int R = VEC == 1 && R0 < 96 ? 96 : R0;
                 constexpr int RS = R;
                 const std::size_t sm = seg_smem(nt);
-                if (a.rmax) {  // softmax mode (fused attention over 16-bit V): values are raw scores
+                if (a.rmax) {  // softmax mode (fused attention over 16-bit V): values are the stats pass ex
                     if (!has_val) throw LogicError("spmm softmax mode needs the score values");
                     if (pieces) spmm_seg_kernel<VEC, LPR, NCH, true, true, U, RS, true, WT><<<nb, nt, sm, s>>>(a);
                     else spmm_seg_kernel<VEC, LPR, NCH, true, false, U, RS, true, WT><<<nb, nt, sm, s>>>(a);

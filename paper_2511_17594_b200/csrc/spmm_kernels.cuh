@@ -34,8 +34,8 @@ struct SegArgs {
     const std::uint32_t* piece_slot;
     const unsigned* finite;           // device flag: B has no Inf/NaN (nullable)
     const std::uint32_t* vperm;       // values in source order: entry e reads val[vperm[e]] (nullable)
-    const float* rmax;                // softmax mode: val holds raw scores, and
-    const double* rsum;               // p_e = softmax of the row (softmax.cuh)
+    const float* rmax;                // softmax mode (non-null): val holds each entry's ex from
+    const double* rsum;               // the stats pass, p_e = sm_prob(ex, row sum) (softmax.cuh)
     int off32;                        // n_cols * f < 2^32: 32-bit element offsets
     int wt;                           // B word type (half.cuh): 0 f32, 1 bf16, 2 f16
     int keep_b;                       // B fits L2 (kKeepMaxBytes): gathers evict_last
@@ -150,8 +150,8 @@ __device__ __forceinline__ void seg_accumulate(double (&acc)[NCH][VEC], double v
 // a whole row (row mode) or a hub piece (PIECES).  MIX selects the widening
 // of B: 0 = F2F only, 1 = components 2,3 of each float4 (or every scalar)
 // re-biased on the ALU pipe.  SMX: the entry values are softmax
-// probabilities computed from raw scores and the row's (max, sum) by the lane
-// that loads them (fused attention), instead of stored values.
+// probabilities computed from the stats pass's ex and the row's sum by the
+// lane that loads them (fused attention), instead of stored values.
 // CARRY (column-blocked SpMM, spmm_blocked.cu): every item is a segment
 // with an f64 state slot; the accumulators start from scratch[slot] instead
 // of 0.0 and are written back there, so a row's entries can be consumed in
@@ -210,11 +210,9 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
     }
     std::uint32_t maxdeg = deg;
     if constexpr (GPW > 1) maxdeg = __reduce_max_sync(FULL, deg);
-    float rmx = 0.f;
     double rsm = 1.0, rrc = 1.0;
     if constexpr (SMX) {
         if (active && deg) {
-            rmx = a.rmax[row];
             rsm = a.rsum[row];
             rrc = sm_rcp(rsm);
         }
@@ -302,7 +300,7 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
                     ASB_DCHECK(k < deg && col < a.n_cols);
                     const std::uint32_t o = col * f;
                     float v;
-                    if constexpr (SMX) v = sm_prob_of(ld_stream(valp + k, pol_s), rmx, rsm, rrc);
+                    if constexpr (SMX) v = sm_prob(ld_stream(valp + k, pol_s), rsm, rrc);
                     else if constexpr (VP) v = __ldg(a.val + ld_stream(vpp + k, pol_s));
                     else if constexpr (HAS_VAL) v = ld_stream(valp + k, pol_s);
                     else v = 1.f;
@@ -349,7 +347,7 @@ __device__ __forceinline__ void seg_body(const SegArgs& a) {
             const bool ok = k < deg;
             cs[s] = ok ? ld_stream(colp + k, pol_s) : 0u;
             ASB_DCHECK(cs[s] < a.n_cols);
-            if constexpr (SMX) vs[s] = ok ? double(sm_prob_of(ld_stream(valp + k, pol_s), rmx, rsm, rrc)) : 0.0;
+            if constexpr (SMX) vs[s] = ok ? double(sm_prob(ld_stream(valp + k, pol_s), rsm, rrc)) : 0.0;
             else if constexpr (VP) vs[s] = ok ? double(__ldg(a.val + ld_stream(vpp + k, pol_s))) : 0.0;
             else if constexpr (HAS_VAL) vs[s] = ok ? double(ld_stream(valp + k, pol_s)) : 0.0;
             else vs[s] = 1.0;
