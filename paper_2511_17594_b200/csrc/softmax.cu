@@ -427,13 +427,31 @@ __global__ void __launch_bounds__(256, 4) softmax_chain_kernel(SoftmaxArgs a) {
             __syncwarp();
             if (lane == 0) {
                 const std::uint32_t m = deg - base < 32 ? deg - base : 32;
-                std::uint32_t j = 0;
-                for (; j + 2 <= m; j += 2) {
-                    const double2 d = *reinterpret_cast<const double2*>(st + j);
-                    sum = __dadd_rn(sum, d.x);
-                    sum = __dadd_rn(sum, d.y);
+                if (m == 32) {
+                    // whole chunk: the shared-memory loads are issued ahead of
+                    // the dependent adds (16 at a time), so the chain runs at
+                    // the DADD latency instead of LDS + DADD per pair
+                    const double2* sp = reinterpret_cast<const double2*>(st);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        double2 d[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) d[i] = sp[8 * h + i];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            sum = __dadd_rn(sum, d[i].x);
+                            sum = __dadd_rn(sum, d[i].y);
+                        }
+                    }
+                } else {
+                    std::uint32_t j = 0;
+                    for (; j + 2 <= m; j += 2) {
+                        const double2 d = *reinterpret_cast<const double2*>(st + j);
+                        sum = __dadd_rn(sum, d.x);
+                        sum = __dadd_rn(sum, d.y);
+                    }
+                    if (j < m) sum = __dadd_rn(sum, st[j]);
                 }
-                if (j < m) sum = __dadd_rn(sum, st[j]);
             }
             __syncwarp();
         }
