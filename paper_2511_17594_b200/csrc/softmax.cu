@@ -392,8 +392,8 @@ __global__ void __launch_bounds__(256, 3) softmax_cta_kernel(SoftmaxArgs a) {
 }
 
 // Rows deferred by the CTA kernel: warp per row, many warps per SM so many
-// chains are in flight.  32 entries at a time the lanes recompute ex in
-// parallel (next chunk's values already loaded) and stage it as f64; lane 0
+// chains are in flight.  64 entries at a time the lanes recompute ex in
+// parallel (next step's values already loaded) and stage it as f64; lane 0
 // folds them into the row's sum in entry order (the reference's chain, one
 // DADD per entry, two entries per LDS.128).  Then the output pass (ex
 // recomputed, coalesced) or the stats write.  (Lane per row -- 32 chains per
@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(256, 3) softmax_cta_kernel(SoftmaxArgs a) {
 // uncoalesced per-lane streams thrash L1.)
 template <bool OUT, bool LIB>
 __global__ void __launch_bounds__(256, 4) softmax_chain_kernel(SoftmaxArgs a) {
-    __shared__ __align__(16) double stage_all[kWarpsPerCta][32];
+    __shared__ __align__(16) double stage_all[kWarpsPerCta][2 * 32];
     const int lane = threadIdx.x & 31;
     double* st = stage_all[threadIdx.x >> 5];
     const unsigned n = *a.chain_n;
@@ -414,26 +414,32 @@ __global__ void __launch_bounds__(256, 4) softmax_chain_kernel(SoftmaxArgs a) {
         const std::uint32_t deg = std::uint32_t(a.rowptr[row + 1] - e0);
         const float* vin = a.vin + e0;
         double sum = 0.0;
-        float vnext = lane < int(deg) ? __ldg(vin + lane) : 0.f;
-        for (std::uint32_t base = 0; base < deg; base += 32) {
-            const float v = vnext;
-            const std::uint32_t kn = base + 32 + lane;
-            vnext = kn < deg ? __ldg(vin + kn) : 0.f;
-            const float ex = ex_of<LIB>(v, dmx);
-            st[lane] = base + lane < deg ? double(ex) : 0.0;
+        // 64 entries per step: each lane's two exps run as independent
+        // chains, and the warp syncs once per 64 adds
+        float vn0 = lane < int(deg) ? __ldg(vin + lane) : 0.f;
+        float vn1 = 32u + lane < deg ? __ldg(vin + 32 + lane) : 0.f;
+        for (std::uint32_t base = 0; base < deg; base += 64) {
+            const float v0 = vn0, v1 = vn1;
+            const std::uint32_t k0 = base + lane, k1 = k0 + 32;
+            vn0 = k0 + 64 < deg ? __ldg(vin + k0 + 64) : 0.f;
+            vn1 = k1 + 64 < deg ? __ldg(vin + k1 + 64) : 0.f;
+            const float ex0 = ex_of<LIB>(v0, dmx), ex1 = ex_of<LIB>(v1, dmx);
+            st[lane] = k0 < deg ? double(ex0) : 0.0;
+            st[32 + lane] = k1 < deg ? double(ex1) : 0.0;
             if constexpr (!OUT) {
-                if (base + lane < deg) a.vout[e0 + base + lane] = ex;
+                if (k0 < deg) a.vout[e0 + k0] = ex0;
+                if (k1 < deg) a.vout[e0 + k1] = ex1;
             }
             __syncwarp();
             if (lane == 0) {
-                const std::uint32_t m = deg - base < 32 ? deg - base : 32;
-                if (m == 32) {
-                    // whole chunk: the shared-memory loads are issued ahead of
+                const std::uint32_t m = deg - base < 64 ? deg - base : 64;
+                if (m == 64) {
+                    // whole step: the shared-memory loads are issued ahead of
                     // the dependent adds (16 at a time), so the chain runs at
                     // the DADD latency instead of LDS + DADD per pair
                     const double2* sp = reinterpret_cast<const double2*>(st);
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
+                    for (int h = 0; h < 4; ++h) {
                         double2 d[8];
 #pragma unroll
                         for (int i = 0; i < 8; ++i) d[i] = sp[8 * h + i];
